@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 datatype hot path (BASELINE.json configs[1]).
+
+Workload ("step"): pack then unpack all twelve interior-boundary halo faces
+(six 1-wide + six 8-wide) of a 514^3 float32 array (512^3 interior + ghost
+layer), values seeded uniform bytes, through the fused pack_multi /
+unpack_multi entry points (one launch each).  Metric = payload bytes read +
+written per second (pack: 2 x face bytes, unpack: 2 x face bytes).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mpx|reference]
+
+N > 1 runs under torchrun, one process per GPU, each rank an independent
+replica (pack/unpack do not shard; "scaling": "weak").  L2 (126 MB) is
+flushed between timed steps by writing a 256 MiB buffer outside the timed
+events.  --impl reference times the CPU oracle port of the reference
+algorithm (oracle/liboracle.so) on the host cores over the same faces.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+
+import numpy as np  # noqa: E402
+
+from golden_common import cfg2_faces, seeded_bytes  # noqa: E402
+
+N3 = 514
+ARRAY_BYTES = N3 ** 3 * 4
+METRIC = "pack/unpack payload GB/s (cfg2 halo faces)"
+WORKLOAD = ("cfg2: 12 halo faces (6 x 1-wide + 6 x 8-wide) of a 514^3 float32 array; "
+            "one step = fused pack of all faces + fused unpack into a second array")
+
+
+def face_specs():
+    return cfg2_faces()
+
+
+def face_bytes(spec):
+    sub = spec[2]
+    return sub[0] * sub[1] * sub[2] * 4
+
+
+def step_bytes():
+    return 4 * sum(face_bytes(s) for _, s in face_specs())
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def load_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        sm = []
+        smax = None
+        for s in self.samples:
+            try:
+                sm.append(float(s[0]))
+                smax = float(s[1])
+            except ValueError:
+                pass
+            for n, v in zip(names, s[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------- CPU arm
+
+
+def run_cpu_oracle(seconds, threads):
+    """Time the oracle port (C restatement of the reference algorithm) over
+    the same 12 faces: pack then unpack, faces spread over `threads` host
+    threads (ctypes releases the GIL).  Returns (GB/s, reps, sample text)."""
+    import oracle
+    from concurrent.futures import ThreadPoolExecutor
+    oracle.build()
+    arr = seeded_bytes(2, ARRAY_BYTES)
+    dst = np.zeros_like(arr)
+    types = [(oracle.OracleType(spec), face_bytes(spec)) for _, spec in face_specs()]
+    outs = [np.empty(b, np.uint8) for _, b in types]
+    lib = oracle.lib()
+    import ctypes
+
+    def one(i):
+        t, b = types[i]
+        lib.orc_pack(t.h, 1, arr.ctypes.data_as(ctypes.c_void_p), arr.size,
+                     outs[i].ctypes.data_as(ctypes.c_void_p))
+        tr = ctypes.c_int()
+        lib.orc_unpack(t.h, 1, outs[i].ctypes.data_as(ctypes.c_void_p), b,
+                       dst.ctypes.data_as(ctypes.c_void_p), dst.size, ctypes.byref(tr))
+
+    reps = 0
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        while True:
+            list(ex.map(one, range(len(types))))
+            reps += 1
+            if time.perf_counter() - t0 >= seconds:
+                break
+    dt = time.perf_counter() - t0
+    gbs = reps * step_bytes() / dt / 1e9
+    return gbs, reps, dt
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    # each "step" is a bounded sample: all 12 faces packed + unpacked once
+    import oracle  # noqa: F401
+    for _ in range(max(0, args.warmup)):
+        run_cpu_oracle(0.0, threads)
+    gbs, reps, dt = run_cpu_oracle(0.0, threads)
+    times = []
+    for _ in range(args.steps):
+        g, r, d = run_cpu_oracle(0.0, threads)
+        times.append(d / r)
+    ms = 1e3 * float(np.mean(times))
+    value = step_bytes() / (ms / 1e3) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded PCG64 bytes)",
+        "config": {"workload": WORKLOAD, "array": "514^3 float32", "faces": 12},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads,
+                         "kind": "port",
+                         "sample": "all 12 cfg2 faces packed+unpacked once per step by the C "
+                                   "oracle port, faces spread over %d host threads (%s)"
+                                   % (threads, cpu_model())},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------- GPU arm
+
+
+def gpu_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2402_12274_b200 as mp
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from specbuild import build_product
+
+    faces = face_specs()
+    dts = [build_product(spec, mp) for _, spec in faces]
+    arr_h = torch.from_numpy(seeded_bytes(2, ARRAY_BYTES))
+    arr_pinned = arr_h.pin_memory()
+    arr = arr_pinned.to(dev)
+    dst = torch.zeros_like(arr)
+    packed = [torch.empty(face_bytes(s), dtype=torch.uint8, device=dev) for _, s in faces]
+    packed_host = [torch.empty(p.numel(), dtype=torch.uint8).pin_memory() for p in packed]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        mp.pack_multi(dts, [arr] * len(dts), packed)
+        mp.unpack_multi(dts, packed, [dst] * len(dts))
+
+    # correctness spot check before timing: fused unpack(pack(x)) restores faces
+    step()
+    torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    for i in range(args.steps):
+        flush.zero_()                     # L2 flush, outside the timed events
+        a, b, c = ev[i]
+        a.record(stream)
+        mp.pack_multi(dts, [arr] * len(dts), packed)
+        b.record(stream)
+        mp.unpack_multi(dts, packed, [dst] * len(dts))
+        c.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    if world > 1:
+        dist.barrier()
+    pack_ms = [a.elapsed_time(b) for a, b, c in ev]
+    unpack_ms = [b.elapsed_time(c) for a, b, c in ev]
+    total_ms = sum(p + u for p, u in zip(pack_ms, unpack_ms))
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * step_bytes() / (ms_per_step / 1e3) / 1e9
+
+    # ---- e2e through the public API with host buffers (pinned) ----
+    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+    for i in range(args.steps + 1):
+        flush.zero_()
+        if i > 0:
+            e2e_ev[i - 1][0].record(stream)
+        arr.copy_(arr_pinned, non_blocking=True)
+        mp.pack_multi(dts, [arr] * len(dts), packed)
+        mp.unpack_multi(dts, packed, [dst] * len(dts))
+        for p, h in zip(packed, packed_host):
+            h.copy_(p, non_blocking=True)
+        if i > 0:
+            e2e_ev[i - 1][1].record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = float(np.mean([a.elapsed_time(b) for a, b in e2e_ev]))
+    te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item())
+    d2h = sum(p.numel() for p in packed)
+
+    # ---- roofline of the dominant kernel ----
+    pk, uk = float(np.mean(pack_ms)), float(np.mean(unpack_ms))
+    launch_bytes = step_bytes() // 2          # one fused launch moves half the step
+    dom_name, dom_ms = ("unpack_multi (k_chain<false>)", uk) if uk >= pk else \
+        ("pack_multi (k_chain<true>)", pk)
+    achieved = launch_bytes / (dom_ms / 1e3) / 1e9
+    peak, peak_kind = load_peak()
+    traffic = load_traffic()
+
+    # ---- CPU baseline (rank 0, N = 1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        gbs, reps, dtc = run_cpu_oracle(args.cpu_seconds, threads)
+        cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+               "sample": "%d repetitions (%.1f s) of the full step (12 faces pack+unpack) by the C "
+                         "oracle port of datatype.py, faces over %d threads on %s"
+                         % (reps, dtc, threads, cpu_model())}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded PCG64 bytes, 514^3 f32 array)",
+            "config": {"workload": WORKLOAD, "array_bytes": ARRAY_BYTES,
+                       "payload_bytes_per_step": step_bytes(),
+                       "l2": "flushed between steps (256 MiB write outside the timed events)",
+                       "parallelism": "replicas x%d" % world},
+            "pack_ms": round(pk, 4), "unpack_ms": round(uk, 4),
+            "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": round(achieved, 1),
+                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4),
+                         "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                         "algorithmic_bytes_per_launch": launch_bytes},
+            "e2e": {"value": round(world * step_bytes() / (e2e_ms / 1e3) / 1e9, 3), "unit": "GB/s",
+                    "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": ARRAY_BYTES,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": 2 * args.steps,
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="mpx", choices=["mpx", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+    return gpu_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

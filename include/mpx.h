@@ -1,0 +1,127 @@
+/*
+ * mpx.h -- C ABI of libmpx.so, the B200-native datatype / enqueue hot path.
+ *
+ * Plain C: opaque handles, int64 sizes, raw device pointers, cudaStream_t
+ * passed as void*.  Every function returns an MPX_* status code (0 = OK);
+ * mpx_last_error() gives the calling thread's message for the last failure.
+ * Codes map 1:1 onto the reference's error taxonomy
+ * (/root/reference/pkg/src/minimpi/errors.py:9-70).
+ *
+ * Each entry point names the reference interface it replaces.  Reference
+ * paths are relative to /root/reference/pkg/src/minimpi/.
+ */
+#ifndef MPX_H
+#define MPX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (errors.py:9-70) */
+#define MPX_SUCCESS          0
+#define MPX_ERR_ARG          1   /* ArgError        "ERR_ARG"         */
+#define MPX_ERR_STATE        2   /* StateError      "ERR_STATE"       */
+#define MPX_ERR_PENDING      3   /* PendingError    "ERR_PENDING"     */
+#define MPX_ERR_TRUNCATE     4   /* TruncateError   "ERR_TRUNCATE"    */
+#define MPX_ERR_UNSUPPORTED  5   /* UnsupportedError"ERR_UNSUPPORTED" */
+#define MPX_ERR_EXHAUSTED    6   /* ExhaustedError  "ERR_EXHAUSTED"   */
+#define MPX_ERR_TRANSPORT    7   /* TransportError  "ERR_TRANSPORT"   */
+#define MPX_ERR_OTHER        8   /* MinimpiError    "ERR_OTHER" (CUDA failures) */
+
+/* builtin datatypes (datatype.py:410-422; INT8 is new) */
+#define MPX_BYTE     0
+#define MPX_CHAR     1
+#define MPX_INT8     2
+#define MPX_INT32    3
+#define MPX_INT64    4
+#define MPX_FLOAT32  5
+#define MPX_FLOAT64  6
+
+typedef struct mpx_type_s *mpx_datatype;
+
+int mpx_abi_version(void);
+/* thread-local message of the last failing call */
+const char *mpx_last_error(void);
+
+/* ---- datatype constructors (datatype.py:444-610) ------------------------ */
+/* builtins: datatype.py:410-422 */
+int mpx_type_builtin(int which, mpx_datatype *out);
+/* type_contiguous: datatype.py:444-455 */
+int mpx_type_contiguous(int64_t count, mpx_datatype child, mpx_datatype *out);
+/* type_vector: datatype.py:458-475 (stride in child extents) */
+int mpx_type_vector(int64_t count, int64_t blocklength, int64_t stride,
+                    mpx_datatype child, mpx_datatype *out);
+/* type_hvector: datatype.py:478-495 (stride in bytes) */
+int mpx_type_hvector(int64_t count, int64_t blocklength, int64_t stride_bytes,
+                     mpx_datatype child, mpx_datatype *out);
+/* type_indexed_block: datatype.py:498-516 */
+int mpx_type_indexed_block(int64_t blocklength, int64_t n, const int64_t *displs,
+                           mpx_datatype child, mpx_datatype *out);
+/* MPI_Type_indexed (absent from the reference: SURVEY 8a a3; semantics of
+ * type_create_struct with byte displacement displs[i]*extent, one child) */
+int mpx_type_indexed(int64_t n, const int64_t *blocklengths, const int64_t *displs,
+                     mpx_datatype child, mpx_datatype *out);
+/* type_create_struct: datatype.py:519-547 */
+int mpx_type_create_struct(int64_t n, const int64_t *blocklengths,
+                           const int64_t *byte_displs, const mpx_datatype *children,
+                           mpx_datatype *out);
+/* type_create_subarray (C order): datatype.py:550-583 */
+int mpx_type_create_subarray(int ndims, const int64_t *full, const int64_t *sub,
+                             const int64_t *offs, mpx_datatype child, mpx_datatype *out);
+/* type_create_resized: datatype.py:586-591 */
+int mpx_type_create_resized(mpx_datatype child, int64_t lb, int64_t extent,
+                            mpx_datatype *out);
+/* type_commit / type_free: datatype.py:594-610 */
+int mpx_type_commit(mpx_datatype dt);
+int mpx_type_free(mpx_datatype dt);
+
+/* Datatype attributes (datatype.py:345-401):
+ * info[0..7] = size_bytes, lb, ub, extent_bytes, segment_count, node_count,
+ *              committed, freed */
+int mpx_type_get_info(mpx_datatype dt, int64_t info[8]);
+
+/* ---- queries --------------------------------------------------------- */
+/* type_iov_len: datatype.py:618-628 (host, O(depth * log)) */
+int mpx_type_iov_len(mpx_datatype dt, int64_t max_iov_bytes, int64_t *n, int64_t *bytes);
+/* type_iov: datatype.py:631-650, computed on the device.  Writes *n_out
+ * (offset, length) int64 pairs to dev_pairs (device memory, room for
+ * cap_pairs pairs) for segments [iov_offset, iov_offset + max_iov_len) of
+ * the layout replicated count times (count = 1 is the reference call). */
+int mpx_type_iov(mpx_datatype dt, int64_t count, int64_t iov_offset, int64_t max_iov_len,
+                 int64_t *dev_pairs, int64_t cap_pairs, int64_t *n_out, void *stream);
+/* packed_size: datatype.py:731-734 */
+int mpx_packed_size(mpx_datatype dt, int64_t count, int64_t *out);
+/* Host-side lowering summary of layout_for(count) (datatype.py:658-661):
+ * out[0..7] = runs, nbytes, min_off, max_end, node_count,
+ *             plan kind (0 empty, 1 chain, 2 generic), overlap, chain alignment */
+int mpx_layout_query(mpx_datatype dt, int64_t count, int64_t out[8]);
+
+/* ---- data movement (device buffers, asynchronous on `stream`) ----------- */
+/* pack: datatype.py:695-702 with _checked_view bounds (:680-692).
+ * src = device buffer of src_bytes; dst = device buffer of >= packed bytes. */
+int mpx_pack(mpx_datatype dt, int64_t count, const void *src, int64_t src_bytes,
+             void *dst, int64_t dst_bytes, void *stream);
+/* unpack: datatype.py:705-728.  *written = min(src_bytes, packed size) is
+ * known at call time; when src_bytes exceeds the layout the full layout is
+ * written and MPX_ERR_TRUNCATE is returned (after the launch), exactly as the
+ * reference raises TruncateError after filling. */
+int mpx_unpack(mpx_datatype dt, int64_t count, const void *src, int64_t src_bytes,
+               void *dst, int64_t dst_bytes, int64_t *written, void *stream);
+/* Batched forms: n independent pack (unpack) operations fused into as few
+ * launches as possible (one launch for up to 16 strided layouts, e.g. the
+ * six faces of a halo exchange).  B200 extension; no reference equivalent
+ * beyond calling pack/unpack n times. */
+int mpx_pack_multi(int n, const mpx_datatype *dts, const int64_t *counts,
+                   const void *const *srcs, const int64_t *src_bytes,
+                   void *const *dsts, const int64_t *dst_bytes, void *stream);
+int mpx_unpack_multi(int n, const mpx_datatype *dts, const int64_t *counts,
+                     const void *const *srcs, const int64_t *src_bytes,
+                     void *const *dsts, const int64_t *dst_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MPX_H */

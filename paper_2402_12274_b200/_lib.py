@@ -1,0 +1,84 @@
+"""ctypes binding of libmpx.so (the C ABI declared in include/mpx.h).
+
+The product has no CPU fallback: if libmpx.so is missing or fails to load,
+importing the package raises immediately.  Build it with
+``python -m paper_2402_12274_b200.build``.
+"""
+
+import ctypes
+import os
+
+from .errors import error_for_code
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_HERE, "libmpx.so")
+
+if not os.path.exists(SO_PATH):
+    raise ImportError(
+        "libmpx.so not found at %s -- build it with "
+        "`python -m paper_2402_12274_b200.build` (no CPU fallback exists)" % SO_PATH)
+
+# torch first: it loads the CUDA runtime / NCCL this library talks to
+import torch  # noqa: E402,F401
+
+lib = ctypes.CDLL(SO_PATH, mode=ctypes.RTLD_GLOBAL)
+
+i64 = ctypes.c_int64
+p64 = ctypes.POINTER(ctypes.c_int64)
+vp = ctypes.c_void_p
+pvp = ctypes.POINTER(ctypes.c_void_p)
+cint = ctypes.c_int
+dt_t = ctypes.c_void_p
+pdt = ctypes.POINTER(ctypes.c_void_p)
+
+_SIGS = {
+    "mpx_abi_version": ([], cint),
+    "mpx_last_error": ([], ctypes.c_char_p),
+    "mpx_type_builtin": ([cint, pdt], cint),
+    "mpx_type_contiguous": ([i64, dt_t, pdt], cint),
+    "mpx_type_vector": ([i64, i64, i64, dt_t, pdt], cint),
+    "mpx_type_hvector": ([i64, i64, i64, dt_t, pdt], cint),
+    "mpx_type_indexed_block": ([i64, i64, p64, dt_t, pdt], cint),
+    "mpx_type_indexed": ([i64, p64, p64, dt_t, pdt], cint),
+    "mpx_type_create_struct": ([i64, p64, p64, pdt, pdt], cint),
+    "mpx_type_create_subarray": ([cint, p64, p64, p64, dt_t, pdt], cint),
+    "mpx_type_create_resized": ([dt_t, i64, i64, pdt], cint),
+    "mpx_type_commit": ([dt_t], cint),
+    "mpx_type_free": ([dt_t], cint),
+    "mpx_type_get_info": ([dt_t, p64], cint),
+    "mpx_type_iov_len": ([dt_t, i64, p64, p64], cint),
+    "mpx_type_iov": ([dt_t, i64, i64, i64, vp, i64, p64, vp], cint),
+    "mpx_packed_size": ([dt_t, i64, p64], cint),
+    "mpx_layout_query": ([dt_t, i64, p64], cint),
+    "mpx_pack": ([dt_t, i64, vp, i64, vp, i64, vp], cint),
+    "mpx_unpack": ([dt_t, i64, vp, i64, vp, i64, p64, vp], cint),
+    "mpx_pack_multi": ([cint, pdt, p64, pvp, p64, pvp, p64, vp], cint),
+    "mpx_unpack_multi": ([cint, pdt, p64, pvp, p64, pvp, p64, vp], cint),
+}
+
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+
+def last_error():
+    m = lib.mpx_last_error()
+    return m.decode(errors="replace") if m else ""
+
+
+def check(rc):
+    """Raise the MinimpiError subclass matching a nonzero MPX_* code."""
+    if rc:
+        raise error_for_code(rc, last_error())
+    return rc
+
+
+def exported_symbols():
+    """Names of every function this binding declares (test helper)."""
+    return sorted(_SIGS)
+
+
+def i64_array(values):
+    vals = list(values)
+    return (ctypes.c_int64 * max(1, len(vals)))(*vals)

@@ -1,0 +1,33 @@
+// capi_common.hpp -- helpers shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+
+#include "mpx.h"
+#include "plan.hpp"
+#include "typerep.hpp"
+
+namespace mpx {
+
+extern thread_local std::string g_last_error;
+
+// record a message for mpx_last_error() and return code
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int cuda_fail(cudaError_t e, const char* what);
+
+// handle -> live Datatype (nullptr when the handle is unknown)
+Datatype* lookup(mpx_datatype h);
+
+// validate a typed buffer and fetch its plan on the buffer's device
+int prepare(Datatype* d, int64_t count, const void* layout_buf, int64_t layout_bytes, bool writable,
+            cudaStream_t stream, std::shared_ptr<Plan>* plan, int* device);
+
+// n fused pack (or unpack) operations on one stream
+int movement(int n, const mpx_datatype* dts, const int64_t* counts, const void* const* srcs,
+             const int64_t* src_bytes, void* const* dsts, const int64_t* dst_bytes, bool pack,
+             cudaStream_t stream, int64_t* written_out);
+
+}  // namespace mpx

@@ -1,0 +1,542 @@
+// capi_types.cpp -- extern "C" datatype / pack / unpack / iov entry points.
+//
+// Argument validation mirrors the reference (datatype.py:403-436, 618-692)
+// and happens on the host at call time; the data movement itself is enqueued
+// asynchronously on the caller's stream.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <mutex>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "capi_common.hpp"
+#include "kernels.hpp"
+#include "mpx.h"
+#include "plan.hpp"
+#include "typerep.hpp"
+
+using namespace mpx;
+
+namespace mpx {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(MPX_ERR_OTHER, "%s: %s", what, cudaGetErrorString(e));
+}
+
+namespace {
+std::mutex g_reg_mu;
+std::unordered_set<const void*> g_registry;
+
+Datatype* make_builtin(int64_t size, const char* name) {
+    auto* d = new Datatype();
+    d->layout = tree::run(0, size);
+    d->size = size;
+    d->lb = 0;
+    d->ub = size;
+    d->committed = true;
+    d->builtin = true;
+    d->desc = name;
+    std::lock_guard<std::mutex> g(g_reg_mu);
+    g_registry.insert(d);
+    return d;
+}
+
+Datatype* builtin(int which) {
+    static Datatype* table[7] = {
+        make_builtin(1, "byte"),   make_builtin(1, "char"),    make_builtin(1, "int8"),
+        make_builtin(4, "int32"),  make_builtin(8, "int64"),   make_builtin(4, "float32"),
+        make_builtin(8, "float64")};
+    if (which < 0 || which > 6) return nullptr;
+    return table[which];
+}
+
+mpx_datatype publish(Datatype* d) {
+    std::lock_guard<std::mutex> g(g_reg_mu);
+    g_registry.insert(d);
+    return reinterpret_cast<mpx_datatype>(d);
+}
+}  // namespace
+
+Datatype* lookup(mpx_datatype h) {
+    std::lock_guard<std::mutex> g(g_reg_mu);
+    auto* d = reinterpret_cast<Datatype*>(h);
+    return g_registry.count(d) ? d : nullptr;
+}
+
+namespace {
+// _check_child: datatype.py:425-431
+int check_child(mpx_datatype h, Datatype** out) {
+    Datatype* d = lookup(h);
+    if (!d) return fail(MPX_ERR_ARG, "child must be a Datatype");
+    if (d->freed) return fail(MPX_ERR_ARG, "child datatype was freed");
+    if (!d->committed) return fail(MPX_ERR_ARG, "child datatype must be committed (or basic)");
+    *out = d;
+    return MPX_SUCCESS;
+}
+
+int check_count(int64_t n, const char* what) {  // datatype.py:434-436
+    if (n < 0) return fail(MPX_ERR_ARG, "%s must be an integer >= 0", what);
+    return MPX_SUCCESS;
+}
+
+// _check_usable: datatype.py:403-407
+int check_usable(Datatype* d, const char* what) {
+    if (!d) return fail(MPX_ERR_ARG, "not a datatype handle");
+    if (d->freed) return fail(MPX_ERR_ARG, "datatype %s after free", what);
+    if (!d->committed) return fail(MPX_ERR_ARG, "datatype %s before commit", what);
+    return MPX_SUCCESS;
+}
+
+Datatype* new_type(NodeP lay, int64_t size, int64_t lb, int64_t ub, std::string desc) {
+    auto* d = new Datatype();
+    d->layout = std::move(lay);
+    d->size = size;
+    d->lb = lb;
+    d->ub = ub;
+    d->desc = std::move(desc);
+    return d;
+}
+
+// device owning a pointer (must be device memory)
+int device_of(const void* p, int* dev) {
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(MPX_ERR_ARG, "cannot resolve buffer %p: %s", p, cudaGetErrorString(e));
+    }
+    if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)
+        return fail(MPX_ERR_ARG, "buffer %p is not device memory", p);
+    *dev = a.device;
+    return MPX_SUCCESS;
+}
+
+int ensure_device(int dev) {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != dev) {
+        cudaError_t e = cudaSetDevice(dev);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    }
+    return MPX_SUCCESS;
+}
+}  // namespace
+
+// Validate + lower one pack/unpack operation.  layout_buf is the typed side.
+int prepare(Datatype* d, int64_t count, const void* layout_buf, int64_t layout_bytes, bool writable,
+            cudaStream_t stream, std::shared_ptr<Plan>* plan, int* device) {
+    int rc = check_count(count, "count");
+    if (rc) return rc;
+    rc = check_usable(d, "pack/unpack");
+    if (rc) return rc;
+    (void)writable;
+    NodeP lay = d->layout_for(count);
+    if (lay->runs) {  // _checked_view bounds, datatype.py:685-691
+        if (lay->min_off < 0) return fail(MPX_ERR_ARG, "layout reaches before the start of the buffer");
+        if (lay->max_end > layout_bytes)
+            return fail(MPX_ERR_ARG, "buffer too small: layout spans %lld bytes, buffer has %lld",
+                        (long long)lay->max_end, (long long)layout_bytes);
+    }
+    if (lay->runs == 0) {
+        *plan = nullptr;
+        return MPX_SUCCESS;
+    }
+    int dev = 0;
+    rc = device_of(layout_buf, &dev);
+    if (rc) return rc;
+    rc = ensure_device(dev);
+    if (rc) return rc;
+    std::string err;
+    *plan = get_plan(d, count, dev, stream, &err);
+    if (!*plan) return fail(MPX_ERR_OTHER, "%s", err.c_str());
+    *device = dev;
+    return MPX_SUCCESS;
+}
+
+}  // namespace mpx
+
+extern "C" {
+
+int mpx_abi_version(void) { return 1; }
+
+const char* mpx_last_error(void) { return g_last_error.c_str(); }
+
+int mpx_type_builtin(int which, mpx_datatype* out) {
+    Datatype* d = builtin(which);
+    if (!d || !out) return fail(MPX_ERR_ARG, "unknown builtin %d", which);
+    *out = reinterpret_cast<mpx_datatype>(d);
+    return MPX_SUCCESS;
+}
+
+int mpx_type_contiguous(int64_t count, mpx_datatype child, mpx_datatype* out) {
+    Datatype* c = nullptr;
+    int rc = check_count(count, "count");
+    if (rc || (rc = check_child(child, &c))) return rc;
+    const int64_t ext = c->extent();
+    NodeP lay = tree::replicate(c->layout, count, ext);
+    int64_t lb = 0, ub = 0;
+    if (count) { lb = c->lb; ub = (count - 1) * ext + c->ub; }
+    *out = publish(new_type(lay, count * c->size, lb, ub,
+                            "contiguous(" + std::to_string(count) + ", " + c->desc + ")"));
+    return MPX_SUCCESS;
+}
+
+static int vector_like(int64_t count, int64_t bl, int64_t step, mpx_datatype child, mpx_datatype* out,
+                       const std::string& what) {
+    Datatype* c = nullptr;
+    int rc = check_count(count, "count");
+    if (rc || (rc = check_count(bl, "blocklength")) || (rc = check_child(child, &c))) return rc;
+    const int64_t ext = c->extent();
+    NodeP block = tree::replicate(c->layout, bl, ext);
+    NodeP lay = tree::replicate(block, count, step);
+    int64_t lb = 0, ub = 0;
+    if (count && bl) {
+        const int64_t span = (count - 1) * step;
+        lb = std::min<int64_t>(0, span) + c->lb;
+        ub = std::max<int64_t>(0, span) + (bl - 1) * ext + c->ub;
+    }
+    *out = publish(new_type(lay, count * bl * c->size, lb, ub, what + ", " + c->desc + ")"));
+    return MPX_SUCCESS;
+}
+
+int mpx_type_vector(int64_t count, int64_t bl, int64_t stride, mpx_datatype child, mpx_datatype* out) {
+    Datatype* c = lookup(child);
+    const int64_t ext = c ? c->extent() : 0;
+    return vector_like(count, bl, stride * ext, child, out,
+                       "vector(" + std::to_string(count) + ", " + std::to_string(bl) + ", " +
+                           std::to_string(stride));
+}
+
+int mpx_type_hvector(int64_t count, int64_t bl, int64_t stride_bytes, mpx_datatype child,
+                     mpx_datatype* out) {
+    return vector_like(count, bl, stride_bytes, child, out,
+                       "hvector(" + std::to_string(count) + ", " + std::to_string(bl) + ", " +
+                           std::to_string(stride_bytes) + "b");
+}
+
+int mpx_type_indexed_block(int64_t bl, int64_t n, const int64_t* displs, mpx_datatype child,
+                           mpx_datatype* out) {
+    Datatype* c = nullptr;
+    int rc = check_count(bl, "blocklength");
+    if (rc || (rc = check_child(child, &c))) return rc;
+    if (n < 0 || (n && !displs)) return fail(MPX_ERR_ARG, "displacements must be integers");
+    const int64_t ext = c->extent();
+    NodeP block = tree::replicate(c->layout, bl, ext);
+    std::vector<NodeP> parts;
+    parts.reserve(n);
+    int64_t dmin = 0, dmax = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        parts.push_back(tree::shifted(block, displs[i] * ext));
+        dmin = i ? std::min(dmin, displs[i]) : displs[i];
+        dmax = i ? std::max(dmax, displs[i]) : displs[i];
+    }
+    int64_t lb = 0, ub = 0;
+    if (n && bl) { lb = dmin * ext + c->lb; ub = (dmax + bl - 1) * ext + c->ub; }
+    *out = publish(new_type(tree::concat(parts), n * bl * c->size, lb, ub,
+                            "indexed_block(" + std::to_string(bl) + ", n=" + std::to_string(n) + ", " +
+                                c->desc + ")"));
+    return MPX_SUCCESS;
+}
+
+static int struct_like(int64_t n, const int64_t* bls, const int64_t* displs, Datatype* const* kids,
+                       bool scale_by_extent, mpx_datatype* out, const std::string& desc) {
+    std::vector<NodeP> parts;
+    parts.reserve(n);
+    int64_t size = 0, lb = 0, ub = 0;
+    bool have = false;
+    for (int64_t i = 0; i < n; ++i) {
+        int rc = check_count(bls[i], "blocklength");
+        if (rc) return rc;
+        Datatype* c = kids[i];
+        const int64_t ext = c->extent();
+        const int64_t d = scale_by_extent ? displs[i] * ext : displs[i];
+        parts.push_back(tree::shifted(tree::replicate(c->layout, bls[i], ext), d));
+        size += bls[i] * c->size;
+        if (bls[i] > 0) {
+            const int64_t b_lb = d + c->lb, b_ub = d + (bls[i] - 1) * ext + c->ub;
+            lb = have ? std::min(lb, b_lb) : b_lb;
+            ub = have ? std::max(ub, b_ub) : b_ub;
+            have = true;
+        }
+    }
+    *out = publish(new_type(tree::concat(parts), size, lb, ub, desc));
+    return MPX_SUCCESS;
+}
+
+int mpx_type_indexed(int64_t n, const int64_t* bls, const int64_t* displs, mpx_datatype child,
+                     mpx_datatype* out) {
+    Datatype* c = nullptr;
+    int rc = check_child(child, &c);
+    if (rc) return rc;
+    if (n < 0 || (n && (!bls || !displs))) return fail(MPX_ERR_ARG, "indexed arrays must have equal length");
+    std::vector<Datatype*> kids(n, c);
+    return struct_like(n, bls, displs, kids.data(), true, out,
+                       "indexed(n=" + std::to_string(n) + ", " + c->desc + ")");
+}
+
+int mpx_type_create_struct(int64_t n, const int64_t* bls, const int64_t* displs,
+                           const mpx_datatype* children, mpx_datatype* out) {
+    if (n < 0 || (n && (!bls || !displs || !children)))
+        return fail(MPX_ERR_ARG, "struct arrays must have equal length");
+    std::vector<Datatype*> kids(n);
+    std::string desc = "struct(";
+    for (int64_t i = 0; i < n; ++i) {
+        int rc = check_child(children[i], &kids[i]);
+        if (rc) return rc;
+        desc += (i ? ", " : "") + std::to_string(bls[i]) + "x" + kids[i]->desc + "@" + std::to_string(displs[i]);
+    }
+    return struct_like(n, bls, displs, kids.data(), false, out, desc + ")");
+}
+
+int mpx_type_create_subarray(int nd, const int64_t* full, const int64_t* sub, const int64_t* offs,
+                             mpx_datatype child, mpx_datatype* out) {
+    if (nd < 1 || !full || !sub || !offs)
+        return fail(MPX_ERR_ARG, "subarray dimension arrays must match and be non-empty");
+    for (int i = 0; i < nd; ++i) {
+        int rc;
+        if ((rc = check_count(full[i], "full size")) || (rc = check_count(sub[i], "sub size")) ||
+            (rc = check_count(offs[i], "offset")))
+            return rc;
+        if (sub[i] > full[i] || offs[i] > full[i] - sub[i])
+            return fail(MPX_ERR_ARG, "subarray block must fit inside the full array");
+    }
+    Datatype* c = nullptr;
+    int rc = check_child(child, &c);
+    if (rc) return rc;
+    const int64_t ext = c->extent();
+    std::vector<int64_t> st(nd);
+    st[nd - 1] = ext;
+    for (int k = nd - 2; k >= 0; --k) st[k] = st[k + 1] * full[k + 1];
+    NodeP core = tree::replicate(c->layout, sub[nd - 1], ext);
+    for (int k = nd - 2; k >= 0; --k) core = tree::replicate(core, sub[k], st[k]);
+    int64_t base = 0, size = c->size, vol = 1;
+    for (int k = 0; k < nd; ++k) {
+        base += offs[k] * st[k];
+        size *= sub[k];
+        vol *= full[k];
+    }
+    *out = publish(new_type(tree::shifted(core, base), size, 0, vol * ext,
+                            "subarray(nd=" + std::to_string(nd) + ", " + c->desc + ")"));
+    return MPX_SUCCESS;
+}
+
+int mpx_type_create_resized(mpx_datatype child, int64_t lb, int64_t extent, mpx_datatype* out) {
+    Datatype* c = nullptr;
+    int rc = check_child(child, &c);
+    if (rc) return rc;
+    if (extent < 0) return fail(MPX_ERR_ARG, "resized needs integer lb and extent >= 0");
+    *out = publish(new_type(c->layout, c->size, lb, lb + extent,
+                            "resized(" + c->desc + ", lb=" + std::to_string(lb) + ", extent=" +
+                                std::to_string(extent) + ")"));
+    return MPX_SUCCESS;
+}
+
+int mpx_type_commit(mpx_datatype h) {  // datatype.py:594-600
+    Datatype* d = lookup(h);
+    if (!d) return fail(MPX_ERR_ARG, "type_commit expects a Datatype");
+    if (d->freed) return fail(MPX_ERR_ARG, "cannot commit a freed datatype");
+    d->committed = true;
+    return MPX_SUCCESS;
+}
+
+int mpx_type_free(mpx_datatype h) {  // datatype.py:603-610
+    Datatype* d = lookup(h);
+    if (!d) return fail(MPX_ERR_ARG, "type_free expects a Datatype");
+    if (d->builtin) return fail(MPX_ERR_ARG, "builtin datatypes cannot be freed");
+    if (d->freed) return fail(MPX_ERR_ARG, "datatype already freed");
+    d->freed = true;
+    std::lock_guard<std::mutex> g(d->mu);
+    d->plans.clear();       // releases device descriptors
+    d->replicated.clear();
+    return MPX_SUCCESS;
+}
+
+int mpx_type_get_info(mpx_datatype h, int64_t info[8]) {
+    Datatype* d = lookup(h);
+    if (!d) return fail(MPX_ERR_ARG, "not a datatype handle");
+    info[0] = d->size;
+    info[1] = d->lb;
+    info[2] = d->ub;
+    info[3] = d->extent();
+    info[4] = d->layout->runs;
+    info[5] = d->layout->node_count;
+    info[6] = d->committed;
+    info[7] = d->freed;
+    return MPX_SUCCESS;
+}
+
+int mpx_type_iov_len(mpx_datatype h, int64_t max_bytes, int64_t* n, int64_t* bytes) {
+    Datatype* d = lookup(h);
+    int rc = check_usable(d, "query");
+    if (rc) return rc;
+    if (max_bytes < -1) return fail(MPX_ERR_ARG, "max_iov_bytes must be an integer >= -1");
+    if (max_bytes == -1 || max_bytes >= d->size) {
+        *n = d->layout->runs;
+        *bytes = d->size;
+        return MPX_SUCCESS;
+    }
+    tree::prefix_within(d->layout.get(), max_bytes, n, bytes);
+    return MPX_SUCCESS;
+}
+
+int mpx_packed_size(mpx_datatype h, int64_t count, int64_t* out) {
+    Datatype* d = lookup(h);
+    int rc = check_count(count, "count");
+    if (rc || (rc = check_usable(d, "size query"))) return rc;
+    *out = d->size * count;
+    return MPX_SUCCESS;
+}
+
+int mpx_layout_query(mpx_datatype h, int64_t count, int64_t out[8]) {
+    Datatype* d = lookup(h);
+    int rc = check_count(count, "count");
+    if (rc || (rc = check_usable(d, "query"))) return rc;
+    NodeP lay = d->layout_for(count);
+    Plan p;
+    analyze(lay.get(), &p);
+    out[0] = p.runs;
+    out[1] = p.nbytes;
+    out[2] = p.min_off;
+    out[3] = p.max_end;
+    out[4] = p.node_count;
+    out[5] = p.kind;
+    out[6] = p.overlap;
+    out[7] = p.chain_align;
+    return MPX_SUCCESS;
+}
+
+int mpx_type_iov(mpx_datatype h, int64_t count, int64_t iov_offset, int64_t max_iov_len, int64_t* dev_pairs,
+                 int64_t cap_pairs, int64_t* n_out, void* stream) {
+    Datatype* d = lookup(h);
+    int rc = check_count(count, "count");
+    if (rc || (rc = check_usable(d, "query"))) return rc;
+    NodeP lay = d->layout_for(count);
+    const int64_t total = lay->runs;
+    if (iov_offset < 0 || iov_offset > total)  // datatype.py:639-640
+        return fail(MPX_ERR_ARG, "iov_offset out of range [0, %lld]", (long long)total);
+    if (max_iov_len < -1) return fail(MPX_ERR_ARG, "max_iov_len must be an integer >= -1");
+    int64_t n = total - iov_offset;
+    if (max_iov_len != -1) n = std::min(n, max_iov_len);
+    if (n <= 0) {
+        *n_out = 0;
+        return MPX_SUCCESS;
+    }
+    if (n > cap_pairs) return fail(MPX_ERR_ARG, "iov output holds %lld pairs, need %lld",
+                                   (long long)cap_pairs, (long long)n);
+    int dev = 0;
+    if ((rc = device_of(dev_pairs, &dev)) || (rc = ensure_device(dev))) return rc;
+    std::string err;
+    auto plan = get_plan(d, count, dev, (cudaStream_t)stream, &err);
+    if (!plan) return fail(MPX_ERR_OTHER, "%s", err.c_str());
+    cudaError_t e = launch_iov(*plan, iov_offset, n, dev_pairs, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "iov launch");
+    *n_out = n;
+    return MPX_SUCCESS;
+}
+
+}  // extern "C"
+
+namespace mpx {
+
+// one pack or unpack, possibly fused with others of the same direction
+int movement(int n, const mpx_datatype* dts, const int64_t* counts, const void* const* srcs,
+             const int64_t* src_bytes, void* const* dsts, const int64_t* dst_bytes, bool pack,
+             cudaStream_t stream, int64_t* written_out) {
+    ChainBatch batch;
+    batch.njobs = 0;
+    int batch_dev = -1;
+    bool truncated = false;
+    for (int i = 0; i < n; ++i) {
+        Datatype* d = lookup(dts[i]);
+        std::shared_ptr<Plan> plan;
+        int dev = 0;
+        const void* layout_buf = pack ? srcs[i] : dsts[i];
+        const int64_t layout_bytes = pack ? src_bytes[i] : dst_bytes[i];
+        int rc = prepare(d, counts[i], layout_buf, layout_bytes, !pack, stream, &plan, &dev);
+        if (rc) return rc;
+        const int64_t nbytes = d->size * counts[i];
+        int64_t limit = nbytes;
+        if (pack) {
+            if (dst_bytes[i] < nbytes)
+                return fail(MPX_ERR_ARG, "pack output holds %lld bytes, need %lld", (long long)dst_bytes[i],
+                            (long long)nbytes);
+        } else {
+            limit = std::min(src_bytes[i], nbytes);
+            if (src_bytes[i] > nbytes) truncated = true;
+        }
+        if (written_out) written_out[i] = limit;
+        if (!plan || limit == 0) continue;
+        const uint8_t* s = static_cast<const uint8_t*>(srcs[i]);
+        uint8_t* t = static_cast<uint8_t*>(dsts[i]);
+        if (plan->kind == PLAN_CHAIN && !(!pack && plan->overlap)) {
+            if (batch.njobs == kMaxJobs || (batch_dev >= 0 && batch_dev != dev)) {
+                cudaError_t e = launch_chain_batch(batch, pack, batch_dev, stream);
+                if (e != cudaSuccess) return cuda_fail(e, "chain launch");
+                batch.njobs = 0;
+            }
+            ChainJob& j = batch.job[batch.njobs++];
+            j.c = plan->chain;
+            j.src = s;
+            j.dst = t;
+            j.w = chain_word(*plan, s, t);
+            j.nwords = limit / j.w;
+            j.limit = limit;
+            batch_dev = dev;
+        } else {
+            cudaError_t e = launch_generic(*plan, pack, s, t, limit, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "generic launch");
+        }
+    }
+    if (batch.njobs) {
+        cudaError_t e = launch_chain_batch(batch, pack, batch_dev, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "chain launch");
+    }
+    if (truncated) return fail(MPX_ERR_TRUNCATE, "incoming data larger than the layout");
+    return MPX_SUCCESS;
+}
+
+}  // namespace mpx
+
+extern "C" {
+
+int mpx_pack(mpx_datatype dt, int64_t count, const void* src, int64_t src_bytes, void* dst, int64_t dst_bytes,
+             void* stream) {
+    return movement(1, &dt, &count, &src, &src_bytes, &dst, &dst_bytes, true, (cudaStream_t)stream, nullptr);
+}
+
+int mpx_unpack(mpx_datatype dt, int64_t count, const void* src, int64_t src_bytes, void* dst, int64_t dst_bytes,
+               int64_t* written, void* stream) {
+    int64_t w = 0;
+    int rc = movement(1, &dt, &count, &src, &src_bytes, &dst, &dst_bytes, false, (cudaStream_t)stream, &w);
+    if (written) *written = w;
+    return rc;
+}
+
+int mpx_pack_multi(int n, const mpx_datatype* dts, const int64_t* counts, const void* const* srcs,
+                   const int64_t* src_bytes, void* const* dsts, const int64_t* dst_bytes, void* stream) {
+    if (n < 0) return fail(MPX_ERR_ARG, "n must be >= 0");
+    return movement(n, dts, counts, srcs, src_bytes, dsts, dst_bytes, true, (cudaStream_t)stream, nullptr);
+}
+
+int mpx_unpack_multi(int n, const mpx_datatype* dts, const int64_t* counts, const void* const* srcs,
+                     const int64_t* src_bytes, void* const* dsts, const int64_t* dst_bytes, void* stream) {
+    if (n < 0) return fail(MPX_ERR_ARG, "n must be >= 0");
+    return movement(n, dts, counts, srcs, src_bytes, dsts, dst_bytes, false, (cudaStream_t)stream, nullptr);
+}
+
+}  // extern "C"

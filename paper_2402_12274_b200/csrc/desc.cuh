@@ -1,0 +1,163 @@
+// desc.cuh -- GPU-resident layout descriptors and their device-side walkers.
+//
+// Two lowered forms of a layout tree (typerep.hpp):
+//
+//  * Chain: the tree is Rep^k(Run), k <= 4 (vector / hvector / subarray faces
+//    / contiguous).  Packed byte P maps to layout offset in closed form:
+//      row = P / L, col = P % L, row -> (idx_0..idx_{k-1}) mixed radix,
+//      off = base + col + sum idx_i * stride_i.
+//    All divisions are by launch constants and use precomputed 64-bit
+//    multiply-high magic numbers (Granlund-Montgomery, N = 63).
+//
+//  * DDesc: the whole DAG flattened into a node array (96 B per node), a
+//    child-index table and per-Seq run/byte prefix tables.  Device code
+//    descends it exactly like the reference's emit_from / prefix_within
+//    (datatype.py:145-153, 155-163, 202-215): divide at Rep nodes, binary
+//    search at Seq nodes.
+#pragma once
+
+#include <cstdint>
+
+namespace mpx {
+
+constexpr int kMaxChain = 4;
+
+struct Chain {
+    int64_t base;           // total displacement of the innermost run
+    int64_t L;              // run length in bytes
+    int32_t depth;          // number of Rep levels (0 = a single run)
+    int32_t pad0;
+    int64_t cnt[kMaxChain]; // outermost first
+    int64_t str[kMaxChain];
+    uint64_t m_cnt[kMaxChain];
+    int32_t s_cnt[kMaxChain];
+    uint64_t m_L;
+    int32_t s_L;
+    int32_t pad1;
+};
+
+struct DNode {
+    int32_t kind;           // 0 empty, 1 run, 2 rep, 3 seq
+    int32_t nkids;          // seq
+    int32_t child;          // rep: body node index; seq: first index in kid table
+    int32_t pref;           // seq: first index in the prefix tables
+    int64_t a, b, c;        // run: off, len ; rep: count, stride, base
+    int64_t runs, nbytes;
+    int64_t body_runs, body_nbytes;
+    uint64_t m_runs, m_bytes;
+    int32_t s_runs, s_bytes;
+};
+static_assert(sizeof(DNode) == 96, "DNode layout");
+
+struct DDesc {
+    const DNode* nodes;
+    const int32_t* kids;
+    const int64_t* rp;
+    const int64_t* bp;
+    int32_t root;
+    int32_t pad;
+    int64_t runs;
+    int64_t nbytes;
+};
+
+// magic for q = floor(n / d), 0 <= n < 2^63: m = ceil(2^(63+l)/d), l = ceil(log2 d)
+inline void host_magic(uint64_t d, uint64_t* m, int32_t* s) {
+    if (d <= 1) { *m = 0; *s = 0; return; }
+    const int l = 64 - __builtin_clzll(d - 1);
+    const unsigned __int128 num = (unsigned __int128)1 << (63 + l);
+    *m = (uint64_t)((num + d - 1) / d);
+    *s = l - 1;
+}
+
+#ifdef __CUDACC__
+__device__ __forceinline__ uint64_t fdiv(uint64_t n, uint64_t m, int32_t s) {
+    return m ? (__umul64hi(n, m) >> s) : n;
+}
+
+struct RunLoc {
+    int64_t k;      // run index
+    int64_t src;    // layout offset of the run start
+    int64_t len;    // run length
+    int64_t poff;   // packed offset of the run start
+};
+
+// largest i in [0, n) with a[i] <= key (a[0] == 0 <= key)
+__device__ __forceinline__ int prefix_search(const int64_t* __restrict__ a, int n, int64_t key) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(a + mid) <= key) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// run k -> (layout offset, length, packed offset); emit_from seek, datatype.py:145-153,202-206
+__device__ __forceinline__ RunLoc locate_run(const DDesc& d, int64_t k) {
+    int32_t ni = d.root;
+    int64_t shift = 0, poff = 0, kk = k;
+    for (;;) {
+        const DNode* nd = d.nodes + ni;
+        const int kind = __ldg(&nd->kind);
+        if (kind == 1) return RunLoc{k, shift + __ldg(&nd->a), __ldg(&nd->b), poff};
+        if (kind == 2) {
+            const uint64_t q = fdiv((uint64_t)kk, __ldg(&nd->m_runs), __ldg(&nd->s_runs));
+            kk -= (int64_t)q * __ldg(&nd->body_runs);
+            shift += __ldg(&nd->c) + (int64_t)q * __ldg(&nd->b);
+            poff += (int64_t)q * __ldg(&nd->body_nbytes);
+            ni = __ldg(&nd->child);
+        } else {
+            const int pref = __ldg(&nd->pref);
+            const int i = prefix_search(d.rp + pref, __ldg(&nd->nkids), kk);
+            kk -= __ldg(d.rp + pref + i);
+            poff += __ldg(d.bp + pref + i);
+            ni = __ldg(d.kids + __ldg(&nd->child) + i);
+        }
+    }
+}
+
+// packed byte p (< nbytes) -> the run containing it; prefix_within-style descent
+__device__ __forceinline__ RunLoc locate_byte(const DDesc& d, int64_t p) {
+    int32_t ni = d.root;
+    int64_t shift = 0, poff = 0, k = 0, pp = p;
+    for (;;) {
+        const DNode* nd = d.nodes + ni;
+        const int kind = __ldg(&nd->kind);
+        if (kind == 1) return RunLoc{k, shift + __ldg(&nd->a), __ldg(&nd->b), poff};
+        if (kind == 2) {
+            const uint64_t q = fdiv((uint64_t)pp, __ldg(&nd->m_bytes), __ldg(&nd->s_bytes));
+            const int64_t bn = __ldg(&nd->body_nbytes);
+            pp -= (int64_t)q * bn;
+            k += (int64_t)q * __ldg(&nd->body_runs);
+            shift += __ldg(&nd->c) + (int64_t)q * __ldg(&nd->b);
+            poff += (int64_t)q * bn;
+            ni = __ldg(&nd->child);
+        } else {
+            const int pref = __ldg(&nd->pref);
+            const int i = prefix_search(d.bp + pref, __ldg(&nd->nkids), pp);
+            pp -= __ldg(d.bp + pref + i);
+            k += __ldg(d.rp + pref + i);
+            poff += __ldg(d.bp + pref + i);
+            ni = __ldg(d.kids + __ldg(&nd->child) + i);
+        }
+    }
+}
+
+// closed-form layout offset of packed byte P for a chain
+__device__ __forceinline__ int64_t chain_off(const Chain& c, int64_t P) {
+    const uint64_t row = fdiv((uint64_t)P, c.m_L, c.s_L);
+    int64_t off = c.base + (P - (int64_t)row * c.L);
+    if (c.depth == 0) return off;
+    uint64_t r = row;
+#pragma unroll
+    for (int i = kMaxChain - 1; i >= 1; --i) {
+        if (i < c.depth) {
+            const uint64_t q = fdiv(r, c.m_cnt[i], c.s_cnt[i]);
+            off += (int64_t)(r - q * (uint64_t)c.cnt[i]) * c.str[i];
+            r = q;
+        }
+    }
+    return off + (int64_t)r * c.str[0];
+}
+#endif
+
+}  // namespace mpx

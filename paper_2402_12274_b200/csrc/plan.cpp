@@ -1,0 +1,208 @@
+// plan.cpp -- tree -> {chain | device descriptor} lowering and overlap analysis.
+#include "plan.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <unordered_map>
+
+namespace mpx {
+
+Plan::~Plan() {
+    if (blob) {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (device >= 0 && cur != device) cudaSetDevice(device);
+        cudaFree(blob);
+        if (device >= 0 && cur != device && cur >= 0) cudaSetDevice(cur);
+    }
+}
+
+namespace {
+
+int64_t pow2_div(int64_t v) {  // largest power of two (<=16) dividing v
+    v = v < 0 ? -v : v;
+    if (v == 0) return 16;
+    int64_t a = 1;
+    while (a < 16 && (v % (a * 2)) == 0) a *= 2;
+    return a;
+}
+
+// Conservative structural test: can two runs of this subtree touch the same byte?
+bool may_overlap(const Node* n) {
+    switch (n->kind) {
+    case Kind::Empty:
+    case Kind::Run: return false;
+    case Kind::Rep: {
+        const int64_t span = n->body->max_end - n->body->min_off;
+        const int64_t st = n->stride < 0 ? -n->stride : n->stride;
+        return st < span || may_overlap(n->body.get());
+    }
+    case Kind::Seq: {
+        std::vector<std::pair<int64_t, int64_t>> iv;
+        iv.reserve(n->kids.size());
+        for (const auto& c : n->kids) {
+            if (may_overlap(c.get())) return true;
+            iv.emplace_back(c->min_off, c->max_end);
+        }
+        std::sort(iv.begin(), iv.end());
+        for (size_t i = 1; i < iv.size(); ++i)
+            if (iv[i].first < iv[i - 1].second) return true;
+        return false;
+    }
+    }
+    return true;
+}
+
+// Exact test on small layouts: sort the iov and look for intersecting runs.
+bool exact_overlap(const Node* n) {
+    std::vector<int64_t> flat;
+    tree::enumerate(n, 0, flat, n->runs);
+    const size_t r = flat.size() / 2;
+    std::vector<std::pair<int64_t, int64_t>> iv(r);
+    for (size_t i = 0; i < r; ++i) iv[i] = {flat[2 * i], flat[2 * i] + flat[2 * i + 1]};
+    std::sort(iv.begin(), iv.end());
+    for (size_t i = 1; i < r; ++i)
+        if (iv[i].first < iv[i - 1].second) return true;
+    return false;
+}
+
+struct Flattener {
+    std::vector<DNode> nodes;
+    std::vector<int32_t> kids;
+    std::vector<int64_t> rp, bp;
+    std::unordered_map<const Node*, int32_t> memo;
+
+    int32_t add(const Node* n) {
+        auto it = memo.find(n);
+        if (it != memo.end()) return it->second;
+        DNode d;
+        std::memset(&d, 0, sizeof d);
+        d.kind = (int32_t)n->kind;
+        d.runs = n->runs;
+        d.nbytes = n->nbytes;
+        if (n->kind == Kind::Run) {
+            d.a = n->off;
+            d.b = n->len;
+        } else if (n->kind == Kind::Rep) {
+            d.a = n->count;
+            d.b = n->stride;
+            d.c = n->base;
+            d.body_runs = n->body->runs;
+            d.body_nbytes = n->body->nbytes;
+            host_magic((uint64_t)d.body_runs, &d.m_runs, &d.s_runs);
+            host_magic((uint64_t)d.body_nbytes, &d.m_bytes, &d.s_bytes);
+            d.child = add(n->body.get());
+        } else if (n->kind == Kind::Seq) {
+            std::vector<int32_t> ids;
+            ids.reserve(n->kids.size());
+            for (const auto& c : n->kids) ids.push_back(add(c.get()));
+            d.nkids = (int32_t)n->kids.size();
+            d.child = (int32_t)kids.size();
+            kids.insert(kids.end(), ids.begin(), ids.end());
+            d.pref = (int32_t)rp.size();
+            rp.insert(rp.end(), n->run_prefix.begin(), n->run_prefix.end());
+            bp.insert(bp.end(), n->byte_prefix.begin(), n->byte_prefix.end());
+        }
+        const int32_t id = (int32_t)nodes.size();
+        nodes.push_back(d);
+        memo.emplace(n, id);
+        return id;
+    }
+};
+
+}  // namespace
+
+void analyze(const Node* layout, Plan* p) {
+    p->runs = layout->runs;
+    p->nbytes = layout->nbytes;
+    p->min_off = layout->min_off;
+    p->max_end = layout->max_end;
+    p->node_count = layout->node_count;
+    if (layout->runs == 0) {
+        p->kind = PLAN_EMPTY;
+        return;
+    }
+    // chain: Rep^k(Run), k <= kMaxChain
+    const Node* n = layout;
+    Chain c;
+    std::memset(&c, 0, sizeof c);
+    int64_t align = 16;
+    while (n->kind == Kind::Rep && c.depth < kMaxChain) {
+        c.cnt[c.depth] = n->count;
+        c.str[c.depth] = n->stride;
+        c.base += n->base;
+        align = std::min(align, pow2_div(n->stride));
+        ++c.depth;
+        n = n->body.get();
+    }
+    if (n->kind == Kind::Run) {
+        c.base += n->off;
+        c.L = n->len;
+        align = std::min(align, pow2_div(c.L));
+        align = std::min(align, pow2_div(c.base));
+        for (int i = 0; i < c.depth; ++i) host_magic((uint64_t)c.cnt[i], &c.m_cnt[i], &c.s_cnt[i]);
+        host_magic((uint64_t)c.L, &c.m_L, &c.s_L);
+        p->kind = PLAN_CHAIN;
+        p->chain = c;
+        p->chain_align = (int32_t)align;
+    } else {
+        p->kind = PLAN_GENERIC;
+    }
+    p->overlap = may_overlap(layout);
+    if (p->overlap && layout->runs <= (int64_t(1) << 22)) p->overlap = exact_overlap(layout);
+}
+
+std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStream_t stream,
+                               std::string* err) {
+    {
+        std::lock_guard<std::mutex> g(dt->mu);
+        auto it = dt->plans.find({device, count});
+        if (it != dt->plans.end()) return it->second;
+    }
+    NodeP lay = dt->layout_for(count);
+    auto p = std::make_shared<Plan>();
+    p->device = device;
+    analyze(lay.get(), p.get());
+    if (p->kind != PLAN_EMPTY) {
+        Flattener f;
+        const int32_t root = f.add(lay.get());
+        const size_t nb = f.nodes.size() * sizeof(DNode);
+        const size_t kb = ((f.kids.size() * sizeof(int32_t)) + 15) & ~size_t(15);
+        const size_t pb = f.rp.size() * sizeof(int64_t);
+        std::vector<uint8_t> host(nb + kb + 2 * pb + 16, 0);
+        std::memcpy(host.data(), f.nodes.data(), nb);
+        if (!f.kids.empty()) std::memcpy(host.data() + nb, f.kids.data(), f.kids.size() * sizeof(int32_t));
+        if (pb) {
+            std::memcpy(host.data() + nb + kb, f.rp.data(), pb);
+            std::memcpy(host.data() + nb + kb + pb, f.bp.data(), pb);
+        }
+        void* dev = nullptr;
+        cudaError_t e = cudaMalloc(&dev, host.size());
+        if (e != cudaSuccess) {
+            *err = std::string("cudaMalloc(descriptor): ") + cudaGetErrorString(e);
+            return nullptr;
+        }
+        e = cudaMemcpyAsync(dev, host.data(), host.size(), cudaMemcpyHostToDevice, stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess) {
+            cudaFree(dev);
+            *err = std::string("descriptor upload: ") + cudaGetErrorString(e);
+            return nullptr;
+        }
+        p->blob = dev;
+        p->blob_bytes = host.size();
+        uint8_t* b = (uint8_t*)dev;
+        p->desc.nodes = (const DNode*)b;
+        p->desc.kids = (const int32_t*)(b + nb);
+        p->desc.rp = (const int64_t*)(b + nb + kb);
+        p->desc.bp = (const int64_t*)(b + nb + kb + pb);
+        p->desc.root = root;
+        p->desc.runs = lay->runs;
+        p->desc.nbytes = lay->nbytes;
+    }
+    std::lock_guard<std::mutex> g(dt->mu);
+    auto ins = dt->plans.emplace(std::make_pair(device, count), p);
+    return ins.first->second;
+}
+
+}  // namespace mpx

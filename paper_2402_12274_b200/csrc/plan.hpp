@@ -1,0 +1,38 @@
+// plan.hpp -- lowering of a layout tree to a GPU execution plan.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "desc.cuh"
+#include "typerep.hpp"
+
+namespace mpx {
+
+enum PlanKind : int32_t { PLAN_EMPTY = 0, PLAN_CHAIN = 1, PLAN_GENERIC = 2 };
+
+struct Plan {
+    int32_t kind = PLAN_EMPTY;
+    int device = -1;
+    int64_t runs = 0, nbytes = 0, min_off = 0, max_end = 0, node_count = 1;
+    bool overlap = false;   // unpack must keep traversal order (last writer wins)
+    Chain chain{};          // valid for PLAN_CHAIN
+    int32_t chain_align = 16;  // largest power of two dividing base, L and strides
+    DDesc desc{};           // device descriptor (always built, used by iov + generic)
+    void* blob = nullptr;   // device allocation backing desc
+    size_t blob_bytes = 0;
+    ~Plan();
+};
+
+// Build (or fetch from the datatype's cache) the plan for (layout_for(count), device).
+std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStream_t stream,
+                               std::string* err);
+
+// Lower one layout on the host (no device allocation); used by tests via the C ABI.
+void analyze(const Node* layout, Plan* p);
+
+}  // namespace mpx

@@ -1,0 +1,193 @@
+"""GPU parity of the datatype hot path (libmpx.so kernels) against the
+reference's golden vectors and the CPU oracle.  Bit-exact everywhere.
+
+Covers: type_iov (full list digest + windows), pack, unpack (full, partial
+prefix, overflow -> TruncateError after filling), count replication, the
+BASELINE configs at full size (cfg1, 12 cfg2 halo faces of a 514^3 f32
+array, cfg3 = hvector(256) of indexed(2048) of a resized-40 struct), fused
+multi-face pack/unpack, host-buffer staging, and the reference's error
+cases (test_datatype.py:288-310).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2402_12274_b200 as mp
+from paper_2402_12274_b200 import ArgError, TruncateError
+from conftest import load_golden, to_tuple_spec
+from golden_common import (CFG1_SPEC, cfg2_faces, cfg3_spec, iov_digest,
+                           seeded_bytes, sha)
+from specbuild import build_product
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def dev_bytes(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def check_record_gpu(rec):
+    dt = build_product(to_tuple_spec(rec["spec"]), mp)
+    name = rec["name"]
+    if "iov_sha" in rec:
+        iov = host(mp.type_iov_tensor(dt))
+        assert iov_digest(iov) == rec["iov_sha"], name
+    for off, ml, n, dig, _ in rec["windows"]:
+        w = host(mp.type_iov_tensor(dt, off, ml))
+        assert len(w) == n and iov_digest(w) == dig, (name, off, ml)
+    span, total = rec["span"], rec["size"]
+    if "pack_sha" in rec:
+        buf = dev_bytes(seeded_bytes(rec["seed"], span))
+        assert sha(host(mp.pack(dt, buf))) == rec["pack_sha"], name
+        data = dev_bytes(seeded_bytes(rec["seed"] + 1, total))
+        out = torch.zeros(max(span, 1), dtype=torch.uint8, device=DEV)[:span]
+        wrote = mp.unpack(dt, data, out)
+        assert [wrote, sha(host(out))] == rec["unpack"], name
+        half, w2, dig2 = rec["unpack_partial"]
+        out2 = torch.zeros(max(span, 1), dtype=torch.uint8, device=DEV)[:span]
+        assert mp.unpack(dt, data[:half], out2) == w2, name
+        assert sha(host(out2)) == dig2, name
+        err, dig3 = rec["unpack_over"]
+        out3 = torch.zeros(max(span, 1), dtype=torch.uint8, device=DEV)[:span]
+        over = torch.cat([data, torch.tensor([120, 121, 122], dtype=torch.uint8, device=DEV)])
+        with pytest.raises(TruncateError):
+            mp.unpack(dt, over, out3)
+        assert err == "ERR_TRUNCATE" and sha(host(out3)) == dig3, name
+    if "pack_count2" in rec:
+        span2, dig, ln = rec["pack_count2"]
+        buf2 = dev_bytes(seeded_bytes(rec["seed"] + 2, span2))
+        if dig == "ERR_ARG":
+            with pytest.raises(ArgError):
+                mp.pack(dt, buf2, count=2)
+        else:
+            p2 = host(mp.pack(dt, buf2, count=2))
+            assert len(p2) == ln and sha(p2) == dig, name
+    if "pack_neg" in rec:
+        with pytest.raises(ArgError):
+            mp.pack(dt, torch.zeros(max(span, 1), dtype=torch.uint8, device=DEV))
+    if dt not in mp.datatypes.BUILTINS:
+        mp.type_free(dt)
+
+
+@pytest.mark.parametrize("corpus", ["frozen", "unit", "crit1"])
+def test_gpu_matches_reference_corpus(corpus):
+    for rec in load_golden(corpus):
+        check_record_gpu(rec)
+
+
+def test_gpu_configs_golden():
+    for rec in load_golden("configs"):
+        if rec["name"] in ("cfg3",):
+            continue
+        check_record_gpu(rec)
+
+
+def test_gpu_cfg2_faces_full_array():
+    """All 12 halo faces of the seeded 514^3 f32 array, single and fused."""
+    arr_h = seeded_bytes(2, 514 ** 3 * 4)
+    arr = dev_bytes(arr_h)
+    recs = {r["name"]: r for r in load_golden("configs")}
+    faces = cfg2_faces()
+    dts = [build_product(s, mp) for _, s in faces]
+    outs = []
+    for (name, _), dt in zip(faces, dts):
+        p = mp.pack(dt, arr)
+        assert sha(host(p)) == recs["cfg2-" + name]["pack_sha_array2"], name
+        outs.append(p)
+    fused = [torch.empty_like(o) for o in outs]
+    mp.pack_multi(dts, [arr] * len(dts), fused)
+    for o, f in zip(outs, fused):
+        assert torch.equal(o, f)
+    # unpack every face into a zero array, then compare against the oracle
+    dst = torch.zeros_like(arr)
+    mp.unpack_multi(dts, outs, [dst] * len(dts))
+    ref = np.zeros_like(arr_h)
+    for (name, spec), o in zip(faces, outs):
+        oracle.OracleType(spec).unpack(host(o), ref)
+    assert sha(host(dst)) == sha(ref)
+
+
+def test_gpu_cfg1_roundtrip_float64():
+    rng = np.random.default_rng(1)
+    src = rng.uniform(-1, 1, 32768)
+    dt = build_product(CFG1_SPEC, mp)
+    t = torch.from_numpy(src).to(DEV)
+    packed = mp.pack(dt, t)
+    assert packed.numel() == 131072
+    ot = oracle.OracleType(CFG1_SPEC)
+    assert sha(host(packed)) == sha(ot.pack(src.view(np.uint8)))
+    back = torch.zeros_like(t)
+    assert mp.unpack(dt, packed, back) == 131072
+    exp = np.zeros_like(src)
+    ot.unpack(host(packed), exp.view(np.uint8))
+    assert np.array_equal(host(back), exp)
+    iov = host(mp.type_iov_tensor(dt))
+    assert iov.shape == (4096, 2) and (iov[:, 1] == 32).all()
+    assert (iov[:, 0] == np.arange(4096) * 64).all()
+
+
+@pytest.mark.parametrize("hcount", [8, 256])
+def test_gpu_cfg3_full_size(hcount):
+    """cfg3 against the oracle: iov digest, pack, unpack round trip."""
+    spec = cfg3_spec(3, hcount=hcount)
+    dt = build_product(spec, mp)
+    ot = oracle.OracleType(spec)
+    span = ot.max_end
+    src_h = seeded_bytes(5, span)
+    src = dev_bytes(src_h)
+    packed = mp.pack(dt, src)
+    ref = ot.pack(src_h)
+    assert packed.numel() == ref.size
+    assert sha(host(packed)) == sha(ref)
+    out = torch.zeros_like(src)
+    assert mp.unpack(dt, packed, out) == ref.size
+    exp = np.zeros(span, np.uint8)
+    ot.unpack(ref, exp)
+    assert sha(host(out)) == sha(exp)
+    iov = host(mp.type_iov_tensor(dt))
+    assert iov_digest(iov) == iov_digest(ot.iov())
+    if hcount == 256:
+        rec = [r for r in load_golden("configs") if r["name"] == "cfg3"][0]
+        for off, ml, n, dig, _ in rec["windows"]:
+            w = host(mp.type_iov_tensor(dt, off, ml))
+            assert len(w) == n and iov_digest(w) == dig
+
+
+def test_gpu_host_buffers_reference_contract():  # test_datatype.py:288-310
+    dt = mp.type_vector(2, 1, 4, mp.INT32).commit()
+    with pytest.raises(ArgError):
+        mp.pack(dt, bytes(19))
+    out = mp.pack(dt, bytes(range(20)))
+    assert out == bytes([0, 1, 2, 3, 16, 17, 18, 19])
+    with pytest.raises(ArgError):
+        mp.unpack(dt, out, bytes(20))
+    c4 = mp.type_contiguous(4, mp.BYTE).commit()
+    buf = bytearray(4)
+    with pytest.raises(TruncateError):
+        mp.unpack(c4, b"\x01\x02\x03\x04\x05", buf)
+    assert bytes(buf) == b"\x01\x02\x03\x04"
+    b16 = bytes(range(16))
+    assert mp.pack(mp.INT32, b16, count=4) == b16
+    segs, n = mp.type_iov(mp.type_vector(3, 2, 4, mp.INT32).commit(), 1, 10)
+    assert n == 2 and [(s.base_offset, s.length) for s in segs] == [(16, 8), (32, 8)]
+    e = mp.type_contiguous(0, mp.INT32).commit()
+    assert mp.pack(e, b"") == b""
+    assert mp.type_iov(e, 0, -1) == ([], 0)
+
+
+def test_gpu_overlapping_unpack_last_writer_wins():
+    """vector with negative stride over overlapping blocks: sequential order."""
+    dt = mp.type_create_struct([4, 4], [0, 2], [mp.BYTE, mp.BYTE]).commit()
+    assert dt.layout_query()["overlap"] == 1
+    data = torch.arange(8, dtype=torch.uint8, device=DEV)
+    out = torch.zeros(6, dtype=torch.uint8, device=DEV)
+    mp.unpack(dt, data, out)
+    assert host(out).tolist() == [0, 1, 4, 5, 6, 7]
