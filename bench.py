@@ -19,7 +19,6 @@ algorithm (oracle/liboracle.so) on the host cores over the same faces.
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -76,58 +75,51 @@ def load_traffic():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled through NVML every ~0.5 ms while
+    the timed region runs (nvidia-smi's 100 ms period is longer than the
+    whole region)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20),
+               ("hw_thermal_slowdown", 0x40), ("hw_power_brake", 0x80),
+               ("sw_power_cap", 0x4))
 
     def __init__(self, index):
         self.index = index
         self.samples = []
-        self.proc = None
+        self.reasons = 0
+        self.smax = None
+        self._stop = threading.Event()
+        self.thread = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
         except Exception:
-            self.proc = None
+            return
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
-                self.samples.append(parts)
+        def run():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                    self.reasons |= pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except Exception:
+                    pass
+                time.sleep(0.0005)
+
+        self.thread = threading.Thread(target=run, daemon=True)
+        self.thread.start()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except Exception:
-            self.proc.kill()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        sm = []
-        smax = None
-        for s in self.samples:
-            try:
-                sm.append(float(s[0]))
-                smax = float(s[1])
-            except ValueError:
-                pass
-            for n, v in zip(names, s[2:]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if self.thread is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        self._stop.set()
+        self.thread.join()
+        names = [n for n, bit in self.REASONS if self.reasons & bit]
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.smax, "reasons": names, "samples": len(self.samples)}
 
 
 def cpu_model():
@@ -144,39 +136,48 @@ def cpu_model():
 # ------------------------------------------------------------- CPU arm
 
 
-def run_cpu_oracle(seconds, threads):
-    """Time the oracle port (C restatement of the reference algorithm) over
-    the same 12 faces: pack then unpack, faces spread over `threads` host
-    threads (ctypes releases the GIL).  Returns (GB/s, reps, sample text)."""
-    import oracle
-    from concurrent.futures import ThreadPoolExecutor
-    oracle.build()
-    arr = seeded_bytes(2, ARRAY_BYTES)
-    dst = np.zeros_like(arr)
-    types = [(oracle.OracleType(spec), face_bytes(spec)) for _, spec in face_specs()]
-    outs = [np.empty(b, np.uint8) for _, b in types]
-    lib = oracle.lib()
-    import ctypes
+class CpuOracle:
+    """The oracle port (C restatement of the reference algorithm,
+    oracle/dt_oracle.c) over the same 12 faces: pack then unpack, faces
+    spread over `threads` host threads (ctypes releases the GIL)."""
 
-    def one(i):
-        t, b = types[i]
-        lib.orc_pack(t.h, 1, arr.ctypes.data_as(ctypes.c_void_p), arr.size,
-                     outs[i].ctypes.data_as(ctypes.c_void_p))
-        tr = ctypes.c_int()
-        lib.orc_unpack(t.h, 1, outs[i].ctypes.data_as(ctypes.c_void_p), b,
-                       dst.ctypes.data_as(ctypes.c_void_p), dst.size, ctypes.byref(tr))
+    def __init__(self, threads):
+        import ctypes
+        from concurrent.futures import ThreadPoolExecutor
+        import oracle
+        oracle.build()
+        self.threads = threads
+        self.arr = seeded_bytes(2, ARRAY_BYTES)
+        self.dst = np.zeros_like(self.arr)
+        self.types = [(oracle.OracleType(spec), face_bytes(spec)) for _, spec in face_specs()]
+        self.outs = [np.empty(b, np.uint8) for _, b in self.types]
+        self.lib = oracle.lib()
+        self.ex = ThreadPoolExecutor(max_workers=threads)
+        self.c = ctypes
 
-    reps = 0
-    t0 = time.perf_counter()
-    with ThreadPoolExecutor(max_workers=threads) as ex:
+    def _one(self, i):
+        c = self.c
+        t, b = self.types[i]
+        self.lib.orc_pack(t.h, 1, self.arr.ctypes.data_as(c.c_void_p), self.arr.size,
+                          self.outs[i].ctypes.data_as(c.c_void_p))
+        tr = c.c_int()
+        self.lib.orc_unpack(t.h, 1, self.outs[i].ctypes.data_as(c.c_void_p), b,
+                            self.dst.ctypes.data_as(c.c_void_p), self.dst.size, c.byref(tr))
+
+    def step(self):
+        t0 = time.perf_counter()
+        list(self.ex.map(self._one, range(len(self.types))))
+        return time.perf_counter() - t0
+
+    def run_for(self, seconds):
+        reps, t0 = 0, time.perf_counter()
         while True:
-            list(ex.map(one, range(len(types))))
+            self.step()
             reps += 1
             if time.perf_counter() - t0 >= seconds:
                 break
-    dt = time.perf_counter() - t0
-    gbs = reps * step_bytes() / dt / 1e9
-    return gbs, reps, dt
+        dt = time.perf_counter() - t0
+        return reps * step_bytes() / dt / 1e9, reps, dt
 
 
 def reference_arm(args):
@@ -184,15 +185,10 @@ def reference_arm(args):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    # each "step" is a bounded sample: all 12 faces packed + unpacked once
-    import oracle  # noqa: F401
+    cpu = CpuOracle(threads)
     for _ in range(max(0, args.warmup)):
-        run_cpu_oracle(0.0, threads)
-    gbs, reps, dt = run_cpu_oracle(0.0, threads)
-    times = []
-    for _ in range(args.steps):
-        g, r, d = run_cpu_oracle(0.0, threads)
-        times.append(d / r)
+        cpu.step()
+    times = [cpu.step() for _ in range(args.steps)]   # one step = all 12 faces once
     ms = 1e3 * float(np.mean(times))
     value = step_bytes() / (ms / 1e3) / 1e9
     line = {
@@ -203,8 +199,8 @@ def reference_arm(args):
         "config": {"workload": WORKLOAD, "array": "514^3 float32", "faces": 12},
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads,
                          "kind": "port",
-                         "sample": "all 12 cfg2 faces packed+unpacked once per step by the C "
-                                   "oracle port, faces spread over %d host threads (%s)"
+                         "sample": "each step packs+unpacks all 12 cfg2 faces once with the C "
+                                   "oracle port of datatype.py, faces over %d host threads (%s)"
                                    % (threads, cpu_model())},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -283,26 +279,46 @@ def gpu_arm(args):
     ms_per_step = total_ms / args.steps
     value = world * step_bytes() / (ms_per_step / 1e3) / 1e9
 
-    # ---- e2e through the public API with host buffers (pinned) ----
-    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(args.steps)]
-    for i in range(args.steps + 1):
-        flush.zero_()
-        if i > 0:
-            e2e_ev[i - 1][0].record(stream)
+    # ---- e2e through the public API with HOST buffers ----
+    # (a) zero-copy: the array, the packed faces and the unpack destination all
+    #     live in pinned host memory; the fused kernels read/write them over
+    #     PCIe through their UVA addresses (h2d = bytes the kernels pull from
+    #     host memory, d2h = bytes they push back).
+    dst_pinned = torch.zeros(ARRAY_BYTES, dtype=torch.uint8).pin_memory()
+
+    def e2e_zero_copy():
+        mp.pack_multi(dts, [arr_pinned] * len(dts), packed_host)
+        mp.unpack_multi(dts, packed_host, [dst_pinned] * len(dts))
+
+    # (b) staged: explicit H2D copy of the whole array, device kernels, D2H of
+    #     the packed faces (what a caller without pinned-host support would do).
+    def e2e_staged():
         arr.copy_(arr_pinned, non_blocking=True)
         mp.pack_multi(dts, [arr] * len(dts), packed)
         mp.unpack_multi(dts, packed, [dst] * len(dts))
-        for p, h in zip(packed, packed_host):
-            h.copy_(p, non_blocking=True)
-        if i > 0:
-            e2e_ev[i - 1][1].record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = float(np.mean([a.elapsed_time(b) for a, b in e2e_ev]))
-    te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_ms = float(te.item())
+        for p_, h in zip(packed, packed_host):
+            h.copy_(p_, non_blocking=True)
+
+    def time_steps(fn):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        for _ in range(max(1, args.warmup)):
+            fn()
+        for a, b in evs:
+            flush.zero_()
+            a.record(stream)
+            fn()
+            b.record(stream)
+        torch.cuda.synchronize()
+        ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
+    e2e_ms = time_steps(e2e_zero_copy)
+    staged_ms = time_steps(e2e_staged)
+    payload = step_bytes() // 4
     d2h = sum(p.numel() for p in packed)
 
     # ---- roofline of the dominant kernel ----
@@ -318,7 +334,7 @@ def gpu_arm(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        gbs, reps, dtc = run_cpu_oracle(args.cpu_seconds, threads)
+        gbs, reps, dtc = CpuOracle(threads).run_for(args.cpu_seconds)
         cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "port",
                "sample": "%d repetitions (%.1f s) of the full step (12 faces pack+unpack) by the C "
                          "oracle port of datatype.py, faces over %d threads on %s"
@@ -341,8 +357,11 @@ def gpu_arm(args):
                          "traffic": traffic.get("bytes_per_launch") if traffic else None,
                          "algorithmic_bytes_per_launch": launch_bytes},
             "e2e": {"value": round(world * step_bytes() / (e2e_ms / 1e3) / 1e9, 3), "unit": "GB/s",
-                    "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": ARRAY_BYTES,
-                    "d2h_bytes_per_step": d2h},
+                    "ms_per_step": round(e2e_ms, 3), "mode": "zero-copy pinned host buffers",
+                    "h2d_bytes_per_step": 2 * payload, "d2h_bytes_per_step": 2 * payload},
+            "e2e_staged": {"value": round(world * step_bytes() / (staged_ms / 1e3) / 1e9, 3),
+                           "unit": "GB/s", "ms_per_step": round(staged_ms, 3),
+                           "h2d_bytes_per_step": ARRAY_BYTES, "d2h_bytes_per_step": d2h},
             "gpu_launches": 2 * args.steps,
             "clocks": clocks,
             "cpu_baseline": cpu,

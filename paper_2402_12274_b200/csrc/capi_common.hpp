@@ -22,7 +22,9 @@ int cuda_fail(cudaError_t e, const char* what);
 Datatype* lookup(mpx_datatype h);
 
 // validate a typed buffer and fetch its plan on the buffer's device
-int prepare(Datatype* d, int64_t count, const void* layout_buf, int64_t layout_bytes, bool writable,
+// (other_buf = the packed-side buffer, used to pick the execution device;
+// pinned host buffers are addressed zero-copy)
+int prepare(Datatype* d, int64_t count, const void* layout_buf, int64_t layout_bytes, const void* other_buf,
             cudaStream_t stream, std::shared_ptr<Plan>* plan, int* device);
 
 // n fused pack (or unpack) operations on one stream

@@ -112,17 +112,43 @@ Datatype* new_type(NodeP lay, int64_t size, int64_t lb, int64_t ub, std::string 
     return d;
 }
 
-// device owning a pointer (must be device memory)
-int device_of(const void* p, int* dev) {
+// Where a buffer lives.  Device memory -> its device.  Pinned / registered
+// host memory is accepted too (*dev = -1): kernels address it directly over
+// PCIe through its UVA device pointer (zero-copy).  Pageable memory is refused.
+int resolve_ptr(const void* p, int* dev) {
     cudaPointerAttributes a;
     cudaError_t e = cudaPointerGetAttributes(&a, p);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(MPX_ERR_ARG, "cannot resolve buffer %p: %s", p, cudaGetErrorString(e));
     }
-    if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)
-        return fail(MPX_ERR_ARG, "buffer %p is not device memory", p);
-    *dev = a.device;
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+        *dev = a.device;
+        return MPX_SUCCESS;
+    }
+    if (a.type == cudaMemoryTypeHost) {
+        if (a.devicePointer != p)
+            return fail(MPX_ERR_ARG, "pinned host buffer %p is not mapped at the same UVA address", p);
+        *dev = -1;
+        return MPX_SUCCESS;
+    }
+    return fail(MPX_ERR_ARG, "buffer %p is pageable host memory: pass a CUDA tensor or pinned memory", p);
+}
+
+int device_of(const void* p, int* dev) {
+    int rc = resolve_ptr(p, dev);
+    if (rc == MPX_SUCCESS && *dev < 0) cudaGetDevice(dev);
+    return rc;
+}
+
+// execution device for an operation touching buffers a and b
+int device_for(const void* a, const void* b, int* dev) {
+    int da = -1, db = -1, rc;
+    if ((rc = resolve_ptr(a, &da)) || (rc = resolve_ptr(b, &db))) return rc;
+    if (da >= 0 && db >= 0 && da != db)
+        return fail(MPX_ERR_ARG, "buffers live on different devices (%d, %d)", da, db);
+    *dev = da >= 0 ? da : db;
+    if (*dev < 0) cudaGetDevice(dev);
     return MPX_SUCCESS;
 }
 
@@ -138,13 +164,12 @@ int ensure_device(int dev) {
 }  // namespace
 
 // Validate + lower one pack/unpack operation.  layout_buf is the typed side.
-int prepare(Datatype* d, int64_t count, const void* layout_buf, int64_t layout_bytes, bool writable,
+int prepare(Datatype* d, int64_t count, const void* layout_buf, int64_t layout_bytes, const void* other_buf,
             cudaStream_t stream, std::shared_ptr<Plan>* plan, int* device) {
     int rc = check_count(count, "count");
     if (rc) return rc;
     rc = check_usable(d, "pack/unpack");
     if (rc) return rc;
-    (void)writable;
     NodeP lay = d->layout_for(count);
     if (lay->runs) {  // _checked_view bounds, datatype.py:685-691
         if (lay->min_off < 0) return fail(MPX_ERR_ARG, "layout reaches before the start of the buffer");
@@ -157,7 +182,7 @@ int prepare(Datatype* d, int64_t count, const void* layout_buf, int64_t layout_b
         return MPX_SUCCESS;
     }
     int dev = 0;
-    rc = device_of(layout_buf, &dev);
+    rc = device_for(layout_buf, other_buf ? other_buf : layout_buf, &dev);
     if (rc) return rc;
     rc = ensure_device(dev);
     if (rc) return rc;
@@ -466,8 +491,9 @@ int movement(int n, const mpx_datatype* dts, const int64_t* counts, const void* 
         std::shared_ptr<Plan> plan;
         int dev = 0;
         const void* layout_buf = pack ? srcs[i] : dsts[i];
+        const void* packed_buf = pack ? dsts[i] : srcs[i];
         const int64_t layout_bytes = pack ? src_bytes[i] : dst_bytes[i];
-        int rc = prepare(d, counts[i], layout_buf, layout_bytes, !pack, stream, &plan, &dev);
+        int rc = prepare(d, counts[i], layout_buf, layout_bytes, packed_buf, stream, &plan, &dev);
         if (rc) return rc;
         const int64_t nbytes = d->size * counts[i];
         int64_t limit = nbytes;

@@ -309,6 +309,25 @@ def _cuda_tensor(obj):
     return None
 
 
+def _gpu_visible(obj):
+    """CUDA tensor, or pinned CPU tensor (kernels address it zero-copy)."""
+    t = _cuda_tensor(obj)
+    if t is not None:
+        return t
+    if isinstance(obj, torch.Tensor) and obj.is_pinned():
+        if not obj.is_contiguous():
+            raise ArgError("buffer must be C-contiguous")
+        return obj
+    return None
+
+
+def _exec_device(*tensors):
+    for t in tensors:
+        if t is not None and t.is_cuda:
+            return t.device
+    return _default_device()
+
+
 def _host_view(buf, writable):
     """Reference as_byte_view (datatype.py:664-677), plus CPU tensors."""
     if isinstance(buf, torch.Tensor):
@@ -386,13 +405,18 @@ def pack(d, buf, count=1):
     if not isinstance(d, Datatype):
         raise ArgError("expected a Datatype")
     _count(count, "count")
-    src = _cuda_tensor(buf)
+    src = _gpu_visible(buf)
     if src is not None:
         n = packed_size(d, count)
-        out = torch.empty(max(n, 1), dtype=torch.uint8, device=src.device)[:n]
+        if src.is_cuda:
+            out = torch.empty(max(n, 1), dtype=torch.uint8, device=src.device)[:n]
+        else:
+            out = torch.empty(max(n, 1), dtype=torch.uint8, pin_memory=True)[:n]
+        dev = _exec_device(src)
         check(lib.mpx_pack(d._h, count, src.data_ptr(), _nbytes(src),
-                           out.data_ptr() if n else src.data_ptr(), n,
-                           _stream_ptr(src.device)))
+                           out.data_ptr() if n else src.data_ptr(), n, _stream_ptr(dev)))
+        if not src.is_cuda:          # host-facing result: complete before returning
+            torch.cuda.current_stream(dev).synchronize()
         return out
     # reference contract for host buffers: validate like _checked_view first
     view = _host_view(buf, writable=False)
@@ -422,12 +446,17 @@ def unpack(d, data, buf, count=1):
     if not isinstance(d, Datatype):
         raise ArgError("expected a Datatype")
     _count(count, "count")
-    dst = _cuda_tensor(buf)
+    dst = _gpu_visible(buf)
     written = ctypes.c_int64()
     if dst is not None:
-        src = _to_cuda_bytes(data, dst.device)
+        src = _gpu_visible(data)
+        dev = _exec_device(dst, src)
+        if src is None:
+            src = _to_cuda_bytes(data, dev)
         rc = lib.mpx_unpack(d._h, count, src.data_ptr(), _nbytes(src), dst.data_ptr(),
-                            _nbytes(dst), ctypes.byref(written), _stream_ptr(dst.device))
+                            _nbytes(dst), ctypes.byref(written), _stream_ptr(dev))
+        if not dst.is_cuda:
+            torch.cuda.current_stream(dev).synchronize()
         if rc and rc != 4:
             check(rc)
         if rc == 4:
@@ -468,14 +497,18 @@ def _multi(fn, dts, counts, srcs, dsts):
     sb = i64_array([_nbytes(s) for s in srcs])
     db = i64_array([_nbytes(t) for t in dsts])
     cs = i64_array(counts)
-    stream = _stream_ptr(srcs[0].device) if n else 0
+    for t in list(srcs) + list(dsts):
+        if _gpu_visible(t) is None:
+            raise ArgError("multi operations need CUDA or pinned CPU tensors")
+    stream = _stream_ptr(_exec_device(*srcs, *dsts)) if n else 0
     return fn(n, hs, cs, sp, sb, dp, db, stream)
 
 
 def pack_multi(dts, bufs, outs, counts=None):
-    """Fused pack of several (datatype, CUDA buffer) pairs into their CUDA
-    outputs -- one launch for up to 16 strided layouts (e.g. six halo
-    faces).  B200 extension of pack()."""
+    """Fused pack of several (datatype, buffer) pairs into their outputs --
+    one launch for up to 16 strided layouts (e.g. six halo faces).  Buffers
+    are CUDA tensors or pinned CPU tensors (zero-copy over PCIe).
+    Asynchronous on the current stream.  B200 extension of pack()."""
     counts = counts or [1] * len(dts)
     check(_multi(lib.mpx_pack_multi, dts, counts, bufs, outs))
 

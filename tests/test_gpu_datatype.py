@@ -191,3 +191,29 @@ def test_gpu_overlapping_unpack_last_writer_wins():
     out = torch.zeros(6, dtype=torch.uint8, device=DEV)
     mp.unpack(dt, data, out)
     assert host(out).tolist() == [0, 1, 4, 5, 6, 7]
+
+
+def test_gpu_pinned_host_zero_copy():
+    """Pinned CPU tensors are addressed by the kernels directly (UVA)."""
+    specs = [("subarray", [40, 40, 40], [38, 38, 1], [1, 1, 1], ("basic", 4)),
+             ("subarray", [40, 40, 40], [8, 38, 38], [31, 1, 1], ("basic", 4)),
+             cfg3_spec(3, hcount=2, nblocks=64)]
+    for spec in specs:
+        dt = build_product(spec, mp)
+        ot = oracle.OracleType(spec)
+        span = ot.max_end
+        src_h = seeded_bytes(9, span)
+        pinned = torch.from_numpy(src_h).pin_memory()
+        packed = mp.pack(dt, pinned)
+        assert not packed.is_cuda and packed.is_pinned()
+        ref = ot.pack(src_h)
+        assert np.array_equal(packed.numpy(), ref)
+        out = torch.zeros(span, dtype=torch.uint8).pin_memory()
+        assert mp.unpack(dt, packed, out) == ref.size
+        exp = np.zeros(span, np.uint8)
+        ot.unpack(ref, exp)
+        assert np.array_equal(out.numpy(), exp)
+        # fused multi with mixed device / pinned operands
+        outs = [torch.empty(ref.size, dtype=torch.uint8, device=DEV)]
+        mp.pack_multi([dt], [pinned], outs)
+        assert np.array_equal(host(outs[0]), ref)
