@@ -519,9 +519,8 @@ int movement(int n, const mpx_datatype* dts, const int64_t* counts, const void* 
             j.c = plan->chain;
             j.src = s;
             j.dst = t;
-            j.w = chain_word(*plan, s, t);
-            j.nwords = limit / j.w;
             j.limit = limit;
+            chain_setup(*plan, pack, &j);
             batch_dev = dev;
         } else {
             cudaError_t e = launch_generic(*plan, pack, s, t, limit, stream);

@@ -33,7 +33,9 @@ struct Chain {
     int32_t s_cnt[kMaxChain];
     uint64_t m_L;
     int32_t s_L;
-    int32_t pad1;
+    int32_t small;          // rows < 2^31 and counts < 2^31: 32-bit index math
+    uint32_t m32_cnt[kMaxChain];
+    int32_t s32_cnt[kMaxChain];
 };
 
 struct DNode {
@@ -69,7 +71,49 @@ inline void host_magic(uint64_t d, uint64_t* m, int32_t* s) {
     *s = l - 1;
 }
 
+// 32-bit variant, 0 <= n < 2^31: m = ceil(2^(31+l)/d)
+inline void host_magic32(uint32_t d, uint32_t* m, int32_t* s) {
+    if (d <= 1) { *m = 0; *s = 0; return; }
+    const int l = 32 - __builtin_clz(d - 1);
+    const uint64_t num = (uint64_t)1 << (31 + l);
+    *m = (uint32_t)((num + d - 1) / d);
+    *s = l - 1;
+}
+
 #ifdef __CUDACC__
+__device__ __forceinline__ uint32_t fdiv32(uint32_t n, uint32_t m, int32_t s) {
+    return m ? (__umulhi(n, m) >> s) : n;
+}
+
+// layout offset of the start of row r of a chain
+__device__ __forceinline__ int64_t chain_row(const Chain& c, int64_t r) {
+    int64_t off = c.base;
+    if (c.depth == 0) return off;
+    if (c.small) {
+        uint32_t rr = (uint32_t)r;
+#pragma unroll
+        for (int i = kMaxChain - 1; i >= 1; --i) {
+            if (i < c.depth) {
+                const uint32_t q = fdiv32(rr, c.m32_cnt[i], c.s32_cnt[i]);
+                off += (int64_t)(int32_t)(rr - q * (uint32_t)c.cnt[i]) * c.str[i];
+                rr = q;
+            }
+        }
+        return off + (int64_t)rr * c.str[0];
+    }
+    uint64_t rr = (uint64_t)r;
+#pragma unroll
+    for (int i = kMaxChain - 1; i >= 1; --i) {
+        if (i < c.depth) {
+            const uint64_t q = __umul64hi(rr, c.m_cnt[i]) >> c.s_cnt[i];
+            const uint64_t qq = c.m_cnt[i] ? q : rr;
+            off += (int64_t)(rr - qq * (uint64_t)c.cnt[i]) * c.str[i];
+            rr = qq;
+        }
+    }
+    return off + (int64_t)rr * c.str[0];
+}
+
 __device__ __forceinline__ uint64_t fdiv(uint64_t n, uint64_t m, int32_t s) {
     return m ? (__umul64hi(n, m) >> s) : n;
 }

@@ -40,40 +40,134 @@ template <> struct Vec<2> { using T = uint16_t; };
 template <> struct Vec<1> { using T = uint8_t; };
 
 constexpr int kChainThreads = 256;
-constexpr int kUnroll = 4;
 
-template <int W, bool PACK>
-__device__ __forceinline__ void chain_job_body(const ChainJob& j, int64_t blk, int64_t nblk) {
-    using T = typename Vec<W>::T;
-    const Chain& c = j.c;
-    const int64_t T_ = nblk * kChainThreads;
-    const int64_t nw = j.nwords;
-    for (int64_t u = blk * kChainThreads + threadIdx.x; u < nw; u += T_ * kUnroll) {
-        T v[kUnroll];
-        int64_t lo[kUnroll];
+// bytes [a, a + 16) of the 32-byte concatenation lo || hi, 0 <= a < 16
+__device__ __forceinline__ uint4 funnel16(const uint4& lo, const uint4& hi, int a) {
+    const uint32_t w0 = lo.x, w1 = lo.y, w2 = lo.z, w3 = lo.w;
+    const uint32_t w4 = hi.x, w5 = hi.y, w6 = hi.z, w7 = hi.w;
+    const int r = (a & 3) * 8;
+#define MPX_F(x, y) __funnelshift_r((x), (y), r)
+    switch (a >> 2) {
+    case 0: return make_uint4(MPX_F(w0, w1), MPX_F(w1, w2), MPX_F(w2, w3), MPX_F(w3, w4));
+    case 1: return make_uint4(MPX_F(w1, w2), MPX_F(w2, w3), MPX_F(w3, w4), MPX_F(w4, w5));
+    case 2: return make_uint4(MPX_F(w2, w3), MPX_F(w3, w4), MPX_F(w4, w5), MPX_F(w5, w6));
+    default: return make_uint4(MPX_F(w3, w4), MPX_F(w4, w5), MPX_F(w5, w6), MPX_F(w6, w7));
+    }
+#undef MPX_F
+}
+
+__device__ __forceinline__ uint4 shfl_down16(const uint4& v, int d) {
+    return make_uint4(__shfl_down_sync(0xffffffffu, v.x, d), __shfl_down_sync(0xffffffffu, v.y, d),
+                      __shfl_down_sync(0xffffffffu, v.z, d), __shfl_down_sync(0xffffffffu, v.w, d));
+}
+__device__ __forceinline__ uint4 shfl_up16(const uint4& v, int d) {
+    return make_uint4(__shfl_up_sync(0xffffffffu, v.x, d), __shfl_up_sync(0xffffffffu, v.y, d),
+                      __shfl_up_sync(0xffffffffu, v.z, d), __shfl_up_sync(0xffffffffu, v.w, d));
+}
+__device__ __forceinline__ uint4 shfl16(const uint4& v, int src) {
+    return make_uint4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
+                      __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
+}
+
+// store bytes [lo, hi) of v into the 16-byte aligned chunk at p
+__device__ __forceinline__ void store_partial16(uint8_t* p, const uint4& v, int lo, int hi) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int q = 0; q < kUnroll; ++q) {
-            const int64_t uu = u + q * T_;
-            if (uu < nw) {
-                const int64_t P = uu * W;
-                lo[q] = chain_off(c, P);
-                if (PACK) v[q] = *reinterpret_cast<const T*>(j.src + lo[q]);
-                else v[q] = *reinterpret_cast<const T*>(j.src + P);
-            }
+    for (int i = 0; i < 4; ++i) {
+        const int b0 = 4 * i, b1 = 4 * i + 4;
+        if (b0 >= lo && b1 <= hi) {
+            *reinterpret_cast<uint32_t*>(p + b0) = w[i];
+        } else {
+#pragma unroll
+            for (int b = b0; b < b1; ++b)
+                if (b >= lo && b < hi) p[b] = (uint8_t)(w[i] >> (8 * (b - b0)));
         }
-#pragma unroll
-        for (int q = 0; q < kUnroll; ++q) {
-            const int64_t uu = u + q * T_;
-            if (uu < nw) {
-                const int64_t P = uu * W;
-                if (PACK) *reinterpret_cast<T*>(j.dst + P) = v[q];
-                else *reinterpret_cast<T*>(j.dst + lo[q]) = v[q];
+    }
+}
+
+// Warp per row, 16-byte vectors on both sides.  The packed side is 16-byte
+// aligned (L % 16 == 0); the layout side may start at any byte: aligned
+// 16-byte loads (pack) or stores (unpack) are realigned with funnel shifts
+// through neighbouring lanes, so no access is narrower than 16 bytes except
+// the two partial chunks at the ends of an unpacked row.
+template <bool PACK>
+__device__ __forceinline__ void chain_rows(const ChainJob& j, int64_t warp0, int64_t nwarps) {
+    const int lane = threadIdx.x & 31;
+    const Chain& c = j.c;
+    const int nch = (int)(c.L >> 4);
+    for (int64_t r = warp0; r < j.rows; r += nwarps) {
+        const int64_t s = chain_row(c, r);
+        if (PACK) {
+            const uint8_t* srow = j.src + s;
+            const int a = (int)(reinterpret_cast<uintptr_t>(srow) & 15);
+            const uint4* s16 = reinterpret_cast<const uint4*>(srow - a);
+            uint4* d16 = reinterpret_cast<uint4*>(j.dst + r * c.L);
+            for (int k0 = 0; k0 < nch; k0 += 32) {
+                const int k = k0 + lane;
+                uint4 c0 = make_uint4(0, 0, 0, 0);
+                if (k < nch) c0 = __ldg(s16 + k);
+                if (a) {
+                    uint4 c1 = shfl_down16(c0, 1);
+                    if (k < nch && (lane == 31 || k + 1 == nch)) c1 = __ldg(s16 + k + 1);
+                    c0 = funnel16(c0, c1, a);
+                }
+                if (k < nch) d16[k] = c0;
+            }
+        } else {
+            const uint4* p16 = reinterpret_cast<const uint4*>(j.src + r * c.L);
+            uint8_t* drow = j.dst + s;
+            const int a = (int)(reinterpret_cast<uintptr_t>(drow) & 15);
+            uint8_t* d16 = drow - a;
+            const int nout = a ? nch + 1 : nch;
+            uint4 carry = make_uint4(0, 0, 0, 0);
+            for (int k0 = 0; k0 < nout; k0 += 32) {
+                const int k = k0 + lane;
+                uint4 cur = make_uint4(0, 0, 0, 0);
+                if (k < nch) cur = __ldg(p16 + k);
+                if (a == 0) {
+                    if (k < nch) reinterpret_cast<uint4*>(d16)[k] = cur;
+                    continue;
+                }
+                uint4 prev = shfl_up16(cur, 1);
+                if (lane == 0) prev = carry;
+                carry = shfl16(cur, 31);
+                const uint4 out = funnel16(prev, cur, 16 - a);
+                if (k == 0) store_partial16(d16, out, a, 16);
+                else if (k == nch) store_partial16(d16 + 16 * (int64_t)k, out, 0, a);
+                else if (k < nch) reinterpret_cast<uint4*>(d16)[k] = out;
             }
         }
     }
-    // unpack with a partial last word (data shorter than the layout): bytewise tail
-    if (!PACK && blk == 0 && threadIdx.x == 0) {
-        for (int64_t P = nw * W; P < j.limit; ++P) j.dst[chain_off(c, P)] = j.src[P];
+}
+
+// Thread per row (short rows): row offset computed once, W-byte words, four
+// rows in flight per thread.
+template <int W, bool PACK>
+__device__ __forceinline__ void chain_elems(const ChainJob& j, int64_t t0, int64_t nthr) {
+    using T = typename Vec<W>::T;
+    const Chain& c = j.c;
+    const int nw = (int)(c.L / W);
+    constexpr int R = 4;
+    for (int64_t r0 = t0; r0 < j.rows; r0 += nthr * R) {
+        int64_t lo[R], po[R];
+        bool ok[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const int64_t r = r0 + q * nthr;
+            ok[q] = r < j.rows;
+            lo[q] = ok[q] ? chain_row(c, r) : 0;
+            po[q] = r * c.L;
+        }
+        for (int w = 0; w < nw; ++w) {
+            T v[R];
+#pragma unroll
+            for (int q = 0; q < R; ++q)
+                if (ok[q])
+                    v[q] = *reinterpret_cast<const T*>(j.src + (PACK ? lo[q] : po[q]) + w * W);
+#pragma unroll
+            for (int q = 0; q < R; ++q)
+                if (ok[q]) *reinterpret_cast<T*>(j.dst + (PACK ? po[q] : lo[q]) + w * W) = v[q];
+        }
     }
 }
 
@@ -83,12 +177,22 @@ __global__ void __launch_bounds__(kChainThreads) k_chain(const ChainBatch b) {
     while (ji + 1 < b.njobs && (int)blockIdx.x >= b.job[ji + 1].blk0) ++ji;
     const ChainJob& j = b.job[ji];
     const int64_t blk = blockIdx.x - j.blk0;
-    switch (j.w) {
-    case 16: chain_job_body<16, PACK>(j, blk, j.nblk); break;
-    case 8: chain_job_body<8, PACK>(j, blk, j.nblk); break;
-    case 4: chain_job_body<4, PACK>(j, blk, j.nblk); break;
-    case 2: chain_job_body<2, PACK>(j, blk, j.nblk); break;
-    default: chain_job_body<1, PACK>(j, blk, j.nblk); break;
+    if (j.mode == CHAIN_ROW) {
+        chain_rows<PACK>(j, blk * (kChainThreads / 32) + (threadIdx.x >> 5),
+                         (int64_t)j.nblk * (kChainThreads / 32));
+    } else {
+        const int64_t t0 = blk * kChainThreads + threadIdx.x, nthr = (int64_t)j.nblk * kChainThreads;
+        switch (j.w) {
+        case 16: chain_elems<16, PACK>(j, t0, nthr); break;
+        case 8: chain_elems<8, PACK>(j, t0, nthr); break;
+        case 4: chain_elems<4, PACK>(j, t0, nthr); break;
+        case 2: chain_elems<2, PACK>(j, t0, nthr); break;
+        default: chain_elems<1, PACK>(j, t0, nthr); break;
+        }
+    }
+    // unpack with data ending inside a row: bytewise tail
+    if (!PACK && blk == 0 && threadIdx.x == 0) {
+        for (int64_t P = j.rows * j.c.L; P < j.limit; ++P) j.dst[chain_off(j.c, P)] = j.src[P];
     }
 }
 
@@ -201,22 +305,37 @@ int sm_count(int device) {
 
 }  // namespace
 
-int chain_word(const Plan& p, const void* a, const void* b) {
+void chain_setup(const Plan& p, bool pack, ChainJob* j) {
+    const Chain& c = p.chain;
+    const uint8_t* layout_ptr = pack ? j->src : j->dst;
+    const uint8_t* packed_ptr = pack ? j->dst : j->src;
+    j->rows = j->limit / c.L;
+    const bool packed_aligned = (reinterpret_cast<uintptr_t>(packed_ptr) & 15) == 0;
+    if (c.L >= 64 && (c.L & 15) == 0 && packed_aligned) {
+        j->mode = CHAIN_ROW;
+        j->w = 16;
+        return;
+    }
     int64_t w = p.chain_align;
-    const uintptr_t m = reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b);
+    const uintptr_t m = reinterpret_cast<uintptr_t>(layout_ptr) | reinterpret_cast<uintptr_t>(packed_ptr);
     while (w > 1 && (m & (uintptr_t)(w - 1))) w >>= 1;
-    return (int)w;
+    j->mode = CHAIN_ELEM;
+    j->w = (int32_t)w;
 }
 
 cudaError_t launch_chain_batch(ChainBatch& b, bool pack, int device, cudaStream_t stream) {
     if (b.njobs == 0) return cudaSuccess;
-    // blocks per job proportional to words, capped so one wave of the batch
-    // covers ~8 CTAs per SM
+    (void)pack;
+    // Blocks per job proportional to the DRAM sectors it touches (a run
+    // shorter than a sector still costs one), ~64 KiB of sector traffic per
+    // block, capped at 8 CTAs per SM per job.
     const int64_t cap = (int64_t)sm_count(device) * 8;
     int64_t total = 0;
     for (int i = 0; i < b.njobs; ++i) {
         ChainJob& j = b.job[i];
-        const int64_t want = (j.nwords + (int64_t)kChainThreads * kUnroll - 1) / ((int64_t)kChainThreads * kUnroll);
+        const int64_t per_row = ((j.c.L + 31) / 32 + 1) * 32;
+        const int64_t work = j.rows * per_row;
+        const int64_t want = (work + (64 << 10) - 1) / (64 << 10);
         j.nblk = (int32_t)std::max<int64_t>(1, std::min<int64_t>(want, cap));
         j.blk0 = (int32_t)total;
         total += j.nblk;

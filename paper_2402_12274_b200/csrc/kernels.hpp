@@ -12,16 +12,18 @@ namespace mpx {
 
 constexpr int kMaxJobs = 16;
 
+enum ChainMode : int32_t { CHAIN_ELEM = 0, CHAIN_ROW = 1 };
+
 struct ChainJob {
     Chain c;
     const uint8_t* src;
     uint8_t* dst;
-    int64_t nwords;   // whole W-byte words to move
-    int64_t limit;    // packed bytes to move (unpack may stop mid-word)
-    int32_t w;        // word width in bytes
+    int64_t rows;     // whole rows moved by the main path
+    int64_t limit;    // packed bytes to move (unpack may stop mid-row: bytewise tail)
+    int32_t w;        // element mode: word width in bytes
+    int32_t mode;     // CHAIN_ELEM: thread per row; CHAIN_ROW: warp per row, 16 B + funnel
     int32_t blk0;     // first block of this job (filled by the launcher)
     int32_t nblk;     // blocks of this job (filled by the launcher)
-    int32_t pad;
 };
 
 struct ChainBatch {
@@ -30,8 +32,8 @@ struct ChainBatch {
     ChainJob job[kMaxJobs];
 };
 
-// widest word (<= plan alignment) that both pointers are aligned to
-int chain_word(const Plan& p, const void* a, const void* b);
+// fill mode / word width / row counts of a chain job from its plan and pointers
+void chain_setup(const Plan& p, bool pack, ChainJob* j);
 
 cudaError_t launch_chain_batch(ChainBatch& b, bool pack, int device, cudaStream_t stream);
 cudaError_t launch_generic(const Plan& p, bool pack, const uint8_t* src, uint8_t* dst, int64_t limit,

@@ -140,7 +140,15 @@ void analyze(const Node* layout, Plan* p) {
         c.L = n->len;
         align = std::min(align, pow2_div(c.L));
         align = std::min(align, pow2_div(c.base));
-        for (int i = 0; i < c.depth; ++i) host_magic((uint64_t)c.cnt[i], &c.m_cnt[i], &c.s_cnt[i]);
+        int64_t rows = 1;
+        bool small = true;
+        for (int i = 0; i < c.depth; ++i) {
+            host_magic((uint64_t)c.cnt[i], &c.m_cnt[i], &c.s_cnt[i]);
+            rows *= c.cnt[i];
+            small = small && c.cnt[i] < (int64_t(1) << 31);
+            if (c.cnt[i] < (int64_t(1) << 31)) host_magic32((uint32_t)c.cnt[i], &c.m32_cnt[i], &c.s32_cnt[i]);
+        }
+        c.small = small && rows < (int64_t(1) << 31);
         host_magic((uint64_t)c.L, &c.m_L, &c.s_L);
         p->kind = PLAN_CHAIN;
         p->chain = c;
