@@ -45,6 +45,12 @@ int mpx_abi_version(void);
 /* thread-local message of the last failing call */
 const char *mpx_last_error(void);
 
+/* Device tuning: L2 fetch granularity (cudaLimitMaxL2FetchGranularity,
+ * 0/32/64/128 bytes) for the calling process on `device`.  Sparse layouts
+ * (single-element halo faces) read 32 B sectors; a larger fetch size would
+ * drag in bytes that are never used.  Returns the previous value in *prev. */
+int mpx_device_set_l2_fetch(int device, int bytes, int *prev);
+
 /* ---- datatype constructors (datatype.py:444-610) ------------------------ */
 /* builtins: datatype.py:410-422 */
 int mpx_type_builtin(int which, mpx_datatype *out);

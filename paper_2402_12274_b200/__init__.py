@@ -19,7 +19,7 @@ from .datatypes import (  # noqa: F401
     type_indexed, type_create_struct, type_create_subarray,
     type_create_resized, type_commit, type_free, type_iov_len, type_iov,
     type_iov_tensor, pack, pack_into, unpack, pack_multi, unpack_multi,
-    packed_size, check_region, parse_type_expr,
+    packed_size, check_region, parse_type_expr, set_l2_fetch_granularity,
 )
 
 ANY_SOURCE = -1

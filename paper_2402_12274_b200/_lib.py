@@ -2,7 +2,7 @@
 
 The product has no CPU fallback: if libmpx.so is missing or fails to load,
 importing the package raises immediately.  Build it with
-``python -m paper_2402_12274_b200.build``.
+``python paper_2402_12274_b200/build.py``.
 """
 
 import ctypes
@@ -16,7 +16,7 @@ SO_PATH = os.path.join(_HERE, "libmpx.so")
 if not os.path.exists(SO_PATH):
     raise ImportError(
         "libmpx.so not found at %s -- build it with "
-        "`python -m paper_2402_12274_b200.build` (no CPU fallback exists)" % SO_PATH)
+        "`python paper_2402_12274_b200/build.py` (no CPU fallback exists)" % SO_PATH)
 
 # torch first: it loads the CUDA runtime / NCCL this library talks to
 import torch  # noqa: E402,F401
@@ -34,6 +34,7 @@ pdt = ctypes.POINTER(ctypes.c_void_p)
 _SIGS = {
     "mpx_abi_version": ([], cint),
     "mpx_last_error": ([], ctypes.c_char_p),
+    "mpx_device_set_l2_fetch": ([cint, cint, ctypes.POINTER(cint)], cint),
     "mpx_type_builtin": ([cint, pdt], cint),
     "mpx_type_contiguous": ([i64, dt_t, pdt], cint),
     "mpx_type_vector": ([i64, i64, i64, dt_t, pdt], cint),

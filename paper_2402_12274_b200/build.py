@@ -1,6 +1,6 @@
 """Build libmpx.so in-tree with nvcc for sm_100a.
 
-    python -m paper_2402_12274_b200.build [--force]
+    python paper_2402_12274_b200/build.py [--force] [-v]
 
 One shared library from csrc/*.cu + csrc/*.cpp, static cudart, -lineinfo so
 ncu's source page maps to the kernels.  The .so is git-ignored but travels to

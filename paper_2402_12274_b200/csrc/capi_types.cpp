@@ -201,6 +201,20 @@ int mpx_abi_version(void) { return 1; }
 
 const char* mpx_last_error(void) { return g_last_error.c_str(); }
 
+int mpx_device_set_l2_fetch(int device, int bytes, int* prev) {
+    int rc = ensure_device(device);
+    if (rc) return rc;
+    size_t old = 0;
+    cudaError_t e = cudaDeviceGetLimit(&old, cudaLimitMaxL2FetchGranularity);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetLimit");
+    if (prev) *prev = (int)old;
+    if (bytes >= 0) {
+        e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)bytes);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceSetLimit(L2 fetch)");
+    }
+    return MPX_SUCCESS;
+}
+
 int mpx_type_builtin(int which, mpx_datatype* out) {
     Datatype* d = builtin(which);
     if (!d || !out) return fail(MPX_ERR_ARG, "unknown builtin %d", which);

@@ -92,6 +92,7 @@ __device__ __forceinline__ void store_partial16(uint8_t* p, const uint4& v, int 
 // the two partial chunks at the ends of an unpacked row.
 template <bool PACK>
 __device__ __forceinline__ void chain_rows(const ChainJob& j, int64_t warp0, int64_t nwarps) {
+    constexpr int U = 4;   // 16-byte chunks in flight per lane
     const int lane = threadIdx.x & 31;
     const Chain& c = j.c;
     const int nch = (int)(c.L >> 4);
@@ -102,16 +103,27 @@ __device__ __forceinline__ void chain_rows(const ChainJob& j, int64_t warp0, int
             const int a = (int)(reinterpret_cast<uintptr_t>(srow) & 15);
             const uint4* s16 = reinterpret_cast<const uint4*>(srow - a);
             uint4* d16 = reinterpret_cast<uint4*>(j.dst + r * c.L);
-            for (int k0 = 0; k0 < nch; k0 += 32) {
-                const int k = k0 + lane;
-                uint4 c0 = make_uint4(0, 0, 0, 0);
-                if (k < nch) c0 = __ldg(s16 + k);
-                if (a) {
-                    uint4 c1 = shfl_down16(c0, 1);
-                    if (k < nch && (lane == 31 || k + 1 == nch)) c1 = __ldg(s16 + k + 1);
-                    c0 = funnel16(c0, c1, a);
+            for (int k0 = 0; k0 < nch; k0 += 32 * U) {
+                uint4 v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = k0 + 32 * u + lane;
+                    v[u] = k < nch ? __ldg(s16 + k) : make_uint4(0, 0, 0, 0);
                 }
-                if (k < nch) d16[k] = c0;
+                if (a) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int k = k0 + 32 * u + lane;
+                        uint4 c1 = shfl_down16(v[u], 1);
+                        if (k < nch && (lane == 31 || k + 1 == nch)) c1 = __ldg(s16 + k + 1);
+                        v[u] = funnel16(v[u], c1, a);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = k0 + 32 * u + lane;
+                    if (k < nch) d16[k] = v[u];
+                }
             }
         } else {
             const uint4* p16 = reinterpret_cast<const uint4*>(j.src + r * c.L);
@@ -120,21 +132,32 @@ __device__ __forceinline__ void chain_rows(const ChainJob& j, int64_t warp0, int
             uint8_t* d16 = drow - a;
             const int nout = a ? nch + 1 : nch;
             uint4 carry = make_uint4(0, 0, 0, 0);
-            for (int k0 = 0; k0 < nout; k0 += 32) {
-                const int k = k0 + lane;
-                uint4 cur = make_uint4(0, 0, 0, 0);
-                if (k < nch) cur = __ldg(p16 + k);
+            for (int k0 = 0; k0 < nout; k0 += 32 * U) {
+                uint4 v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = k0 + 32 * u + lane;
+                    v[u] = k < nch ? __ldg(p16 + k) : make_uint4(0, 0, 0, 0);
+                }
                 if (a == 0) {
-                    if (k < nch) reinterpret_cast<uint4*>(d16)[k] = cur;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int k = k0 + 32 * u + lane;
+                        if (k < nch) reinterpret_cast<uint4*>(d16)[k] = v[u];
+                    }
                     continue;
                 }
-                uint4 prev = shfl_up16(cur, 1);
-                if (lane == 0) prev = carry;
-                carry = shfl16(cur, 31);
-                const uint4 out = funnel16(prev, cur, 16 - a);
-                if (k == 0) store_partial16(d16, out, a, 16);
-                else if (k == nch) store_partial16(d16 + 16 * (int64_t)k, out, 0, a);
-                else if (k < nch) reinterpret_cast<uint4*>(d16)[k] = out;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = k0 + 32 * u + lane;
+                    uint4 prev = shfl_up16(v[u], 1);
+                    if (lane == 0) prev = carry;
+                    carry = shfl16(v[u], 31);
+                    const uint4 out = funnel16(prev, v[u], 16 - a);
+                    if (k == 0) store_partial16(d16, out, a, 16);
+                    else if (k == nch) store_partial16(d16 + 16 * (int64_t)k, out, 0, a);
+                    else if (k < nch) reinterpret_cast<uint4*>(d16)[k] = out;
+                }
             }
         }
     }
@@ -326,16 +349,15 @@ void chain_setup(const Plan& p, bool pack, ChainJob* j) {
 cudaError_t launch_chain_batch(ChainBatch& b, bool pack, int device, cudaStream_t stream) {
     if (b.njobs == 0) return cudaSuccess;
     (void)pack;
-    // Blocks per job proportional to the DRAM sectors it touches (a run
-    // shorter than a sector still costs one), ~64 KiB of sector traffic per
-    // block, capped at 8 CTAs per SM per job.
+    // Enough CTAs that every row gets its own warp (row mode, <= 2 KiB per
+    // warp pass) or its own thread (element mode) up to 8 CTAs per SM per
+    // job; bigger jobs loop (grid-stride) with 4 rows / 4 chunks in flight.
     const int64_t cap = (int64_t)sm_count(device) * 8;
     int64_t total = 0;
     for (int i = 0; i < b.njobs; ++i) {
         ChainJob& j = b.job[i];
-        const int64_t per_row = ((j.c.L + 31) / 32 + 1) * 32;
-        const int64_t work = j.rows * per_row;
-        const int64_t want = (work + (64 << 10) - 1) / (64 << 10);
+        const int64_t per_blk = j.mode == CHAIN_ROW ? kChainThreads / 32 : kChainThreads;
+        const int64_t want = (j.rows + per_blk - 1) / per_blk;
         j.nblk = (int32_t)std::max<int64_t>(1, std::min<int64_t>(want, cap));
         j.blk0 = (int32_t)total;
         total += j.nblk;

@@ -534,6 +534,15 @@ def check_region(d, buf, count=1, writable=False):
                            % (q["max_end"], size))
 
 
+def set_l2_fetch_granularity(nbytes, device=None):
+    """Set cudaLimitMaxL2FetchGranularity (bytes) on a device; returns the
+    previous value.  nbytes = -1 only queries."""
+    dev = torch.cuda.current_device() if device is None else torch.device(device).index or 0
+    prev = ctypes.c_int()
+    check(lib.mpx_device_set_l2_fetch(dev, nbytes, ctypes.byref(prev)))
+    return prev.value
+
+
 # ------------------------------------------------------- type expressions
 
 _EXPR = {

@@ -52,8 +52,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--cfg3", action="store_true")
+    ap.add_argument("--l2fetch", type=int, default=-1)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
+    torch.cuda.init()
+    prev = mp.set_l2_fetch_granularity(args.l2fetch, dev)
+    print(json.dumps({"l2_fetch_prev": prev, "l2_fetch_now": mp.set_l2_fetch_granularity(-1, dev)}))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     cases = [("cfg1", CFG1_SPEC, 32768 * 8)]
     cases += [("cfg2-" + n, s, 514 ** 3 * 4) for n, s in cfg2_faces()]
