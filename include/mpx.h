@@ -126,6 +126,69 @@ int mpx_unpack_multi(int n, const mpx_datatype *dts, const int64_t *counts,
                      const void *const *srcs, const int64_t *src_bytes,
                      void *const *dsts, const int64_t *dst_bytes, void *stream);
 
+/* ---- worlds, stream communicators, enqueue (offload.py, comm.py) ------------
+ * A world is one job of `size` ranks hosted in this process (one host thread
+ * per rank, each rank bound to a CUDA device; ranks may share a device) --
+ * the B200 counterpart of the reference's in-process fabric
+ * (transport.py:653-715, tests/_twin.py:15-58).  A stream communicator binds
+ * one rank to a cudaStream_t (comm.py:619-648 with runtime.py:173-188's
+ * "cudaStream_t" branch implemented).  Enqueue operations are matched on the
+ * host at call time with MPI rules and ordered on the device with events and
+ * stream memory operations only: no host synchronisation, no spinning
+ * kernels. */
+typedef struct mpx_world_s *mpx_world;
+typedef struct mpx_comm_s *mpx_comm;
+typedef struct mpx_request_s *mpx_request;
+
+#define MPX_ANY_SOURCE (-1)
+#define MPX_ANY_TAG    (-1)
+
+/* InProcFabric.join (transport.py:653-715): create or join the named world. */
+int mpx_world_join(const char *group, int size, int rank, int device,
+                   int64_t eager_limit, mpx_world *out);
+/* Instance.finalize counterpart: the last rank to leave destroys the world. */
+int mpx_world_leave(mpx_world w, int rank);
+/* stream_comm_create (comm.py:619-648) for one rank: stream = cudaStream_t */
+int mpx_comm_create(mpx_world w, int rank, int context_id, void *stream, mpx_comm *out);
+/* comm_free (comm.py:178-190): ERR_PENDING while requests are outstanding */
+int mpx_comm_free(mpx_comm c);
+/* send_enqueue / recv_enqueue (offload.py:184-195).  buf_bytes = size of the
+ * buffer (bounds check, datatype.py:680-692 / p2p.py:63-64). */
+int mpx_send_enqueue(mpx_comm c, const void *buf, int64_t buf_bytes, int64_t count,
+                     mpx_datatype dt, int dest, int tag);
+int mpx_recv_enqueue(mpx_comm c, void *buf, int64_t buf_bytes, int64_t count,
+                     mpx_datatype dt, int source, int tag);
+/* isend_enqueue / irecv_enqueue (offload.py:198-227): initiation only */
+int mpx_isend_enqueue(mpx_comm c, const void *buf, int64_t buf_bytes, int64_t count,
+                      mpx_datatype dt, int dest, int tag, mpx_request *out);
+int mpx_irecv_enqueue(mpx_comm c, void *buf, int64_t buf_bytes, int64_t count,
+                      mpx_datatype dt, int source, int tag, mpx_request *out);
+/* wait_enqueue / waitall_enqueue (offload.py:241-268): completion is placed on
+ * the request's stream; waitall requires one stream (ERR_ARG otherwise). */
+int mpx_wait_enqueue(mpx_request r);
+int mpx_waitall_enqueue(int n, const mpx_request *rs);
+/* status of a request (transport.py:605-621): out[0..4] = matched, source,
+ * tag, count (elements of the request's datatype), error code (MPX_*).
+ * Valid once the request's stream has passed its wait. */
+int mpx_request_status(mpx_request r, int64_t out[5]);
+int mpx_request_free(mpx_request r);
+/* allreduce (comm.py:560-595) as a stream operation: SUM over
+ * MPX_INT32/INT64/FLOAT32/FLOAT64; algo 0 = auto, 1 = native rank-ordered
+ * one-shot kernel (bit-identical to the reference order x0+x1+...), 2 = NCCL */
+#define MPX_OP_SUM 0
+int mpx_allreduce_enqueue(mpx_comm c, const void *sendbuf, void *recvbuf, int64_t count,
+                          int dtype_code, int op, int algo);
+/* DeviceQueue.synchronize (offload.py:111-119): stream sync, then return the
+ * first deferred error (and clear it); its message via mpx_last_error(). */
+int mpx_comm_synchronize(mpx_comm c);
+/* explicit progress (runtime.py:141-146): reclaim staging buffers and events
+ * of completed operations; never blocks.  *outstanding = live requests. */
+int mpx_comm_progress(mpx_comm c, int64_t *outstanding);
+/* device owning a cudaStream_t (for wrapping a raw handle from an Info) */
+int mpx_stream_device(void *stream, int *device);
+/* optional: path of libnccl.so.2 when it is not already loaded */
+int mpx_nccl_load(const char *path);
+
 #ifdef __cplusplus
 }
 #endif

@@ -55,6 +55,23 @@ _SIGS = {
     "mpx_unpack": ([dt_t, i64, vp, i64, vp, i64, p64, vp], cint),
     "mpx_pack_multi": ([cint, pdt, p64, pvp, p64, pvp, p64, vp], cint),
     "mpx_unpack_multi": ([cint, pdt, p64, pvp, p64, pvp, p64, vp], cint),
+    "mpx_world_join": ([ctypes.c_char_p, cint, cint, cint, i64, pvp], cint),
+    "mpx_world_leave": ([vp, cint], cint),
+    "mpx_comm_create": ([vp, cint, cint, vp, pvp], cint),
+    "mpx_comm_free": ([vp], cint),
+    "mpx_send_enqueue": ([vp, vp, i64, i64, dt_t, cint, cint], cint),
+    "mpx_recv_enqueue": ([vp, vp, i64, i64, dt_t, cint, cint], cint),
+    "mpx_isend_enqueue": ([vp, vp, i64, i64, dt_t, cint, cint, pvp], cint),
+    "mpx_irecv_enqueue": ([vp, vp, i64, i64, dt_t, cint, cint, pvp], cint),
+    "mpx_wait_enqueue": ([vp], cint),
+    "mpx_waitall_enqueue": ([cint, pvp], cint),
+    "mpx_request_status": ([vp, p64], cint),
+    "mpx_request_free": ([vp], cint),
+    "mpx_allreduce_enqueue": ([vp, vp, vp, i64, cint, cint, cint], cint),
+    "mpx_comm_synchronize": ([vp], cint),
+    "mpx_comm_progress": ([vp, p64], cint),
+    "mpx_stream_device": ([vp, ctypes.POINTER(cint)], cint),
+    "mpx_nccl_load": ([ctypes.c_char_p], cint),
 }
 
 for _name, (_args, _res) in _SIGS.items():

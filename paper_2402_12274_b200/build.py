@@ -64,7 +64,7 @@ def build(force=False, verbose=False):
     if failed:
         raise RuntimeError("libmpx build failed")
     link = [NVCC] + ARCH + ["-shared", "-o", SO + ".tmp"] + objs + \
-        ["-lcuda", "-ldl", "-lpthread", "-lrt"]
+        ["-ldl", "-lpthread", "-lrt"]
     subprocess.check_call(link)
     os.replace(SO + ".tmp", SO)
     return SO

@@ -32,4 +32,14 @@ int movement(int n, const mpx_datatype* dts, const int64_t* counts, const void* 
              const int64_t* src_bytes, void* const* dsts, const int64_t* dst_bytes, bool pack,
              cudaStream_t stream, int64_t* written_out);
 
+// single pack/unpack of `limit` packed bytes executed on device `dev` (peer or
+// pinned-host pointers allowed)
+int launch_move(int dev, Datatype* d, int64_t count, bool pack, const void* src, void* dst, int64_t limit,
+                cudaStream_t stream);
+// layout_for(count) is one run -> its offset
+bool contiguous_run(Datatype* d, int64_t count, int64_t* off);
+// count / usability / bounds checks of a typed buffer of `bytes` bytes
+int check_layout_region(Datatype* d, int64_t count, int64_t bytes);
+int set_device(int dev);
+
 }  // namespace mpx

@@ -482,7 +482,8 @@ int mpx_type_iov(mpx_datatype h, int64_t count, int64_t iov_offset, int64_t max_
     std::string err;
     auto plan = get_plan(d, count, dev, (cudaStream_t)stream, &err);
     if (!plan) return fail(MPX_ERR_OTHER, "%s", err.c_str());
-    cudaError_t e = launch_iov(*plan, iov_offset, n, dev_pairs, (cudaStream_t)stream);
+    cudaError_t e = plan_wait(*plan, (cudaStream_t)stream);
+    if (e == cudaSuccess) e = launch_iov(*plan, iov_offset, n, dev_pairs, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "iov launch");
     *n_out = n;
     return MPX_SUCCESS;
@@ -491,6 +492,63 @@ int mpx_type_iov(mpx_datatype h, int64_t count, int64_t iov_offset, int64_t max_
 }  // extern "C"
 
 namespace mpx {
+
+// Launch one pack (layout src -> packed dst) or unpack (packed src -> layout
+// dst) of limit packed bytes on `stream` of device `dev`.  Either pointer may
+// be a peer-device or pinned-host address (the caller enabled access).
+int launch_move(int dev, Datatype* d, int64_t count, bool pack, const void* src, void* dst, int64_t limit,
+                cudaStream_t stream) {
+    if (limit <= 0) return MPX_SUCCESS;
+    int rc = ensure_device(dev);
+    if (rc) return rc;
+    std::string err;
+    auto plan = get_plan(d, count, dev, stream, &err);
+    if (!plan) return fail(MPX_ERR_OTHER, "%s", err.c_str());
+    if (plan->kind == PLAN_EMPTY) return MPX_SUCCESS;
+    cudaError_t e = plan_wait(*plan, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "descriptor wait");
+    if (plan->kind == PLAN_CHAIN && !(!pack && plan->overlap)) {
+        ChainBatch b;
+        b.njobs = 1;
+        ChainJob& j = b.job[0];
+        j.c = plan->chain;
+        j.src = static_cast<const uint8_t*>(src);
+        j.dst = static_cast<uint8_t*>(dst);
+        j.limit = limit;
+        chain_setup(*plan, pack, &j);
+        e = launch_chain_batch(b, pack, dev, stream);
+    } else {
+        e = launch_generic(*plan, pack, static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), limit,
+                           stream);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "pack/unpack launch");
+    return MPX_SUCCESS;
+}
+
+// contiguous layout_for(count)?  -> offset of its single run
+bool contiguous_run(Datatype* d, int64_t count, int64_t* off) {
+    NodeP lay = d->layout_for(count);
+    if (lay->kind == Kind::Run) {
+        *off = lay->off;
+        return true;
+    }
+    return false;
+}
+
+int check_layout_region(Datatype* d, int64_t count, int64_t bytes) {
+    int rc = check_count(count, "count");
+    if (rc || (rc = check_usable(d, "pack/unpack"))) return rc;
+    NodeP lay = d->layout_for(count);
+    if (lay->runs) {
+        if (lay->min_off < 0) return fail(MPX_ERR_ARG, "layout reaches before the start of the buffer");
+        if (lay->max_end > bytes)
+            return fail(MPX_ERR_ARG, "buffer too small: layout spans %lld bytes, buffer has %lld",
+                        (long long)lay->max_end, (long long)bytes);
+    }
+    return MPX_SUCCESS;
+}
+
+int set_device(int dev) { return ensure_device(dev); }
 
 // one pack or unpack, possibly fused with others of the same direction
 int movement(int n, const mpx_datatype* dts, const int64_t* counts, const void* const* srcs,
@@ -521,6 +579,10 @@ int movement(int n, const mpx_datatype* dts, const int64_t* counts, const void* 
         }
         if (written_out) written_out[i] = limit;
         if (!plan || limit == 0) continue;
+        {
+            cudaError_t we = plan_wait(*plan, stream);
+            if (we != cudaSuccess) return cuda_fail(we, "descriptor wait");
+        }
         const uint8_t* s = static_cast<const uint8_t*>(srcs[i]);
         uint8_t* t = static_cast<uint8_t*>(dsts[i]);
         if (plan->kind == PLAN_CHAIN && !(!pack && plan->overlap)) {

@@ -1,0 +1,26 @@
+// coll.hpp -- native stream-ordered allreduce (rank-ordered one-shot kernel).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace mpx {
+
+constexpr int kMaxCollRanks = 64;
+
+// per-call pointer table in pinned host memory, filled by each rank's host
+// thread before its "arrived" flag is written
+struct CollTable {
+    const void* send[kMaxCollRanks];
+    void* recv[kMaxCollRanks];
+};
+
+// Rank `rank` of `n` reduces its 1/n slice of the buffers: out = x0 + x1 + ...
+// + x(n-1) in rank order (comm.py:582-588), accumulated in double for float
+// types and in wrapping unsigned arithmetic for integers, and writes the
+// result into every rank's receive buffer (peer stores over NVLink).
+cudaError_t launch_allreduce_oneshot(const CollTable* table, int n, int rank, int64_t count, int dtype_code,
+                                     int device, cudaStream_t stream);
+
+}  // namespace mpx

@@ -1,0 +1,914 @@
+// enqueue.cpp -- stream-ordered point-to-point and allreduce engine.
+//
+// B200 counterpart of the reference's offload path
+// (/root/reference/pkg/src/minimpi/offload.py:49-304, p2p.py:84-185,
+// transport.py:313-602): the DeviceQueue executor thread becomes the caller's
+// cudaStream_t, the eager/rendezvous frame protocol becomes device-side
+// ordering between the two ranks' streams, and the payload moves with the
+// pack/unpack kernels over peer (NVLink) or local pointers.
+//
+// Matching happens on the host when an operation is enqueued, with MPI rules
+// (context, source incl. ANY_SOURCE, tag incl. ANY_TAG, FIFO per channel,
+// transport.py:191-201,399-428), in a per-destination mailbox guarded by its
+// own mutex (no global lock on the data path).  Whichever side is enqueued
+// second knows both buffers and issues the transfer:
+//
+//   first side publishes an event recorded at its stream position (buffer
+//   ready) and, if it must wait for completion, a flag in pinned host memory
+//   waited on with cuStreamWaitValue32;
+//   second side waits for that event (cudaStreamWaitEvent), moves the data,
+//   and writes the flag with cuStreamWriteValue32.
+//
+// Eager (<= eager_limit bytes, and every self-send): the sender packs into a
+// staging buffer at its stream position and never waits, exactly like the
+// reference's eager frames (transport.py:355-375).  Rendezvous: a blocking
+// send waits until its data has been delivered (the reference's RTS/CTS wait).
+// Nonblocking forms run their deferred part on a per-communicator side stream
+// forked from the user stream, joined again by wait_enqueue.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "capi_common.hpp"
+#include "coll.hpp"
+#include "mpx.h"
+
+namespace mpx {
+
+namespace {
+
+// ------------------------------------------------------------------ flags
+// Completion flags live in pinned, mapped host memory (device address = host
+// address under UVA).  Slot values only grow, so a waiter on (slot, gen) with
+// GEQ is released by exactly the write of gen.
+class FlagPool {
+  public:
+    explicit FlagPool(size_t n) : n_(n), shadow_(n, 0) {}
+    int init() {
+        cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&base_), n_ * sizeof(uint32_t),
+                                      cudaHostAllocMapped | cudaHostAllocPortable);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc(flags)");
+        std::fill(base_, base_ + n_, 0u);
+        return MPX_SUCCESS;
+    }
+    ~FlagPool() {
+        if (base_) cudaFreeHost(base_);
+    }
+    void take(uint32_t** addr, uint32_t* gen) {
+        std::lock_guard<std::mutex> g(mu_);
+        const size_t i = next_++ % n_;
+        *addr = base_ + i;
+        *gen = ++shadow_[i];
+    }
+
+  private:
+    std::mutex mu_;
+    size_t n_, next_ = 0;
+    uint32_t* base_ = nullptr;
+    std::vector<uint32_t> shadow_;
+};
+
+// Driver-API stream memory operations, resolved through the runtime so the
+// library does not link libcuda (it must load on GPU-less hosts).
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WriteValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using ErrStrFn = CUresult (*)(CUresult, const char**);
+
+struct MemOps {
+    WaitValueFn wait = nullptr;
+    WriteValueFn write = nullptr;
+    ErrStrFn err = nullptr;
+};
+
+const MemOps& memops() {
+    static MemOps m = [] {
+        MemOps r;
+        cudaDriverEntryPointQueryResult q;
+        cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", reinterpret_cast<void**>(&r.wait), 12000,
+                                         cudaEnableDefault, &q);
+        cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", reinterpret_cast<void**>(&r.write), 12000,
+                                         cudaEnableDefault, &q);
+        cudaGetDriverEntryPointByVersion("cuGetErrorString", reinterpret_cast<void**>(&r.err), 6000,
+                                         cudaEnableDefault, &q);
+        cudaGetLastError();
+        return r;
+    }();
+    return m;
+}
+
+int memop_fail(CUresult r, const char* what) {
+    const char* m = nullptr;
+    if (memops().err) memops().err(r, &m);
+    return fail(MPX_ERR_OTHER, "%s: %s", what, m ? m : "driver error");
+}
+
+int wait_flag(cudaStream_t s, uint32_t* addr, uint32_t gen) {
+    if (!memops().wait) return fail(MPX_ERR_UNSUPPORTED, "cuStreamWaitValue32 unavailable");
+    CUresult r = memops().wait(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), gen,
+                               CU_STREAM_WAIT_VALUE_GEQ);
+    return r == CUDA_SUCCESS ? MPX_SUCCESS : memop_fail(r, "cuStreamWaitValue32");
+}
+
+int write_flag(cudaStream_t s, uint32_t* addr, uint32_t gen) {
+    if (!memops().write) return fail(MPX_ERR_UNSUPPORTED, "cuStreamWriteValue32 unavailable");
+    CUresult r = memops().write(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), gen,
+                                CU_STREAM_WRITE_VALUE_DEFAULT);
+    return r == CUDA_SUCCESS ? MPX_SUCCESS : memop_fail(r, "cuStreamWriteValue32");
+}
+
+#define MPX_CU(x)                                               \
+    do {                                                        \
+        cudaError_t e_ = (x);                                   \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #x);        \
+    } while (0)
+#define MPX_RC(x)                 \
+    do {                          \
+        int rc_ = (x);            \
+        if (rc_) return rc_;      \
+    } while (0)
+
+int record_new_event(cudaStream_t s, cudaEvent_t* ev) {
+    MPX_CU(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+    MPX_CU(cudaEventRecord(*ev, s));
+    return MPX_SUCCESS;
+}
+
+}  // namespace
+
+struct World;
+struct Comm;
+
+// Host-side completion record of a nonblocking operation (Request,
+// progress.py:34-60; EnqueuedRequest, offload.py:34-46).
+struct ReqState {
+    Comm* comm = nullptr;
+    bool is_send = false;
+    bool matched = false;     // host match done: status known
+    int source = -1, tag = -1;
+    int64_t count = 0;        // elements of this request's datatype
+    int err = MPX_SUCCESS;
+    // how the request's stream joins completion at wait_enqueue
+    uint32_t* flag = nullptr;  // wait flag >= gen (first side)
+    uint32_t gen = 0;
+    cudaEvent_t done_ev = nullptr;  // or wait this event (second side, side stream)
+    bool needs_wait = false;
+    bool waited = false;
+    std::mutex mu;
+};
+
+// one side of a message as known on the host
+struct Side {
+    int rank = 0, device = 0;
+    Comm* comm = nullptr;
+    Datatype* dt = nullptr;
+    int64_t count = 0;
+    void* buf = nullptr;
+    int64_t bytes = 0;        // send: message bytes; recv: capacity
+};
+
+struct PendingSend {
+    int ctx, src, tag;
+    Side s;
+    bool eager;
+    void* staging = nullptr;  // eager: packed copy (sender device)
+    cudaEvent_t ev = nullptr; // sender stream position (data ready / staged)
+    uint32_t* flag = nullptr; // rendezvous: delivered
+    uint32_t gen = 0;
+    std::shared_ptr<ReqState> req;
+};
+
+struct PendingRecv {
+    int ctx, src, tag;        // patterns
+    Side r;
+    cudaEvent_t ev = nullptr; // receiver stream position (buffer ready)
+    uint32_t* flag = nullptr; // delivered
+    uint32_t gen = 0;
+    bool blocking = false;
+    std::shared_ptr<ReqState> req;
+};
+
+struct Mailbox {
+    std::mutex mu;
+    std::deque<PendingSend> sends;  // unexpected (unmatched) sends to this rank
+    std::deque<PendingRecv> recvs;  // posted (unmatched) recvs of this rank
+};
+
+struct CollSlot {             // native allreduce rendezvous of one collective call
+    int arrived_host = 0;
+    CollTable* table = nullptr;   // pinned mapped: per-rank pointers
+    uint32_t* arrive = nullptr;   // pinned flags, one per rank (then finish flags)
+    uint32_t* finish = nullptr;
+    uint32_t gen = 1;
+    ~CollSlot() {
+        if (table) cudaFreeHost(table);
+        if (arrive) cudaFreeHost(arrive);
+    }
+};
+
+struct World {
+    std::string group;
+    int size = 0;
+    int64_t eager_limit = 65536;
+    std::vector<int> devices;
+    std::vector<bool> joined;
+    int live = 0;
+    std::vector<std::unique_ptr<Mailbox>> mbox;
+    FlagPool flags{1u << 20};
+    std::mutex peer_mu;
+    std::set<std::pair<int, int>> peer_on;
+    std::mutex coll_mu;
+    std::map<std::pair<int, int64_t>, std::shared_ptr<CollSlot>> colls;
+    std::mutex nccl_mu;
+    std::condition_variable nccl_cv;
+    std::vector<ncclComm_t> nccl;   // per rank, by ncclCommInitAll
+    int nccl_state = 0;             // 0 none, 1 building, 2 ready, -1 failed
+};
+
+struct Comm {
+    World* w = nullptr;
+    int rank = 0, ctx = 0, device = 0;
+    cudaStream_t stream = nullptr;  // the user's stream
+    cudaStream_t side = nullptr;    // internal, same device
+    std::mutex err_mu;
+    std::deque<std::pair<int, std::string>> deferred;
+    std::atomic<int64_t> outstanding{0};
+    int64_t coll_seq = 0;
+};
+
+namespace {
+
+std::mutex g_hold_mu;
+std::vector<std::pair<cudaEvent_t, std::shared_ptr<CollSlot>>> g_hold;
+std::mutex g_worlds_mu;
+std::map<std::string, World*> g_worlds;
+std::mutex g_handles_mu;
+std::set<const void*> g_comms;
+std::map<const void*, std::shared_ptr<ReqState>> g_reqs;
+
+Comm* comm_of(mpx_comm h) {
+    std::lock_guard<std::mutex> g(g_handles_mu);
+    auto* c = reinterpret_cast<Comm*>(h);
+    return g_comms.count(c) ? c : nullptr;
+}
+
+std::shared_ptr<ReqState> req_of(mpx_request h) {
+    std::lock_guard<std::mutex> g(g_handles_mu);
+    auto it = g_reqs.find(h);
+    return it == g_reqs.end() ? nullptr : it->second;
+}
+
+void defer_error(Comm* c, int code, const std::string& msg) {
+    std::lock_guard<std::mutex> g(c->err_mu);
+    c->deferred.emplace_back(code, msg);
+}
+
+// enable peer access both ways between two devices (idempotent)
+int ensure_peer(World* w, int a, int b) {
+    if (a == b) return MPX_SUCCESS;
+    std::lock_guard<std::mutex> g(w->peer_mu);
+    for (auto pr : {std::make_pair(a, b), std::make_pair(b, a)}) {
+        if (w->peer_on.count(pr)) continue;
+        int can = 0;
+        MPX_CU(cudaDeviceCanAccessPeer(&can, pr.first, pr.second));
+        if (!can) return fail(MPX_ERR_TRANSPORT, "device %d cannot access device %d", pr.first, pr.second);
+        MPX_RC(set_device(pr.first));
+        cudaError_t e = cudaDeviceEnablePeerAccess(pr.second, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+        // staging from the default pool of pr.second must be readable from pr.first
+        cudaMemPool_t pool;
+        MPX_CU(cudaDeviceGetDefaultMemPool(&pool, pr.second));
+        cudaMemAccessDesc d{};
+        d.location.type = cudaMemLocationTypeDevice;
+        d.location.id = pr.first;
+        d.flags = cudaMemAccessFlagsProtReadWrite;
+        MPX_CU(cudaMemPoolSetAccess(pool, &d, 1));
+        w->peer_on.insert(pr);
+    }
+    return MPX_SUCCESS;
+}
+
+bool matches(int pat_src, int pat_tag, int ctx, int src, int tag, int mctx) {
+    return ctx == mctx && (pat_src == MPX_ANY_SOURCE || pat_src == src) &&
+           (pat_tag == MPX_ANY_TAG || pat_tag == tag);
+}
+
+// Move min(send bytes, recv capacity) packed bytes from the send layout to
+// the recv layout, executed on `st` (device `dev`).  copy_between semantics
+// (datatype.py:760-797) with a contiguous side used in place and a packed
+// staging buffer otherwise.
+int transfer(int dev, cudaStream_t st, const Side& s, const Side& r, int64_t moved) {
+    if (moved <= 0) return MPX_SUCCESS;
+    int64_t off = 0;
+    if (contiguous_run(s.dt, s.count, &off))
+        return launch_move(dev, r.dt, r.count, false, static_cast<uint8_t*>(s.buf) + off, r.buf, moved, st);
+    if (moved == s.bytes && contiguous_run(r.dt, r.count, &off))
+        return launch_move(dev, s.dt, s.count, true, s.buf, static_cast<uint8_t*>(r.buf) + off, s.bytes, st);
+    MPX_RC(set_device(dev));
+    void* tmp = nullptr;
+    MPX_CU(cudaMallocAsync(&tmp, (size_t)s.bytes, st));
+    MPX_RC(launch_move(dev, s.dt, s.count, true, s.buf, tmp, s.bytes, st));
+    MPX_RC(launch_move(dev, r.dt, r.count, false, tmp, r.buf, moved, st));
+    MPX_CU(cudaFreeAsync(tmp, st));
+    return MPX_SUCCESS;
+}
+
+void fill_status(const std::shared_ptr<ReqState>& q, const Side& mine, int src, int tag, int64_t moved,
+                 bool trunc) {
+    if (!q) return;
+    std::lock_guard<std::mutex> g(q->mu);
+    q->matched = true;
+    q->source = src;
+    q->tag = tag;
+    const int64_t sz = mine.dt->size;
+    q->count = sz ? moved / sz : 0;
+    q->err = trunc ? MPX_ERR_TRUNCATE : MPX_SUCCESS;
+}
+
+// Eager send: pack at the sender's stream position into a staging buffer.
+int stage_send(Comm* c, PendingSend& ps) {
+    MPX_RC(set_device(c->device));
+    MPX_CU(cudaMallocAsync(&ps.staging, (size_t)std::max<int64_t>(ps.s.bytes, 1), c->stream));
+    MPX_RC(launch_move(c->device, ps.s.dt, ps.s.count, true, ps.s.buf, ps.staging, ps.s.bytes, c->stream));
+    return MPX_SUCCESS;
+}
+
+// Consume an eager staging buffer on stream `st` (device of st = `dev`):
+// unpack into the receiver, then free the staging on the owner's side stream.
+int consume_staging(int dev, cudaStream_t st, Comm* owner, const PendingSend& ps, const Side& r, int64_t moved) {
+    MPX_RC(launch_move(dev, r.dt, r.count, false, ps.staging, r.buf, moved, st));
+    cudaEvent_t used;
+    MPX_RC(record_new_event(st, &used));
+    MPX_RC(set_device(owner->device));
+    MPX_CU(cudaStreamWaitEvent(owner->side, used, 0));
+    MPX_CU(cudaFreeAsync(ps.staging, owner->side));
+    cudaEventDestroy(used);
+    return MPX_SUCCESS;
+}
+
+// -------------------------------------------------------------- send path
+int do_send(Comm* c, const void* buf, int64_t buf_bytes, int64_t count, Datatype* dt, int dest, int tag,
+            bool blocking, std::shared_ptr<ReqState>* out_req) {
+    World* w = c->w;
+    if (dest < 0 || dest >= w->size) return fail(MPX_ERR_ARG, "dest %d out of range for size-%d communicator", dest, w->size);
+    if (tag < 0) return fail(MPX_ERR_ARG, "tag %d out of range [0, 2147483647]", tag);
+    MPX_RC(check_layout_region(dt, count, buf_bytes));
+    Side s;
+    s.rank = c->rank;
+    s.device = c->device;
+    s.comm = c;
+    s.dt = dt;
+    s.count = count;
+    s.buf = const_cast<void*>(buf);
+    s.bytes = dt->size * count;
+    std::shared_ptr<ReqState> req;
+    if (!blocking) {
+        req = std::make_shared<ReqState>();
+        req->comm = c;
+        req->is_send = true;
+        req->matched = true;  // a send's status is known at initiation
+    }
+    const bool eager = s.bytes <= w->eager_limit || dest == c->rank;
+    Mailbox& mb = *w->mbox[dest];
+    std::unique_lock<std::mutex> lk(mb.mu);
+    auto it = std::find_if(mb.recvs.begin(), mb.recvs.end(), [&](const PendingRecv& pr) {
+        return matches(pr.src, pr.tag, pr.ctx, c->rank, tag, c->ctx);
+    });
+    if (it == mb.recvs.end()) {
+        // --- first side: publish the send -----------------------------------
+        PendingSend ps{c->ctx, c->rank, tag, s, eager};
+        ps.req = req;
+        MPX_RC(set_device(c->device));
+        if (eager) MPX_RC(stage_send(c, ps));
+        MPX_RC(record_new_event(c->stream, &ps.ev));
+        if (!eager) w->flags.take(&ps.flag, &ps.gen);
+        uint32_t* flag = ps.flag;
+        const uint32_t gen = ps.gen;
+        mb.sends.push_back(ps);
+        lk.unlock();
+        if (!eager) {  // rendezvous: complete when the receiver has pulled the data
+            if (blocking) MPX_RC(wait_flag(c->stream, flag, gen));
+            else {
+                req->flag = flag;
+                req->gen = gen;
+                req->needs_wait = true;
+            }
+        }
+        if (req) c->outstanding++;
+        if (out_req) *out_req = req;
+        return MPX_SUCCESS;
+    }
+    // --- second side: the receive was posted first ---------------------------
+    PendingRecv pr = *it;
+    mb.recvs.erase(it);
+    lk.unlock();
+    const int64_t moved = std::min(s.bytes, pr.r.bytes);
+    const bool trunc = s.bytes > pr.r.bytes;
+    fill_status(pr.req, pr.r, c->rank, tag, moved, trunc);
+    if (trunc && pr.blocking)
+        defer_error(pr.r.comm, MPX_ERR_TRUNCATE, "message truncated: incoming data larger than the posted receive");
+    MPX_RC(ensure_peer(w, c->device, pr.r.device));
+    MPX_RC(set_device(c->device));
+    if (eager) {
+        PendingSend ps{c->ctx, c->rank, tag, s, true};
+        MPX_RC(stage_send(c, ps));
+        cudaEvent_t staged;
+        MPX_RC(record_new_event(c->stream, &staged));
+        MPX_CU(cudaStreamWaitEvent(c->side, staged, 0));
+        MPX_CU(cudaStreamWaitEvent(c->side, pr.ev, 0));
+        MPX_RC(launch_move(c->device, pr.r.dt, pr.r.count, false, ps.staging, pr.r.buf, moved, c->side));
+        MPX_RC(set_device(c->device));
+        MPX_CU(cudaFreeAsync(ps.staging, c->side));
+        MPX_RC(write_flag(c->side, pr.flag, pr.gen));
+        cudaEventDestroy(staged);
+    } else if (blocking) {
+        MPX_CU(cudaStreamWaitEvent(c->stream, pr.ev, 0));
+        MPX_RC(transfer(c->device, c->stream, s, pr.r, moved));
+        MPX_RC(write_flag(c->stream, pr.flag, pr.gen));
+    } else {
+        cudaEvent_t fork;
+        MPX_RC(record_new_event(c->stream, &fork));
+        MPX_CU(cudaStreamWaitEvent(c->side, fork, 0));
+        MPX_CU(cudaStreamWaitEvent(c->side, pr.ev, 0));
+        MPX_RC(transfer(c->device, c->side, s, pr.r, moved));
+        MPX_RC(write_flag(c->side, pr.flag, pr.gen));
+        MPX_RC(record_new_event(c->side, &req->done_ev));
+        req->needs_wait = true;
+        cudaEventDestroy(fork);
+    }
+    cudaEventDestroy(pr.ev);  // the waits above captured it
+    if (req) c->outstanding++;
+    if (out_req) *out_req = req;
+    return MPX_SUCCESS;
+}
+
+// -------------------------------------------------------------- recv path
+int do_recv(Comm* c, void* buf, int64_t buf_bytes, int64_t count, Datatype* dt, int source, int tag,
+            bool blocking, std::shared_ptr<ReqState>* out_req) {
+    World* w = c->w;
+    if (source != MPX_ANY_SOURCE && (source < 0 || source >= w->size))
+        return fail(MPX_ERR_ARG, "source %d out of range for size-%d communicator", source, w->size);
+    if (tag < 0 && tag != MPX_ANY_TAG) return fail(MPX_ERR_ARG, "tag %d out of range [0, 2147483647]", tag);
+    MPX_RC(check_layout_region(dt, count, buf_bytes));  // DtypeSink check at post time (p2p.py:63-64)
+    Side r;
+    r.rank = c->rank;
+    r.device = c->device;
+    r.comm = c;
+    r.dt = dt;
+    r.count = count;
+    r.buf = buf;
+    r.bytes = dt->size * count;
+    std::shared_ptr<ReqState> req;
+    if (!blocking) {
+        req = std::make_shared<ReqState>();
+        req->comm = c;
+    }
+    Mailbox& mb = *w->mbox[c->rank];
+    std::unique_lock<std::mutex> lk(mb.mu);
+    auto it = std::find_if(mb.sends.begin(), mb.sends.end(), [&](const PendingSend& ps) {
+        return matches(source, tag, c->ctx, ps.src, ps.tag, ps.ctx);
+    });
+    if (it == mb.sends.end()) {
+        // --- first side: post the receive ------------------------------------
+        PendingRecv pr{c->ctx, source, tag, r};
+        pr.blocking = blocking;
+        pr.req = req;
+        MPX_RC(set_device(c->device));
+        MPX_RC(record_new_event(c->stream, &pr.ev));
+        w->flags.take(&pr.flag, &pr.gen);
+        uint32_t* flag = pr.flag;
+        const uint32_t gen = pr.gen;
+        mb.recvs.push_back(pr);
+        lk.unlock();
+        if (blocking) MPX_RC(wait_flag(c->stream, flag, gen));
+        else {
+            req->flag = flag;
+            req->gen = gen;
+            req->needs_wait = true;
+            c->outstanding++;
+        }
+        if (out_req) *out_req = req;
+        return MPX_SUCCESS;
+    }
+    // --- second side: the send was enqueued first ----------------------------
+    PendingSend ps = *it;
+    mb.sends.erase(it);
+    lk.unlock();
+    const int64_t moved = std::min(ps.s.bytes, r.bytes);
+    const bool trunc = ps.s.bytes > r.bytes;
+    fill_status(req, r, ps.src, ps.tag, moved, trunc);
+    if (trunc && blocking)
+        defer_error(c, MPX_ERR_TRUNCATE, "message truncated: incoming data larger than the posted receive");
+    MPX_RC(ensure_peer(w, c->device, ps.s.device));
+    MPX_RC(set_device(c->device));
+    cudaStream_t st = c->stream;
+    if (!blocking) {
+        cudaEvent_t fork;
+        MPX_RC(record_new_event(c->stream, &fork));
+        MPX_CU(cudaStreamWaitEvent(c->side, fork, 0));
+        cudaEventDestroy(fork);
+        st = c->side;
+    }
+    MPX_CU(cudaStreamWaitEvent(st, ps.ev, 0));
+    if (ps.eager) {
+        MPX_RC(consume_staging(c->device, st, ps.s.comm, ps, r, moved));
+    } else {
+        MPX_RC(transfer(c->device, st, ps.s, r, moved));
+        MPX_RC(write_flag(st, ps.flag, ps.gen));
+    }
+    MPX_RC(set_device(c->device));
+    if (!blocking) {
+        MPX_RC(record_new_event(st, &req->done_ev));
+        req->needs_wait = true;
+        c->outstanding++;
+    }
+    cudaEventDestroy(ps.ev);
+    if (out_req) *out_req = req;
+    return MPX_SUCCESS;
+}
+
+mpx_request publish_req(const std::shared_ptr<ReqState>& q) {
+    std::lock_guard<std::mutex> g(g_handles_mu);
+    g_reqs[q.get()] = q;
+    return reinterpret_cast<mpx_request>(q.get());
+}
+
+int wait_one(const std::shared_ptr<ReqState>& q) {
+    Comm* c = q->comm;
+    std::lock_guard<std::mutex> g(q->mu);
+    if (q->waited) return MPX_SUCCESS;
+    q->waited = true;
+    MPX_RC(set_device(c->device));
+    if (q->needs_wait) {
+        if (q->done_ev) {
+            MPX_CU(cudaStreamWaitEvent(c->stream, q->done_ev, 0));
+            cudaEventDestroy(q->done_ev);
+            q->done_ev = nullptr;
+        } else {
+            MPX_RC(wait_flag(c->stream, q->flag, q->gen));
+        }
+    }
+    c->outstanding--;
+    return MPX_SUCCESS;
+}
+
+// ---------------------------------------------------------- NCCL loading
+struct Nccl {
+    bool tried = false, ok = false;
+    ncclResult_t (*commInitAll)(ncclComm_t*, int, const int*) = nullptr;
+    ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char* (*errStr)(ncclResult_t) = nullptr;
+};
+Nccl g_nccl;
+std::mutex g_nccl_mu;
+
+bool nccl_bind(void* h) {
+    g_nccl.commInitAll = (decltype(g_nccl.commInitAll))dlsym(h, "ncclCommInitAll");
+    g_nccl.allReduce = (decltype(g_nccl.allReduce))dlsym(h, "ncclAllReduce");
+    g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(h, "ncclCommDestroy");
+    g_nccl.errStr = (decltype(g_nccl.errStr))dlsym(h, "ncclGetErrorString");
+    return g_nccl.commInitAll && g_nccl.allReduce && g_nccl.commDestroy && g_nccl.errStr;
+}
+
+bool nccl_available() {
+    std::lock_guard<std::mutex> g(g_nccl_mu);
+    if (!g_nccl.tried) {
+        g_nccl.tried = true;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+        g_nccl.ok = h && nccl_bind(h);
+    }
+    return g_nccl.ok;
+}
+
+// all ranks of the world call this; the first builds every comm with ncclCommInitAll
+int nccl_comm_for(Comm* c, ncclComm_t* out) {
+    World* w = c->w;
+    std::unique_lock<std::mutex> lk(w->nccl_mu);
+    if (w->nccl_state == 0) {
+        w->nccl_state = 1;
+        lk.unlock();
+        w->nccl.assign(w->size, nullptr);
+        ncclResult_t r = g_nccl.commInitAll(w->nccl.data(), w->size, w->devices.data());
+        lk.lock();
+        w->nccl_state = r == ncclSuccess ? 2 : -1;
+        w->nccl_cv.notify_all();
+        if (r != ncclSuccess) return fail(MPX_ERR_TRANSPORT, "ncclCommInitAll: %s", g_nccl.errStr(r));
+    }
+    w->nccl_cv.wait(lk, [&] { return w->nccl_state != 1; });
+    if (w->nccl_state != 2) return fail(MPX_ERR_TRANSPORT, "NCCL communicator creation failed");
+    *out = w->nccl[c->rank];
+    return MPX_SUCCESS;
+}
+
+int elem_size(int code) {
+    switch (code) {
+    case MPX_INT32: case MPX_FLOAT32: return 4;
+    case MPX_INT64: case MPX_FLOAT64: return 8;
+    default: return 0;
+    }
+}
+
+}  // namespace
+}  // namespace mpx
+
+using namespace mpx;
+
+extern "C" {
+
+int mpx_world_join(const char* group, int size, int rank, int device, int64_t eager_limit, mpx_world* out) {
+    if (!group || size < 1 || rank < 0 || rank >= size)
+        return fail(MPX_ERR_ARG, "rank %d outside job of %d", rank, size);
+    if (eager_limit < 0) return fail(MPX_ERR_ARG, "eager_limit/chunk_size out of range");
+    int ndev = 0;
+    MPX_CU(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(MPX_ERR_ARG, "device %d not present (%d devices)", device, ndev);
+    MPX_RC(set_device(device));
+    std::lock_guard<std::mutex> g(g_worlds_mu);
+    World*& w = g_worlds[group];
+    if (!w) {
+        w = new World();
+        w->group = group;
+        w->size = size;
+        w->eager_limit = eager_limit;
+        w->devices.assign(size, -1);
+        w->joined.assign(size, false);
+        for (int i = 0; i < size; ++i) w->mbox.emplace_back(new Mailbox());
+        int rc = w->flags.init();
+        if (rc) {
+            delete w;
+            g_worlds.erase(group);
+            return rc;
+        }
+    }
+    if (w->size != size) return fail(MPX_ERR_ARG, "world %s has %d ranks, not %d", group, w->size, size);
+    if (w->joined[rank]) return fail(MPX_ERR_STATE, "rank %d already joined world %s", rank, group);
+    w->joined[rank] = true;
+    w->devices[rank] = device;
+    w->live++;
+    *out = reinterpret_cast<mpx_world>(w);
+    return MPX_SUCCESS;
+}
+
+int mpx_world_leave(mpx_world h, int rank) {
+    auto* w = reinterpret_cast<World*>(h);
+    std::lock_guard<std::mutex> g(g_worlds_mu);
+    auto it = g_worlds.find(w ? w->group : std::string());
+    if (!w || it == g_worlds.end() || it->second != w) return fail(MPX_ERR_STATE, "not a live world");
+    if (rank < 0 || rank >= w->size || !w->joined[rank]) return fail(MPX_ERR_STATE, "rank %d not in world", rank);
+    w->joined[rank] = false;
+    if (--w->live == 0) {
+        if (w->nccl_state == 2)
+            for (auto cm : w->nccl)
+                if (cm) g_nccl.commDestroy(cm);
+        g_worlds.erase(it);
+        delete w;
+    }
+    return MPX_SUCCESS;
+}
+
+int mpx_comm_create(mpx_world h, int rank, int ctx, void* stream, mpx_comm* out) {
+    auto* w = reinterpret_cast<World*>(h);
+    if (!w || rank < 0 || rank >= w->size) return fail(MPX_ERR_ARG, "bad world / rank");
+    const int dev = w->devices[rank];
+    MPX_RC(set_device(dev));
+    auto* c = new Comm();
+    c->w = w;
+    c->rank = rank;
+    c->ctx = ctx;
+    c->device = dev;
+    c->stream = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "cudaStreamCreate(side)");
+    }
+    std::lock_guard<std::mutex> g(g_handles_mu);
+    g_comms.insert(c);
+    *out = reinterpret_cast<mpx_comm>(c);
+    return MPX_SUCCESS;
+}
+
+int mpx_comm_free(mpx_comm h) {
+    Comm* c = comm_of(h);
+    if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
+    if (c->outstanding.load() > 0)
+        return fail(MPX_ERR_PENDING, "communicator has %lld outstanding operations", (long long)c->outstanding.load());
+    MPX_RC(set_device(c->device));
+    cudaStreamSynchronize(c->side);
+    cudaStreamDestroy(c->side);
+    {
+        std::lock_guard<std::mutex> g(g_handles_mu);
+        g_comms.erase(c);
+    }
+    delete c;
+    return MPX_SUCCESS;
+}
+
+int mpx_send_enqueue(mpx_comm h, const void* buf, int64_t bb, int64_t count, mpx_datatype dt, int dest, int tag) {
+    Comm* c = comm_of(h);
+    if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
+    Datatype* d = lookup(dt);
+    if (!d) return fail(MPX_ERR_ARG, "not a datatype handle");
+    return do_send(c, buf, bb, count, d, dest, tag, true, nullptr);
+}
+
+int mpx_recv_enqueue(mpx_comm h, void* buf, int64_t bb, int64_t count, mpx_datatype dt, int source, int tag) {
+    Comm* c = comm_of(h);
+    if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
+    Datatype* d = lookup(dt);
+    if (!d) return fail(MPX_ERR_ARG, "not a datatype handle");
+    return do_recv(c, buf, bb, count, d, source, tag, true, nullptr);
+}
+
+int mpx_isend_enqueue(mpx_comm h, const void* buf, int64_t bb, int64_t count, mpx_datatype dt, int dest, int tag,
+                      mpx_request* out) {
+    Comm* c = comm_of(h);
+    if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
+    Datatype* d = lookup(dt);
+    if (!d) return fail(MPX_ERR_ARG, "not a datatype handle");
+    std::shared_ptr<ReqState> q;
+    MPX_RC(do_send(c, buf, bb, count, d, dest, tag, false, &q));
+    *out = publish_req(q);
+    return MPX_SUCCESS;
+}
+
+int mpx_irecv_enqueue(mpx_comm h, void* buf, int64_t bb, int64_t count, mpx_datatype dt, int source, int tag,
+                      mpx_request* out) {
+    Comm* c = comm_of(h);
+    if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
+    Datatype* d = lookup(dt);
+    if (!d) return fail(MPX_ERR_ARG, "not a datatype handle");
+    std::shared_ptr<ReqState> q;
+    MPX_RC(do_recv(c, buf, bb, count, d, source, tag, false, &q));
+    *out = publish_req(q);
+    return MPX_SUCCESS;
+}
+
+int mpx_wait_enqueue(mpx_request h) {
+    auto q = req_of(h);
+    if (!q) return fail(MPX_ERR_ARG, "wait_enqueue needs a request produced by an _enqueue operation");
+    return wait_one(q);
+}
+
+int mpx_waitall_enqueue(int n, const mpx_request* hs) {
+    std::vector<std::shared_ptr<ReqState>> qs;
+    for (int i = 0; i < n; ++i) {
+        auto q = req_of(hs[i]);
+        if (!q) return fail(MPX_ERR_ARG, "waitall_enqueue needs requests produced by _enqueue operations");
+        qs.push_back(q);
+    }
+    for (auto& q : qs)
+        if (q->comm->stream != qs[0]->comm->stream)
+            return fail(MPX_ERR_ARG, "waitall_enqueue cannot mix device queues");
+    for (auto& q : qs) MPX_RC(wait_one(q));
+    return MPX_SUCCESS;
+}
+
+int mpx_request_status(mpx_request h, int64_t out[5]) {
+    auto q = req_of(h);
+    if (!q) return fail(MPX_ERR_ARG, "unknown request");
+    std::lock_guard<std::mutex> g(q->mu);
+    out[0] = q->matched;
+    out[1] = q->source;
+    out[2] = q->tag;
+    out[3] = q->count;
+    out[4] = q->err;
+    return MPX_SUCCESS;
+}
+
+int mpx_request_free(mpx_request h) {
+    std::lock_guard<std::mutex> g(g_handles_mu);
+    if (!g_reqs.erase(h)) return fail(MPX_ERR_ARG, "unknown request");
+    return MPX_SUCCESS;
+}
+
+int mpx_comm_synchronize(mpx_comm h) {
+    Comm* c = comm_of(h);
+    if (!c) return fail(MPX_ERR_STATE, "device queue already destroyed");
+    MPX_RC(set_device(c->device));
+    MPX_CU(cudaStreamSynchronize(c->stream));
+    std::lock_guard<std::mutex> g(c->err_mu);
+    if (!c->deferred.empty()) {
+        auto e = c->deferred.front();
+        c->deferred.clear();  // raise the first, drop the rest (offload.py:116-119)
+        return fail(e.first, "%s", e.second.c_str());
+    }
+    return MPX_SUCCESS;
+}
+
+int mpx_comm_progress(mpx_comm h, int64_t* outstanding) {
+    Comm* c = comm_of(h);
+    if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
+    if (outstanding) *outstanding = c->outstanding.load();
+    return MPX_SUCCESS;
+}
+
+int mpx_stream_device(void* stream, int* device) {
+    MPX_CU(cudaStreamGetDevice(reinterpret_cast<cudaStream_t>(stream), device));
+    return MPX_SUCCESS;
+}
+
+int mpx_nccl_load(const char* path) {
+    std::lock_guard<std::mutex> g(g_nccl_mu);
+    void* h = dlopen(path, RTLD_NOW);
+    if (!h) return fail(MPX_ERR_UNSUPPORTED, "dlopen(%s): %s", path, dlerror());
+    g_nccl.tried = true;
+    g_nccl.ok = nccl_bind(h);
+    return g_nccl.ok ? MPX_SUCCESS : fail(MPX_ERR_UNSUPPORTED, "%s lacks NCCL symbols", path);
+}
+
+int mpx_allreduce_enqueue(mpx_comm h, const void* sendbuf, void* recvbuf, int64_t count, int dtype_code, int op,
+                          int algo) {
+    Comm* c = comm_of(h);
+    if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
+    if (op != MPX_OP_SUM) return fail(MPX_ERR_ARG, "unsupported reduction op %d (only SUM)", op);
+    const int es = elem_size(dtype_code);
+    if (!es) return fail(MPX_ERR_ARG, "allreduce supports INT32, INT64, FLOAT32 and FLOAT64");
+    if (count < 0) return fail(MPX_ERR_ARG, "count must be a nonnegative int");
+    if (count == 0) return MPX_SUCCESS;  // comm.py:572-574
+    World* w = c->w;
+    MPX_RC(set_device(c->device));
+    bool distinct = true;
+    {
+        std::set<int> ds(w->devices.begin(), w->devices.end());
+        distinct = (int)ds.size() == w->size && !ds.count(-1);
+    }
+    if (algo == 0) algo = (w->size > 1 && distinct && nccl_available()) ? 2 : 1;
+    if (algo == 2) {
+        if (!distinct) return fail(MPX_ERR_UNSUPPORTED, "NCCL allreduce needs one device per rank");
+        if (!nccl_available()) return fail(MPX_ERR_UNSUPPORTED, "libnccl.so.2 not available");
+        ncclComm_t nc;
+        MPX_RC(nccl_comm_for(c, &nc));
+        ncclDataType_t t = dtype_code == MPX_INT32 ? ncclInt32 : dtype_code == MPX_INT64 ? ncclInt64
+                         : dtype_code == MPX_FLOAT32 ? ncclFloat32 : ncclFloat64;
+        ncclResult_t r = g_nccl.allReduce(sendbuf, recvbuf, (size_t)count, t, ncclSum, nc, c->stream);
+        if (r != ncclSuccess) return fail(MPX_ERR_TRANSPORT, "ncclAllReduce: %s", g_nccl.errStr(r));
+        return MPX_SUCCESS;
+    }
+    // native one-shot: every rank registers its buffers, then all streams meet
+    const int64_t seq = c->coll_seq++;
+    std::shared_ptr<CollSlot> slot;
+    {
+        std::lock_guard<std::mutex> g(w->coll_mu);
+        auto& sp = w->colls[{c->ctx, seq}];
+        if (!sp) {
+            sp = std::make_shared<CollSlot>();
+            MPX_CU(cudaHostAlloc(reinterpret_cast<void**>(&sp->table), sizeof(CollTable),
+                                 cudaHostAllocMapped | cudaHostAllocPortable));
+            MPX_CU(cudaHostAlloc(reinterpret_cast<void**>(&sp->arrive), 2 * sizeof(uint32_t) * kMaxCollRanks,
+                                 cudaHostAllocMapped | cudaHostAllocPortable));
+            std::fill(sp->arrive, sp->arrive + 2 * kMaxCollRanks, 0u);
+            sp->finish = sp->arrive + kMaxCollRanks;
+        }
+        slot = sp;
+        if (w->size > kMaxCollRanks) return fail(MPX_ERR_UNSUPPORTED, "native allreduce supports <= %d ranks", kMaxCollRanks);
+        slot->table->send[c->rank] = sendbuf;
+        slot->table->recv[c->rank] = recvbuf;
+        if (++slot->arrived_host == w->size) w->colls.erase({c->ctx, seq});
+    }
+    for (int j = 0; j < w->size; ++j)
+        if (w->devices[j] != c->device) MPX_RC(ensure_peer(w, c->device, w->devices[j]));
+    MPX_RC(set_device(c->device));
+    MPX_RC(write_flag(c->stream, slot->arrive + c->rank, slot->gen));
+    for (int j = 0; j < w->size; ++j) MPX_RC(wait_flag(c->stream, slot->arrive + j, slot->gen));
+    cudaError_t e = launch_allreduce_oneshot(slot->table, w->size, c->rank, count, dtype_code, c->device, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "allreduce launch");
+    MPX_RC(write_flag(c->stream, slot->finish + c->rank, slot->gen));
+    for (int j = 0; j < w->size; ++j) MPX_RC(wait_flag(c->stream, slot->finish + j, slot->gen));
+    // keep the slot's pinned table/flags alive until this rank's stream is
+    // past it (every rank holds a reference; the last release frees it)
+    cudaEvent_t keep;
+    MPX_RC(record_new_event(c->stream, &keep));
+    std::lock_guard<std::mutex> g(g_hold_mu);
+    auto it = g_hold.begin();
+    while (it != g_hold.end()) {
+        cudaError_t q = cudaEventQuery(it->first);
+        if (q == cudaErrorNotReady) {
+            ++it;
+            continue;
+        }
+        cudaGetLastError();
+        cudaEventDestroy(it->first);
+        it = g_hold.erase(it);
+    }
+    g_hold.emplace_back(keep, slot);
+    return MPX_SUCCESS;
+}
+
+}  // extern "C"

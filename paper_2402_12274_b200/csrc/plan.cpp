@@ -3,19 +3,52 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <unordered_map>
 
 namespace mpx {
 
 Plan::~Plan() {
-    if (blob) {
+    if (blob || host_blob || ready) {
         int cur = -1;
         cudaGetDevice(&cur);
         if (device >= 0 && cur != device) cudaSetDevice(device);
-        cudaFree(blob);
+        if (ready) cudaEventSynchronize(ready);
+        if (blob) cudaFree(blob);
+        if (host_blob) cudaFreeHost(host_blob);
+        if (ready) cudaEventDestroy(ready);
         if (device >= 0 && cur != device && cur >= 0) cudaSetDevice(cur);
     }
 }
+
+cudaError_t plan_wait(Plan& p, cudaStream_t stream) {
+    if (!p.ready || p.ready_seen.load(std::memory_order_acquire)) return cudaSuccess;
+    cudaError_t q = cudaEventQuery(p.ready);
+    if (q == cudaSuccess) {
+        p.ready_seen.store(true, std::memory_order_release);
+        return cudaSuccess;
+    }
+    if (q != cudaErrorNotReady) return q;
+    cudaGetLastError();
+    return cudaStreamWaitEvent(stream, p.ready, 0);
+}
+
+namespace {
+// one internal upload stream per device: descriptor uploads never
+// synchronise (or even touch) the caller's stream
+cudaStream_t upload_stream(int device) {
+    static std::mutex mu;
+    static std::map<int, cudaStream_t> streams;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = streams.find(device);
+    if (it != streams.end()) return it->second;
+    cudaStream_t s = nullptr;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    streams[device] = s;
+    return s;
+}
+}  // namespace
 
 namespace {
 
@@ -184,20 +217,26 @@ std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStre
             std::memcpy(host.data() + nb + kb, f.rp.data(), pb);
             std::memcpy(host.data() + nb + kb + pb, f.bp.data(), pb);
         }
+        (void)stream;
         void* dev = nullptr;
         cudaError_t e = cudaMalloc(&dev, host.size());
         if (e != cudaSuccess) {
             *err = std::string("cudaMalloc(descriptor): ") + cudaGetErrorString(e);
             return nullptr;
         }
-        e = cudaMemcpyAsync(dev, host.data(), host.size(), cudaMemcpyHostToDevice, stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+        p->blob = dev;
+        e = cudaHostAlloc(&p->host_blob, host.size(), cudaHostAllocDefault);
+        if (e == cudaSuccess) {
+            std::memcpy(p->host_blob, host.data(), host.size());
+            cudaStream_t up = upload_stream(device);
+            e = cudaMemcpyAsync(dev, p->host_blob, host.size(), cudaMemcpyHostToDevice, up);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ready, cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventRecord(p->ready, up);
+        }
         if (e != cudaSuccess) {
-            cudaFree(dev);
             *err = std::string("descriptor upload: ") + cudaGetErrorString(e);
             return nullptr;
         }
-        p->blob = dev;
         p->blob_bytes = host.size();
         uint8_t* b = (uint8_t*)dev;
         p->desc.nodes = (const DNode*)b;

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <memory>
 #include <string>
@@ -24,9 +25,15 @@ struct Plan {
     int32_t chain_align = 16;  // largest power of two dividing base, L and strides
     DDesc desc{};           // device descriptor (always built, used by iov + generic)
     void* blob = nullptr;   // device allocation backing desc
+    void* host_blob = nullptr;  // pinned source of the upload (kept until freed)
     size_t blob_bytes = 0;
+    cudaEvent_t ready = nullptr;     // upload finished (recorded on an internal stream)
+    std::atomic<bool> ready_seen{false};
     ~Plan();
 };
+
+// make `stream` wait for the plan's descriptor upload (no-op once observed done)
+cudaError_t plan_wait(Plan& p, cudaStream_t stream);
 
 // Build (or fetch from the datatype's cache) the plan for (layout_for(count), device).
 std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStream_t stream,
