@@ -154,7 +154,7 @@ struct Comm;
 // Host-side completion record of a nonblocking operation (Request,
 // progress.py:34-60; EnqueuedRequest, offload.py:34-46).
 struct ReqState {
-    Comm* comm = nullptr;
+    std::shared_ptr<Comm> comm;
     bool is_send = false;
     bool matched = false;     // host match done: status known
     int source = -1, tag = -1;
@@ -172,7 +172,7 @@ struct ReqState {
 // one side of a message as known on the host
 struct Side {
     int rank = 0, device = 0;
-    Comm* comm = nullptr;
+    std::shared_ptr<Comm> comm;   // keeps a freed communicator alive while referenced
     Datatype* dt = nullptr;
     int64_t count = 0;
     void* buf = nullptr;
@@ -235,9 +235,34 @@ struct World {
     std::condition_variable nccl_cv;
     std::vector<ncclComm_t> nccl;   // per rank, by ncclCommInitAll
     int nccl_state = 0;             // 0 none, 1 building, 2 ready, -1 failed
+    std::mutex svc_mu;
+    std::map<int, cudaStream_t> svc;  // per-device service streams (deferred frees)
+    cudaStream_t service(int dev) {
+        std::lock_guard<std::mutex> g(svc_mu);
+        auto it = svc.find(dev);
+        if (it != svc.end()) return it->second;
+        cudaStream_t st = nullptr;
+        int cur = -1;
+        cudaGetDevice(&cur);
+        cudaSetDevice(dev);
+        cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+        cudaSetDevice(cur);
+        svc[dev] = st;
+        return st;
+    }
 };
 
 struct Comm {
+    ~Comm() {
+        if (side) {
+            int cur = -1;
+            cudaGetDevice(&cur);
+            cudaSetDevice(device);
+            cudaStreamSynchronize(side);
+            cudaStreamDestroy(side);
+            cudaSetDevice(cur);
+        }
+    }
     World* w = nullptr;
     int rank = 0, ctx = 0, device = 0;
     cudaStream_t stream = nullptr;  // the user's stream
@@ -255,13 +280,13 @@ std::vector<std::pair<cudaEvent_t, std::shared_ptr<CollSlot>>> g_hold;
 std::mutex g_worlds_mu;
 std::map<std::string, World*> g_worlds;
 std::mutex g_handles_mu;
-std::set<const void*> g_comms;
+std::map<const void*, std::shared_ptr<Comm>> g_comms;
 std::map<const void*, std::shared_ptr<ReqState>> g_reqs;
 
-Comm* comm_of(mpx_comm h) {
+std::shared_ptr<Comm> comm_of(mpx_comm h) {
     std::lock_guard<std::mutex> g(g_handles_mu);
-    auto* c = reinterpret_cast<Comm*>(h);
-    return g_comms.count(c) ? c : nullptr;
+    auto it = g_comms.find(h);
+    return it == g_comms.end() ? nullptr : it->second;
 }
 
 std::shared_ptr<ReqState> req_of(mpx_request h) {
@@ -270,7 +295,7 @@ std::shared_ptr<ReqState> req_of(mpx_request h) {
     return it == g_reqs.end() ? nullptr : it->second;
 }
 
-void defer_error(Comm* c, int code, const std::string& msg) {
+void defer_error(const std::shared_ptr<Comm>& c, int code, const std::string& msg) {
     std::lock_guard<std::mutex> g(c->err_mu);
     c->deferred.emplace_back(code, msg);
 }
@@ -339,7 +364,7 @@ void fill_status(const std::shared_ptr<ReqState>& q, const Side& mine, int src, 
 }
 
 // Eager send: pack at the sender's stream position into a staging buffer.
-int stage_send(Comm* c, PendingSend& ps) {
+int stage_send(const std::shared_ptr<Comm>& c, PendingSend& ps) {
     MPX_RC(set_device(c->device));
     MPX_CU(cudaMallocAsync(&ps.staging, (size_t)std::max<int64_t>(ps.s.bytes, 1), c->stream));
     MPX_RC(launch_move(c->device, ps.s.dt, ps.s.count, true, ps.s.buf, ps.staging, ps.s.bytes, c->stream));
@@ -347,20 +372,22 @@ int stage_send(Comm* c, PendingSend& ps) {
 }
 
 // Consume an eager staging buffer on stream `st` (device of st = `dev`):
-// unpack into the receiver, then free the staging on the owner's side stream.
-int consume_staging(int dev, cudaStream_t st, Comm* owner, const PendingSend& ps, const Side& r, int64_t moved) {
+// unpack into the receiver, then free the staging on the world's service
+// stream of the owner's device (the sender may have freed its communicator).
+int consume_staging(World* w, int dev, cudaStream_t st, const PendingSend& ps, const Side& r, int64_t moved) {
     MPX_RC(launch_move(dev, r.dt, r.count, false, ps.staging, r.buf, moved, st));
     cudaEvent_t used;
     MPX_RC(record_new_event(st, &used));
-    MPX_RC(set_device(owner->device));
-    MPX_CU(cudaStreamWaitEvent(owner->side, used, 0));
-    MPX_CU(cudaFreeAsync(ps.staging, owner->side));
+    cudaStream_t svc = w->service(ps.s.device);
+    MPX_RC(set_device(ps.s.device));
+    MPX_CU(cudaStreamWaitEvent(svc, used, 0));
+    MPX_CU(cudaFreeAsync(ps.staging, svc));
     cudaEventDestroy(used);
     return MPX_SUCCESS;
 }
 
 // -------------------------------------------------------------- send path
-int do_send(Comm* c, const void* buf, int64_t buf_bytes, int64_t count, Datatype* dt, int dest, int tag,
+int do_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t buf_bytes, int64_t count, Datatype* dt, int dest, int tag,
             bool blocking, std::shared_ptr<ReqState>* out_req) {
     World* w = c->w;
     if (dest < 0 || dest >= w->size) return fail(MPX_ERR_ARG, "dest %d out of range for size-%d communicator", dest, w->size);
@@ -456,7 +483,7 @@ int do_send(Comm* c, const void* buf, int64_t buf_bytes, int64_t count, Datatype
 }
 
 // -------------------------------------------------------------- recv path
-int do_recv(Comm* c, void* buf, int64_t buf_bytes, int64_t count, Datatype* dt, int source, int tag,
+int do_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t buf_bytes, int64_t count, Datatype* dt, int source, int tag,
             bool blocking, std::shared_ptr<ReqState>* out_req) {
     World* w = c->w;
     if (source != MPX_ANY_SOURCE && (source < 0 || source >= w->size))
@@ -524,7 +551,7 @@ int do_recv(Comm* c, void* buf, int64_t buf_bytes, int64_t count, Datatype* dt, 
     }
     MPX_CU(cudaStreamWaitEvent(st, ps.ev, 0));
     if (ps.eager) {
-        MPX_RC(consume_staging(c->device, st, ps.s.comm, ps, r, moved));
+        MPX_RC(consume_staging(w, c->device, st, ps, r, moved));
     } else {
         MPX_RC(transfer(c->device, st, ps.s, r, moved));
         MPX_RC(write_flag(st, ps.flag, ps.gen));
@@ -547,7 +574,7 @@ mpx_request publish_req(const std::shared_ptr<ReqState>& q) {
 }
 
 int wait_one(const std::shared_ptr<ReqState>& q) {
-    Comm* c = q->comm;
+    Comm* c = q->comm.get();
     std::lock_guard<std::mutex> g(q->mu);
     if (q->waited) return MPX_SUCCESS;
     q->waited = true;
@@ -597,7 +624,7 @@ bool nccl_available() {
 }
 
 // all ranks of the world call this; the first builds every comm with ncclCommInitAll
-int nccl_comm_for(Comm* c, ncclComm_t* out) {
+int nccl_comm_for(const std::shared_ptr<Comm>& c, ncclComm_t* out) {
     World* w = c->w;
     std::unique_lock<std::mutex> lk(w->nccl_mu);
     if (w->nccl_state == 0) {
@@ -687,41 +714,32 @@ int mpx_comm_create(mpx_world h, int rank, int ctx, void* stream, mpx_comm* out)
     if (!w || rank < 0 || rank >= w->size) return fail(MPX_ERR_ARG, "bad world / rank");
     const int dev = w->devices[rank];
     MPX_RC(set_device(dev));
-    auto* c = new Comm();
+    auto c = std::make_shared<Comm>();
     c->w = w;
     c->rank = rank;
     c->ctx = ctx;
     c->device = dev;
     c->stream = reinterpret_cast<cudaStream_t>(stream);
     cudaError_t e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
-    if (e != cudaSuccess) {
-        delete c;
-        return cuda_fail(e, "cudaStreamCreate(side)");
-    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate(side)");
     std::lock_guard<std::mutex> g(g_handles_mu);
-    g_comms.insert(c);
-    *out = reinterpret_cast<mpx_comm>(c);
+    g_comms[c.get()] = c;
+    *out = reinterpret_cast<mpx_comm>(c.get());
     return MPX_SUCCESS;
 }
 
 int mpx_comm_free(mpx_comm h) {
-    Comm* c = comm_of(h);
+    auto c = comm_of(h);
     if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
     if (c->outstanding.load() > 0)
         return fail(MPX_ERR_PENDING, "communicator has %lld outstanding operations", (long long)c->outstanding.load());
-    MPX_RC(set_device(c->device));
-    cudaStreamSynchronize(c->side);
-    cudaStreamDestroy(c->side);
-    {
-        std::lock_guard<std::mutex> g(g_handles_mu);
-        g_comms.erase(c);
-    }
-    delete c;
+    std::lock_guard<std::mutex> g(g_handles_mu);
+    g_comms.erase(h);   // destroyed once no pending operation references it
     return MPX_SUCCESS;
 }
 
 int mpx_send_enqueue(mpx_comm h, const void* buf, int64_t bb, int64_t count, mpx_datatype dt, int dest, int tag) {
-    Comm* c = comm_of(h);
+    auto c = comm_of(h);
     if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
     Datatype* d = lookup(dt);
     if (!d) return fail(MPX_ERR_ARG, "not a datatype handle");
@@ -729,7 +747,7 @@ int mpx_send_enqueue(mpx_comm h, const void* buf, int64_t bb, int64_t count, mpx
 }
 
 int mpx_recv_enqueue(mpx_comm h, void* buf, int64_t bb, int64_t count, mpx_datatype dt, int source, int tag) {
-    Comm* c = comm_of(h);
+    auto c = comm_of(h);
     if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
     Datatype* d = lookup(dt);
     if (!d) return fail(MPX_ERR_ARG, "not a datatype handle");
@@ -738,7 +756,7 @@ int mpx_recv_enqueue(mpx_comm h, void* buf, int64_t bb, int64_t count, mpx_datat
 
 int mpx_isend_enqueue(mpx_comm h, const void* buf, int64_t bb, int64_t count, mpx_datatype dt, int dest, int tag,
                       mpx_request* out) {
-    Comm* c = comm_of(h);
+    auto c = comm_of(h);
     if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
     Datatype* d = lookup(dt);
     if (!d) return fail(MPX_ERR_ARG, "not a datatype handle");
@@ -750,7 +768,7 @@ int mpx_isend_enqueue(mpx_comm h, const void* buf, int64_t bb, int64_t count, mp
 
 int mpx_irecv_enqueue(mpx_comm h, void* buf, int64_t bb, int64_t count, mpx_datatype dt, int source, int tag,
                       mpx_request* out) {
-    Comm* c = comm_of(h);
+    auto c = comm_of(h);
     if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
     Datatype* d = lookup(dt);
     if (!d) return fail(MPX_ERR_ARG, "not a datatype handle");
@@ -799,7 +817,7 @@ int mpx_request_free(mpx_request h) {
 }
 
 int mpx_comm_synchronize(mpx_comm h) {
-    Comm* c = comm_of(h);
+    auto c = comm_of(h);
     if (!c) return fail(MPX_ERR_STATE, "device queue already destroyed");
     MPX_RC(set_device(c->device));
     MPX_CU(cudaStreamSynchronize(c->stream));
@@ -813,7 +831,7 @@ int mpx_comm_synchronize(mpx_comm h) {
 }
 
 int mpx_comm_progress(mpx_comm h, int64_t* outstanding) {
-    Comm* c = comm_of(h);
+    auto c = comm_of(h);
     if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
     if (outstanding) *outstanding = c->outstanding.load();
     return MPX_SUCCESS;
@@ -835,7 +853,7 @@ int mpx_nccl_load(const char* path) {
 
 int mpx_allreduce_enqueue(mpx_comm h, const void* sendbuf, void* recvbuf, int64_t count, int dtype_code, int op,
                           int algo) {
-    Comm* c = comm_of(h);
+    auto c = comm_of(h);
     if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
     if (op != MPX_OP_SUM) return fail(MPX_ERR_ARG, "unsupported reduction op %d (only SUM)", op);
     const int es = elem_size(dtype_code);
