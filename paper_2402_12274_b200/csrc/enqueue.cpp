@@ -140,6 +140,44 @@ int write_flag(cudaStream_t s, uint32_t* addr, uint32_t gen) {
         if (rc_) return rc_;      \
     } while (0)
 
+// Staging memory comes from a private per-device pool that never inserts
+// hidden stream dependencies (cudaMemPoolReuseAllowInternalDependencies = 0):
+// the default pool may make an allocation on one rank's stream wait for a
+// free on another rank's stream, which can be blocked in a memop wait on the
+// first -- a deadlock the protocol must never contain.
+cudaMemPool_t staging_pool(int dev) {
+    static std::mutex mu;
+    static std::map<int, cudaMemPool_t> pools;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = pools.find(dev);
+    if (it != pools.end()) return it->second;
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    int zero = 0, one = 1;
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &zero);
+    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowOpportunistic, &one);
+    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseFollowEventDependencies, &one);
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    pools[dev] = pool;
+    return pool;
+}
+
+int staging_alloc(int dev, size_t bytes, cudaStream_t st, void** out) {
+    cudaMemPool_t pool = staging_pool(dev);
+    if (!pool) return fail(MPX_ERR_OTHER, "cannot create the staging memory pool on device %d", dev);
+    MPX_CU(cudaMallocFromPoolAsync(out, bytes ? bytes : 1, pool, st));
+    return MPX_SUCCESS;
+}
+
 int record_new_event(cudaStream_t s, cudaEvent_t* ev) {
     MPX_CU(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     MPX_CU(cudaEventRecord(*ev, s));
@@ -313,9 +351,9 @@ int ensure_peer(World* w, int a, int b) {
         cudaError_t e = cudaDeviceEnablePeerAccess(pr.second, 0);
         if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
         else if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
-        // staging from the default pool of pr.second must be readable from pr.first
-        cudaMemPool_t pool;
-        MPX_CU(cudaDeviceGetDefaultMemPool(&pool, pr.second));
+        // staging of pr.second must be readable from pr.first
+        cudaMemPool_t pool = staging_pool(pr.second);
+        if (!pool) return fail(MPX_ERR_OTHER, "no staging pool on device %d", pr.second);
         cudaMemAccessDesc d{};
         d.location.type = cudaMemLocationTypeDevice;
         d.location.id = pr.first;
@@ -344,7 +382,7 @@ int transfer(int dev, cudaStream_t st, const Side& s, const Side& r, int64_t mov
         return launch_move(dev, s.dt, s.count, true, s.buf, static_cast<uint8_t*>(r.buf) + off, s.bytes, st);
     MPX_RC(set_device(dev));
     void* tmp = nullptr;
-    MPX_CU(cudaMallocAsync(&tmp, (size_t)s.bytes, st));
+    MPX_RC(staging_alloc(dev, (size_t)s.bytes, st, &tmp));
     MPX_RC(launch_move(dev, s.dt, s.count, true, s.buf, tmp, s.bytes, st));
     MPX_RC(launch_move(dev, r.dt, r.count, false, tmp, r.buf, moved, st));
     MPX_CU(cudaFreeAsync(tmp, st));
@@ -366,7 +404,7 @@ void fill_status(const std::shared_ptr<ReqState>& q, const Side& mine, int src, 
 // Eager send: pack at the sender's stream position into a staging buffer.
 int stage_send(const std::shared_ptr<Comm>& c, PendingSend& ps) {
     MPX_RC(set_device(c->device));
-    MPX_CU(cudaMallocAsync(&ps.staging, (size_t)std::max<int64_t>(ps.s.bytes, 1), c->stream));
+    MPX_RC(staging_alloc(c->device, (size_t)ps.s.bytes, c->stream, &ps.staging));
     MPX_RC(launch_move(c->device, ps.s.dt, ps.s.count, true, ps.s.buf, ps.staging, ps.s.bytes, c->stream));
     return MPX_SUCCESS;
 }

@@ -3,6 +3,11 @@ import json
 import os
 import sys
 
+# one hardware queue per stream (set before any CUDA context exists): stream
+# communicators block streams in memop waits, which must never stall an
+# unrelated stream that shares a hardware queue
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
