@@ -24,6 +24,9 @@ import threading
 import time
 
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# eager module loading: with lazy loading the first launch of any kernel waits
+# behind a stream parked in a stream-memop wait (measured: tools/diag_memop.py)
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))

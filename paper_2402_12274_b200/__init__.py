@@ -18,6 +18,11 @@ import os as _os
 # give every stream its own hardware queue so a waiting stream never blocks
 # an unrelated one (takes effect if set before the CUDA context exists).
 _os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# Lazy module loading makes the first launch of any kernel wait behind a
+# stream parked in a stream-memop wait -- even on other streams (measured with
+# tools/diag_memop.py).  libmpx force-loads its own kernels at world join;
+# eager loading covers the caller's kernels too.
+_os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 from .errors import (  # noqa: F401,E402
     MinimpiError, StateError, PendingError, ArgError, TransportError,

@@ -35,6 +35,16 @@ int sms(int device) {
 
 }  // namespace
 
+cudaError_t preload_coll_kernels() {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaSuccess, r;
+    if ((r = cudaFuncGetAttributes(&a, k_allreduce_oneshot<int32_t, uint32_t>)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_allreduce_oneshot<long long, unsigned long long>)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_allreduce_oneshot<float, double>)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_allreduce_oneshot<double, double>)) != cudaSuccess) e = r;
+    return e;
+}
+
 cudaError_t launch_allreduce_oneshot(const CollTable* table, int n, int rank, int64_t count, int dtype_code,
                                      int device, cudaStream_t stream) {
     const int64_t chunk = (count + n - 1) / n;

@@ -23,4 +23,6 @@ struct CollTable {
 cudaError_t launch_allreduce_oneshot(const CollTable* table, int n, int rank, int64_t count, int dtype_code,
                                      int device, cudaStream_t stream);
 
+cudaError_t preload_coll_kernels();
+
 }  // namespace mpx

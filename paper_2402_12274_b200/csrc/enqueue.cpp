@@ -44,6 +44,7 @@
 
 #include "capi_common.hpp"
 #include "coll.hpp"
+#include "kernels.hpp"
 #include "mpx.h"
 
 namespace mpx {
@@ -704,6 +705,8 @@ int mpx_world_join(const char* group, int size, int rank, int device, int64_t ea
     MPX_CU(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(MPX_ERR_ARG, "device %d not present (%d devices)", device, ndev);
     MPX_RC(set_device(device));
+    MPX_CU(preload_pack_kernels());
+    MPX_CU(preload_coll_kernels());
     std::lock_guard<std::mutex> g(g_worlds_mu);
     World*& w = g_worlds[group];
     if (!w) {

@@ -382,6 +382,22 @@ cudaError_t launch_generic(const Plan& p, bool pack, const uint8_t* src, uint8_t
     return cudaGetLastError();
 }
 
+// Force-load every kernel of this translation unit on the current device.
+// With CUDA lazy module loading, the first launch of a kernel loads its module
+// and that load waits behind any stream parked in a stream-memop wait (even on
+// other streams): a rank's first pack could then deadlock against a peer.
+cudaError_t preload_pack_kernels() {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaSuccess, r;
+    if ((r = cudaFuncGetAttributes(&a, k_chain<true>)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_chain<false>)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_generic<true>)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_generic<false>)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_ordered_unpack)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_iov)) != cudaSuccess) e = r;
+    return e;
+}
+
 cudaError_t launch_iov(const Plan& p, int64_t k0, int64_t n, int64_t* out, cudaStream_t stream) {
     if (n <= 0) return cudaSuccess;
     const int64_t want = (n + 255) / 256;

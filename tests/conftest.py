@@ -7,6 +7,9 @@ import sys
 # communicators block streams in memop waits, which must never stall an
 # unrelated stream that shares a hardware queue
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# eager module loading: with lazy loading the first launch of any kernel waits
+# behind a stream parked in a stream-memop wait (measured: tools/diag_memop.py)
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 import pytest
 
