@@ -9,11 +9,21 @@ namespace mpx {
 
 constexpr int kMaxCollRanks = 64;
 
-// per-call pointer table in pinned host memory, filled by each rank's host
-// thread before its "arrived" flag is written
+constexpr int kCollSlots = 64;
+
+// per-call pointer table in pinned host memory; each rank's STREAM writes its
+// two pointers with 64-bit stream memops before its "arrived" flag, so a slot
+// is only rewritten once every rank's stream is past the previous use
 struct CollTable {
     const void* send[kMaxCollRanks];
     void* recv[kMaxCollRanks];
+};
+
+// ring of collective slots of one communicator context (pinned, mapped)
+struct CollRing {
+    CollTable table[kCollSlots];
+    uint32_t arrive[kCollSlots][kMaxCollRanks];
+    uint32_t finish[kCollSlots][kMaxCollRanks];
 };
 
 // Rank `rank` of `n` reduces its 1/n slice of the buffers: out = x0 + x1 + ...

@@ -31,6 +31,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstring>
 #include <atomic>
 #include <condition_variable>
 #include <deque>
@@ -88,9 +89,12 @@ using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int
 using WriteValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 using ErrStrFn = CUresult (*)(CUresult, const char**);
 
+using WriteValue64Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+
 struct MemOps {
     WaitValueFn wait = nullptr;
     WriteValueFn write = nullptr;
+    WriteValue64Fn write64 = nullptr;
     ErrStrFn err = nullptr;
 };
 
@@ -101,6 +105,8 @@ const MemOps& memops() {
         cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", reinterpret_cast<void**>(&r.wait), 12000,
                                          cudaEnableDefault, &q);
         cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", reinterpret_cast<void**>(&r.write), 12000,
+                                         cudaEnableDefault, &q);
+        cudaGetDriverEntryPointByVersion("cuStreamWriteValue64", reinterpret_cast<void**>(&r.write64), 12000,
                                          cudaEnableDefault, &q);
         cudaGetDriverEntryPointByVersion("cuGetErrorString", reinterpret_cast<void**>(&r.err), 6000,
                                          cudaEnableDefault, &q);
@@ -121,6 +127,13 @@ int wait_flag(cudaStream_t s, uint32_t* addr, uint32_t gen) {
     CUresult r = memops().wait(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), gen,
                                CU_STREAM_WAIT_VALUE_GEQ);
     return r == CUDA_SUCCESS ? MPX_SUCCESS : memop_fail(r, "cuStreamWaitValue32");
+}
+
+int write_ptr(cudaStream_t s, const void* const* addr, const void* value) {
+    if (!memops().write64) return fail(MPX_ERR_UNSUPPORTED, "cuStreamWriteValue64 unavailable");
+    CUresult r = memops().write64(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr),
+                                  (cuuint64_t) reinterpret_cast<uintptr_t>(value), CU_STREAM_WRITE_VALUE_DEFAULT);
+    return r == CUDA_SUCCESS ? MPX_SUCCESS : memop_fail(r, "cuStreamWriteValue64");
 }
 
 int write_flag(cudaStream_t s, uint32_t* addr, uint32_t gen) {
@@ -245,18 +258,6 @@ struct Mailbox {
     std::deque<PendingRecv> recvs;  // posted (unmatched) recvs of this rank
 };
 
-struct CollSlot {             // native allreduce rendezvous of one collective call
-    int arrived_host = 0;
-    CollTable* table = nullptr;   // pinned mapped: per-rank pointers
-    uint32_t* arrive = nullptr;   // pinned flags, one per rank (then finish flags)
-    uint32_t* finish = nullptr;
-    uint32_t gen = 1;
-    ~CollSlot() {
-        if (table) cudaFreeHost(table);
-        if (arrive) cudaFreeHost(arrive);
-    }
-};
-
 struct World {
     std::string group;
     int size = 0;
@@ -269,7 +270,7 @@ struct World {
     std::mutex peer_mu;
     std::set<std::pair<int, int>> peer_on;
     std::mutex coll_mu;
-    std::map<std::pair<int, int64_t>, std::shared_ptr<CollSlot>> colls;
+    std::map<int, CollRing*> rings;  // per context id, created at comm creation
     std::mutex nccl_mu;
     std::condition_variable nccl_cv;
     std::vector<ncclComm_t> nccl;   // per rank, by ncclCommInitAll
@@ -310,12 +311,11 @@ struct Comm {
     std::deque<std::pair<int, std::string>> deferred;
     std::atomic<int64_t> outstanding{0};
     int64_t coll_seq = 0;
+    CollRing* ring = nullptr;
 };
 
 namespace {
 
-std::mutex g_hold_mu;
-std::vector<std::pair<cudaEvent_t, std::shared_ptr<CollSlot>>> g_hold;
 std::mutex g_worlds_mu;
 std::map<std::string, World*> g_worlds;
 std::mutex g_handles_mu;
@@ -339,29 +339,44 @@ void defer_error(const std::shared_ptr<Comm>& c, int code, const std::string& ms
     c->deferred.emplace_back(code, msg);
 }
 
-// enable peer access both ways between two devices (idempotent)
-int ensure_peer(World* w, int a, int b) {
-    if (a == b) return MPX_SUCCESS;
-    std::lock_guard<std::mutex> g(w->peer_mu);
-    for (auto pr : {std::make_pair(a, b), std::make_pair(b, a)}) {
-        if (w->peer_on.count(pr)) continue;
-        int can = 0;
-        MPX_CU(cudaDeviceCanAccessPeer(&can, pr.first, pr.second));
-        if (!can) return fail(MPX_ERR_TRANSPORT, "device %d cannot access device %d", pr.first, pr.second);
-        MPX_RC(set_device(pr.first));
-        cudaError_t e = cudaDeviceEnablePeerAccess(pr.second, 0);
-        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
-        else if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
-        // staging of pr.second must be readable from pr.first
-        cudaMemPool_t pool = staging_pool(pr.second);
-        if (!pool) return fail(MPX_ERR_OTHER, "no staging pool on device %d", pr.second);
-        cudaMemAccessDesc d{};
-        d.location.type = cudaMemLocationTypeDevice;
-        d.location.id = pr.first;
-        d.flags = cudaMemAccessFlagsProtReadWrite;
-        MPX_CU(cudaMemPoolSetAccess(pool, &d, 1));
-        w->peer_on.insert(pr);
+// Per-device setup done once, at world join (never on the data path: these
+// calls may synchronise with streams that are parked in memop waits):
+// peer access to every peer device, the staging pool readable from them, the
+// world's service stream.
+int setup_device(World* w, int dev, int ndev) {
+    static std::mutex mu;
+    static std::set<int> done;
+    std::lock_guard<std::mutex> g(mu);
+    MPX_RC(set_device(dev));
+    if (!done.count(dev)) {
+        cudaMemPool_t pool = staging_pool(dev);
+        if (!pool) return fail(MPX_ERR_OTHER, "cannot create the staging memory pool on device %d", dev);
+        for (int peer = 0; peer < ndev; ++peer) {
+            if (peer == dev) continue;
+            int can = 0;
+            MPX_CU(cudaDeviceCanAccessPeer(&can, dev, peer));
+            if (!can) continue;
+            cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            else if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+            cudaMemAccessDesc d{};
+            d.location.type = cudaMemLocationTypeDevice;
+            d.location.id = peer;
+            d.flags = cudaMemAccessFlagsProtReadWrite;
+            MPX_CU(cudaMemPoolSetAccess(pool, &d, 1));
+        }
+        done.insert(dev);
     }
+    w->service(dev);
+    return set_device(dev);
+}
+
+int ensure_peer(World* w, int a, int b) {
+    (void)w;
+    if (a == b) return MPX_SUCCESS;
+    int can = 0;
+    MPX_CU(cudaDeviceCanAccessPeer(&can, a, b));
+    if (!can) return fail(MPX_ERR_TRANSPORT, "device %d cannot access device %d", a, b);
     return MPX_SUCCESS;
 }
 
@@ -707,6 +722,7 @@ int mpx_world_join(const char* group, int size, int rank, int device, int64_t ea
     MPX_RC(set_device(device));
     MPX_CU(preload_pack_kernels());
     MPX_CU(preload_coll_kernels());
+    (void)staging_pool(device);
     std::lock_guard<std::mutex> g(g_worlds_mu);
     World*& w = g_worlds[group];
     if (!w) {
@@ -726,6 +742,7 @@ int mpx_world_join(const char* group, int size, int rank, int device, int64_t ea
     }
     if (w->size != size) return fail(MPX_ERR_ARG, "world %s has %d ranks, not %d", group, w->size, size);
     if (w->joined[rank]) return fail(MPX_ERR_STATE, "rank %d already joined world %s", rank, group);
+    MPX_RC(setup_device(w, device, ndev));
     w->joined[rank] = true;
     w->devices[rank] = device;
     w->live++;
@@ -741,6 +758,7 @@ int mpx_world_leave(mpx_world h, int rank) {
     if (rank < 0 || rank >= w->size || !w->joined[rank]) return fail(MPX_ERR_STATE, "rank %d not in world", rank);
     w->joined[rank] = false;
     if (--w->live == 0) {
+        for (auto& kv : w->rings) cudaFreeHost(kv.second);
         if (w->nccl_state == 2)
             for (auto cm : w->nccl)
                 if (cm) g_nccl.commDestroy(cm);
@@ -763,6 +781,17 @@ int mpx_comm_create(mpx_world h, int rank, int ctx, void* stream, mpx_comm* out)
     c->stream = reinterpret_cast<cudaStream_t>(stream);
     cudaError_t e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate(side)");
+    {   // collective slot ring shared by every rank of this context (setup time:
+        // cudaHostAlloc must not run while peers' streams may be parked)
+        std::lock_guard<std::mutex> g(w->coll_mu);
+        CollRing*& ring = w->rings[ctx];
+        if (!ring) {
+            MPX_CU(cudaHostAlloc(reinterpret_cast<void**>(&ring), sizeof(CollRing),
+                                 cudaHostAllocMapped | cudaHostAllocPortable));
+            std::memset(ring, 0, sizeof(CollRing));
+        }
+        c->ring = ring;
+    }
     std::lock_guard<std::mutex> g(g_handles_mu);
     g_comms[c.get()] = c;
     *out = reinterpret_cast<mpx_comm>(c.get());
@@ -920,53 +949,25 @@ int mpx_allreduce_enqueue(mpx_comm h, const void* sendbuf, void* recvbuf, int64_
         if (r != ncclSuccess) return fail(MPX_ERR_TRANSPORT, "ncclAllReduce: %s", g_nccl.errStr(r));
         return MPX_SUCCESS;
     }
-    // native one-shot: every rank registers its buffers, then all streams meet
+    // native one-shot: every rank's stream publishes its buffers and arrives,
+    // waits for all, reduces its slice into every rank, then meets again
+    if (w->size > kMaxCollRanks) return fail(MPX_ERR_UNSUPPORTED, "native allreduce supports <= %d ranks", kMaxCollRanks);
     const int64_t seq = c->coll_seq++;
-    std::shared_ptr<CollSlot> slot;
-    {
-        std::lock_guard<std::mutex> g(w->coll_mu);
-        auto& sp = w->colls[{c->ctx, seq}];
-        if (!sp) {
-            sp = std::make_shared<CollSlot>();
-            MPX_CU(cudaHostAlloc(reinterpret_cast<void**>(&sp->table), sizeof(CollTable),
-                                 cudaHostAllocMapped | cudaHostAllocPortable));
-            MPX_CU(cudaHostAlloc(reinterpret_cast<void**>(&sp->arrive), 2 * sizeof(uint32_t) * kMaxCollRanks,
-                                 cudaHostAllocMapped | cudaHostAllocPortable));
-            std::fill(sp->arrive, sp->arrive + 2 * kMaxCollRanks, 0u);
-            sp->finish = sp->arrive + kMaxCollRanks;
-        }
-        slot = sp;
-        if (w->size > kMaxCollRanks) return fail(MPX_ERR_UNSUPPORTED, "native allreduce supports <= %d ranks", kMaxCollRanks);
-        slot->table->send[c->rank] = sendbuf;
-        slot->table->recv[c->rank] = recvbuf;
-        if (++slot->arrived_host == w->size) w->colls.erase({c->ctx, seq});
-    }
+    const int slot = (int)(seq % kCollSlots);
+    const uint32_t gen = (uint32_t)(seq / kCollSlots + 1);
+    CollRing* ring = c->ring;
     for (int j = 0; j < w->size; ++j)
         if (w->devices[j] != c->device) MPX_RC(ensure_peer(w, c->device, w->devices[j]));
     MPX_RC(set_device(c->device));
-    MPX_RC(write_flag(c->stream, slot->arrive + c->rank, slot->gen));
-    for (int j = 0; j < w->size; ++j) MPX_RC(wait_flag(c->stream, slot->arrive + j, slot->gen));
-    cudaError_t e = launch_allreduce_oneshot(slot->table, w->size, c->rank, count, dtype_code, c->device, c->stream);
+    CollTable* tab = &ring->table[slot];
+    MPX_RC(write_ptr(c->stream, &tab->send[c->rank], sendbuf));
+    MPX_RC(write_ptr(c->stream, (const void* const*)&tab->recv[c->rank], recvbuf));
+    MPX_RC(write_flag(c->stream, &ring->arrive[slot][c->rank], gen));
+    for (int j = 0; j < w->size; ++j) MPX_RC(wait_flag(c->stream, &ring->arrive[slot][j], gen));
+    cudaError_t e = launch_allreduce_oneshot(tab, w->size, c->rank, count, dtype_code, c->device, c->stream);
     if (e != cudaSuccess) return cuda_fail(e, "allreduce launch");
-    MPX_RC(write_flag(c->stream, slot->finish + c->rank, slot->gen));
-    for (int j = 0; j < w->size; ++j) MPX_RC(wait_flag(c->stream, slot->finish + j, slot->gen));
-    // keep the slot's pinned table/flags alive until this rank's stream is
-    // past it (every rank holds a reference; the last release frees it)
-    cudaEvent_t keep;
-    MPX_RC(record_new_event(c->stream, &keep));
-    std::lock_guard<std::mutex> g(g_hold_mu);
-    auto it = g_hold.begin();
-    while (it != g_hold.end()) {
-        cudaError_t q = cudaEventQuery(it->first);
-        if (q == cudaErrorNotReady) {
-            ++it;
-            continue;
-        }
-        cudaGetLastError();
-        cudaEventDestroy(it->first);
-        it = g_hold.erase(it);
-    }
-    g_hold.emplace_back(keep, slot);
+    MPX_RC(write_flag(c->stream, &ring->finish[slot][c->rank], gen));
+    for (int j = 0; j < w->size; ++j) MPX_RC(wait_flag(c->stream, &ring->finish[slot][j], gen));
     return MPX_SUCCESS;
 }
 

@@ -9,14 +9,20 @@
 
 namespace mpx {
 
+namespace {
+cudaStream_t upload_stream(int device);
+cudaMemPool_t desc_pool(int device);
+}  // namespace
+
+// Never blocks: the descriptor goes back to its stream-ordered pool on the
+// upload stream (cudaFree would synchronise the device, which may hold
+// streams parked in stream-memop waits on other ranks).
 Plan::~Plan() {
-    if (blob || host_blob || ready) {
+    if (blob || ready) {
         int cur = -1;
         cudaGetDevice(&cur);
         if (device >= 0 && cur != device) cudaSetDevice(device);
-        if (ready) cudaEventSynchronize(ready);
-        if (blob) cudaFree(blob);
-        if (host_blob) cudaFreeHost(host_blob);
+        if (blob) cudaFreeAsync(blob, upload_stream(device));
         if (ready) cudaEventDestroy(ready);
         if (device >= 0 && cur != device && cur >= 0) cudaSetDevice(cur);
     }
@@ -35,6 +41,30 @@ cudaError_t plan_wait(Plan& p, cudaStream_t stream) {
 }
 
 namespace {
+// stream-ordered pool for descriptors (no hidden inter-stream dependencies)
+cudaMemPool_t desc_pool(int device) {
+    static std::mutex mu;
+    static std::map<int, cudaMemPool_t> pools;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = pools.find(device);
+    if (it != pools.end()) return it->second;
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    int zero = 0;
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &zero);
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    pools[device] = pool;
+    return pool;
+}
+
 // one internal upload stream per device: descriptor uploads never
 // synchronise (or even touch) the caller's stream
 cudaStream_t upload_stream(int device) {
@@ -219,20 +249,19 @@ std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStre
         }
         (void)stream;
         void* dev = nullptr;
-        cudaError_t e = cudaMalloc(&dev, host.size());
+        cudaStream_t up = upload_stream(device);
+        cudaMemPool_t pool = desc_pool(device);
+        cudaError_t e = pool ? cudaMallocFromPoolAsync(&dev, host.size(), pool, up) : cudaErrorMemoryAllocation;
         if (e != cudaSuccess) {
-            *err = std::string("cudaMalloc(descriptor): ") + cudaGetErrorString(e);
+            *err = std::string("descriptor allocation: ") + cudaGetErrorString(e);
             return nullptr;
         }
         p->blob = dev;
-        e = cudaHostAlloc(&p->host_blob, host.size(), cudaHostAllocDefault);
-        if (e == cudaSuccess) {
-            std::memcpy(p->host_blob, host.data(), host.size());
-            cudaStream_t up = upload_stream(device);
-            e = cudaMemcpyAsync(dev, p->host_blob, host.size(), cudaMemcpyHostToDevice, up);
-            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ready, cudaEventDisableTiming);
-            if (e == cudaSuccess) e = cudaEventRecord(p->ready, up);
-        }
+        // pageable source: the call returns once the bytes are staged, so the
+        // host vector may die; only the (private) upload stream is involved
+        e = cudaMemcpyAsync(dev, host.data(), host.size(), cudaMemcpyHostToDevice, up);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ready, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventRecord(p->ready, up);
         if (e != cudaSuccess) {
             *err = std::string("descriptor upload: ") + cudaGetErrorString(e);
             return nullptr;

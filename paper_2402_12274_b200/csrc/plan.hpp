@@ -25,7 +25,6 @@ struct Plan {
     int32_t chain_align = 16;  // largest power of two dividing base, L and strides
     DDesc desc{};           // device descriptor (always built, used by iov + generic)
     void* blob = nullptr;   // device allocation backing desc
-    void* host_blob = nullptr;  // pinned source of the upload (kept until freed)
     size_t blob_bytes = 0;
     cudaEvent_t ready = nullptr;     // upload finished (recorded on an internal stream)
     std::atomic<bool> ready_seen{false};
