@@ -38,6 +38,52 @@ struct Chain {
     int32_t s32_cnt[kMaxChain];
 };
 
+// ---- span lowering (struct / indexed / nested types with small elements) ----
+// Outer Rep levels stay symbolic; everything below is decomposed on the host
+// into chunks of consecutive elements of a small "body" (<= kSpanMaxBody bytes
+// of span).  A chunk's source span is contiguous, so a warp stages it in
+// shared memory with aligned 16-byte loads and produces the other side word by
+// word through the body's byte maps.
+constexpr int kSpanMaxBody = 256;
+constexpr int kSpanMaxBodies = 8;
+constexpr int kSpanStage = 4096;     // bytes staged per warp (plus 16 B slack)
+constexpr int kSpanMaxOuter = 2;
+
+struct SpanBody {
+    int32_t span_lo;        // element span start relative to its frame origin
+    int32_t span_len;       // element span bytes (<= kSpanMaxBody)
+    int32_t nbytes;         // payload bytes per element
+    uint32_t m32_nbytes;    // magic for q / nbytes
+    int32_t s32_nbytes;
+    int32_t pad;
+    int16_t fwd[kSpanMaxBody];  // span offset -> packed offset in element, -1 = gap
+    int16_t inv[kSpanMaxBody];  // packed offset in element -> span offset
+    int32_t pad2[2];
+};
+static_assert(sizeof(SpanBody) % 16 == 0, "SpanBody must be 16-byte sized");
+
+struct SpanChunk {
+    int64_t src;            // frame origin of element 0 (layout offset)
+    int64_t pk;             // packed offset of element 0
+    int32_t n;              // elements
+    int32_t body;           // body index, -1 = raw contiguous piece of `stride` bytes
+    int32_t stride;         // element stride in bytes (>= span_len when n > 1)
+    uint32_t m32_stride;
+    int32_t s32_stride;
+    int32_t pad;
+};
+
+struct SpanPlan {
+    const SpanChunk* chunks;
+    const SpanBody* bodies;
+    int32_t nchunks, nbodies;
+    int32_t outer_depth, pad;
+    int64_t outer_cnt[kSpanMaxOuter];
+    int64_t outer_str[kSpanMaxOuter];   // layout stride per outer level
+    int64_t outer_pk[kSpanMaxOuter];    // packed stride per outer level
+    int64_t nunits;                     // prod(outer_cnt) * nchunks
+};
+
 struct DNode {
     int32_t kind;           // 0 empty, 1 run, 2 rep, 3 seq
     int32_t nkids;          // seq

@@ -285,6 +285,129 @@ k_generic(const DDesc d, const uint8_t* __restrict__ src, uint8_t* __restrict__ 
     }
 }
 
+// ---------------------------------------------------------------- span
+constexpr int kSpanWarps = 8;
+constexpr size_t kSpanSmem = size_t(kSpanMaxBodies) * sizeof(SpanBody) + size_t(kSpanWarps) * (kSpanStage + 32);
+
+// One warp per chunk: stage the chunk's contiguous input span (layout span for
+// pack, packed bytes for unpack) in shared memory with aligned 16-byte loads,
+// then produce the output side as 4-byte words aligned to the destination
+// (coalesced 128 B per warp instruction), every byte located in O(1) through
+// the body's byte maps.  Bytes outside the runs are never written.
+template <bool PACK>
+__global__ void __launch_bounds__(kSpanWarps * 32)
+k_span(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t limit) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    SpanBody* bodies = reinterpret_cast<SpanBody*>(sm);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint8_t* stage = sm + kSpanMaxBodies * sizeof(SpanBody) + warp * (kSpanStage + 32);
+    {
+        const int nv = sp.nbodies * (int)(sizeof(SpanBody) / 16);
+        const uint4* g = reinterpret_cast<const uint4*>(sp.bodies);
+        for (int i = threadIdx.x; i < nv; i += blockDim.x) reinterpret_cast<uint4*>(sm)[i] = __ldg(g + i);
+    }
+    __syncthreads();
+    const int64_t stride_u = (int64_t)gridDim.x * kSpanWarps;
+    for (int64_t u = (int64_t)blockIdx.x * kSpanWarps + warp; u < sp.nunits; u += stride_u) {
+        const int64_t c = u % sp.nchunks;
+        int64_t o = u / sp.nchunks, loff = 0, poff = 0;
+        for (int i = sp.outer_depth - 1; i >= 0; --i) {
+            const int64_t idx = o % sp.outer_cnt[i];
+            o /= sp.outer_cnt[i];
+            loff += idx * sp.outer_str[i];
+            poff += idx * sp.outer_pk[i];
+        }
+        const SpanChunk* chp = sp.chunks + c;
+        const int64_t ch_src = __ldg(&chp->src), ch_pk = __ldg(&chp->pk);
+        const int ch_n = __ldg(&chp->n), ch_body = __ldg(&chp->body), ch_stride = __ldg(&chp->stride);
+        const bool raw = ch_body < 0;
+        const SpanBody* B = raw ? nullptr : bodies + ch_body;
+        const int span_len = raw ? ch_stride : (ch_n - 1) * ch_stride + B->span_len;
+        const int out_len = raw ? ch_stride : ch_n * B->nbytes;
+        const int64_t lay0 = ch_src + loff, pk0 = ch_pk + poff;
+        if (!PACK && pk0 >= limit) continue;
+        const int qlim = (int)min((int64_t)out_len, limit - pk0);
+        if (PACK) {
+            const uint8_t* g = src + lay0;
+            const int a = (int)(reinterpret_cast<uintptr_t>(g) & 15);
+            const uint4* g16 = reinterpret_cast<const uint4*>(g - a);
+            const int nv = (a + span_len + 15) >> 4;
+            for (int i = lane; i < nv; i += 32) reinterpret_cast<uint4*>(stage)[i] = __ldg(g16 + i);
+            __syncwarp();
+            uint8_t* d = dst + pk0;
+            const int b = (int)(reinterpret_cast<uintptr_t>(d) & 3);
+            uint32_t* d4 = reinterpret_cast<uint32_t*>(d - b);
+            const int nw = (b + out_len + 3) >> 2;
+            for (int w = lane; w < nw; w += 32) {
+                uint32_t word = 0;
+                int mask = 0;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int q = 4 * w + t - b;
+                    if (q >= 0 && q < out_len) {
+                        int so = q;
+                        if (!raw) {
+                            const int e = (int)fdiv32((uint32_t)q, B->m32_nbytes, B->s32_nbytes);
+                            so = e * ch_stride + B->inv[q - e * B->nbytes];
+                        }
+                        word |= (uint32_t)stage[a + so] << (8 * t);
+                        mask |= 1 << t;
+                    }
+                }
+                if (mask == 0xF) {
+                    d4[w] = word;
+                } else {
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        if (mask & (1 << t)) reinterpret_cast<uint8_t*>(d4)[4 * w + t] = (uint8_t)(word >> (8 * t));
+                }
+            }
+        } else {
+            const uint8_t* g = src + pk0;
+            const int a = (int)(reinterpret_cast<uintptr_t>(g) & 15);
+            const uint4* g16 = reinterpret_cast<const uint4*>(g - a);
+            const int nv = (a + qlim + 15) >> 4;
+            for (int i = lane; i < nv; i += 32) reinterpret_cast<uint4*>(stage)[i] = __ldg(g16 + i);
+            __syncwarp();
+            uint8_t* d = dst + lay0;
+            const int b = (int)(reinterpret_cast<uintptr_t>(d) & 3);
+            uint32_t* d4 = reinterpret_cast<uint32_t*>(d - b);
+            const int nw = (b + span_len + 3) >> 2;
+            for (int w = lane; w < nw; w += 32) {
+                uint32_t word = 0;
+                int mask = 0;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int dd = 4 * w + t - b;
+                    if (dd >= 0 && dd < span_len) {
+                        int q = dd;
+                        if (!raw) {
+                            const int e = ch_n > 1 ? (int)fdiv32((uint32_t)dd, __ldg(&chp->m32_stride),
+                                                                 __ldg(&chp->s32_stride))
+                                                   : 0;
+                            const int off = dd - e * ch_stride;
+                            const int fw = off < B->span_len ? B->fwd[off] : -1;
+                            q = fw < 0 ? -1 : e * B->nbytes + fw;
+                        }
+                        if (q >= 0 && q < qlim) {
+                            word |= (uint32_t)stage[a + q] << (8 * t);
+                            mask |= 1 << t;
+                        }
+                    }
+                }
+                if (mask == 0xF) {
+                    d4[w] = word;
+                } else if (mask) {
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        if (mask & (1 << t)) reinterpret_cast<uint8_t*>(d4)[4 * w + t] = (uint8_t)(word >> (8 * t));
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
 // ------------------------------------------------------- ordered unpack
 __global__ void __launch_bounds__(32)
 k_ordered_unpack(const DDesc d, const uint8_t* __restrict__ src, uint8_t* dst, int64_t limit) {
@@ -395,7 +518,19 @@ cudaError_t preload_pack_kernels() {
     if ((r = cudaFuncGetAttributes(&a, k_generic<false>)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_ordered_unpack)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_iov)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_span<true>)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_span<false>)) != cudaSuccess) e = r;
     return e;
+}
+
+cudaError_t launch_span(const Plan& p, bool pack, const uint8_t* src, uint8_t* dst, int64_t limit,
+                        cudaStream_t stream) {
+    if (limit <= 0 || p.span.nunits == 0) return cudaSuccess;
+    const int64_t want = (p.span.nunits + kSpanWarps - 1) / kSpanWarps;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count(p.device) * 5));
+    if (pack) k_span<true><<<(unsigned)grid, kSpanWarps * 32, kSpanSmem, stream>>>(p.span, src, dst, limit);
+    else k_span<false><<<(unsigned)grid, kSpanWarps * 32, kSpanSmem, stream>>>(p.span, src, dst, limit);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_iov(const Plan& p, int64_t k0, int64_t n, int64_t* out, cudaStream_t stream) {

@@ -38,6 +38,8 @@ void chain_setup(const Plan& p, bool pack, ChainJob* j);
 cudaError_t launch_chain_batch(ChainBatch& b, bool pack, int device, cudaStream_t stream);
 cudaError_t launch_generic(const Plan& p, bool pack, const uint8_t* src, uint8_t* dst, int64_t limit,
                            cudaStream_t stream);
+cudaError_t launch_span(const Plan& p, bool pack, const uint8_t* src, uint8_t* dst, int64_t limit,
+                        cudaStream_t stream);
 cudaError_t launch_iov(const Plan& p, int64_t k0, int64_t n, int64_t* out, cudaStream_t stream);
 // force-load the pack/unpack/iov kernels on the current device (lazy loading)
 cudaError_t preload_pack_kernels();

@@ -173,6 +173,146 @@ struct Flattener {
     }
 };
 
+// ------------------------------------------------------------ span lowering
+class SpanBuilder {
+  public:
+    static constexpr int64_t kMaxChunks = int64_t(1) << 21;
+    std::vector<SpanChunk> chunks;
+    std::vector<SpanBody> bodies;
+    bool ok = true;
+
+    bool small(const Node* n) const {
+        return n->runs > 0 && n->runs <= 32 && n->max_end - n->min_off <= kSpanMaxBody;
+    }
+
+    void emit(const Node* n, int64_t shift, int64_t poff) {
+        if (!ok || n->runs == 0) return;
+        if ((int64_t)chunks.size() > kMaxChunks) { ok = false; return; }
+        if (small(n)) {   // chunk src = span start of the element
+            add(shift + n->min_off, poff, 1, body_of(n), 0);
+            return;
+        }
+        switch (n->kind) {
+        case Kind::Run: {   // large contiguous run: raw pieces
+            const int64_t piece = kSpanStage - 16;
+            for (int64_t o = 0; o < n->len; o += piece)
+                add_raw(shift + n->off + o, poff + o, std::min(piece, n->len - o));
+            return;
+        }
+        case Kind::Rep: {
+            const Node* b = n->body.get();
+            if (small(b)) {
+                const int64_t span = b->max_end - b->min_off;
+                if (n->stride < span) {   // element spans interleave or stride < 0
+                    ok = false;
+                    return;
+                }
+                const int64_t room = kSpanStage - 16;
+                int64_t epc = n->stride > 0 ? (room - span) / n->stride + 1 : 1;
+                epc = std::max<int64_t>(1, std::min({epc, room / std::max<int64_t>(1, b->nbytes), n->count}));
+                const int body = body_of(b);
+                for (int64_t k = 0; k < n->count && ok; k += epc)
+                    add(shift + n->base + b->min_off + k * n->stride, poff + k * b->nbytes,
+                        std::min(epc, n->count - k), body, n->stride);
+                return;
+            }
+            for (int64_t k = 0; k < n->count && ok; ++k)
+                emit(b, shift + n->base + k * n->stride, poff + k * b->nbytes);
+            return;
+        }
+        case Kind::Seq:
+            for (size_t i = 0; i < n->kids.size() && ok; ++i) emit(n->kids[i].get(), shift, poff + n->byte_prefix[i]);
+            return;
+        default: return;
+        }
+    }
+
+  private:
+    std::map<std::vector<int64_t>, int> ids_;
+
+    // body = the element's runs relative to its span start (dedupe key)
+    int body_of(const Node* n) {
+        std::vector<int64_t> runs;
+        tree::enumerate(n, -n->min_off, runs, 64);
+        auto it = ids_.find(runs);
+        if (it != ids_.end()) return it->second;
+        if ((int)bodies.size() >= kSpanMaxBodies) { ok = false; return 0; }
+        SpanBody b;
+        std::memset(&b, 0, sizeof b);
+        b.span_lo = 0;
+        b.span_len = (int32_t)(n->max_end - n->min_off);
+        b.nbytes = (int32_t)n->nbytes;
+        host_magic32((uint32_t)b.nbytes, &b.m32_nbytes, &b.s32_nbytes);
+        for (int i = 0; i < kSpanMaxBody; ++i) b.fwd[i] = b.inv[i] = -1;
+        int64_t q = 0;
+        for (size_t r = 0; r + 1 < runs.size(); r += 2)
+            for (int64_t x = 0; x < runs[r + 1]; ++x, ++q) {
+                const int64_t so = runs[r] + x;
+                if (b.fwd[so] >= 0) { ok = false; return 0; }   // self-overlapping element
+                b.fwd[so] = (int16_t)q;
+                b.inv[q] = (int16_t)so;
+            }
+        const int id = (int)bodies.size();
+        bodies.push_back(b);
+        ids_[runs] = id;
+        return id;
+    }
+
+    void add(int64_t src, int64_t pk, int64_t n, int body, int64_t stride) {
+        SpanChunk c;
+        std::memset(&c, 0, sizeof c);
+        c.src = src;
+        c.pk = pk;
+        c.n = (int32_t)n;
+        c.body = body;
+        c.stride = (int32_t)(n > 1 ? stride : 0);
+        host_magic32((uint32_t)std::max(1, c.stride), &c.m32_stride, &c.s32_stride);
+        chunks.push_back(c);
+    }
+
+    void add_raw(int64_t src, int64_t pk, int64_t len) {
+        SpanChunk c;
+        std::memset(&c, 0, sizeof c);
+        c.src = src;
+        c.pk = pk;
+        c.n = 1;
+        c.body = -1;
+        c.stride = (int32_t)len;
+        chunks.push_back(c);
+    }
+};
+
+// Try the span lowering; true when it applies.
+bool build_span(const Node* layout, Plan* p) {
+    if (layout->runs == 0) return false;
+    SpanPlan sp;
+    std::memset(&sp, 0, sizeof sp);
+    const Node* n = layout;
+    SpanBuilder b;
+    int64_t base = 0;
+    while (n->kind == Kind::Rep && !b.small(n->body.get()) && sp.outer_depth < kSpanMaxOuter) {
+        sp.outer_cnt[sp.outer_depth] = n->count;
+        sp.outer_str[sp.outer_depth] = n->stride;
+        sp.outer_pk[sp.outer_depth] = n->body->nbytes;
+        base += n->base;
+        ++sp.outer_depth;
+        n = n->body.get();
+    }
+    b.emit(n, base, 0);
+    if (!b.ok || b.chunks.empty()) return false;
+    // worth it only when elements are small enough that the descriptor walk
+    // would be per-byte bound: average packed bytes per chunk element
+    sp.nchunks = (int32_t)b.chunks.size();
+    sp.nbodies = (int32_t)b.bodies.size();
+    int64_t units = sp.nchunks;
+    for (int i = 0; i < sp.outer_depth; ++i) units *= sp.outer_cnt[i];
+    sp.nunits = units;
+    p->span = sp;
+    p->span_chunks = std::move(b.chunks);
+    p->span_bodies = std::move(b.bodies);
+    return true;
+}
+
 }  // namespace
 
 void analyze(const Node* layout, Plan* p) {
@@ -217,7 +357,7 @@ void analyze(const Node* layout, Plan* p) {
         p->chain = c;
         p->chain_align = (int32_t)align;
     } else {
-        p->kind = PLAN_GENERIC;
+        p->kind = build_span(layout, p) ? PLAN_SPAN : PLAN_GENERIC;
     }
     p->overlap = may_overlap(layout);
     if (p->overlap && layout->runs <= (int64_t(1) << 22)) p->overlap = exact_overlap(layout);
@@ -240,13 +380,19 @@ std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStre
         const size_t nb = f.nodes.size() * sizeof(DNode);
         const size_t kb = ((f.kids.size() * sizeof(int32_t)) + 15) & ~size_t(15);
         const size_t pb = f.rp.size() * sizeof(int64_t);
-        std::vector<uint8_t> host(nb + kb + 2 * pb + 16, 0);
+        const size_t bo = (nb + kb + 2 * pb + 15) & ~size_t(15);           // span bodies
+        const size_t bb = p->span_bodies.size() * sizeof(SpanBody);
+        const size_t co = (bo + bb + 15) & ~size_t(15);                     // span chunks
+        const size_t cb = p->span_chunks.size() * sizeof(SpanChunk);
+        std::vector<uint8_t> host(co + cb + 16, 0);
         std::memcpy(host.data(), f.nodes.data(), nb);
         if (!f.kids.empty()) std::memcpy(host.data() + nb, f.kids.data(), f.kids.size() * sizeof(int32_t));
         if (pb) {
             std::memcpy(host.data() + nb + kb, f.rp.data(), pb);
             std::memcpy(host.data() + nb + kb + pb, f.bp.data(), pb);
         }
+        if (bb) std::memcpy(host.data() + bo, p->span_bodies.data(), bb);
+        if (cb) std::memcpy(host.data() + co, p->span_chunks.data(), cb);
         (void)stream;
         void* dev = nullptr;
         cudaStream_t up = upload_stream(device);
@@ -273,6 +419,8 @@ std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStre
         p->desc.rp = (const int64_t*)(b + nb + kb);
         p->desc.bp = (const int64_t*)(b + nb + kb + pb);
         p->desc.root = root;
+        p->span.bodies = (const SpanBody*)(b + bo);
+        p->span.chunks = (const SpanChunk*)(b + co);
         p->desc.runs = lay->runs;
         p->desc.nbytes = lay->nbytes;
     }

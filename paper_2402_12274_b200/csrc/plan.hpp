@@ -14,7 +14,7 @@
 
 namespace mpx {
 
-enum PlanKind : int32_t { PLAN_EMPTY = 0, PLAN_CHAIN = 1, PLAN_GENERIC = 2 };
+enum PlanKind : int32_t { PLAN_EMPTY = 0, PLAN_CHAIN = 1, PLAN_GENERIC = 2, PLAN_SPAN = 3 };
 
 struct Plan {
     int32_t kind = PLAN_EMPTY;
@@ -24,6 +24,9 @@ struct Plan {
     Chain chain{};          // valid for PLAN_CHAIN
     int32_t chain_align = 16;  // largest power of two dividing base, L and strides
     DDesc desc{};           // device descriptor (always built, used by iov + generic)
+    SpanPlan span{};        // valid for PLAN_SPAN (pointers into blob)
+    std::vector<SpanChunk> span_chunks;   // host copies, uploaded with the descriptor
+    std::vector<SpanBody> span_bodies;
     void* blob = nullptr;   // device allocation backing desc
     size_t blob_bytes = 0;
     cudaEvent_t ready = nullptr;     // upload finished (recorded on an internal stream)

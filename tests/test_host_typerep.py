@@ -57,7 +57,7 @@ def test_config_plans():
         q = build_product(spec, mp).layout_query()
         assert q["plan"] == 1 and not q["overlap"], name
     q = build_product(cfg3_spec(3, hcount=8), mp).layout_query()
-    assert q["plan"] == 2 and not q["overlap"]
+    assert q["plan"] == 3 and not q["overlap"]      # span lowering
 
 
 def test_frozen_examples_host():
