@@ -45,31 +45,29 @@ struct Chain {
 // shared memory with aligned 16-byte loads and produces the other side word by
 // word through the body's byte maps.
 constexpr int kSpanMaxBody = 256;
+constexpr int kSpanMaxRuns = 32;
 constexpr int kSpanMaxBodies = 8;
-constexpr int kSpanStage = 4096;     // bytes staged per warp (plus 16 B slack)
+constexpr int kSpanStage = 2048;     // bytes staged per warp per buffer (plus 32 B slack)
 constexpr int kSpanMaxOuter = 2;
 
+// one element of a span chunk: its runs relative to the element's span start
 struct SpanBody {
-    int32_t span_lo;        // element span start relative to its frame origin
     int32_t span_len;       // element span bytes (<= kSpanMaxBody)
     int32_t nbytes;         // payload bytes per element
-    uint32_t m32_nbytes;    // magic for q / nbytes
-    int32_t s32_nbytes;
+    int32_t nruns;
     int32_t pad;
-    int16_t fwd[kSpanMaxBody];  // span offset -> packed offset in element, -1 = gap
-    int16_t inv[kSpanMaxBody];  // packed offset in element -> span offset
-    int32_t pad2[2];
+    int16_t roff[kSpanMaxRuns];  // run offset in the element span
+    int16_t rpk[kSpanMaxRuns];   // run offset in the element's packed bytes
+    int16_t rlen[kSpanMaxRuns];
 };
 static_assert(sizeof(SpanBody) % 16 == 0, "SpanBody must be 16-byte sized");
 
 struct SpanChunk {
-    int64_t src;            // frame origin of element 0 (layout offset)
+    int64_t src;            // span start of element 0 (layout offset)
     int64_t pk;             // packed offset of element 0
     int32_t n;              // elements
     int32_t body;           // body index, -1 = raw contiguous piece of `stride` bytes
     int32_t stride;         // element stride in bytes (>= span_len when n > 1)
-    uint32_t m32_stride;
-    int32_t s32_stride;
     int32_t pad;
 };
 

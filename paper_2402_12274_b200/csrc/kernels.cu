@@ -287,20 +287,70 @@ k_generic(const DDesc d, const uint8_t* __restrict__ src, uint8_t* __restrict__ 
 
 // ---------------------------------------------------------------- span
 constexpr int kSpanWarps = 8;
-constexpr size_t kSpanSmem = size_t(kSpanMaxBodies) * sizeof(SpanBody) + size_t(kSpanWarps) * (kSpanStage + 32);
+constexpr int kSpanBuf = kSpanStage + 32;
+constexpr size_t kSpanSmem = size_t(kSpanMaxBodies) * sizeof(SpanBody) + size_t(kSpanWarps) * 3 * kSpanBuf;
 
-// One warp per chunk: stage the chunk's contiguous input span (layout span for
-// pack, packed bytes for unpack) in shared memory with aligned 16-byte loads,
-// then produce the output side as 4-byte words aligned to the destination
-// (coalesced 128 B per warp instruction), every byte located in O(1) through
-// the body's byte maps.  Bytes outside the runs are never written.
+// global [g, g+len) -> smem buf[a, a+len) with aligned 16-byte loads (a = g & 15)
+__device__ __forceinline__ int stage_in(uint8_t* buf, const uint8_t* g, int len, int lane) {
+    const int a = (int)(reinterpret_cast<uintptr_t>(g) & 15);
+    const uint4* g16 = reinterpret_cast<const uint4*>(g - a);
+    const int nv = (a + len + 15) >> 4;
+    for (int i = lane; i < nv; i += 32) reinterpret_cast<uint4*>(buf)[i] = __ldg(g16 + i);
+    return a;
+}
+
+// smem buf[b, b+len) -> global [g, g+len) with aligned 16-byte stores
+// (b = g & 15); mask (optional) selects the bytes to write (0xFF = write)
+__device__ __forceinline__ void stage_out(uint8_t* g, const uint8_t* buf, const uint8_t* mask, int b, int len,
+                                          int lane) {
+    uint8_t* g0 = g - b;
+    const int nv = (b + len + 15) >> 4;
+    for (int k = lane; k < nv; k += 32) {
+        const int lo = k == 0 ? b : 0;
+        const int hi = min(16, b + len - 16 * k);
+        const uint4 v = reinterpret_cast<const uint4*>(buf)[k];
+        uint4 m = make_uint4(~0u, ~0u, ~0u, ~0u);
+        if (mask) m = reinterpret_cast<const uint4*>(mask)[k];
+        const bool full = lo == 0 && hi == 16 && (m.x & m.y & m.z & m.w) == ~0u;
+        if (full) {
+            reinterpret_cast<uint4*>(g0)[k] = v;
+            continue;
+        }
+        const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+        const uint32_t mw[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int b0 = 4 * i;
+            if (b0 >= lo && b0 + 4 <= hi && mw[i] == ~0u) {
+                reinterpret_cast<uint32_t*>(g0 + 16 * k)[i] = vw[i];
+            } else {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int bb = b0 + t;
+                    if (bb >= lo && bb < hi && ((mw[i] >> (8 * t)) & 0xFF))
+                        g0[16 * k + bb] = (uint8_t)(vw[i] >> (8 * t));
+                }
+            }
+        }
+    }
+}
+
+// One warp per chunk, three phases:
+//   1. the chunk's contiguous input (layout span for pack, packed bytes for
+//      unpack) -> shared memory with aligned 16-byte loads;
+//   2. shared -> shared permutation, one lane per element walking the body's
+//      run table (unpack also marks the covered bytes);
+//   3. shared -> global with aligned 16-byte stores; unpack writes only marked
+//      bytes (bytes outside the runs are never touched).
 template <bool PACK>
 __global__ void __launch_bounds__(kSpanWarps * 32)
 k_span(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t limit) {
     extern __shared__ __align__(16) uint8_t sm[];
     SpanBody* bodies = reinterpret_cast<SpanBody*>(sm);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint8_t* stage = sm + kSpanMaxBodies * sizeof(SpanBody) + warp * (kSpanStage + 32);
+    uint8_t* A = sm + kSpanMaxBodies * sizeof(SpanBody) + warp * 3 * kSpanBuf;
+    uint8_t* B = A + kSpanBuf;
+    uint8_t* M = B + kSpanBuf;
     {
         const int nv = sp.nbodies * (int)(sizeof(SpanBody) / 16);
         const uint4* g = reinterpret_cast<const uint4*>(sp.bodies);
@@ -318,91 +368,66 @@ k_span(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__
             poff += idx * sp.outer_pk[i];
         }
         const SpanChunk* chp = sp.chunks + c;
-        const int64_t ch_src = __ldg(&chp->src), ch_pk = __ldg(&chp->pk);
-        const int ch_n = __ldg(&chp->n), ch_body = __ldg(&chp->body), ch_stride = __ldg(&chp->stride);
-        const bool raw = ch_body < 0;
-        const SpanBody* B = raw ? nullptr : bodies + ch_body;
-        const int span_len = raw ? ch_stride : (ch_n - 1) * ch_stride + B->span_len;
-        const int out_len = raw ? ch_stride : ch_n * B->nbytes;
-        const int64_t lay0 = ch_src + loff, pk0 = ch_pk + poff;
+        const int64_t lay0 = __ldg(&chp->src) + loff, pk0 = __ldg(&chp->pk) + poff;
+        const int n = __ldg(&chp->n), body = __ldg(&chp->body), stride = __ldg(&chp->stride);
+        const bool raw = body < 0;
+        const SpanBody& Bd = bodies[raw ? 0 : body];
+        const int span_len = raw ? stride : (n - 1) * stride + Bd.span_len;
+        const int out_len = raw ? stride : n * Bd.nbytes;
         if (!PACK && pk0 >= limit) continue;
         const int qlim = (int)min((int64_t)out_len, limit - pk0);
         if (PACK) {
-            const uint8_t* g = src + lay0;
-            const int a = (int)(reinterpret_cast<uintptr_t>(g) & 15);
-            const uint4* g16 = reinterpret_cast<const uint4*>(g - a);
-            const int nv = (a + span_len + 15) >> 4;
-            for (int i = lane; i < nv; i += 32) reinterpret_cast<uint4*>(stage)[i] = __ldg(g16 + i);
+            const int a = stage_in(A, src + lay0, span_len, lane);
+            const int b = (int)(reinterpret_cast<uintptr_t>(dst + pk0) & 15);
             __syncwarp();
-            uint8_t* d = dst + pk0;
-            const int b = (int)(reinterpret_cast<uintptr_t>(d) & 3);
-            uint32_t* d4 = reinterpret_cast<uint32_t*>(d - b);
-            const int nw = (b + out_len + 3) >> 2;
-            for (int w = lane; w < nw; w += 32) {
-                uint32_t word = 0;
-                int mask = 0;
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const int q = 4 * w + t - b;
-                    if (q >= 0 && q < out_len) {
-                        int so = q;
-                        if (!raw) {
-                            const int e = (int)fdiv32((uint32_t)q, B->m32_nbytes, B->s32_nbytes);
-                            so = e * ch_stride + B->inv[q - e * B->nbytes];
-                        }
-                        word |= (uint32_t)stage[a + so] << (8 * t);
-                        mask |= 1 << t;
+            if (raw) {
+                for (int i = lane; i < out_len; i += 32) B[b + i] = A[a + i];
+            } else {
+                const int nr = Bd.nruns, nb = Bd.nbytes;
+                for (int e = lane; e < n; e += 32) {
+                    const uint8_t* s0 = A + a + e * stride;
+                    uint8_t* d0 = B + b + e * nb;
+                    for (int r = 0; r < nr; ++r) {
+                        const uint8_t* sr = s0 + Bd.roff[r];
+                        uint8_t* dr = d0 + Bd.rpk[r];
+                        const int len = Bd.rlen[r];
+                        for (int x = 0; x < len; ++x) dr[x] = sr[x];
                     }
                 }
-                if (mask == 0xF) {
-                    d4[w] = word;
-                } else {
-#pragma unroll
-                    for (int t = 0; t < 4; ++t)
-                        if (mask & (1 << t)) reinterpret_cast<uint8_t*>(d4)[4 * w + t] = (uint8_t)(word >> (8 * t));
-                }
             }
+            __syncwarp();
+            stage_out(dst + pk0, B, nullptr, b, out_len, lane);
         } else {
-            const uint8_t* g = src + pk0;
-            const int a = (int)(reinterpret_cast<uintptr_t>(g) & 15);
-            const uint4* g16 = reinterpret_cast<const uint4*>(g - a);
-            const int nv = (a + qlim + 15) >> 4;
-            for (int i = lane; i < nv; i += 32) reinterpret_cast<uint4*>(stage)[i] = __ldg(g16 + i);
+            const int a = stage_in(A, src + pk0, qlim, lane);
+            const int b = (int)(reinterpret_cast<uintptr_t>(dst + lay0) & 15);
+            const int nvm = (b + span_len + 15) >> 4;
+            for (int i = lane; i < nvm; i += 32) reinterpret_cast<uint4*>(M)[i] = make_uint4(0, 0, 0, 0);
             __syncwarp();
-            uint8_t* d = dst + lay0;
-            const int b = (int)(reinterpret_cast<uintptr_t>(d) & 3);
-            uint32_t* d4 = reinterpret_cast<uint32_t*>(d - b);
-            const int nw = (b + span_len + 3) >> 2;
-            for (int w = lane; w < nw; w += 32) {
-                uint32_t word = 0;
-                int mask = 0;
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const int dd = 4 * w + t - b;
-                    if (dd >= 0 && dd < span_len) {
-                        int q = dd;
-                        if (!raw) {
-                            const int e = ch_n > 1 ? (int)fdiv32((uint32_t)dd, __ldg(&chp->m32_stride),
-                                                                 __ldg(&chp->s32_stride))
-                                                   : 0;
-                            const int off = dd - e * ch_stride;
-                            const int fw = off < B->span_len ? B->fwd[off] : -1;
-                            q = fw < 0 ? -1 : e * B->nbytes + fw;
-                        }
-                        if (q >= 0 && q < qlim) {
-                            word |= (uint32_t)stage[a + q] << (8 * t);
-                            mask |= 1 << t;
+            if (raw) {
+                for (int i = lane; i < qlim; i += 32) {
+                    B[b + i] = A[a + i];
+                    M[b + i] = 0xFF;
+                }
+            } else {
+                const int nr = Bd.nruns, nb = Bd.nbytes;
+                for (int e = lane; e < n; e += 32) {
+                    const int q0 = e * nb;
+                    if (q0 >= qlim) break;
+                    const uint8_t* s0 = A + a + q0;
+                    const int d0 = b + e * stride;
+                    for (int r = 0; r < nr; ++r) {
+                        const int len = min((int)Bd.rlen[r], qlim - q0 - Bd.rpk[r]);
+                        const uint8_t* sr = s0 + Bd.rpk[r];
+                        const int dr = d0 + Bd.roff[r];
+                        for (int x = 0; x < len; ++x) {
+                            B[dr + x] = sr[x];
+                            M[dr + x] = 0xFF;
                         }
                     }
                 }
-                if (mask == 0xF) {
-                    d4[w] = word;
-                } else if (mask) {
-#pragma unroll
-                    for (int t = 0; t < 4; ++t)
-                        if (mask & (1 << t)) reinterpret_cast<uint8_t*>(d4)[4 * w + t] = (uint8_t)(word >> (8 * t));
-                }
             }
+            __syncwarp();
+            stage_out(dst + lay0, B, M, b, span_len, lane);
         }
         __syncwarp();
     }
@@ -527,7 +552,14 @@ cudaError_t launch_span(const Plan& p, bool pack, const uint8_t* src, uint8_t* d
                         cudaStream_t stream) {
     if (limit <= 0 || p.span.nunits == 0) return cudaSuccess;
     const int64_t want = (p.span.nunits + kSpanWarps - 1) / kSpanWarps;
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count(p.device) * 5));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count(p.device) * 4));
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[pack]) {   // > 48 KiB of dynamic shared memory needs an opt-in
+        cudaError_t e = pack ? cudaFuncSetAttribute(k_span<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSpanSmem)
+                             : cudaFuncSetAttribute(k_span<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSpanSmem);
+        if (e != cudaSuccess) return e;
+        attr_set[pack] = true;
+    }
     if (pack) k_span<true><<<(unsigned)grid, kSpanWarps * 32, kSpanSmem, stream>>>(p.span, src, dst, limit);
     else k_span<false><<<(unsigned)grid, kSpanWarps * 32, kSpanSmem, stream>>>(p.span, src, dst, limit);
     return cudaGetLastError();

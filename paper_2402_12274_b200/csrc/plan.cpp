@@ -236,22 +236,25 @@ class SpanBuilder {
         tree::enumerate(n, -n->min_off, runs, 64);
         auto it = ids_.find(runs);
         if (it != ids_.end()) return it->second;
-        if ((int)bodies.size() >= kSpanMaxBodies) { ok = false; return 0; }
+        const int nr = (int)(runs.size() / 2);
+        if ((int)bodies.size() >= kSpanMaxBodies || nr > kSpanMaxRuns) { ok = false; return 0; }
         SpanBody b;
         std::memset(&b, 0, sizeof b);
-        b.span_lo = 0;
         b.span_len = (int32_t)(n->max_end - n->min_off);
         b.nbytes = (int32_t)n->nbytes;
-        host_magic32((uint32_t)b.nbytes, &b.m32_nbytes, &b.s32_nbytes);
-        for (int i = 0; i < kSpanMaxBody; ++i) b.fwd[i] = b.inv[i] = -1;
+        b.nruns = nr;
+        std::vector<bool> seen((size_t)b.span_len, false);
         int64_t q = 0;
-        for (size_t r = 0; r + 1 < runs.size(); r += 2)
-            for (int64_t x = 0; x < runs[r + 1]; ++x, ++q) {
-                const int64_t so = runs[r] + x;
-                if (b.fwd[so] >= 0) { ok = false; return 0; }   // self-overlapping element
-                b.fwd[so] = (int16_t)q;
-                b.inv[q] = (int16_t)so;
+        for (int r = 0; r < nr; ++r) {
+            b.roff[r] = (int16_t)runs[2 * r];
+            b.rlen[r] = (int16_t)runs[2 * r + 1];
+            b.rpk[r] = (int16_t)q;
+            for (int64_t x = 0; x < runs[2 * r + 1]; ++x) {
+                if (seen[(size_t)(runs[2 * r] + x)]) { ok = false; return 0; }   // self-overlapping element
+                seen[(size_t)(runs[2 * r] + x)] = true;
             }
+            q += runs[2 * r + 1];
+        }
         const int id = (int)bodies.size();
         bodies.push_back(b);
         ids_[runs] = id;
@@ -266,7 +269,6 @@ class SpanBuilder {
         c.n = (int32_t)n;
         c.body = body;
         c.stride = (int32_t)(n > 1 ? stride : 0);
-        host_magic32((uint32_t)std::max(1, c.stride), &c.m32_stride, &c.s32_stride);
         chunks.push_back(c);
     }
 
