@@ -60,6 +60,23 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
+def max_over_ranks(value, device=None):
+    """Max of a per-rank float over the job (the contract's timing rule).
+    Works with NCCL (device tensor) and gloo (CPU tensor)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_value(bytes_per_rank, world, ms_per_step_max):
+    """Whole-job GB/s: the units every rank processed / the slowest rank."""
+    return world * bytes_per_rank / (ms_per_step_max / 1e3) / 1e9
+
+
 def load_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -213,6 +230,60 @@ def reference_arm(args):
     return 0
 
 
+# ------------------------------------------------------------- extras
+
+
+def _time_launch(fn, flush, reps):
+    import torch
+    fn()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def run_extras(dev, flush, args):
+    """BASELINE configs[0] and [2] (pack/unpack, L2 flushed per launch) and the
+    enqueue path (1-GPU: ranks share the device, so the ring is an HBM copy,
+    not NVLink).  Reported beside, not inside, the headline metric."""
+    import torch
+    import paper_2402_12274_b200 as mp
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from golden_common import CFG1_SPEC, cfg3_spec
+    from specbuild import build_product
+    out = {}
+    reps = max(3, min(args.steps, 10))
+    for name, spec in (("cfg1_vector", CFG1_SPEC), ("cfg3_struct_indexed_hvector", cfg3_spec(3))):
+        dt = build_product(spec, mp)
+        span = dt.layout_query()["max_end"]
+        src = torch.from_numpy(seeded_bytes(11, span)).to(dev)
+        back = torch.zeros_like(src)
+        n = mp.packed_size(dt)
+        packed = torch.empty(n, dtype=torch.uint8, device=dev)
+        tp = _time_launch(lambda: mp.pack_into(dt, src, packed), flush, reps)
+        tu = _time_launch(lambda: mp.unpack(dt, packed, back), flush, reps)
+        out[name] = {"payload_bytes": n, "segments": dt.segment_count,
+                     "pack_us": round(tp * 1e3, 1), "unpack_us": round(tu * 1e3, 1),
+                     "pack_GBs": round(2 * n / tp / 1e6, 1), "unpack_GBs": round(2 * n / tu / 1e6, 1)}
+        del src, back, packed
+    try:
+        import enqueue_bench as eb
+        out["ring_2ranks_1gpu_64MiB"] = eb.ring(2, 64 << 20, iters=reps)
+        out["allreduce_native_2ranks_1gpu_64MiB_f32"] = eb.allreduce(2, 16 << 20, iters=reps, algo="native")
+        out["allreduce_nccl_1rank_64MiB_f32"] = eb.allreduce(1, 16 << 20, iters=reps, algo="nccl",
+                                                             group="bench-ar1")
+    except Exception as exc:  # report, never fail the headline
+        out["enqueue_error"] = repr(exc)
+    return out
+
+
 # ------------------------------------------------------------- GPU arm
 
 
@@ -275,13 +346,9 @@ def gpu_arm(args):
         dist.barrier()
     pack_ms = [a.elapsed_time(b) for a, b, c in ev]
     unpack_ms = [b.elapsed_time(c) for a, b, c in ev]
-    total_ms = sum(p + u for p, u in zip(pack_ms, unpack_ms))
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms = max_over_ranks(sum(p + u for p, u in zip(pack_ms, unpack_ms)), dev)
     ms_per_step = total_ms / args.steps
-    value = world * step_bytes() / (ms_per_step / 1e3) / 1e9
+    value = job_value(step_bytes(), world, ms_per_step)
 
     # ---- e2e through the public API with HOST buffers ----
     # (a) halo-exchange step: the 514^3 array is simulation state resident in
@@ -338,11 +405,7 @@ def gpu_arm(args):
             fn()
             b.record(stream)
         torch.cuda.synchronize()
-        ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        return float(tt.item())
+        return max_over_ranks(float(np.mean([a.elapsed_time(b) for a, b in evs])), dev)
 
     e2e_ms = time_steps(e2e_halo)
     staged_ms = time_steps(e2e_staged)
@@ -368,6 +431,11 @@ def gpu_arm(args):
                          "oracle port of datatype.py, faces over %d threads on %s"
                          % (reps, dtc, threads, cpu_model())}
 
+    # ---- other BASELINE configs and the enqueue path (rank 0, N = 1) ----
+    extras = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        extras = run_extras(dev, flush, args)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
@@ -384,19 +452,20 @@ def gpu_arm(args):
                          "frac": round(achieved / peak, 4),
                          "traffic": traffic.get("bytes_per_launch") if traffic else None,
                          "algorithmic_bytes_per_launch": launch_bytes},
-            "e2e": {"value": round(world * step_bytes() / (e2e_ms / 1e3) / 1e9, 3), "unit": "GB/s",
+            "e2e": {"value": round(job_value(step_bytes(), world, e2e_ms), 3), "unit": "GB/s",
                     "ms_per_step": round(e2e_ms, 3),
                     "mode": "halo step: array resident in HBM; received packed faces H2D "
                             "(overlapped with the fused pack) and packed faces D2H (overlapped "
                             "with the fused unpack), pinned host buffers",
                     "h2d_bytes_per_step": payload, "d2h_bytes_per_step": payload},
-            "e2e_staged": {"value": round(world * step_bytes() / (staged_ms / 1e3) / 1e9, 3),
+            "e2e_staged": {"value": round(job_value(step_bytes(), world, staged_ms), 3),
                            "unit": "GB/s", "ms_per_step": round(staged_ms, 3),
                            "mode": "array on host: whole-array H2D copy + kernels + D2H of packed faces",
                            "h2d_bytes_per_step": ARRAY_BYTES, "d2h_bytes_per_step": d2h},
             "gpu_launches": 2 * args.steps,
             "clocks": clocks,
             "cpu_baseline": cpu,
+            "extras": extras,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -412,6 +481,7 @@ def main():
     ap.add_argument("--impl", default="mpx", choices=["mpx", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)

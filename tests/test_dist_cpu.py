@@ -1,0 +1,85 @@
+"""The N > 1 host path of bench.py on CPU: two gloo ranks (torch.distributed
+over 127.0.0.1) agree on the max-over-ranks time and the whole-job value, as
+the driver's torchrun launch of `bench.py --gpus N` requires."""
+
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import os, sys, json
+sys.path.insert(0, %(root)r)
+import torch.distributed as dist
+dist.init_process_group("gloo", init_method="env://")
+import bench
+r, w, _ = bench.dist_env()
+ms = 2.0 + 3.0 * r                       # rank 1 is the slow one
+m = bench.max_over_ranks(ms)
+v = bench.job_value(bench.step_bytes(), w, m)
+print(json.dumps({"rank": r, "world": w, "max_ms": m, "value": v}), flush=True)
+dist.destroy_process_group()
+"""
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.timeout(120)
+def test_bench_max_over_ranks_gloo_world2():
+    import json
+    port = _free_port()
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", LOCAL_RANK=str(r),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, "-c", CHILD % {"root": ROOT}],
+                                      env=env, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                      text=True))
+    outs = [p.communicate(timeout=100) for p in procs]
+    for p, (o, e) in zip(procs, outs):
+        assert p.returncode == 0, e
+    rows = [json.loads(o.strip().splitlines()[-1]) for o, _ in outs]
+    import bench
+    assert all(row["max_ms"] == 5.0 and row["world"] == 2 for row in rows)
+    expect = 2 * bench.step_bytes() / 5e-3 / 1e9
+    assert all(abs(row["value"] - expect) < 1e-6 * expect for row in rows)
+
+
+def test_reference_arm_exits_on_nonzero_rank():
+    """Under torchrun only rank 0 runs the CPU reference arm."""
+    env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--gpus", "2", "--steps", "1", "--warmup", "0"],
+                       env=env, capture_output=True, text=True, timeout=120)
+    assert p.returncode == 0 and p.stdout.strip() == ""
+
+
+@pytest.mark.timeout(300)
+def test_reference_arm_json_contract():
+    """bench.py --impl reference prints one JSON line with the contract keys
+    (CPU oracle port on the host cores, no GPU needed)."""
+    import json
+    env = dict(os.environ)
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK"):
+        env.pop(k, None)
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--steps", "1", "--warmup", "0"],
+                       env=env, capture_output=True, text=True, timeout=280)
+    assert p.returncode == 0, p.stderr
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    for k in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0

@@ -1,0 +1,135 @@
+"""Enqueue-path measurements on the GPUs of this process (library helper used
+by bench.py's "extras"; also runnable alone).
+
+ring(n, nbytes): n in-process ranks (round-robin over the visible GPUs; with
+one GPU every rank shares it, so the "link" is the device's own HBM), each
+rank isend -> (r+1)%n and irecv <- (r-1)%n of nbytes contiguous uint8 on its
+own CUDA stream, waitall_enqueue; time = wall clock over `iters` iterations
+after warm-up, bracketed by a host barrier + stream sync on every rank.
+allreduce(n, count): allreduce_enqueue of float32 on n ranks, same timing.
+"""
+
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def _run_ranks(n, body, group):
+    import paper_2402_12274_b200 as mp
+    import torch
+    ndev = torch.cuda.device_count()
+    out, errs = [None] * n, []
+    bar = threading.Barrier(n)
+
+    def runner(r):
+        inst = None
+        try:
+            inst = mp.init(rank=r, ranks=n, group=group, device=r % ndev)
+            out[r] = body(inst, bar)
+        except BaseException as e:  # noqa: B902
+            errs.append(e)
+            bar.abort()
+        finally:
+            if inst is not None and not inst.finalized:
+                try:
+                    inst.finalize()
+                except Exception:
+                    pass
+
+    th = [threading.Thread(target=runner, args=(r,), daemon=True) for r in range(n)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(300)
+    if errs:
+        raise errs[0]
+    return out
+
+
+def ring(n=2, nbytes=64 << 20, iters=20, warmup=3, group="bench-ring"):
+    import paper_2402_12274_b200 as mp
+    import torch
+
+    def body(inst, bar):
+        q = mp.queue_create(inst)
+        info = mp.info_create()
+        info.set("type", "devstream")
+        mp.info_set_hex(info, "value", bytes.fromhex(q.handle))
+        s = inst.stream_create(info)
+        c = mp.stream_comm_create(inst.world, s)
+        r = inst.rank
+        src = torch.full((nbytes,), r, dtype=torch.uint8, device=inst.device)
+        dst = torch.zeros_like(src)
+
+        def one():
+            rr = mp.irecv_enqueue(c, dst, nbytes, mp.BYTE, (r - 1) % n, 0)
+            sr = mp.isend_enqueue(c, src, nbytes, mp.BYTE, (r + 1) % n, 0)
+            mp.waitall_enqueue([rr, sr])
+
+        for _ in range(warmup):
+            one()
+        mp.queue_synchronize(q)
+        bar.wait()
+        t0 = time.perf_counter()
+        for _ in range(iters):
+            one()
+        mp.queue_synchronize(q)
+        bar.wait()
+        dt = time.perf_counter() - t0
+        ok = bool((dst == (r - 1) % n).all())
+        mp.comm_free(c)
+        mp.free_stream(s)
+        return dt, ok
+
+    res = _run_ranks(n, body, group)
+    dt = max(r[0] for r in res)
+    return {"ranks": n, "bytes": nbytes, "iters": iters, "ms_per_iter": 1e3 * dt / iters,
+            "GBps_per_rank": nbytes * iters / dt / 1e9, "correct": all(r[1] for r in res)}
+
+
+def allreduce(n=2, count=16 << 20, iters=20, warmup=3, algo=None, group="bench-ar"):
+    import paper_2402_12274_b200 as mp
+    import torch
+
+    def body(inst, bar):
+        q = mp.queue_create(inst)
+        info = mp.info_create()
+        info.set("type", "devstream")
+        mp.info_set_hex(info, "value", bytes.fromhex(q.handle))
+        s = inst.stream_create(info)
+        c = mp.stream_comm_create(inst.world, s)
+        x = torch.full((count,), float(inst.rank + 1), device=inst.device)
+        y = torch.zeros_like(x)
+        for _ in range(warmup):
+            mp.allreduce_enqueue(c, x, y, count, mp.FLOAT32, algo=algo)
+        mp.queue_synchronize(q)
+        bar.wait()
+        t0 = time.perf_counter()
+        for _ in range(iters):
+            mp.allreduce_enqueue(c, x, y, count, mp.FLOAT32, algo=algo)
+        mp.queue_synchronize(q)
+        bar.wait()
+        dt = time.perf_counter() - t0
+        ok = bool((y == n * (n + 1) / 2).all())
+        mp.comm_free(c)
+        mp.free_stream(s)
+        return dt, ok
+
+    res = _run_ranks(n, body, group)
+    dt = max(r[0] for r in res)
+    S = 4 * count
+    return {"ranks": n, "bytes": S, "algo": algo or "auto", "ms_per_iter": 1e3 * dt / iters,
+            "algbw_GBps": S * iters / dt / 1e9,
+            "busbw_GBps": S * iters / dt / 1e9 * (2 * (n - 1) / n if n > 1 else 1),
+            "correct": all(r[1] for r in res)}
+
+
+if __name__ == "__main__":
+    import json
+    print(json.dumps(ring(2)))
+    print(json.dumps(allreduce(2, algo="native")))
+    print(json.dumps(allreduce(1, algo="nccl", group="bench-ar1")))
