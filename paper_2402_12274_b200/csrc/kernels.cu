@@ -90,74 +90,87 @@ __device__ __forceinline__ void store_partial16(uint8_t* p, const uint4& v, int 
 // 16-byte loads (pack) or stores (unpack) are realigned with funnel shifts
 // through neighbouring lanes, so no access is narrower than 16 bytes except
 // the two partial chunks at the ends of an unpacked row.
+// Work items are (row, piece): a piece is kRowPiece = 32 lanes x U x 16 B of a
+// row, so long rows (a 64 MiB contiguous message is a single row) spread over
+// the whole grid.
+constexpr int kRowU = 4;
+constexpr int kRowPieceChunks = 32 * kRowU;
+
 template <bool PACK>
 __device__ __forceinline__ void chain_rows(const ChainJob& j, int64_t warp0, int64_t nwarps) {
-    constexpr int U = 4;   // 16-byte chunks in flight per lane
     const int lane = threadIdx.x & 31;
     const Chain& c = j.c;
-    const int nch = (int)(c.L >> 4);
-    for (int64_t r = warp0; r < j.rows; r += nwarps) {
+    const int64_t nch = c.L >> 4;
+    const int64_t npieces = (nch + kRowPieceChunks - 1) / kRowPieceChunks;
+    const int64_t items = j.rows * npieces;
+    for (int64_t it = warp0; it < items; it += nwarps) {
+        const int64_t r = it / npieces;
+        const int64_t k0 = (it - r * npieces) * kRowPieceChunks;
         const int64_t s = chain_row(c, r);
         if (PACK) {
             const uint8_t* srow = j.src + s;
             const int a = (int)(reinterpret_cast<uintptr_t>(srow) & 15);
             const uint4* s16 = reinterpret_cast<const uint4*>(srow - a);
             uint4* d16 = reinterpret_cast<uint4*>(j.dst + r * c.L);
-            for (int k0 = 0; k0 < nch; k0 += 32 * U) {
-                uint4 v[U];
+            uint4 v[kRowU];
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int k = k0 + 32 * u + lane;
-                    v[u] = k < nch ? __ldg(s16 + k) : make_uint4(0, 0, 0, 0);
-                }
-                if (a) {
+            for (int u = 0; u < kRowU; ++u) {
+                const int64_t k = k0 + 32 * u + lane;
+                v[u] = k < nch ? __ldg(s16 + k) : make_uint4(0, 0, 0, 0);
+            }
+            if (a) {
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int k = k0 + 32 * u + lane;
-                        uint4 c1 = shfl_down16(v[u], 1);
-                        if (k < nch && (lane == 31 || k + 1 == nch)) c1 = __ldg(s16 + k + 1);
-                        v[u] = funnel16(v[u], c1, a);
-                    }
+                for (int u = 0; u < kRowU; ++u) {
+                    const int64_t k = k0 + 32 * u + lane;
+                    uint4 c1 = shfl_down16(v[u], 1);
+                    if (k < nch && (lane == 31 || k + 1 == nch)) c1 = __ldg(s16 + k + 1);
+                    v[u] = funnel16(v[u], c1, a);
                 }
+            }
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int k = k0 + 32 * u + lane;
-                    if (k < nch) d16[k] = v[u];
-                }
+            for (int u = 0; u < kRowU; ++u) {
+                const int64_t k = k0 + 32 * u + lane;
+                if (k < nch) d16[k] = v[u];
             }
         } else {
             const uint4* p16 = reinterpret_cast<const uint4*>(j.src + r * c.L);
             uint8_t* drow = j.dst + s;
             const int a = (int)(reinterpret_cast<uintptr_t>(drow) & 15);
             uint8_t* d16 = drow - a;
-            const int nout = a ? nch + 1 : nch;
-            uint4 carry = make_uint4(0, 0, 0, 0);
-            for (int k0 = 0; k0 < nout; k0 += 32 * U) {
-                uint4 v[U];
+            const int64_t nout = a ? nch + 1 : nch;
+            uint4 v[kRowU];
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int k = k0 + 32 * u + lane;
-                    v[u] = k < nch ? __ldg(p16 + k) : make_uint4(0, 0, 0, 0);
+            for (int u = 0; u < kRowU; ++u) {
+                const int64_t k = k0 + 32 * u + lane;
+                v[u] = k < nch ? __ldg(p16 + k) : make_uint4(0, 0, 0, 0);
+            }
+            if (a == 0) {
+#pragma unroll
+                for (int u = 0; u < kRowU; ++u) {
+                    const int64_t k = k0 + 32 * u + lane;
+                    if (k < nch) reinterpret_cast<uint4*>(d16)[k] = v[u];
                 }
-                if (a == 0) {
+                continue;
+            }
+            // the last piece also owns output chunk nch (the tail of the row)
+            uint4 carry = (k0 > 0) ? __ldg(p16 + k0 - 1) : make_uint4(0, 0, 0, 0);
+            const int64_t kend = min(k0 + (int64_t)kRowPieceChunks, nout);
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int k = k0 + 32 * u + lane;
-                        if (k < nch) reinterpret_cast<uint4*>(d16)[k] = v[u];
-                    }
-                    continue;
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int k = k0 + 32 * u + lane;
-                    uint4 prev = shfl_up16(v[u], 1);
-                    if (lane == 0) prev = carry;
-                    carry = shfl16(v[u], 31);
-                    const uint4 out = funnel16(prev, v[u], 16 - a);
+            for (int u = 0; u < kRowU; ++u) {
+                const int64_t k = k0 + 32 * u + lane;
+                uint4 prev = shfl_up16(v[u], 1);
+                if (lane == 0) prev = carry;
+                carry = shfl16(v[u], 31);
+                const uint4 out = funnel16(prev, v[u], 16 - a);
+                if (k < kend) {
                     if (k == 0) store_partial16(d16, out, a, 16);
-                    else if (k == nch) store_partial16(d16 + 16 * (int64_t)k, out, 0, a);
-                    else if (k < nch) reinterpret_cast<uint4*>(d16)[k] = out;
+                    else if (k == nch) store_partial16(d16 + 16 * k, out, 0, a);
+                    else reinterpret_cast<uint4*>(d16)[k] = out;
                 }
+            }
+            // output chunk nch falls just past the last full piece
+            if (nout > k0 + kRowPieceChunks && k0 + kRowPieceChunks == nch && lane == 0) {
+                store_partial16(d16 + 16 * nch, funnel16(carry, make_uint4(0, 0, 0, 0), 16 - a), 0, a);
             }
         }
     }
@@ -504,8 +517,14 @@ cudaError_t launch_chain_batch(ChainBatch& b, bool pack, int device, cudaStream_
     int64_t total = 0;
     for (int i = 0; i < b.njobs; ++i) {
         ChainJob& j = b.job[i];
-        const int64_t per_blk = j.mode == CHAIN_ROW ? kChainThreads / 32 : kChainThreads;
-        const int64_t want = (j.rows + per_blk - 1) / per_blk;
+        int64_t want;
+        if (j.mode == CHAIN_ROW) {
+            const int64_t nch = j.c.L >> 4;
+            const int64_t items = j.rows * ((nch + kRowPieceChunks - 1) / kRowPieceChunks);
+            want = (items + kChainThreads / 32 - 1) / (kChainThreads / 32);
+        } else {
+            want = (j.rows + kChainThreads - 1) / kChainThreads;
+        }
         j.nblk = (int32_t)std::max<int64_t>(1, std::min<int64_t>(want, cap));
         j.blk0 = (int32_t)total;
         total += j.nblk;
