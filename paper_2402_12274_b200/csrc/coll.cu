@@ -13,7 +13,7 @@ __global__ void __launch_bounds__(256)
 k_allreduce_oneshot(const CollTable* __restrict__ tab, int n, int64_t lo, int64_t hi) {
     __shared__ const T* src[kMaxCollRanks];
     __shared__ T* dst[kMaxCollRanks];
-    if (threadIdx.x < n) {   // uncached reads: the slot is reused by later calls
+    if (threadIdx.x < n) {   // volatile: the slot is rewritten by later calls
         const volatile CollTable* vt = tab;
         src[threadIdx.x] = static_cast<const T*>(const_cast<const void*>(vt->send[threadIdx.x]));
         dst[threadIdx.x] = static_cast<T*>(const_cast<void*>(vt->recv[threadIdx.x]));

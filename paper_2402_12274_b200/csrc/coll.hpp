@@ -11,15 +11,16 @@ constexpr int kMaxCollRanks = 64;
 
 constexpr int kCollSlots = 64;
 
-// per-call pointer table in pinned host memory; each rank's STREAM writes its
-// two pointers with 64-bit stream memops before its "arrived" flag, so a slot
-// is only rewritten once every rank's stream is past the previous use
+// per-call pointer table in device memory (one copy per participating
+// device); each rank's STREAM writes its two pointers with 64-bit stream
+// memops before its "arrived" flag, so a slot is only rewritten once every
+// rank's stream is past the previous use
 struct CollTable {
     const void* send[kMaxCollRanks];
     void* recv[kMaxCollRanks];
 };
 
-// ring of collective slots of one communicator context (pinned, mapped)
+// ring of collective slots of one communicator context
 struct CollRing {
     CollTable table[kCollSlots];
     uint32_t arrive[kCollSlots][kMaxCollRanks];

@@ -269,8 +269,14 @@ struct World {
     FlagPool flags{1u << 20};
     std::mutex peer_mu;
     std::set<std::pair<int, int>> peer_on;
+    // collective rings live in DEVICE memory, one copy per participating
+    // device (system-scope reads of pinned host memory serialise across the
+    // GPU); kMaxRings ring slots per device are allocated when the device is
+    // set up, context ids map to a ring index at comm creation
+    static constexpr int kMaxRings = 16;
     std::mutex coll_mu;
-    std::map<int, CollRing*> rings;  // per context id, created at comm creation
+    std::map<int, CollRing*> area;      // device -> kMaxRings rings
+    std::map<int, int> ring_index;      // context id -> ring index
     std::mutex nccl_mu;
     std::condition_variable nccl_cv;
     std::vector<ncclComm_t> nccl;   // per rank, by ncclCommInitAll
@@ -311,7 +317,7 @@ struct Comm {
     std::deque<std::pair<int, std::string>> deferred;
     std::atomic<int64_t> outstanding{0};
     int64_t coll_seq = 0;
-    CollRing* ring = nullptr;
+    int ring = -1;                  // index into every device's ring area
 };
 
 namespace {
@@ -368,6 +374,18 @@ int setup_device(World* w, int dev, int ndev) {
         done.insert(dev);
     }
     w->service(dev);
+    {
+        std::lock_guard<std::mutex> g2(w->coll_mu);
+        if (!w->area.count(dev)) {
+            CollRing* area = nullptr;
+            const size_t bytes = sizeof(CollRing) * World::kMaxRings;
+            MPX_CU(cudaMalloc(reinterpret_cast<void**>(&area), bytes));
+            cudaStream_t svc = w->service(dev);
+            MPX_CU(cudaMemsetAsync(area, 0, bytes, svc));
+            MPX_CU(cudaStreamSynchronize(svc));   // only the private service stream
+            w->area[dev] = area;
+        }
+    }
     return set_device(dev);
 }
 
@@ -758,7 +776,10 @@ int mpx_world_leave(mpx_world h, int rank) {
     if (rank < 0 || rank >= w->size || !w->joined[rank]) return fail(MPX_ERR_STATE, "rank %d not in world", rank);
     w->joined[rank] = false;
     if (--w->live == 0) {
-        for (auto& kv : w->rings) cudaFreeHost(kv.second);
+        for (auto& kv : w->area) {
+            set_device(kv.first);
+            cudaFree(kv.second);
+        }
         if (w->nccl_state == 2)
             for (auto cm : w->nccl)
                 if (cm) g_nccl.commDestroy(cm);
@@ -781,16 +802,15 @@ int mpx_comm_create(mpx_world h, int rank, int ctx, void* stream, mpx_comm* out)
     c->stream = reinterpret_cast<cudaStream_t>(stream);
     cudaError_t e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate(side)");
-    {   // collective slot ring shared by every rank of this context (setup time:
-        // cudaHostAlloc must not run while peers' streams may be parked)
+    {   // ring index of this context (the same in every device's area)
         std::lock_guard<std::mutex> g(w->coll_mu);
-        CollRing*& ring = w->rings[ctx];
-        if (!ring) {
-            MPX_CU(cudaHostAlloc(reinterpret_cast<void**>(&ring), sizeof(CollRing),
-                                 cudaHostAllocMapped | cudaHostAllocPortable));
-            std::memset(ring, 0, sizeof(CollRing));
+        auto it = w->ring_index.find(ctx);
+        if (it == w->ring_index.end()) {
+            const int idx = (int)w->ring_index.size();
+            if (idx >= World::kMaxRings) return fail(MPX_ERR_EXHAUSTED, "too many communicator contexts with collectives");
+            it = w->ring_index.emplace(ctx, idx).first;
         }
-        c->ring = ring;
+        c->ring = it->second;
     }
     std::lock_guard<std::mutex> g(g_handles_mu);
     g_comms[c.get()] = c;
@@ -949,25 +969,40 @@ int mpx_allreduce_enqueue(mpx_comm h, const void* sendbuf, void* recvbuf, int64_
         if (r != ncclSuccess) return fail(MPX_ERR_TRANSPORT, "ncclAllReduce: %s", g_nccl.errStr(r));
         return MPX_SUCCESS;
     }
-    // native one-shot: every rank's stream publishes its buffers and arrives,
-    // waits for all, reduces its slice into every rank, then meets again
+    // native one-shot: every rank's stream publishes its buffers and arrives
+    // (memops into every participating device's ring copy), waits for all on
+    // its own device's copy, reduces its slice into every rank, meets again
     if (w->size > kMaxCollRanks) return fail(MPX_ERR_UNSUPPORTED, "native allreduce supports <= %d ranks", kMaxCollRanks);
     const int64_t seq = c->coll_seq++;
     const int slot = (int)(seq % kCollSlots);
     const uint32_t gen = (uint32_t)(seq / kCollSlots + 1);
-    CollRing* ring = c->ring;
+    std::vector<CollRing*> copies;
+    CollRing* mine = nullptr;
+    {
+        std::lock_guard<std::mutex> g(w->coll_mu);
+        std::set<int> devs(w->devices.begin(), w->devices.end());
+        for (int d : devs) {
+            auto it = w->area.find(d);
+            if (it == w->area.end()) return fail(MPX_ERR_STATE, "device %d of the world is not set up", d);
+            copies.push_back(it->second + c->ring);
+            if (d == c->device) mine = it->second + c->ring;
+        }
+    }
     for (int j = 0; j < w->size; ++j)
         if (w->devices[j] != c->device) MPX_RC(ensure_peer(w, c->device, w->devices[j]));
     MPX_RC(set_device(c->device));
-    CollTable* tab = &ring->table[slot];
-    MPX_RC(write_ptr(c->stream, &tab->send[c->rank], sendbuf));
-    MPX_RC(write_ptr(c->stream, (const void* const*)&tab->recv[c->rank], recvbuf));
-    MPX_RC(write_flag(c->stream, &ring->arrive[slot][c->rank], gen));
-    for (int j = 0; j < w->size; ++j) MPX_RC(wait_flag(c->stream, &ring->arrive[slot][j], gen));
-    cudaError_t e = launch_allreduce_oneshot(tab, w->size, c->rank, count, dtype_code, c->device, c->stream);
+    for (CollRing* r : copies) {
+        CollTable* tab = &r->table[slot];
+        MPX_RC(write_ptr(c->stream, &tab->send[c->rank], sendbuf));
+        MPX_RC(write_ptr(c->stream, (const void* const*)&tab->recv[c->rank], recvbuf));
+        MPX_RC(write_flag(c->stream, &r->arrive[slot][c->rank], gen));
+    }
+    for (int j = 0; j < w->size; ++j) MPX_RC(wait_flag(c->stream, &mine->arrive[slot][j], gen));
+    cudaError_t e = launch_allreduce_oneshot(&mine->table[slot], w->size, c->rank, count, dtype_code, c->device,
+                                             c->stream);
     if (e != cudaSuccess) return cuda_fail(e, "allreduce launch");
-    MPX_RC(write_flag(c->stream, &ring->finish[slot][c->rank], gen));
-    for (int j = 0; j < w->size; ++j) MPX_RC(wait_flag(c->stream, &ring->finish[slot][j], gen));
+    for (CollRing* r : copies) MPX_RC(write_flag(c->stream, &r->finish[slot][c->rank], gen));
+    for (int j = 0; j < w->size; ++j) MPX_RC(wait_flag(c->stream, &mine->finish[slot][j], gen));
     return MPX_SUCCESS;
 }
 
