@@ -1,5 +1,6 @@
 // coll.cu -- native allreduce kernel (see coll.hpp).
 #include <algorithm>
+#include <cstdint>
 
 #include "coll.hpp"
 #include "mpx.h"
@@ -9,22 +10,59 @@ namespace mpx {
 namespace {
 
 template <typename T, typename A>
+__device__ __forceinline__ void reduce_one(const T* const* src, T* const* dst, int n, int64_t i) {
+    A acc = (A)src[0][i];
+    for (int j = 1; j < n; ++j) acc += (A)src[j][i];
+    const T out = (T)acc;
+    for (int j = 0; j < n; ++j) dst[j][i] = out;
+}
+
+// 16-byte vector form: V = 16 / sizeof(T) elements per access
+template <typename T, typename A>
+__device__ __forceinline__ void reduce_vec(const T* const* src, T* const* dst, int n, int64_t v) {
+    constexpr int V = 16 / sizeof(T);
+    union U { uint4 q; T e[V]; };
+    A acc[V];
+    U u;
+    u.q = __ldg(reinterpret_cast<const uint4*>(src[0]) + v);
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc[k] = (A)u.e[k];
+    for (int j = 1; j < n; ++j) {
+        u.q = __ldg(reinterpret_cast<const uint4*>(src[j]) + v);
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[k] += (A)u.e[k];
+    }
+#pragma unroll
+    for (int k = 0; k < V; ++k) u.e[k] = (T)acc[k];
+    for (int j = 0; j < n; ++j) reinterpret_cast<uint4*>(dst[j])[v] = u.q;
+}
+
+template <typename T, typename A>
 __global__ void __launch_bounds__(256)
 k_allreduce_oneshot(const CollTable* __restrict__ tab, int n, int64_t lo, int64_t hi) {
     __shared__ const T* src[kMaxCollRanks];
     __shared__ T* dst[kMaxCollRanks];
+    __shared__ int aligned;
+    if (threadIdx.x == 0) aligned = 1;
+    __syncthreads();
     if (threadIdx.x < n) {   // volatile: the slot is rewritten by later calls
         const volatile CollTable* vt = tab;
         src[threadIdx.x] = static_cast<const T*>(const_cast<const void*>(vt->send[threadIdx.x]));
         dst[threadIdx.x] = static_cast<T*>(const_cast<void*>(vt->recv[threadIdx.x]));
+        if (((reinterpret_cast<uintptr_t>(src[threadIdx.x]) | reinterpret_cast<uintptr_t>(dst[threadIdx.x])) & 15) != 0)
+            aligned = 0;
     }
     __syncthreads();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += stride) {
-        A acc = (A)src[0][i];
-        for (int j = 1; j < n; ++j) acc += (A)src[j][i];
-        const T out = (T)acc;
-        for (int j = 0; j < n; ++j) dst[j][i] = out;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    constexpr int V = 16 / sizeof(T);
+    if (aligned) {
+        const int64_t vlo = (lo + V - 1) / V, vhi = hi / V;
+        for (int64_t v = vlo + t0; v < vhi; v += stride) reduce_vec<T, A>(src, dst, n, v);
+        for (int64_t i = lo + t0; i < min(hi, vlo * V); i += stride) reduce_one<T, A>(src, dst, n, i);
+        for (int64_t i = max(lo, vhi * V) + t0; i < hi; i += stride) reduce_one<T, A>(src, dst, n, i);
+    } else {
+        for (int64_t i = lo + t0; i < hi; i += stride) reduce_one<T, A>(src, dst, n, i);
     }
 }
 

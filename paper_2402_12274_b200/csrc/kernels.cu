@@ -209,10 +209,20 @@ __device__ __forceinline__ void chain_elems(const ChainJob& j, int64_t t0, int64
 
 template <bool PACK>
 __global__ void __launch_bounds__(kChainThreads) k_chain(const ChainBatch b) {
+    // jobs with equal block counts are interleaved block by block, so e.g. the
+    // lo and hi x-faces touch the same DRAM pages at the same time
     int ji = 0;
-    while (ji + 1 < b.njobs && (int)blockIdx.x >= b.job[ji + 1].blk0) ++ji;
+    const int bid = (int)blockIdx.x;
+    for (int i = 0; i < b.njobs; ++i) {
+        const ChainJob& q = b.job[i];
+        const int rel = bid - q.blk0;
+        if (rel >= 0 && rel < q.nblk * q.gsize && rel % q.gsize == q.gpos) {
+            ji = i;
+            break;
+        }
+    }
     const ChainJob& j = b.job[ji];
-    const int64_t blk = blockIdx.x - j.blk0;
+    const int64_t blk = (bid - j.blk0) / j.gsize;
     if (j.mode == CHAIN_ROW) {
         chain_rows<PACK>(j, blk * (kChainThreads / 32) + (threadIdx.x >> 5),
                          (int64_t)j.nblk * (kChainThreads / 32));
@@ -526,8 +536,25 @@ cudaError_t launch_chain_batch(ChainBatch& b, bool pack, int device, cudaStream_
             want = (j.rows + kChainThreads - 1) / kChainThreads;
         }
         j.nblk = (int32_t)std::max<int64_t>(1, std::min<int64_t>(want, cap));
-        j.blk0 = (int32_t)total;
-        total += j.nblk;
+        j.gsize = 1;
+        j.gpos = 0;
+        j.blk0 = -1;
+    }
+    for (int i = 0; i < b.njobs; ++i) {   // groups of equal nblk, interleaved
+        ChainJob& j = b.job[i];
+        if (j.blk0 >= 0) continue;
+        int g = 0;
+        for (int k = i; k < b.njobs; ++k)
+            if (b.job[k].blk0 < 0 && b.job[k].nblk == j.nblk) ++g;
+        int pos = 0;
+        for (int k = i; k < b.njobs; ++k) {
+            ChainJob& q = b.job[k];
+            if (q.blk0 >= 0 || q.nblk != j.nblk) continue;
+            q.blk0 = (int32_t)total;
+            q.gsize = g;
+            q.gpos = pos++;
+        }
+        total += (int64_t)j.nblk * g;
     }
     if (pack) k_chain<true><<<(unsigned)total, kChainThreads, 0, stream>>>(b);
     else k_chain<false><<<(unsigned)total, kChainThreads, 0, stream>>>(b);

@@ -22,8 +22,10 @@ struct ChainJob {
     int64_t limit;    // packed bytes to move (unpack may stop mid-row: bytewise tail)
     int32_t w;        // element mode: word width in bytes
     int32_t mode;     // CHAIN_ELEM: thread per row; CHAIN_ROW: warp per row, 16 B + funnel
-    int32_t blk0;     // first block of this job (filled by the launcher)
-    int32_t nblk;     // blocks of this job (filled by the launcher)
+    int32_t blk0;     // first block of this job's interleave group (launcher)
+    int32_t nblk;     // blocks of this job (launcher)
+    int32_t gsize;    // jobs in the group; group blocks alternate between them
+    int32_t gpos;     // this job's position in the group
 };
 
 struct ChainBatch {
