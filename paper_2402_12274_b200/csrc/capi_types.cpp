@@ -455,7 +455,7 @@ int mpx_layout_query(mpx_datatype h, int64_t count, int64_t out[8]) {
     out[4] = p.node_count;
     out[5] = p.kind;
     out[6] = p.overlap;
-    out[7] = p.chain_align;
+    out[7] = p.kind == PLAN_SPAN ? (int64_t)p.perm_specs.size() : p.chain_align;
     return MPX_SUCCESS;
 }
 

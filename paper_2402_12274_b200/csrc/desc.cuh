@@ -65,21 +65,64 @@ static_assert(sizeof(SpanBody) % 16 == 0, "SpanBody must be 16-byte sized");
 struct SpanChunk {
     int64_t src;            // span start of element 0 (layout offset)
     int64_t pk;             // packed offset of element 0
+    int32_t span;           // layout bytes covered: (n - 1) * stride + span_len (raw: stride)
+    int32_t plen;           // packed bytes: n * nbytes (raw: stride)
     int32_t n;              // elements
     int32_t body;           // body index, -1 = raw contiguous piece of `stride` bytes
     int32_t stride;         // element stride in bytes (>= span_len when n > 1)
-    int32_t pad;
+    int16_t perm[2];        // word-gather spec for [unpack, pack] (index into SpanPlan::perms)
+    int32_t pad[2];
 };
+static_assert(sizeof(SpanChunk) == 48, "SpanChunk layout");
+
+// ---- periodic word gather (k_perm) ----
+// For a chunk of n equal elements the output stream (packed bytes for pack,
+// the layout span for unpack) is a periodic function of the input stream:
+// output element size Eo, input element size Ei, and every E elements
+// (E in {1,2,4}, chosen so E*Eo and E*Ei are multiples of 4) the pattern of
+// 32-bit output words repeats with the input advanced by E*Ei bytes.  A warp
+// step produces W = M*E*Eo/4 consecutive aligned output words (lane l owns
+// words l, l+32, ... < W: its "slots"); each output word is assembled from a
+// window of <= 4 consecutive input words with byte_perm selectors.  The
+// selectors depend only on the slot and on the two address phases
+// (output address & 3, input address & 3), so the host precomputes them:
+// tab[(po * 4 + ap) * W + j].  byte_perm reads only the low 16 bits of its
+// selector, so `sel` and `mix` feed it directly.
+constexpr int kPermMaxSlots = 4;     // W <= 128 words per step
+constexpr int kPermMaxSpecs = 16;
+
+struct PermEntry {
+    int32_t wo;             // first window word, relative to the staged input's word 0 (+ step * Dw)
+    uint32_t sel;           // byte_perm selectors: words (0, 1) in bits 0-15, words (2, 3) in bits 16-31
+    uint32_t mix;           // bits 0-15: selector merging the two halves; 16-19: cover (byte i is
+                            // written; unpack leaves layout gaps alone); 20-23: byte i comes from words (2, 3)
+    uint32_t pad;
+};
+static_assert(sizeof(PermEntry) == 16, "PermEntry layout");
+
+struct PermSpec {
+    int32_t W;              // output words per warp step
+    int32_t Dw;             // input words advanced per step
+    int32_t ns;             // slots per lane: ceil(W / 32)
+    int32_t pad;
+    const PermEntry* tab;   // [16][W]
+};
+static_assert(sizeof(PermSpec) == 24, "PermSpec layout");
 
 struct SpanPlan {
     const SpanChunk* chunks;
     const SpanBody* bodies;
+    const PermSpec* perms;              // nullptr: no word-gather form (k_span fallback)
     int32_t nchunks, nbodies;
-    int32_t outer_depth, pad;
+    int32_t nperms, outer_depth;
     int64_t outer_cnt[kSpanMaxOuter];
     int64_t outer_str[kSpanMaxOuter];   // layout stride per outer level
     int64_t outer_pk[kSpanMaxOuter];    // packed stride per outer level
     int64_t nunits;                     // prod(outer_cnt) * nchunks
+    uint64_t m_nchunks;                 // magic divisors for the unit decode
+    uint64_t m_outer1;
+    int32_t s_nchunks, s_outer1;
+    int32_t ns_max[2];                  // most slots any spec needs, [unpack, pack]
 };
 
 struct DNode {

@@ -1,0 +1,345 @@
+// k_perm.cu -- periodic word-gather pack / unpack for span plans (sm_100a).
+//
+// Layouts lowered to span chunks (plan.cpp: struct / indexed / nested types,
+// e.g. BASELINE cfg3) move through this kernel whenever every chunk has a
+// PermSpec (desc.cuh).  Data movement per warp and chunk:
+//
+//   1. the chunk's contiguous input (the layout span for pack, the packed
+//      bytes for unpack) streams into shared memory with 16-byte cp.async,
+//      double-buffered: chunk i+1 loads while chunk i is permuted;
+//   2. each lane assembles whole aligned 32-bit output words from a window of
+//      <= 4 staged input words with byte_perm (selectors precomputed per slot
+//      and address phase on the host) and stores them straight to global
+//      memory, a warp step covering W consecutive words;
+//   3. words at the two ends of a chunk, words straddling a layout gap
+//      (unpack) and chunks cut by the data limit take a per-byte path, so no
+//      byte outside the layout (or past the limit) is ever written.
+//
+// Reference semantics: datatype.py:695-702 (pack) and :705-728 (unpack, prefix
+// writes for short data); span plans never hold overlapping runs.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "desc.cuh"
+#include "kernels.hpp"
+
+namespace mpx {
+
+namespace {
+
+constexpr int kWarps = 8;
+constexpr int kBuf = kSpanStage + 32;     // staged input + window slack at the end
+constexpr int kFront = 16;                // window slack before the staged input
+constexpr int kSlot = kFront + kBuf;
+template <int NS> constexpr int blocks_per_sm() { return NS <= 2 ? 4 : 3; }
+constexpr size_t kSmem = size_t(kWarps) * 2 * kSlot;
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];\n" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds8(uint32_t a) {
+    uint16_t v;
+    asm volatile("ld.shared.u8 %0, [%1];\n" : "=h"(v) : "r"(a));
+    return v;
+}
+
+struct Unit {
+    const uint8_t* in;   // chunk input
+    uint8_t* out;        // chunk output
+    int32_t in_len;      // input bytes present (unpack: cut by the data limit)
+    int32_t out_len;     // output bytes (pack: cut by the limit)
+    int32_t spec;
+    int32_t flags;       // bit 0: live (starts before the limit), bit 1: input holds the whole chunk
+};
+
+// Walks the units [u, u_end) of one warp in order without per-unit division:
+// unit = (outer indices o0, o1; chunk c).
+struct UnitIter {
+    int64_t u, u_end;
+    int64_t c, o1;
+    int64_t loff, poff;
+};
+
+__device__ __forceinline__ void iter_init(UnitIter& it, const SpanPlan& sp, int64_t u0, int64_t u1) {
+    it.u = u0;
+    it.u_end = u1;
+    const uint64_t o = fdiv((uint64_t)u0, sp.m_nchunks, sp.s_nchunks);
+    it.c = u0 - (int64_t)o * sp.nchunks;
+    it.o1 = 0;
+    it.loff = it.poff = 0;
+    if (sp.outer_depth == 1) {
+        it.loff = (int64_t)o * sp.outer_str[0];
+        it.poff = (int64_t)o * sp.outer_pk[0];
+    } else if (sp.outer_depth == 2) {
+        const uint64_t o0 = fdiv(o, sp.m_outer1, sp.s_outer1);
+        it.o1 = (int64_t)(o - o0 * (uint64_t)sp.outer_cnt[1]);
+        it.loff = (int64_t)o0 * sp.outer_str[0] + it.o1 * sp.outer_str[1];
+        it.poff = (int64_t)o0 * sp.outer_pk[0] + it.o1 * sp.outer_pk[1];
+    }
+}
+
+__device__ __forceinline__ void iter_next(UnitIter& it, const SpanPlan& sp) {
+    ++it.u;
+    if (++it.c < sp.nchunks) return;
+    it.c = 0;
+    if (sp.outer_depth == 1) {
+        it.loff += sp.outer_str[0];
+        it.poff += sp.outer_pk[0];
+    } else if (sp.outer_depth == 2) {
+        it.loff += sp.outer_str[1];
+        it.poff += sp.outer_pk[1];
+        if (++it.o1 == sp.outer_cnt[1]) {
+            it.o1 = 0;
+            it.loff += sp.outer_str[0] - sp.outer_cnt[1] * sp.outer_str[1];
+            it.poff += sp.outer_pk[0] - sp.outer_cnt[1] * sp.outer_pk[1];
+        }
+    }
+}
+
+template <bool PACK>
+__device__ __forceinline__ Unit make_unit(const UnitIter& it, const SpanPlan& sp, const uint8_t* src, uint8_t* dst,
+                                          int64_t limit) {
+    const SpanChunk* ch = sp.chunks + it.c;
+    const int64_t lay0 = __ldg(&ch->src) + it.loff, pk0 = __ldg(&ch->pk) + it.poff;
+    const int2 sl = __ldg(reinterpret_cast<const int2*>(&ch->span));   // span, plen
+    const int32_t pp = __ldg(reinterpret_cast<const int32_t*>(&ch->perm[0]));
+    Unit r;
+    r.spec = PACK ? (pp >> 16) : (int32_t)(int16_t)(pp & 0xFFFF);
+    const int32_t avail = (int32_t)min((int64_t)sl.y, limit - pk0);
+    if (PACK) {
+        r.in = src + lay0;
+        r.out = dst + pk0;
+        r.in_len = sl.x;
+        r.out_len = avail;
+        r.flags = (pk0 < limit ? 1 : 0) | 2;
+    } else {
+        r.in = src + pk0;
+        r.out = dst + lay0;
+        r.in_len = avail;
+        r.out_len = sl.x;
+        r.flags = (pk0 < limit ? 1 : 0) | (avail >= sl.y ? 2 : 0);
+    }
+    return r;
+}
+
+__device__ __forceinline__ void stage(uint32_t sbuf, const Unit& U, int lane) {
+    const int a = (int)(reinterpret_cast<uintptr_t>(U.in) & 15);
+    const uint8_t* g = U.in - a;
+    const int nv = (a + U.in_len + 15) >> 4;
+    for (int i = lane; i < nv; i += 32) cp_async16(sbuf + 16 * i, g + 16 * i);
+}
+
+__device__ __forceinline__ uint32_t lds32_if(uint32_t a, uint32_t pred) {
+    uint32_t v = 0;
+    asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.shared.b32 %0, [%1];\n}\n"
+                 : "+r"(v) : "r"(a), "r"(pred));
+    return v;
+}
+
+// Bytes of output word gw written this step: cover, minus bytes before the
+// chunk (first word) and past its end (last word).
+__device__ __forceinline__ uint32_t valid_mask(uint32_t cov, int gw, int po, int out_len) {
+    const uint32_t lo = gw == 0 ? (0xFu << po) & 0xFu : 0xFu;
+    const int nb = out_len + po - 4 * gw;
+    const uint32_t hi = nb >= 4 ? 0xFu : (nb > 0 ? (1u << nb) - 1 : 0u);
+    return cov & lo & hi;
+}
+
+template <int NS>
+__device__ __forceinline__ void permute(const PermSpec& S, const Unit& U, uint32_t sbuf, int lane) {
+    const int a = (int)(reinterpret_cast<uintptr_t>(U.in) & 15);
+    const int ap = a & 3;
+    const int po = (int)(reinterpret_cast<uintptr_t>(U.out) & 3);
+    const int W = S.W, Dw = S.Dw;
+    const uint4* tab = reinterpret_cast<const uint4*>(S.tab) + (po * 4 + ap) * W;
+    const uint32_t A = sbuf + (uint32_t)(a & ~3);      // shared address of input word 0
+    uint32_t* ow = reinterpret_cast<uint32_t*>(U.out - po);
+    uint8_t* ob = U.out - po;
+    // per slot: shared address of the window at step 0, selectors, mix word
+    uint32_t wa[NS], sel[NS], mix[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        const int j = lane + 32 * s;
+        uint4 e = make_uint4(0, 0, 0, 0);
+        if (j < W) e = __ldg(tab + j);
+        wa[s] = A + 4u * e.x;
+        sel[s] = e.y;
+        mix[s] = e.z;
+    }
+    const int words = (po + U.out_len + 3) >> 2;
+    const int nsteps = (words + W - 1) / W;
+
+    if (!(U.flags & 2)) {
+        // input cut by the data limit (one chunk per call): bytes whose input
+        // is missing are skipped one by one
+        for (int k = 0; k < nsteps; ++k) {
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+                const int gw = k * W + lane + 32 * s;
+                const uint32_t vm = valid_mask((mix[s] >> 16) & 0xF, gw, po, U.out_len);
+                if (!vm || gw >= words) continue;
+                const int wb = (int)(wa[s] - A) / 4 + k * Dw;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    if (!((vm >> i) & 1)) continue;
+                    const uint32_t pr = (mix[s] >> (20 + i)) & 1;
+                    const uint32_t nib = ((pr ? sel[s] >> 16 : sel[s]) >> (4 * i)) & 7;
+                    const int in_off = 4 * (wb + 2 * (int)pr + (int)(nib >> 2)) + (int)(nib & 3) - ap;
+                    if (in_off < U.in_len) ob[4 * gw + i] = (uint8_t)lds8(A + (uint32_t)(in_off + ap));
+                }
+            }
+        }
+        return;
+    }
+
+    // first and last steps: windows may reach up to 16 bytes before the staged
+    // input (buffer front slack) or past its end; only valid bytes are stored
+    auto edge = [&](int k) {
+        const uint32_t kd = 4u * (uint32_t)(k * Dw);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            const int gw = k * W + lane + 32 * s;
+            const uint32_t vm = valid_mask((mix[s] >> 16) & 0xF, gw, po, U.out_len);
+            if (!vm || gw >= words) continue;
+            const uint32_t w = wa[s] + kd;
+            const uint32_t pr = mix[s] >> 20;
+            uint32_t r = __byte_perm(lds32(w), lds32(w + 4), sel[s]);
+            r = __byte_perm(r, __byte_perm(lds32_if(w + 8, pr), lds32_if(w + 12, pr), sel[s] >> 16), mix[s]);
+            if (vm == 0xF) {
+                ow[gw] = r;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if ((vm >> i) & 1) ob[4 * gw + i] = (uint8_t)(r >> (8 * i));
+            }
+        }
+    };
+
+    const int kf = (U.out_len + po) / (4 * W);   // steps [.., kf) hold only whole words
+    int k = 0;
+    if (po != 0 || kf == 0) {
+        edge(0);
+        k = 1;
+    }
+    for (; k < kf; ++k) {
+        const uint32_t kd = 4u * (uint32_t)(k * Dw);
+        const int kw = k * W;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            const uint32_t cov = (mix[s] >> 16) & 0xF;
+            if (!cov) continue;
+            const uint32_t w = wa[s] + kd;
+            const uint32_t pr = mix[s] >> 20;
+            uint32_t r = __byte_perm(lds32(w), lds32(w + 4), sel[s]);
+            r = __byte_perm(r, __byte_perm(lds32_if(w + 8, pr), lds32_if(w + 12, pr), sel[s] >> 16), mix[s]);
+            const int gw = kw + lane + 32 * s;
+            if (cov == 0xF) {
+                ow[gw] = r;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if ((cov >> i) & 1) ob[4 * gw + i] = (uint8_t)(r >> (8 * i));
+            }
+        }
+    }
+    for (; k < nsteps; ++k) edge(k);
+}
+
+template <bool PACK, int NS>
+__global__ void __launch_bounds__(kWarps * 32, blocks_per_sm<NS>())
+k_perm(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t limit) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    __shared__ PermSpec specs[2 * kPermMaxSpecs];
+    for (int i = threadIdx.x; i < sp.nperms; i += blockDim.x) specs[i] = sp.perms[i];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm) + (uint32_t)(warp * 2 * kSlot + kFront);
+    // a contiguous range of units per warp: consecutive chunks, no per-unit division
+    const int64_t nw = (int64_t)gridDim.x * kWarps, gwid = (int64_t)blockIdx.x * kWarps + warp;
+    const int64_t u0 = sp.nunits / nw * gwid + min(gwid, sp.nunits % nw);
+    const int64_t u1 = u0 + sp.nunits / nw + (gwid < sp.nunits % nw ? 1 : 0);
+    if (u0 >= u1) return;
+    UnitIter it;
+    iter_init(it, sp, u0, u1);
+    Unit cur = make_unit<PACK>(it, sp, src, dst, limit);
+    if (cur.flags & 1) stage(sbase, cur, lane);
+    cp_async_commit();
+    int pb = 0;
+    for (;;) {
+        iter_next(it, sp);
+        const bool more = it.u < it.u_end;
+        Unit nxt;
+        nxt.flags = 0;
+        if (more) {
+            nxt = make_unit<PACK>(it, sp, src, dst, limit);
+            if (nxt.flags & 1) stage(sbase + (uint32_t)((pb ^ 1) * kSlot), nxt, lane);
+        }
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp();
+        if (cur.flags & 1) permute<NS>(specs[cur.spec], cur, sbase + (uint32_t)(pb * kSlot), lane);
+        __syncwarp();
+        if (!more) break;
+        cur = nxt;
+        pb ^= 1;
+    }
+    cp_async_wait<0>();
+}
+
+template <bool PACK>
+cudaError_t launch_dir(const Plan& p, const uint8_t* src, uint8_t* dst, int64_t limit, cudaStream_t stream) {
+    const int ns = p.span.ns_max[PACK ? 1 : 0];
+    const int64_t want = (p.span.nunits + kWarps - 1) / kWarps;
+    const int64_t grid = std::max<int64_t>(
+        1, std::min<int64_t>(want, (int64_t)sm_count(p.device) * (ns <= 2 ? blocks_per_sm<2>() : blocks_per_sm<4>())));
+    switch (ns) {
+    case 1: k_perm<PACK, 1><<<(unsigned)grid, kWarps * 32, kSmem, stream>>>(p.span, src, dst, limit); break;
+    case 2: k_perm<PACK, 2><<<(unsigned)grid, kWarps * 32, kSmem, stream>>>(p.span, src, dst, limit); break;
+    case 3: k_perm<PACK, 3><<<(unsigned)grid, kWarps * 32, kSmem, stream>>>(p.span, src, dst, limit); break;
+    default: k_perm<PACK, 4><<<(unsigned)grid, kWarps * 32, kSmem, stream>>>(p.span, src, dst, limit); break;
+    }
+    return cudaGetLastError();
+}
+
+template <typename F>
+cudaError_t attr(F f, cudaFuncAttributes* a) {
+    return cudaFuncGetAttributes(a, f);
+}
+
+}  // namespace
+
+static_assert(kPermMaxSlots == 4, "launch_dir instantiates NS = 1..4");
+
+cudaError_t launch_perm(const Plan& p, bool pack, const uint8_t* src, uint8_t* dst, int64_t limit,
+                        cudaStream_t stream) {
+    if (limit <= 0 || p.span.nunits == 0) return cudaSuccess;
+    return pack ? launch_dir<true>(p, src, dst, limit, stream) : launch_dir<false>(p, src, dst, limit, stream);
+}
+
+cudaError_t preload_perm_kernels() {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaSuccess, r;
+    if ((r = attr(k_perm<true, 1>, &a)) != cudaSuccess) e = r;
+    if ((r = attr(k_perm<true, 2>, &a)) != cudaSuccess) e = r;
+    if ((r = attr(k_perm<true, 3>, &a)) != cudaSuccess) e = r;
+    if ((r = attr(k_perm<true, 4>, &a)) != cudaSuccess) e = r;
+    if ((r = attr(k_perm<false, 1>, &a)) != cudaSuccess) e = r;
+    if ((r = attr(k_perm<false, 2>, &a)) != cudaSuccess) e = r;
+    if ((r = attr(k_perm<false, 3>, &a)) != cudaSuccess) e = r;
+    if ((r = attr(k_perm<false, 4>, &a)) != cudaSuccess) e = r;
+    return e;
+}
+
+}  // namespace mpx

@@ -486,6 +486,8 @@ k_iov(const DDesc d, int64_t k0, int64_t n, int64_t* __restrict__ out) {
     }
 }
 
+}  // namespace
+
 int sm_count(int device) {
     static int cached[64] = {0};
     if (device < 0 || device >= 64) return 148;
@@ -496,8 +498,6 @@ int sm_count(int device) {
     }
     return cached[device];
 }
-
-}  // namespace
 
 void chain_setup(const Plan& p, bool pack, ChainJob* j) {
     const Chain& c = p.chain;
@@ -591,12 +591,14 @@ cudaError_t preload_pack_kernels() {
     if ((r = cudaFuncGetAttributes(&a, k_iov)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_span<true>)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_span<false>)) != cudaSuccess) e = r;
+    if ((r = preload_perm_kernels()) != cudaSuccess) e = r;
     return e;
 }
 
 cudaError_t launch_span(const Plan& p, bool pack, const uint8_t* src, uint8_t* dst, int64_t limit,
                         cudaStream_t stream) {
     if (limit <= 0 || p.span.nunits == 0) return cudaSuccess;
+    if (p.span.perms) return launch_perm(p, pack, src, dst, limit, stream);
     const int64_t want = (p.span.nunits + kSpanWarps - 1) / kSpanWarps;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count(p.device) * 4));
     static bool attr_set[2] = {false, false};

@@ -43,7 +43,12 @@ cudaError_t launch_generic(const Plan& p, bool pack, const uint8_t* src, uint8_t
 cudaError_t launch_span(const Plan& p, bool pack, const uint8_t* src, uint8_t* dst, int64_t limit,
                         cudaStream_t stream);
 cudaError_t launch_iov(const Plan& p, int64_t k0, int64_t n, int64_t* out, cudaStream_t stream);
+// word-gather pack/unpack of span plans with PermSpecs (k_perm.cu)
+cudaError_t launch_perm(const Plan& p, bool pack, const uint8_t* src, uint8_t* dst, int64_t limit,
+                        cudaStream_t stream);
 // force-load the pack/unpack/iov kernels on the current device (lazy loading)
 cudaError_t preload_pack_kernels();
+cudaError_t preload_perm_kernels();
+int sm_count(int device);
 
 }  // namespace mpx

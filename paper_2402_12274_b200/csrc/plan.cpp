@@ -2,7 +2,9 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <climits>
 #include <cstring>
+#include <tuple>
 #include <map>
 #include <mutex>
 #include <unordered_map>
@@ -262,6 +264,7 @@ class SpanBuilder {
     }
 
     void add(int64_t src, int64_t pk, int64_t n, int body, int64_t stride) {
+        if (!ok) return;
         SpanChunk c;
         std::memset(&c, 0, sizeof c);
         c.src = src;
@@ -269,6 +272,8 @@ class SpanBuilder {
         c.n = (int32_t)n;
         c.body = body;
         c.stride = (int32_t)(n > 1 ? stride : 0);
+        c.span = (int32_t)((n - 1) * c.stride + bodies[body].span_len);
+        c.plen = (int32_t)(n * bodies[body].nbytes);
         chunks.push_back(c);
     }
 
@@ -280,9 +285,190 @@ class SpanBuilder {
         c.n = 1;
         c.body = -1;
         c.stride = (int32_t)len;
+        c.span = (int32_t)len;
+        c.plen = (int32_t)len;
         chunks.push_back(c);
     }
 };
+
+int64_t floor_div(int64_t a, int64_t b) {   // b > 0
+    return a >= 0 ? a / b : -((-a + b - 1) / b);
+}
+
+// One table entry from the input offsets r[i] of output bytes i (cov[i]:
+// byte written) at input phase ap; false if the bytes span >= 16 input bytes.
+bool make_entry(const int64_t r[4], const bool cov[4], int ap, PermEntry* en) {
+    std::memset(en, 0, sizeof *en);
+    int64_t mn = INT64_MAX;
+    for (int i = 0; i < 4; ++i)
+        if (cov[i]) mn = std::min(mn, ap + r[i]);
+    if (mn == INT64_MAX) return true;
+    const int64_t wo = floor_div(mn, 4);
+    if (wo < INT16_MIN || wo > INT16_MAX) return false;
+    en->wo = (int32_t)wo;
+    uint32_t s01 = 0, s23 = 0, pairs = 0, cover = 0;
+    for (int i = 0; i < 4; ++i) {
+        if (!cov[i]) continue;
+        const int64_t rel = ap + r[i] - 4 * wo;
+        if (rel < 0 || rel >= 16) return false;
+        const uint32_t wi = (uint32_t)(rel >> 2), bi = (uint32_t)(rel & 3);
+        const uint32_t nib = (wi & 1) * 4 + bi;
+        if (wi >> 1) {
+            s23 |= nib << (4 * i);
+            pairs |= 1u << i;
+        } else {
+            s01 |= nib << (4 * i);
+        }
+        cover |= 1u << i;
+    }
+    uint32_t mixsel = 0;
+    for (int i = 0; i < 4; ++i) mixsel |= (uint32_t)(i + ((pairs >> i) & 1) * 4) << (4 * i);
+    en->sel = s01 | (s23 << 16);
+    en->mix = mixsel | (cover << 16) | (pairs << 20);
+    return true;
+}
+
+// Word-gather tables for one (element map, direction): output element of Eo
+// bytes, input element of Ei bytes, map[t] = input offset of output byte t
+// within its element (-1: not written).  False if the period or a word's
+// input window is too wide for k_perm.
+bool build_perm(int64_t Eo, int64_t Ei, const std::vector<int64_t>& map, PermSpec* spec,
+                std::vector<PermEntry>* tab) {
+    int64_t E = 1;
+    while (((E * Eo) % 4) || ((E * Ei) % 4)) E *= 2;
+    const int64_t P = E * Eo / 4;
+    const int64_t wmax = 32 * kPermMaxSlots;
+    if (P > wmax) return false;
+    int64_t M = 1;
+    double best = -1;
+    for (int64_t m = 1; m * P <= wmax; ++m) {
+        const int64_t w = m * P;
+        const double eff = double(w) / double(32 * ((w + 31) / 32));
+        if (eff > best + 1e-9) { best = eff; M = m; }
+    }
+    const int64_t W = M * P;
+    const int64_t Din = M * E * Ei;      // input bytes per step (multiple of 4)
+    spec->W = (int32_t)W;
+    spec->Dw = (int32_t)(Din / 4);
+    spec->ns = (int32_t)((W + 31) / 32);
+    spec->pad = 0;
+    spec->tab = reinterpret_cast<const PermEntry*>((uintptr_t)tab->size());   // patched at upload
+    for (int po = 0; po < 4; ++po) {
+        for (int ap = 0; ap < 4; ++ap) {
+            for (int64_t j = 0; j < W; ++j) {
+                PermEntry en;
+                int64_t r[4];
+                bool cov[4];
+                for (int i = 0; i < 4; ++i) {
+                    // one step later, so every byte of the slot is a real byte
+                    const int64_t q = 4 * j + i - po + 4 * W;
+                    const int64_t e = q / Eo, t = q % Eo;
+                    cov[i] = map[(size_t)t] >= 0;
+                    r[i] = cov[i] ? e * Ei + map[(size_t)t] - Din : 0;
+                }
+                if (!make_entry(r, cov, ap, &en)) return false;
+                tab->push_back(en);
+            }
+        }
+    }
+    return true;
+}
+
+// Single-element chunks have no period: one step of W >= ceil((Eo + 3) / 4)
+// words covers the element at any output phase; bytes outside it are left
+// uncovered.
+bool build_perm_single(int64_t Eo, const std::vector<int64_t>& map, PermSpec* spec,
+                       std::vector<PermEntry>* tab) {
+    const int64_t need = (Eo + 3 + 3) / 4;
+    if (need > 32 * kPermMaxSlots) return false;
+    const int64_t W = need;
+    spec->W = (int32_t)W;
+    spec->Dw = 0;
+    spec->ns = (int32_t)((W + 31) / 32);
+    spec->pad = 0;
+    spec->tab = reinterpret_cast<const PermEntry*>((uintptr_t)tab->size());
+    for (int po = 0; po < 4; ++po) {
+        for (int ap = 0; ap < 4; ++ap) {
+            for (int64_t j = 0; j < W; ++j) {
+                PermEntry en;
+                int64_t r[4];
+                bool cov[4];
+                for (int i = 0; i < 4; ++i) {
+                    const int64_t q = 4 * j + i - po;
+                    cov[i] = q >= 0 && q < Eo && map[(size_t)q] >= 0;
+                    r[i] = cov[i] ? map[(size_t)q] : 0;
+                }
+                if (!make_entry(r, cov, ap, &en)) return false;
+                tab->push_back(en);
+            }
+        }
+    }
+    return true;
+}
+
+// Attach word-gather specs to every chunk; false leaves the plan on k_span.
+bool build_perms(std::vector<SpanChunk>& chunks, const std::vector<SpanBody>& bodies, Plan* p) {
+    std::map<std::tuple<int, int64_t, int>, int> ids;   // (body, stride, pack) -> spec
+    std::vector<PermSpec> specs;
+    std::vector<PermEntry> tab;
+    for (auto& c : chunks) {
+        for (int pack = 0; pack < 2; ++pack) {
+            int64_t S;
+            if (c.body < 0) S = 4;
+            else if (c.n > 1) S = c.stride;
+            else S = -1;                          // single element: no period
+            const auto key = std::make_tuple(c.body, S, pack);
+            auto it = ids.find(key);
+            if (it == ids.end()) {
+                if ((int)specs.size() >= 2 * kPermMaxSpecs) return false;
+                std::vector<int64_t> map;
+                int64_t Eo, Ei;
+                if (c.body < 0) {
+                    Eo = Ei = 4;
+                    map = {0, 1, 2, 3};
+                } else {
+                    const SpanBody& b = bodies[c.body];
+                    if (S < 0) {
+                        Eo = pack ? b.nbytes : b.span_len;
+                        map.assign((size_t)Eo, -1);
+                        for (int r = 0; r < b.nruns; ++r)
+                            for (int x = 0; x < b.rlen[r]; ++x) {
+                                if (pack) map[(size_t)(b.rpk[r] + x)] = b.roff[r] + x;
+                                else map[(size_t)(b.roff[r] + x)] = b.rpk[r] + x;
+                            }
+                        PermSpec sp;
+                        if (!build_perm_single(Eo, map, &sp, &tab)) return false;
+                        it = ids.emplace(key, (int)specs.size()).first;
+                        specs.push_back(sp);
+                        c.perm[pack] = (int16_t)it->second;
+                        continue;
+                    }
+                    if (pack) {
+                        Eo = b.nbytes;
+                        Ei = S;
+                        map.assign((size_t)Eo, -1);
+                        for (int r = 0; r < b.nruns; ++r)
+                            for (int x = 0; x < b.rlen[r]; ++x) map[(size_t)(b.rpk[r] + x)] = b.roff[r] + x;
+                    } else {
+                        Eo = S;
+                        Ei = b.nbytes;
+                        map.assign((size_t)Eo, -1);
+                        for (int r = 0; r < b.nruns; ++r)
+                            for (int x = 0; x < b.rlen[r]; ++x) map[(size_t)(b.roff[r] + x)] = b.rpk[r] + x;
+                    }
+                }
+                PermSpec sp;
+                if (!build_perm(Eo, Ei, map, &sp, &tab)) return false;
+                it = ids.emplace(key, (int)specs.size()).first;
+                specs.push_back(sp);
+            }
+            c.perm[pack] = (int16_t)it->second;
+        }
+    }
+    p->perm_specs = std::move(specs);
+    p->perm_tab = std::move(tab);
+    return true;
+}
 
 // Try the span lowering; true when it applies.
 bool build_span(const Node* layout, Plan* p) {
@@ -302,13 +488,22 @@ bool build_span(const Node* layout, Plan* p) {
     }
     b.emit(n, base, 0);
     if (!b.ok || b.chunks.empty()) return false;
-    // worth it only when elements are small enough that the descriptor walk
-    // would be per-byte bound: average packed bytes per chunk element
     sp.nchunks = (int32_t)b.chunks.size();
     sp.nbodies = (int32_t)b.bodies.size();
     int64_t units = sp.nchunks;
     for (int i = 0; i < sp.outer_depth; ++i) units *= sp.outer_cnt[i];
     sp.nunits = units;
+    host_magic((uint64_t)sp.nchunks, &sp.m_nchunks, &sp.s_nchunks);
+    if (sp.outer_depth == 2) host_magic((uint64_t)sp.outer_cnt[1], &sp.m_outer1, &sp.s_outer1);
+    if (!build_perms(b.chunks, b.bodies, p)) {
+        p->perm_specs.clear();
+        p->perm_tab.clear();
+    }
+    sp.nperms = (int32_t)p->perm_specs.size();
+    sp.ns_max[0] = sp.ns_max[1] = 0;
+    for (const auto& c : b.chunks)
+        for (int d = 0; d < 2 && sp.nperms; ++d)
+            sp.ns_max[d] = std::max(sp.ns_max[d], p->perm_specs[(size_t)c.perm[d]].ns);
     p->span = sp;
     p->span_chunks = std::move(b.chunks);
     p->span_bodies = std::move(b.bodies);
@@ -386,7 +581,11 @@ std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStre
         const size_t bb = p->span_bodies.size() * sizeof(SpanBody);
         const size_t co = (bo + bb + 15) & ~size_t(15);                     // span chunks
         const size_t cb = p->span_chunks.size() * sizeof(SpanChunk);
-        std::vector<uint8_t> host(co + cb + 16, 0);
+        const size_t so = (co + cb + 15) & ~size_t(15);                     // perm specs
+        const size_t sb = p->perm_specs.size() * sizeof(PermSpec);
+        const size_t to = (so + sb + 15) & ~size_t(15);                     // perm tables
+        const size_t tb = p->perm_tab.size() * sizeof(PermEntry);
+        std::vector<uint8_t> host(to + tb + 16, 0);
         std::memcpy(host.data(), f.nodes.data(), nb);
         if (!f.kids.empty()) std::memcpy(host.data() + nb, f.kids.data(), f.kids.size() * sizeof(int32_t));
         if (pb) {
@@ -395,6 +594,7 @@ std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStre
         }
         if (bb) std::memcpy(host.data() + bo, p->span_bodies.data(), bb);
         if (cb) std::memcpy(host.data() + co, p->span_chunks.data(), cb);
+        if (tb) std::memcpy(host.data() + to, p->perm_tab.data(), tb);
         (void)stream;
         void* dev = nullptr;
         cudaStream_t up = upload_stream(device);
@@ -403,6 +603,13 @@ std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStre
         if (e != cudaSuccess) {
             *err = std::string("descriptor allocation: ") + cudaGetErrorString(e);
             return nullptr;
+        }
+        if (sb) {   // table pointers are device addresses inside the blob
+            std::vector<PermSpec> specs = p->perm_specs;
+            for (auto& sp : specs)
+                sp.tab = reinterpret_cast<const PermEntry*>(static_cast<uint8_t*>(dev) + to) +
+                         reinterpret_cast<uintptr_t>(sp.tab);
+            std::memcpy(host.data() + so, specs.data(), sb);
         }
         p->blob = dev;
         // pageable source: the call returns once the bytes are staged, so the
@@ -423,6 +630,7 @@ std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStre
         p->desc.root = root;
         p->span.bodies = (const SpanBody*)(b + bo);
         p->span.chunks = (const SpanChunk*)(b + co);
+        p->span.perms = sb ? (const PermSpec*)(b + so) : nullptr;
         p->desc.runs = lay->runs;
         p->desc.nbytes = lay->nbytes;
     }

@@ -27,6 +27,8 @@ struct Plan {
     SpanPlan span{};        // valid for PLAN_SPAN (pointers into blob)
     std::vector<SpanChunk> span_chunks;   // host copies, uploaded with the descriptor
     std::vector<SpanBody> span_bodies;
+    std::vector<PermSpec> perm_specs;     // host copies; tab = offset into perm_tab until upload
+    std::vector<PermEntry> perm_tab;
     void* blob = nullptr;   // device allocation backing desc
     size_t blob_bytes = 0;
     cudaEvent_t ready = nullptr;     // upload finished (recorded on an internal stream)

@@ -113,7 +113,8 @@ class Datatype:
 
     def layout_query(self, count=1):
         """Host-side lowering summary (runs, nbytes, min_off, max_end,
-        node_count, plan kind, overlap, chain alignment)."""
+        node_count, plan kind, overlap, and chain alignment -- or, for span
+        plans, the number of word-gather specs (0: k_span fallback))."""
         out = (ctypes.c_int64 * 8)()
         check(lib.mpx_layout_query(self._h, count, out))
         keys = ("runs", "nbytes", "min_off", "max_end", "node_count", "plan",

@@ -25,6 +25,7 @@ for name, fn in (("pack", lambda: mp.pack_into(dt, src, out)), ("unpack", lambda
     ts = []
     for _ in range(reps):
         flush.zero_()
+        torch.cuda._sleep(100000)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(); fn(); b.record(); torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))

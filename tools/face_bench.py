@@ -41,6 +41,7 @@ def time_op(fn, reps, flush):
     fn()
     for a, b in evs:
         flush.zero_()
+        torch.cuda._sleep(100000)   # keep the host ahead: no launch gap inside the events
         a.record()
         fn()
         b.record()
