@@ -60,23 +60,22 @@ struct Unit {
     uint8_t* out;        // chunk output
     int32_t in_len;      // input bytes present (unpack: cut by the data limit)
     int32_t out_len;     // output bytes (pack: cut by the limit)
-    int32_t spec;
-    int32_t flags;       // bit 0: live (starts before the limit), bit 1: input holds the whole chunk
+    int32_t flags;       // bit 0: live (starts before the limit), bit 1: input holds the
+                         // whole chunk, bits 8+: PermSpec index
 };
 
-// Walks the units [u, u_end) of one warp in order without per-unit division:
-// unit = (outer indices o0, o1; chunk c).
+// Walks one warp's contiguous range of units in order without per-unit
+// division: unit = (outer indices o0, o1; chunk c).
 struct UnitIter {
-    int64_t u, u_end;
-    int64_t c, o1;
+    int32_t left;        // units after the current one
+    int32_t c, o1;
     int64_t loff, poff;
 };
 
 __device__ __forceinline__ void iter_init(UnitIter& it, const SpanPlan& sp, int64_t u0, int64_t u1) {
-    it.u = u0;
-    it.u_end = u1;
+    it.left = (int32_t)(u1 - u0 - 1);
     const uint64_t o = fdiv((uint64_t)u0, sp.m_nchunks, sp.s_nchunks);
-    it.c = u0 - (int64_t)o * sp.nchunks;
+    it.c = (int32_t)(u0 - (int64_t)o * sp.nchunks);
     it.o1 = 0;
     it.loff = it.poff = 0;
     if (sp.outer_depth == 1) {
@@ -84,14 +83,14 @@ __device__ __forceinline__ void iter_init(UnitIter& it, const SpanPlan& sp, int6
         it.poff = (int64_t)o * sp.outer_pk[0];
     } else if (sp.outer_depth == 2) {
         const uint64_t o0 = fdiv(o, sp.m_outer1, sp.s_outer1);
-        it.o1 = (int64_t)(o - o0 * (uint64_t)sp.outer_cnt[1]);
-        it.loff = (int64_t)o0 * sp.outer_str[0] + it.o1 * sp.outer_str[1];
-        it.poff = (int64_t)o0 * sp.outer_pk[0] + it.o1 * sp.outer_pk[1];
+        it.o1 = (int32_t)(o - o0 * (uint64_t)sp.outer_cnt[1]);
+        it.loff = (int64_t)o0 * sp.outer_str[0] + (int64_t)it.o1 * sp.outer_str[1];
+        it.poff = (int64_t)o0 * sp.outer_pk[0] + (int64_t)it.o1 * sp.outer_pk[1];
     }
 }
 
 __device__ __forceinline__ void iter_next(UnitIter& it, const SpanPlan& sp) {
-    ++it.u;
+    --it.left;
     if (++it.c < sp.nchunks) return;
     it.c = 0;
     if (sp.outer_depth == 1) {
@@ -112,24 +111,26 @@ template <bool PACK>
 __device__ __forceinline__ Unit make_unit(const UnitIter& it, const SpanPlan& sp, const uint8_t* src, uint8_t* dst,
                                           int64_t limit) {
     const SpanChunk* ch = sp.chunks + it.c;
-    const int64_t lay0 = __ldg(&ch->src) + it.loff, pk0 = __ldg(&ch->pk) + it.poff;
+    const longlong2 sp0 = __ldg(reinterpret_cast<const longlong2*>(ch));          // src, pk
+    const int64_t lay0 = sp0.x + it.loff, pk0 = sp0.y + it.poff;
     const int2 sl = __ldg(reinterpret_cast<const int2*>(&ch->span));   // span, plen
     const int32_t pp = __ldg(reinterpret_cast<const int32_t*>(&ch->perm[0]));
+    const int32_t spec = PACK ? (pp >> 16) : (int32_t)(int16_t)(pp & 0xFFFF);
     Unit r;
-    r.spec = PACK ? (pp >> 16) : (int32_t)(int16_t)(pp & 0xFFFF);
     const int32_t avail = (int32_t)min((int64_t)sl.y, limit - pk0);
+    const int32_t live = pk0 < limit ? 1 : 0;
     if (PACK) {
         r.in = src + lay0;
         r.out = dst + pk0;
         r.in_len = sl.x;
         r.out_len = avail;
-        r.flags = (pk0 < limit ? 1 : 0) | 2;
+        r.flags = live | 2 | (spec << 8);
     } else {
         r.in = src + pk0;
         r.out = dst + lay0;
         r.in_len = avail;
         r.out_len = sl.x;
-        r.flags = (pk0 < limit ? 1 : 0) | (avail >= sl.y ? 2 : 0);
+        r.flags = live | (avail >= sl.y ? 2 : 0) | (spec << 8);
     }
     return r;
 }
@@ -157,12 +158,34 @@ __device__ __forceinline__ uint32_t valid_mask(uint32_t cov, int gw, int po, int
     return cov & lo & hi;
 }
 
-template <int NS>
+__device__ __forceinline__ uint32_t prmt(uint32_t x, uint32_t y, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;\n" : "=r"(r) : "r"(x), "r"(y), "r"(sel));
+    return r;
+}
+
+// output word for a slot whose window starts at shared address w
+__device__ __forceinline__ uint32_t gather_word(uint32_t w, uint32_t sel, uint32_t mix) {
+    const uint32_t pr = mix >> 20;
+    const uint32_t lo = prmt(lds32(w), lds32(w + 4), sel);
+    const uint32_t hi = prmt(lds32_if(w + 8, pr), lds32_if(w + 12, pr), sel >> 16);
+    return prmt(lo, hi, mix);
+}
+
+__device__ __forceinline__ void store_bytes(uint8_t* p, uint32_t r, uint32_t m) {
+    if (m & 1) p[0] = (uint8_t)r;
+    if (m & 2) p[1] = (uint8_t)(r >> 8);
+    if (m & 4) p[2] = (uint8_t)(r >> 16);
+    if (m & 8) p[3] = (uint8_t)(r >> 24);
+}
+
+template <bool PACK, int NS>
 __device__ __forceinline__ void permute(const PermSpec& S, const Unit& U, uint32_t sbuf, int lane) {
     const int a = (int)(reinterpret_cast<uintptr_t>(U.in) & 15);
     const int ap = a & 3;
     const int po = (int)(reinterpret_cast<uintptr_t>(U.out) & 3);
-    const int W = S.W, Dw = S.Dw;
+    const int W = S.W, ns = S.ns;
+    const uint32_t Dw4 = 4u * (uint32_t)S.Dw;
     const uint4* tab = reinterpret_cast<const uint4*>(S.tab) + (po * 4 + ap) * W;
     const uint32_t A = sbuf + (uint32_t)(a & ~3);      // shared address of input word 0
     uint32_t* ow = reinterpret_cast<uint32_t*>(U.out - po);
@@ -173,30 +196,29 @@ __device__ __forceinline__ void permute(const PermSpec& S, const Unit& U, uint32
     for (int s = 0; s < NS; ++s) {
         const int j = lane + 32 * s;
         uint4 e = make_uint4(0, 0, 0, 0);
-        if (j < W) e = __ldg(tab + j);
+        if (s < ns && j < W) e = __ldg(tab + j);
         wa[s] = A + 4u * e.x;
         sel[s] = e.y;
         mix[s] = e.z;
     }
     const int words = (po + U.out_len + 3) >> 2;
-    const int nsteps = (words + W - 1) / W;
 
     if (!(U.flags & 2)) {
         // input cut by the data limit (one chunk per call): bytes whose input
         // is missing are skipped one by one
-        for (int k = 0; k < nsteps; ++k) {
+        for (int kw = 0, kd = 0; kw < words; kw += W, kd += (int)Dw4) {
 #pragma unroll
             for (int s = 0; s < NS; ++s) {
-                const int gw = k * W + lane + 32 * s;
+                const int gw = kw + lane + 32 * s;
                 const uint32_t vm = valid_mask((mix[s] >> 16) & 0xF, gw, po, U.out_len);
                 if (!vm || gw >= words) continue;
-                const int wb = (int)(wa[s] - A) / 4 + k * Dw;
+                const int wb = (int)(wa[s] - A) + kd;     // window start, bytes from input word 0
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     if (!((vm >> i) & 1)) continue;
                     const uint32_t pr = (mix[s] >> (20 + i)) & 1;
                     const uint32_t nib = ((pr ? sel[s] >> 16 : sel[s]) >> (4 * i)) & 7;
-                    const int in_off = 4 * (wb + 2 * (int)pr + (int)(nib >> 2)) + (int)(nib & 3) - ap;
+                    const int in_off = wb + 8 * (int)pr + 4 * (int)(nib >> 2) + (int)(nib & 3) - ap;
                     if (in_off < U.in_len) ob[4 * gw + i] = (uint8_t)lds8(A + (uint32_t)(in_off + ap));
                 }
             }
@@ -204,57 +226,39 @@ __device__ __forceinline__ void permute(const PermSpec& S, const Unit& U, uint32
         return;
     }
 
-    // first and last steps: windows may reach up to 16 bytes before the staged
-    // input (buffer front slack) or past its end; only valid bytes are stored
-    auto edge = [&](int k) {
-        const uint32_t kd = 4u * (uint32_t)(k * Dw);
+    uint32_t kd = 0;
+    for (int kw = 0; kw < words; kw += W, kd += Dw4) {
+        if ((kw > 0 || po == 0) && 4 * (kw + W) - po <= U.out_len) {
+            // interior step: every word whole
 #pragma unroll
-        for (int s = 0; s < NS; ++s) {
-            const int gw = k * W + lane + 32 * s;
-            const uint32_t vm = valid_mask((mix[s] >> 16) & 0xF, gw, po, U.out_len);
-            if (!vm || gw >= words) continue;
-            const uint32_t w = wa[s] + kd;
-            const uint32_t pr = mix[s] >> 20;
-            uint32_t r = __byte_perm(lds32(w), lds32(w + 4), sel[s]);
-            r = __byte_perm(r, __byte_perm(lds32_if(w + 8, pr), lds32_if(w + 12, pr), sel[s] >> 16), mix[s]);
-            if (vm == 0xF) {
-                ow[gw] = r;
-            } else {
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if ((vm >> i) & 1) ob[4 * gw + i] = (uint8_t)(r >> (8 * i));
+            for (int s = 0; s < NS; ++s) {
+                if (s >= ns) break;
+                const uint32_t r = gather_word(wa[s] + kd, sel[s], mix[s]);
+                const uint32_t cov = (mix[s] >> 16) & 0xF;
+                const int gw = kw + lane + 32 * s;
+                if (PACK) {
+                    if (cov) ow[gw] = r;            // packed words are whole or outside W
+                } else if (cov == 0xF) {
+                    ow[gw] = r;
+                } else if (cov) {
+                    store_bytes(ob + 4 * gw, r, cov);
+                }
             }
-        }
-    };
-
-    const int kf = (U.out_len + po) / (4 * W);   // steps [.., kf) hold only whole words
-    int k = 0;
-    if (po != 0 || kf == 0) {
-        edge(0);
-        k = 1;
-    }
-    for (; k < kf; ++k) {
-        const uint32_t kd = 4u * (uint32_t)(k * Dw);
-        const int kw = k * W;
+        } else {
+            // first / last step: windows may reach up to 16 bytes before the
+            // staged input (buffer front slack) or past its end
 #pragma unroll
-        for (int s = 0; s < NS; ++s) {
-            const uint32_t cov = (mix[s] >> 16) & 0xF;
-            if (!cov) continue;
-            const uint32_t w = wa[s] + kd;
-            const uint32_t pr = mix[s] >> 20;
-            uint32_t r = __byte_perm(lds32(w), lds32(w + 4), sel[s]);
-            r = __byte_perm(r, __byte_perm(lds32_if(w + 8, pr), lds32_if(w + 12, pr), sel[s] >> 16), mix[s]);
-            const int gw = kw + lane + 32 * s;
-            if (cov == 0xF) {
-                ow[gw] = r;
-            } else {
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if ((cov >> i) & 1) ob[4 * gw + i] = (uint8_t)(r >> (8 * i));
+            for (int s = 0; s < NS; ++s) {
+                if (s >= ns) break;
+                const int gw = kw + lane + 32 * s;
+                const uint32_t vm = valid_mask((mix[s] >> 16) & 0xF, gw, po, U.out_len);
+                if (!vm || gw >= words) continue;
+                const uint32_t r = gather_word(wa[s] + kd, sel[s], mix[s]);
+                if (vm == 0xF) ow[gw] = r;
+                else store_bytes(ob + 4 * gw, r, vm);
             }
         }
     }
-    for (; k < nsteps; ++k) edge(k);
 }
 
 template <bool PACK, int NS>
@@ -276,24 +280,24 @@ k_perm(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__
     Unit cur = make_unit<PACK>(it, sp, src, dst, limit);
     if (cur.flags & 1) stage(sbase, cur, lane);
     cp_async_commit();
-    int pb = 0;
+    uint32_t pb = 0;
     for (;;) {
-        iter_next(it, sp);
-        const bool more = it.u < it.u_end;
+        const bool more = it.left > 0;
         Unit nxt;
         nxt.flags = 0;
         if (more) {
+            iter_next(it, sp);
             nxt = make_unit<PACK>(it, sp, src, dst, limit);
-            if (nxt.flags & 1) stage(sbase + (uint32_t)((pb ^ 1) * kSlot), nxt, lane);
+            if (nxt.flags & 1) stage(sbase + (pb ^ kSlot), nxt, lane);
         }
         cp_async_commit();
         cp_async_wait<1>();
         __syncwarp();
-        if (cur.flags & 1) permute<NS>(specs[cur.spec], cur, sbase + (uint32_t)(pb * kSlot), lane);
+        if (cur.flags & 1) permute<PACK, NS>(specs[cur.flags >> 8], cur, sbase + pb, lane);
         __syncwarp();
         if (!more) break;
         cur = nxt;
-        pb ^= 1;
+        pb ^= kSlot;
     }
     cp_async_wait<0>();
 }

@@ -339,9 +339,11 @@ bool build_perm(int64_t Eo, int64_t Ei, const std::vector<int64_t>& map, PermSpe
     const int64_t P = E * Eo / 4;
     const int64_t wmax = 32 * kPermMaxSlots;
     if (P > wmax) return false;
+    // prefer <= 3 slots per lane (4 slots cost registers), then the fullest warp
+    const int64_t wcap = P <= 96 ? 96 : wmax;
     int64_t M = 1;
     double best = -1;
-    for (int64_t m = 1; m * P <= wmax; ++m) {
+    for (int64_t m = 1; m * P <= wcap; ++m) {
         const int64_t w = m * P;
         const double eff = double(w) / double(32 * ((w + 31) / 32));
         if (eff > best + 1e-9) { best = eff; M = m; }
