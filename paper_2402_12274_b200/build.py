@@ -20,7 +20,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-Wall",
-         "--expt-relaxed-constexpr", "-I", CSRC, "-I", INC]
+         "--expt-relaxed-constexpr", "-I", CSRC, "-I", INC] + \
+    os.environ.get("MPX_NVCC_FLAGS", "").split()   # experiments only (e.g. -DMPX_PERM_BPS2=3)
 
 
 def sources():

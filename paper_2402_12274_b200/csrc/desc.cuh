@@ -87,16 +87,17 @@ static_assert(sizeof(SpanChunk) == 48, "SpanChunk layout");
 // selectors depend only on the slot and on the two address phases
 // (output address & 3, input address & 3), so the host precomputes them:
 // tab[(po * 4 + ap) * W + j].  byte_perm reads only the low 16 bits of its
-// selector, so `sel` and `mix` feed it directly.
+// selector, so the entry words feed it directly.
 constexpr int kPermMaxSlots = 4;     // W <= 128 words per step
 constexpr int kPermMaxSpecs = 16;
 
 struct PermEntry {
-    int32_t wo;             // first window word, relative to the staged input's word 0 (+ step * Dw)
-    uint32_t sel;           // byte_perm selectors: words (0, 1) in bits 0-15, words (2, 3) in bits 16-31
-    uint32_t mix;           // bits 0-15: selector merging the two halves; 16-19: cover (byte i is
-                            // written; unpack leaves layout gaps alone); 20-23: byte i comes from words (2, 3)
-    uint32_t pad;
+    int32_t wo4;            // window start: byte offset from the staged input's word 0 (+ step * 4 * Dw)
+    uint32_t lo;            // bits 0-15: byte_perm selector over window words (0, 1);
+                            // 16-19: cover (byte i is written; unpack leaves layout gaps alone);
+                            // 20-23: byte i comes from window words (2, 3)
+    uint32_t hi;            // byte_perm selector over window words (2, 3)
+    uint32_t mix;           // byte_perm selector merging the two halves
 };
 static_assert(sizeof(PermEntry) == 16, "PermEntry layout");
 

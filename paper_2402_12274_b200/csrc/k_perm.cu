@@ -33,7 +33,10 @@ constexpr int kWarps = 8;
 constexpr int kBuf = kSpanStage + 32;     // staged input + window slack at the end
 constexpr int kFront = 16;                // window slack before the staged input
 constexpr int kSlot = kFront + kBuf;
-template <int NS> constexpr int blocks_per_sm() { return NS <= 2 ? 4 : 3; }
+#ifndef MPX_PERM_BPS2
+#define MPX_PERM_BPS2 4
+#endif
+template <int NS> constexpr int blocks_per_sm() { return NS <= 1 ? 4 : NS == 2 ? MPX_PERM_BPS2 : 3; }
 constexpr size_t kSmem = size_t(kWarps) * 2 * kSlot;
 
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
@@ -44,6 +47,8 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
+// shared loads by 32-bit shared-window address; ordered after the
+// cp.async wait / __syncwarp by the asm volatile chain
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
     uint32_t v;
     asm volatile("ld.shared.b32 %0, [%1];\n" : "=r"(v) : "r"(a));
@@ -142,11 +147,10 @@ __device__ __forceinline__ void stage(uint32_t sbuf, const Unit& U, int lane) {
     for (int i = lane; i < nv; i += 32) cp_async16(sbuf + 16 * i, g + 16 * i);
 }
 
-__device__ __forceinline__ uint32_t lds32_if(uint32_t a, uint32_t pred) {
-    uint32_t v = 0;
-    asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.shared.b32 %0, [%1];\n}\n"
-                 : "+r"(v) : "r"(a), "r"(pred));
-    return v;
+__device__ __forceinline__ uint32_t prmt(uint32_t x, uint32_t y, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;\n" : "=r"(r) : "r"(x), "r"(y), "r"(sel));
+    return r;
 }
 
 // Bytes of output word gw written this step: cover, minus bytes before the
@@ -158,18 +162,16 @@ __device__ __forceinline__ uint32_t valid_mask(uint32_t cov, int gw, int po, int
     return cov & lo & hi;
 }
 
-__device__ __forceinline__ uint32_t prmt(uint32_t x, uint32_t y, uint32_t sel) {
-    uint32_t r;
-    asm("prmt.b32 %0, %1, %2, %3;\n" : "=r"(r) : "r"(x), "r"(y), "r"(sel));
-    return r;
-}
+// one table slot, as loaded: window address at step 0 + the three selectors
+struct Slot {
+    uint32_t w, lo, hi, mix;
+};
 
-// output word for a slot whose window starts at shared address w
-__device__ __forceinline__ uint32_t gather_word(uint32_t w, uint32_t sel, uint32_t mix) {
-    const uint32_t pr = mix >> 20;
-    const uint32_t lo = prmt(lds32(w), lds32(w + 4), sel);
-    const uint32_t hi = prmt(lds32_if(w + 8, pr), lds32_if(w + 12, pr), sel >> 16);
-    return prmt(lo, hi, mix);
+// output word of a slot whose window starts at shared address w
+__device__ __forceinline__ uint32_t gather_word(uint32_t w, const Slot& e) {
+    const uint32_t a = prmt(lds32(w), lds32(w + 4), e.lo);
+    const uint32_t b = prmt(lds32(w + 8), lds32(w + 12), e.hi);
+    return prmt(a, b, e.mix);
 }
 
 __device__ __forceinline__ void store_bytes(uint8_t* p, uint32_t r, uint32_t m) {
@@ -188,18 +190,17 @@ __device__ __forceinline__ void permute(const PermSpec& S, const Unit& U, uint32
     const uint32_t Dw4 = 4u * (uint32_t)S.Dw;
     const uint4* tab = reinterpret_cast<const uint4*>(S.tab) + (po * 4 + ap) * W;
     const uint32_t A = sbuf + (uint32_t)(a & ~3);      // shared address of input word 0
-    uint32_t* ow = reinterpret_cast<uint32_t*>(U.out - po);
-    uint8_t* ob = U.out - po;
-    // per slot: shared address of the window at step 0, selectors, mix word
-    uint32_t wa[NS], sel[NS], mix[NS];
+    uint32_t* ow = reinterpret_cast<uint32_t*>(U.out - po) + lane;
+    Slot e[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
         const int j = lane + 32 * s;
-        uint4 e = make_uint4(0, 0, 0, 0);
-        if (s < ns && j < W) e = __ldg(tab + j);
-        wa[s] = A + 4u * e.x;
-        sel[s] = e.y;
-        mix[s] = e.z;
+        uint4 t = make_uint4(0, 0, 0, 0);
+        if (s < ns && j < W) t = __ldg(tab + j);
+        e[s].w = A + t.x;
+        e[s].lo = t.y;
+        e[s].hi = t.z;
+        e[s].mix = t.w;
     }
     const int words = (po + U.out_len + 3) >> 2;
 
@@ -210,52 +211,44 @@ __device__ __forceinline__ void permute(const PermSpec& S, const Unit& U, uint32
 #pragma unroll
             for (int s = 0; s < NS; ++s) {
                 const int gw = kw + lane + 32 * s;
-                const uint32_t vm = valid_mask((mix[s] >> 16) & 0xF, gw, po, U.out_len);
+                const uint32_t vm = valid_mask((e[s].lo >> 16) & 0xF, gw, po, U.out_len);
                 if (!vm || gw >= words) continue;
-                const int wb = (int)(wa[s] - A) + kd;     // window start, bytes from input word 0
+                const int wb = (int)(e[s].w - A) + kd;     // window start, bytes from input word 0
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     if (!((vm >> i) & 1)) continue;
-                    const uint32_t pr = (mix[s] >> (20 + i)) & 1;
-                    const uint32_t nib = ((pr ? sel[s] >> 16 : sel[s]) >> (4 * i)) & 7;
+                    const uint32_t pr = (e[s].lo >> (20 + i)) & 1;
+                    const uint32_t nib = ((pr ? e[s].hi : e[s].lo) >> (4 * i)) & 7;
                     const int in_off = wb + 8 * (int)pr + 4 * (int)(nib >> 2) + (int)(nib & 3) - ap;
-                    if (in_off < U.in_len) ob[4 * gw + i] = (uint8_t)lds8(A + (uint32_t)(in_off + ap));
+                    if (in_off < U.in_len)
+                        reinterpret_cast<uint8_t*>(ow + (gw - lane))[i] = (uint8_t)lds8(A + (uint32_t)(in_off + ap));
                 }
             }
         }
         return;
     }
 
+    // One step covers output words [kw, kw + W).  Words [w_lo, w_hi) are whole
+    // (the first word is partial when po > 0); a window of a word that has a
+    // valid byte lies within [sbuf - 16, sbuf + kBuf) (front slack), windows of
+    // words past the end are clamped into the buffer and never stored.
+    const int w_lo = po ? 1 : 0, w_hi = (U.out_len + po) >> 2;
+    const uint32_t wmax = sbuf + (uint32_t)(kBuf - 16);
     uint32_t kd = 0;
+#pragma unroll 2
     for (int kw = 0; kw < words; kw += W, kd += Dw4) {
-        if ((kw > 0 || po == 0) && 4 * (kw + W) - po <= U.out_len) {
-            // interior step: every word whole
 #pragma unroll
-            for (int s = 0; s < NS; ++s) {
-                if (s >= ns) break;
-                const uint32_t r = gather_word(wa[s] + kd, sel[s], mix[s]);
-                const uint32_t cov = (mix[s] >> 16) & 0xF;
-                const int gw = kw + lane + 32 * s;
-                if (PACK) {
-                    if (cov) ow[gw] = r;            // packed words are whole or outside W
-                } else if (cov == 0xF) {
-                    ow[gw] = r;
-                } else if (cov) {
-                    store_bytes(ob + 4 * gw, r, cov);
-                }
-            }
-        } else {
-            // first / last step: windows may reach up to 16 bytes before the
-            // staged input (buffer front slack) or past its end
-#pragma unroll
-            for (int s = 0; s < NS; ++s) {
-                if (s >= ns) break;
-                const int gw = kw + lane + 32 * s;
-                const uint32_t vm = valid_mask((mix[s] >> 16) & 0xF, gw, po, U.out_len);
-                if (!vm || gw >= words) continue;
-                const uint32_t r = gather_word(wa[s] + kd, sel[s], mix[s]);
-                if (vm == 0xF) ow[gw] = r;
-                else store_bytes(ob + 4 * gw, r, vm);
+        for (int s = 0; s < NS; ++s) {
+            if (s >= ns) break;
+            const uint32_t r = gather_word(min(e[s].w + kd, wmax), e[s]);
+            const int gw = kw + lane + 32 * s;
+            const uint32_t cov = (e[s].lo >> 16) & 0xF;
+            uint32_t* p = ow + kw + 32 * s;
+            if (gw >= w_lo && gw < w_hi) {
+                if (cov == 0xF) *p = r;
+                else if (!PACK && cov) store_bytes(reinterpret_cast<uint8_t*>(p), r, cov);   // layout gap
+            } else if (cov && gw < words) {
+                store_bytes(reinterpret_cast<uint8_t*>(p), r, valid_mask(cov, gw, po, U.out_len));
             }
         }
     }
@@ -266,6 +259,7 @@ __global__ void __launch_bounds__(kWarps * 32, blocks_per_sm<NS>())
 k_perm(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t limit) {
     extern __shared__ __align__(16) uint8_t sm[];
     __shared__ PermSpec specs[2 * kPermMaxSpecs];
+    __shared__ Unit parked[kWarps];
     for (int i = threadIdx.x; i < sp.nperms; i += blockDim.x) specs[i] = sp.perms[i];
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -281,14 +275,16 @@ k_perm(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__
     if (cur.flags & 1) stage(sbase, cur, lane);
     cp_async_commit();
     uint32_t pb = 0;
+    // the next unit waits in shared memory while the current one is permuted
+    // (registers are the scarce resource inside permute)
+    Unit* park = &parked[warp];
     for (;;) {
         const bool more = it.left > 0;
-        Unit nxt;
-        nxt.flags = 0;
         if (more) {
             iter_next(it, sp);
-            nxt = make_unit<PACK>(it, sp, src, dst, limit);
+            const Unit nxt = make_unit<PACK>(it, sp, src, dst, limit);
             if (nxt.flags & 1) stage(sbase + (pb ^ kSlot), nxt, lane);
+            if (lane == 0) *park = nxt;
         }
         cp_async_commit();
         cp_async_wait<1>();
@@ -296,7 +292,7 @@ k_perm(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__
         if (cur.flags & 1) permute<PACK, NS>(specs[cur.flags >> 8], cur, sbase + pb, lane);
         __syncwarp();
         if (!more) break;
-        cur = nxt;
+        cur = *park;
         pb ^= kSlot;
     }
     cp_async_wait<0>();
@@ -307,7 +303,7 @@ cudaError_t launch_dir(const Plan& p, const uint8_t* src, uint8_t* dst, int64_t 
     const int ns = p.span.ns_max[PACK ? 1 : 0];
     const int64_t want = (p.span.nunits + kWarps - 1) / kWarps;
     const int64_t grid = std::max<int64_t>(
-        1, std::min<int64_t>(want, (int64_t)sm_count(p.device) * (ns <= 2 ? blocks_per_sm<2>() : blocks_per_sm<4>())));
+        1, std::min<int64_t>(want, (int64_t)sm_count(p.device) * (ns <= 1 ? blocks_per_sm<1>() : ns == 2 ? blocks_per_sm<2>() : blocks_per_sm<4>())));
     switch (ns) {
     case 1: k_perm<PACK, 1><<<(unsigned)grid, kWarps * 32, kSmem, stream>>>(p.span, src, dst, limit); break;
     case 2: k_perm<PACK, 2><<<(unsigned)grid, kWarps * 32, kSmem, stream>>>(p.span, src, dst, limit); break;

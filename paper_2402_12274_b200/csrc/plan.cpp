@@ -190,7 +190,11 @@ class SpanBuilder {
     void emit(const Node* n, int64_t shift, int64_t poff) {
         if (!ok || n->runs == 0) return;
         if ((int64_t)chunks.size() > kMaxChunks) { ok = false; return; }
-        if (small(n)) {   // chunk src = span start of the element
+        // a small Rep of small elements stays a strided chunk (one shared body
+        // and word-gather period) rather than becoming a one-element body
+        const bool strided = n->kind == Kind::Rep && n->count > 1 && small(n->body.get()) &&
+                             n->stride >= n->body->max_end - n->body->min_off;
+        if (small(n) && !strided) {   // chunk src = span start of the element
             add(shift + n->min_off, poff, 1, body_of(n), 0);
             return;
         }
@@ -305,7 +309,7 @@ bool make_entry(const int64_t r[4], const bool cov[4], int ap, PermEntry* en) {
     if (mn == INT64_MAX) return true;
     const int64_t wo = floor_div(mn, 4);
     if (wo < INT16_MIN || wo > INT16_MAX) return false;
-    en->wo = (int32_t)wo;
+    en->wo4 = (int32_t)(4 * wo);
     uint32_t s01 = 0, s23 = 0, pairs = 0, cover = 0;
     for (int i = 0; i < 4; ++i) {
         if (!cov[i]) continue;
@@ -323,8 +327,9 @@ bool make_entry(const int64_t r[4], const bool cov[4], int ap, PermEntry* en) {
     }
     uint32_t mixsel = 0;
     for (int i = 0; i < 4; ++i) mixsel |= (uint32_t)(i + ((pairs >> i) & 1) * 4) << (4 * i);
-    en->sel = s01 | (s23 << 16);
-    en->mix = mixsel | (cover << 16) | (pairs << 20);
+    en->lo = s01 | (cover << 16) | (pairs << 20);
+    en->hi = s23;
+    en->mix = mixsel;
     return true;
 }
 
