@@ -207,6 +207,63 @@ __device__ __forceinline__ void chain_elems(const ChainJob& j, int64_t t0, int64
     }
 }
 
+// Thread per short row (16 <= L <= 64, L % 16 == 0, rows 4-byte aligned,
+// packed side 16-byte aligned): the row is moved as the aligned 16-byte
+// chunks that cover it -- pack loads <= 5 chunks and realigns them with
+// funnel shifts into L/16 full 16-byte packed stores; unpack loads L/16
+// packed chunks and stores whole 16-byte chunks in the row's middle and
+// 4-byte words at its two ends.  An x-face row of 8 floats at a 4 (mod 16)
+// address takes 3 loads + 2 stores instead of 8 + 8 word accesses.
+template <bool PACK>
+__device__ __forceinline__ void chain_wide(const ChainJob& j, int64_t t0, int64_t nthr) {
+    const Chain& c = j.c;
+    const int nq = (int)(c.L >> 4);
+    for (int64_t r = t0; r < j.rows; r += nthr) {
+        const int64_t off = chain_row(c, r);
+        if (PACK) {
+            const uint8_t* s = j.src + off;
+            const int a = (int)(reinterpret_cast<uintptr_t>(s) & 15);
+            const uint4* s16 = reinterpret_cast<const uint4*>(s - a);
+            const int n16 = (a + (int)c.L + 15) >> 4;
+            uint4 v[5];
+#pragma unroll
+            for (int i = 0; i < 5; ++i) v[i] = i < n16 ? __ldg(s16 + i) : make_uint4(0, 0, 0, 0);
+            uint4* d16 = reinterpret_cast<uint4*>(j.dst + r * c.L);
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+                if (m < nq) d16[m] = funnel16(v[m], v[m + 1], a);
+        } else {
+            const uint4* p16 = reinterpret_cast<const uint4*>(j.src + r * c.L);
+            uint8_t* d = j.dst + off;
+            const int a = (int)(reinterpret_cast<uintptr_t>(d) & 15);
+            uint8_t* d0 = d - a;
+            const int end = a + (int)c.L;              // region bytes [a, end) of the chunks
+            const int n16 = (end + 15) >> 4;
+            uint4 p[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) p[i] = i < nq ? __ldg(p16 + i) : make_uint4(0, 0, 0, 0);
+            const uint4 z = make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int m = 0; m < 5; ++m) {
+                if (m >= n16) break;
+                const uint4 lo = m == 0 ? z : p[m - 1 < 4 ? m - 1 : 3];
+                const uint4 hi = m < nq ? p[m < 4 ? m : 3] : z;
+                const uint4 v = a ? funnel16(lo, hi, 16 - a) : hi;
+                const int blo = m == 0 ? a : 0, bhi = min(16, end - 16 * m);
+                uint8_t* q = d0 + 16 * m;
+                if (blo == 0 && bhi == 16) {
+                    *reinterpret_cast<uint4*>(q) = v;
+                } else {
+                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (4 * k >= blo && 4 * k + 4 <= bhi) reinterpret_cast<uint32_t*>(q)[k] = w[k];
+                }
+            }
+        }
+    }
+}
+
 template <bool PACK>
 __global__ void __launch_bounds__(kChainThreads) k_chain(const ChainBatch b) {
     // jobs with equal block counts are interleaved block by block, so e.g. the
@@ -226,6 +283,8 @@ __global__ void __launch_bounds__(kChainThreads) k_chain(const ChainBatch b) {
     if (j.mode == CHAIN_ROW) {
         chain_rows<PACK>(j, blk * (kChainThreads / 32) + (threadIdx.x >> 5),
                          (int64_t)j.nblk * (kChainThreads / 32));
+    } else if (j.mode == CHAIN_WIDE) {
+        chain_wide<PACK>(j, blk * kChainThreads + threadIdx.x, (int64_t)j.nblk * kChainThreads);
     } else {
         const int64_t t0 = blk * kChainThreads + threadIdx.x, nthr = (int64_t)j.nblk * kChainThreads;
         switch (j.w) {
@@ -513,6 +572,11 @@ void chain_setup(const Plan& p, bool pack, ChainJob* j) {
     int64_t w = p.chain_align;
     const uintptr_t m = reinterpret_cast<uintptr_t>(layout_ptr) | reinterpret_cast<uintptr_t>(packed_ptr);
     while (w > 1 && (m & (uintptr_t)(w - 1))) w >>= 1;
+    if (w >= 4 && w < 16 && (c.L & 15) == 0 && c.L <= 64 && packed_aligned) {
+        j->mode = CHAIN_WIDE;    // short rows at 4/8-byte alignment: aligned 16-byte chunks
+        j->w = 16;
+        return;
+    }
     j->mode = CHAIN_ELEM;
     j->w = (int32_t)w;
 }

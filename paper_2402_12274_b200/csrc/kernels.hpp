@@ -12,7 +12,7 @@ namespace mpx {
 
 constexpr int kMaxJobs = 16;
 
-enum ChainMode : int32_t { CHAIN_ELEM = 0, CHAIN_ROW = 1 };
+enum ChainMode : int32_t { CHAIN_ELEM = 0, CHAIN_ROW = 1, CHAIN_WIDE = 2 };
 
 struct ChainJob {
     Chain c;
@@ -21,7 +21,8 @@ struct ChainJob {
     int64_t rows;     // whole rows moved by the main path
     int64_t limit;    // packed bytes to move (unpack may stop mid-row: bytewise tail)
     int32_t w;        // element mode: word width in bytes
-    int32_t mode;     // CHAIN_ELEM: thread per row; CHAIN_ROW: warp per row, 16 B + funnel
+    int32_t mode;     // CHAIN_ELEM: thread per row; CHAIN_ROW: warp per row, 16 B + funnel;
+                      // CHAIN_WIDE: thread per short row, aligned 16 B chunks on both sides
     int32_t blk0;     // first block of this job's interleave group (launcher)
     int32_t nblk;     // blocks of this job (launcher)
     int32_t gsize;    // jobs in the group; group blocks alternate between them
