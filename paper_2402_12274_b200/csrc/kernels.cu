@@ -270,16 +270,20 @@ __global__ void __launch_bounds__(kChainThreads) k_chain(const ChainBatch b) {
     // lo and hi x-faces touch the same DRAM pages at the same time
     int ji = 0;
     const int bid = (int)blockIdx.x;
+    uint32_t blk32 = 0;
     for (int i = 0; i < b.njobs; ++i) {
         const ChainJob& q = b.job[i];
         const int rel = bid - q.blk0;
-        if (rel >= 0 && rel < q.nblk * q.gsize && rel % q.gsize == q.gpos) {
+        if (rel < 0 || rel >= q.nblk * q.gsize) continue;
+        const uint32_t g = fdiv32((uint32_t)rel, q.m_g, q.s_g);
+        if ((uint32_t)rel - g * (uint32_t)q.gsize == (uint32_t)q.gpos) {
             ji = i;
+            blk32 = g;
             break;
         }
     }
     const ChainJob& j = b.job[ji];
-    const int64_t blk = (bid - j.blk0) / j.gsize;
+    const int64_t blk = blk32;
     if (j.mode == CHAIN_ROW) {
         chain_rows<PACK>(j, blk * (kChainThreads / 32) + (threadIdx.x >> 5),
                          (int64_t)j.nblk * (kChainThreads / 32));
@@ -603,6 +607,8 @@ cudaError_t launch_chain_batch(ChainBatch& b, bool pack, int device, cudaStream_
         j.gsize = 1;
         j.gpos = 0;
         j.blk0 = -1;
+        j.m_g = 0;
+        j.s_g = 0;
     }
     for (int i = 0; i < b.njobs; ++i) {   // groups of equal nblk, interleaved
         ChainJob& j = b.job[i];
@@ -617,6 +623,7 @@ cudaError_t launch_chain_batch(ChainBatch& b, bool pack, int device, cudaStream_
             q.blk0 = (int32_t)total;
             q.gsize = g;
             q.gpos = pos++;
+            host_magic32((uint32_t)g, &q.m_g, &q.s_g);
         }
         total += (int64_t)j.nblk * g;
     }

@@ -27,6 +27,8 @@ struct ChainJob {
     int32_t nblk;     // blocks of this job (launcher)
     int32_t gsize;    // jobs in the group; group blocks alternate between them
     int32_t gpos;     // this job's position in the group
+    uint32_t m_g;     // magic divisor for gsize (32-bit, see host_magic32)
+    int32_t s_g;
 };
 
 struct ChainBatch {
