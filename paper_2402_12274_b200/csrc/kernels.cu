@@ -41,6 +41,23 @@ template <> struct Vec<1> { using T = uint8_t; };
 
 constexpr int kChainThreads = 256;
 
+// Scattered layout-side loads of short rows.  An L1-allocating load of a few
+// bytes makes L1 fetch the whole 128-byte line from L2 (and L2 from DRAM);
+// L2-only loads fetch 32-byte sectors.
+#ifndef MPX_LAYOUT_LD
+#define MPX_LAYOUT_LD 1
+#endif
+template <typename T>
+__device__ __forceinline__ T ld_layout(const T* p) {
+#if MPX_LAYOUT_LD == 1
+    return __ldcg(p);
+#elif MPX_LAYOUT_LD == 2
+    return __ldcs(p);
+#else
+    return *p;
+#endif
+}
+
 // bytes [a, a + 16) of the 32-byte concatenation lo || hi, 0 <= a < 16
 __device__ __forceinline__ uint4 funnel16(const uint4& lo, const uint4& hi, int a) {
     const uint32_t w0 = lo.x, w1 = lo.y, w2 = lo.z, w3 = lo.w;
@@ -199,7 +216,8 @@ __device__ __forceinline__ void chain_elems(const ChainJob& j, int64_t t0, int64
 #pragma unroll
             for (int q = 0; q < R; ++q)
                 if (ok[q])
-                    v[q] = *reinterpret_cast<const T*>(j.src + (PACK ? lo[q] : po[q]) + w * W);
+                    v[q] = PACK ? ld_layout(reinterpret_cast<const T*>(j.src + lo[q] + w * W))
+                                : *reinterpret_cast<const T*>(j.src + po[q] + w * W);
 #pragma unroll
             for (int q = 0; q < R; ++q)
                 if (ok[q]) *reinterpret_cast<T*>(j.dst + (PACK ? po[q] : lo[q]) + w * W) = v[q];
@@ -227,7 +245,7 @@ __device__ __forceinline__ void chain_wide(const ChainJob& j, int64_t t0, int64_
             const int n16 = (a + (int)c.L + 15) >> 4;
             uint4 v[5];
 #pragma unroll
-            for (int i = 0; i < 5; ++i) v[i] = i < n16 ? __ldg(s16 + i) : make_uint4(0, 0, 0, 0);
+            for (int i = 0; i < 5; ++i) v[i] = i < n16 ? ld_layout(s16 + i) : make_uint4(0, 0, 0, 0);
             uint4* d16 = reinterpret_cast<uint4*>(j.dst + r * c.L);
 #pragma unroll
             for (int m = 0; m < 4; ++m)
