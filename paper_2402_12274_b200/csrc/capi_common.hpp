@@ -36,6 +36,10 @@ int movement(int n, const mpx_datatype* dts, const int64_t* counts, const void* 
 // pinned-host pointers allowed)
 int launch_move(int dev, Datatype* d, int64_t count, bool pack, const void* src, void* dst, int64_t limit,
                 cudaStream_t stream);
+// typed -> typed transfer of `bytes` packed bytes in one pass (both layouts
+// chains, destination without overlaps); MPX_ERR_PENDING when not applicable
+int launch_zip_move(int dev, Datatype* sd, int64_t scount, const void* src, Datatype* rd, int64_t rcount, void* dst,
+                    int64_t bytes, cudaStream_t stream);
 // layout_for(count) is one run -> its offset
 bool contiguous_run(Datatype* d, int64_t count, int64_t* off);
 // count / usability / bounds checks of a typed buffer of `bytes` bytes

@@ -527,6 +527,22 @@ int launch_move(int dev, Datatype* d, int64_t count, bool pack, const void* src,
     return MPX_SUCCESS;
 }
 
+int launch_zip_move(int dev, Datatype* sd, int64_t scount, const void* src, Datatype* rd, int64_t rcount, void* dst,
+                    int64_t bytes, cudaStream_t stream) {
+    if (bytes <= 0) return MPX_SUCCESS;
+    int rc = ensure_device(dev);
+    if (rc) return rc;
+    std::string err;
+    auto ps = get_plan(sd, scount, dev, stream, &err);
+    if (!ps) return fail(MPX_ERR_OTHER, "%s", err.c_str());
+    auto pd = get_plan(rd, rcount, dev, stream, &err);
+    if (!pd) return fail(MPX_ERR_OTHER, "%s", err.c_str());
+    if (ps->kind != PLAN_CHAIN || pd->kind != PLAN_CHAIN || pd->overlap) return MPX_ERR_PENDING;
+    cudaError_t e = launch_zip(*ps, *pd, static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), bytes, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "zipper launch");
+    return MPX_SUCCESS;
+}
+
 // contiguous layout_for(count)?  -> offset of its single run
 bool contiguous_run(Datatype* d, int64_t count, int64_t* off) {
     NodeP lay = d->layout_for(count);

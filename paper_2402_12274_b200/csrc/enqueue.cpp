@@ -414,6 +414,9 @@ int transfer(int dev, cudaStream_t st, const Side& s, const Side& r, int64_t mov
         return launch_move(dev, r.dt, r.count, false, static_cast<uint8_t*>(s.buf) + off, r.buf, moved, st);
     if (moved == s.bytes && contiguous_run(r.dt, r.count, &off))
         return launch_move(dev, s.dt, s.count, true, s.buf, static_cast<uint8_t*>(r.buf) + off, s.bytes, st);
+    // both typed: one-pass zipper when both layouts are chains
+    const int z = launch_zip_move(dev, s.dt, s.count, s.buf, r.dt, r.count, r.buf, moved, st);
+    if (z != MPX_ERR_PENDING) return z;
     MPX_RC(set_device(dev));
     void* tmp = nullptr;
     MPX_RC(staging_alloc(dev, (size_t)s.bytes, st, &tmp));

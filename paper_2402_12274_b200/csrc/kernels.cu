@@ -537,6 +537,50 @@ k_span(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__
     }
 }
 
+// ---------------------------------------------------------------- zipper
+// Typed -> typed transfer in one pass (datatype.py:760-797 copy_between, the
+// reference's zipper): both layouts are chains, so packed byte P maps to a
+// source and a destination offset in closed form.  The packed stream is cut
+// into pieces of g = gcd(L_src, L_dst) bytes that are contiguous on both
+// sides; a thread moves a piece with W-byte words, two pieces in flight.
+// No staging buffer: HBM (or NVLink for a peer buffer) is touched once per
+// side.
+template <int W>
+__global__ void __launch_bounds__(256)
+k_zip(const Chain cs, const Chain cd, const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+      int64_t npieces, int g) {
+    using T = typename Vec<W>::T;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < npieces; p0 += 2 * nthr) {
+        int64_t so[2], dof[2];
+        bool ok[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int64_t p = p0 + q * nthr;
+            ok[q] = p < npieces;
+            so[q] = ok[q] ? chain_off(cs, p * g) : 0;
+            dof[q] = ok[q] ? chain_off(cd, p * g) : 0;
+        }
+        for (int w = 0; w < g; w += W) {
+            T v[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                if (ok[q]) v[q] = *reinterpret_cast<const T*>(src + so[q] + w);
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                if (ok[q]) *reinterpret_cast<T*>(dst + dof[q] + w) = v[q];
+        }
+    }
+}
+
+// bytes [from, to) of the packed stream, one thread, byte by byte (the tail
+// that is not a whole piece)
+__global__ void __launch_bounds__(32)
+k_zip_tail(const Chain cs, const Chain cd, const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+           int64_t from, int64_t to) {
+    for (int64_t P = from + threadIdx.x; P < to; P += 32) dst[chain_off(cd, P)] = src[chain_off(cs, P)];
+}
+
 // ------------------------------------------------------- ordered unpack
 __global__ void __launch_bounds__(32)
 k_ordered_unpack(const DDesc d, const uint8_t* __restrict__ src, uint8_t* dst, int64_t limit) {
@@ -681,6 +725,12 @@ cudaError_t preload_pack_kernels() {
     if ((r = cudaFuncGetAttributes(&a, k_span<true>)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_span<false>)) != cudaSuccess) e = r;
     if ((r = preload_perm_kernels()) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_zip<16>)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_zip<8>)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_zip<4>)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_zip<2>)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_zip<1>)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_zip_tail)) != cudaSuccess) e = r;
     return e;
 }
 
@@ -699,6 +749,36 @@ cudaError_t launch_span(const Plan& p, bool pack, const uint8_t* src, uint8_t* d
     }
     if (pack) k_span<true><<<(unsigned)grid, kSpanWarps * 32, kSpanSmem, stream>>>(p.span, src, dst, limit);
     else k_span<false><<<(unsigned)grid, kSpanWarps * 32, kSpanSmem, stream>>>(p.span, src, dst, limit);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_zip(const Plan& ps, const Plan& pd, const uint8_t* src, uint8_t* dst, int64_t bytes,
+                       cudaStream_t stream) {
+    if (bytes <= 0) return cudaSuccess;
+    int64_t a = ps.chain.L, b = pd.chain.L;
+    while (b) {
+        const int64_t t = a % b;
+        a = b;
+        b = t;
+    }
+    const int64_t g = a;
+    const int64_t npieces = bytes / g;
+    int64_t w = std::min<int64_t>(ps.chain_align, pd.chain_align);
+    const uintptr_t m = reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | (uintptr_t)g;
+    while (w > 1 && (m & (uintptr_t)(w - 1))) w >>= 1;
+    if (npieces > 0) {
+        const int64_t want = (npieces + 511) / 512;
+        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count(ps.device) * 8));
+        const int gi = (int)g;
+        switch (w) {
+        case 16: k_zip<16><<<(unsigned)grid, 256, 0, stream>>>(ps.chain, pd.chain, src, dst, npieces, gi); break;
+        case 8: k_zip<8><<<(unsigned)grid, 256, 0, stream>>>(ps.chain, pd.chain, src, dst, npieces, gi); break;
+        case 4: k_zip<4><<<(unsigned)grid, 256, 0, stream>>>(ps.chain, pd.chain, src, dst, npieces, gi); break;
+        case 2: k_zip<2><<<(unsigned)grid, 256, 0, stream>>>(ps.chain, pd.chain, src, dst, npieces, gi); break;
+        default: k_zip<1><<<(unsigned)grid, 256, 0, stream>>>(ps.chain, pd.chain, src, dst, npieces, gi); break;
+        }
+    }
+    if (npieces * g < bytes) k_zip_tail<<<1, 32, 0, stream>>>(ps.chain, pd.chain, src, dst, npieces * g, bytes);
     return cudaGetLastError();
 }
 

@@ -45,6 +45,9 @@ cudaError_t launch_generic(const Plan& p, bool pack, const uint8_t* src, uint8_t
                            cudaStream_t stream);
 cudaError_t launch_span(const Plan& p, bool pack, const uint8_t* src, uint8_t* dst, int64_t limit,
                         cudaStream_t stream);
+// typed -> typed in one pass for two chain plans (copy_between, datatype.py:760-797)
+cudaError_t launch_zip(const Plan& ps, const Plan& pd, const uint8_t* src, uint8_t* dst, int64_t bytes,
+                       cudaStream_t stream);
 cudaError_t launch_iov(const Plan& p, int64_t k0, int64_t n, int64_t* out, cudaStream_t stream);
 // word-gather pack/unpack of span plans with PermSpecs (k_perm.cu)
 cudaError_t launch_perm(const Plan& p, bool pack, const uint8_t* src, uint8_t* dst, int64_t limit,

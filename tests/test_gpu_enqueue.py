@@ -484,6 +484,48 @@ def test_zipper_typed_to_typed_rendezvous():
     pair(rank0, rank1, eager_limit=1024)
 
 
+@pytest.mark.parametrize("st,rt,elem", [
+    # 12-byte runs into 20-byte runs: 4-byte pieces
+    (("vector", 1000, 3, 7, ("basic", 4)), ("vector", 700, 5, 9, ("basic", 4)), 4),
+    # the cfg4 vector layout on both sides with different strides: 16-byte words
+    (("vector", 2048, 4, 8, ("basic", 8)), ("vector", 1024, 8, 12, ("basic", 8)), 8),
+    # odd byte runs: 1-byte words
+    (("vector", 999, 3, 5, ("basic", 1)), ("vector", 1499, 2, 3, ("basic", 1)), 1),
+])
+def test_zipper_chain_to_chain_matches_copy_between(st, rt, elem):
+    """one-pass chain -> chain transfer (k_zip) against the oracle's
+    copy_between (datatype.py:760-797), rendezvous path."""
+    import oracle
+    from specbuild import build_product
+    ot_s, ot_r = oracle.OracleType(st), oracle.OracleType(rt)
+    rng = np.random.default_rng(77)
+    src_h = rng.integers(0, 256, ot_s.max_end, dtype=np.uint8)
+
+    def rank0(inst):
+        q = mp.queue_create(inst)
+        c, s = device_comm(inst, q)
+        src = torch.from_numpy(src_h).to(DEV)
+        mp.send(c, src, 1, build_product(st, mp), 1, 5)
+        mp.queue_synchronize(q)
+        mp.comm_free(c)
+        mp.free_stream(s)
+
+    def rank1(inst):
+        q = mp.queue_create(inst)
+        c, s = device_comm(inst, q)
+        dst = torch.zeros(ot_r.max_end, dtype=torch.uint8, device=DEV)
+        mp.recv(c, dst, 1, build_product(rt, mp), 0, 5)
+        mp.queue_synchronize(q)
+        ref = np.zeros(ot_r.max_end, np.uint8)
+        n = oracle.copy_between(ot_s, 1, src_h, ot_r, 1, ref)
+        assert n == min(ot_s.size_bytes, ot_r.size_bytes)
+        assert np.array_equal(dst.cpu().numpy(), ref)
+        mp.comm_free(c)
+        mp.free_stream(s)
+
+    pair(rank0, rank1, eager_limit=64)
+
+
 # ------------------------------------------------------------- allreduce
 
 
