@@ -276,6 +276,10 @@ def run_extras(dev, flush, args):
     try:
         import enqueue_bench as eb
         out["ring_2ranks_1gpu_64MiB"] = eb.ring(2, 64 << 20, iters=reps)
+        out["ring_2ranks_1gpu_64MiB_vector"] = eb.ring(2, 64 << 20, iters=reps, kind="vector",
+                                                       group="bench-ring-v")
+        out["ring_2ranks_1gpu_64MiB_vector_noscale"] = eb.ring(2, 64 << 20, iters=reps, kind="vector",
+                                                               group="bench-ring-vn", scale=False)
         out["allreduce_native_2ranks_1gpu_64MiB_f32"] = eb.allreduce(2, 16 << 20, iters=reps, algo="native")
         out["allreduce_nccl_1rank_64MiB_f32"] = eb.allreduce(1, 16 << 20, iters=reps, algo="nccl",
                                                              group="bench-ar1")

@@ -50,7 +50,13 @@ def _run_ranks(n, body, group):
     return out
 
 
-def ring(n=2, nbytes=64 << 20, iters=20, warmup=3, group="bench-ring"):
+def ring(n=2, nbytes=64 << 20, iters=20, warmup=3, group="bench-ring", kind="u8", scale=True):
+    """kind "u8": contiguous bytes; "vector": vector(N/32, 4, 8) of float64
+    on both sides (BASELINE configs[3]: payload N bytes over a 2N - 32 byte
+    span; typed -> typed, so the rendezvous path runs the one-pass zipper),
+    with the dependent scale kernel on the stream before the send and after
+    the receive.  Time: CUDA events on every rank's stream, max over ranks
+    (wall clock reported beside)."""
     import paper_2402_12274_b200 as mp
     import torch
 
@@ -62,33 +68,55 @@ def ring(n=2, nbytes=64 << 20, iters=20, warmup=3, group="bench-ring"):
         s = inst.stream_create(info)
         c = mp.stream_comm_create(inst.world, s)
         r = inst.rank
-        src = torch.full((nbytes,), r, dtype=torch.uint8, device=inst.device)
-        dst = torch.zeros_like(src)
+        if kind == "u8":
+            src = torch.full((nbytes,), r, dtype=torch.uint8, device=inst.device)
+            dst = torch.zeros_like(src)
+            count, dt = nbytes, mp.BYTE
+        else:
+            src = torch.full((nbytes // 4,), float(r), dtype=torch.float64, device=inst.device)
+            dst = torch.zeros_like(src)
+            count, dt = 1, mp.type_vector(nbytes // 32, 4, 8, mp.FLOAT64).commit()
 
         def one():
-            rr = mp.irecv_enqueue(c, dst, nbytes, mp.BYTE, (r - 1) % n, 0)
-            sr = mp.isend_enqueue(c, src, nbytes, mp.BYTE, (r + 1) % n, 0)
+            if kind != "u8" and scale:
+                with torch.cuda.stream(q.torch_stream):
+                    src.mul_(1.0)                   # dependent kernel before the send
+            rr = mp.irecv_enqueue(c, dst, count, dt, (r - 1) % n, 0)
+            sr = mp.isend_enqueue(c, src, count, dt, (r + 1) % n, 0)
             mp.waitall_enqueue([rr, sr])
+            if kind != "u8" and scale:
+                with torch.cuda.stream(q.torch_stream):
+                    dst.mul_(1.0)                   # dependent kernel after the receive
 
         for _ in range(warmup):
             one()
         mp.queue_synchronize(q)
         bar.wait()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
+        e0.record(q.torch_stream)
         for _ in range(iters):
             one()
+        e1.record(q.torch_stream)
         mp.queue_synchronize(q)
         bar.wait()
-        dt = time.perf_counter() - t0
-        ok = bool((dst == (r - 1) % n).all())
+        wall = time.perf_counter() - t0
+        dev_ms = e0.elapsed_time(e1)
+        if kind == "u8":
+            ok = bool((dst == (r - 1) % n).all())
+        else:
+            v = dst.view(-1, 8)
+            ok = bool((v[:, :4] == float((r - 1) % n)).all())
         mp.comm_free(c)
         mp.free_stream(s)
-        return dt, ok
+        return dev_ms, wall, ok
 
     res = _run_ranks(n, body, group)
-    dt = max(r[0] for r in res)
-    return {"ranks": n, "bytes": nbytes, "iters": iters, "ms_per_iter": 1e3 * dt / iters,
-            "GBps_per_rank": nbytes * iters / dt / 1e9, "correct": all(r[1] for r in res)}
+    ms = max(x[0] for x in res) / iters
+    wall = max(x[1] for x in res)
+    return {"ranks": n, "kind": kind, "scale_kernels": bool(kind != "u8" and scale), "bytes": nbytes, "iters": iters, "ms_per_iter": ms,
+            "GBps_per_rank": nbytes / ms / 1e6, "wall_ms_per_iter": 1e3 * wall / iters,
+            "correct": all(x[2] for x in res)}
 
 
 def allreduce(n=2, count=16 << 20, iters=20, warmup=3, algo=None, group="bench-ar"):
@@ -131,5 +159,6 @@ def allreduce(n=2, count=16 << 20, iters=20, warmup=3, algo=None, group="bench-a
 if __name__ == "__main__":
     import json
     print(json.dumps(ring(2)))
+    print(json.dumps(ring(2, kind="vector", group="bench-ring-v")))
     print(json.dumps(allreduce(2, algo="native")))
     print(json.dumps(allreduce(1, algo="nccl", group="bench-ar1")))
