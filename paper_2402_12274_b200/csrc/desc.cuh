@@ -95,7 +95,8 @@ struct PermEntry {
     int32_t wo4;            // window start: byte offset from the staged input's word 0 (+ step * 4 * Dw)
     uint32_t lo;            // bits 0-15: byte_perm selector over window words (0, 1);
                             // 16-19: cover (byte i is written; unpack leaves layout gaps alone);
-                            // 20-23: byte i comes from window words (2, 3)
+                            // 20-23: byte i comes from window words (2, 3); 24-31: the word's
+                            // index j in the step (entries are compacted: uncovered words dropped)
     uint32_t hi;            // byte_perm selector over window words (2, 3)
     uint32_t mix;           // byte_perm selector merging the two halves
 };
@@ -104,11 +105,12 @@ static_assert(sizeof(PermEntry) == 16, "PermEntry layout");
 struct PermSpec {
     int32_t W;              // output words per warp step
     int32_t Dw;             // input words advanced per step
-    int32_t ns;             // slots per lane: ceil(W / 32)
+    int32_t ns;             // slots per lane: ceil(max(wc) / 32)
     int32_t pad;
-    const PermEntry* tab;   // [16][W]
+    const PermEntry* tab;   // [16][W]: per phase variant, the words with a written byte first
+    uint8_t wc[16];         // per phase variant: words with a written byte (entries used)
 };
-static_assert(sizeof(PermSpec) == 24, "PermSpec layout");
+static_assert(sizeof(PermSpec) == 40, "PermSpec layout");
 
 struct SpanPlan {
     const SpanChunk* chunks;

@@ -186,17 +186,18 @@ __device__ __forceinline__ void permute(const PermSpec& S, const Unit& U, uint32
     const int a = (int)(reinterpret_cast<uintptr_t>(U.in) & 15);
     const int ap = a & 3;
     const int po = (int)(reinterpret_cast<uintptr_t>(U.out) & 3);
-    const int W = S.W, ns = S.ns;
+    const int W = S.W;
+    const int wc = S.wc[po * 4 + ap];                 // entries (words with a written byte) this phase
     const uint32_t Dw4 = 4u * (uint32_t)S.Dw;
     const uint4* tab = reinterpret_cast<const uint4*>(S.tab) + (po * 4 + ap) * W;
     const uint32_t A = sbuf + (uint32_t)(a & ~3);      // shared address of input word 0
-    uint32_t* ow = reinterpret_cast<uint32_t*>(U.out - po) + lane;
+    uint32_t* ow = reinterpret_cast<uint32_t*>(U.out - po);
     Slot e[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
         const int j = lane + 32 * s;
         uint4 t = make_uint4(0, 0, 0, 0);
-        if (s < ns && j < W) t = __ldg(tab + j);
+        if (j < wc) t = __ldg(tab + j);
         e[s].w = A + t.x;
         e[s].lo = t.y;
         e[s].hi = t.z;
@@ -210,7 +211,7 @@ __device__ __forceinline__ void permute(const PermSpec& S, const Unit& U, uint32
         for (int kw = 0, kd = 0; kw < words; kw += W, kd += (int)Dw4) {
 #pragma unroll
             for (int s = 0; s < NS; ++s) {
-                const int gw = kw + lane + 32 * s;
+                const int gw = kw + (int)(e[s].lo >> 24);
                 const uint32_t vm = valid_mask((e[s].lo >> 16) & 0xF, gw, po, U.out_len);
                 if (!vm || gw >= words) continue;
                 const int wb = (int)(e[s].w - A) + kd;     // window start, bytes from input word 0
@@ -221,7 +222,7 @@ __device__ __forceinline__ void permute(const PermSpec& S, const Unit& U, uint32
                     const uint32_t nib = ((pr ? e[s].hi : e[s].lo) >> (4 * i)) & 7;
                     const int in_off = wb + 8 * (int)pr + 4 * (int)(nib >> 2) + (int)(nib & 3) - ap;
                     if (in_off < U.in_len)
-                        reinterpret_cast<uint8_t*>(ow + (gw - lane))[i] = (uint8_t)lds8(A + (uint32_t)(in_off + ap));
+                        reinterpret_cast<uint8_t*>(ow + gw)[i] = (uint8_t)lds8(A + (uint32_t)(in_off + ap));
                 }
             }
         }
@@ -239,11 +240,11 @@ __device__ __forceinline__ void permute(const PermSpec& S, const Unit& U, uint32
     for (int kw = 0; kw < words; kw += W, kd += Dw4) {
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
-            if (s >= ns) break;
+            if (32 * s >= wc) break;
             const uint32_t r = gather_word(min(e[s].w + kd, wmax), e[s]);
-            const int gw = kw + lane + 32 * s;
+            const int gw = kw + (int)(e[s].lo >> 24);
             const uint32_t cov = (e[s].lo >> 16) & 0xF;
-            uint32_t* p = ow + kw + 32 * s;
+            uint32_t* p = ow + gw;
             if (gw >= w_lo && gw < w_hi) {
                 if (cov == 0xF) *p = r;
                 else if (!PACK && cov) store_bytes(reinterpret_cast<uint8_t*>(p), r, cov);   // layout gap

@@ -740,12 +740,13 @@ cudaError_t launch_span(const Plan& p, bool pack, const uint8_t* src, uint8_t* d
     if (p.span.perms) return launch_perm(p, pack, src, dst, limit, stream);
     const int64_t want = (p.span.nunits + kSpanWarps - 1) / kSpanWarps;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count(p.device) * 4));
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[pack]) {   // > 48 KiB of dynamic shared memory needs an opt-in
+    static bool attr_set[64][2] = {};   // the opt-in is per device
+    const int d = p.device >= 0 && p.device < 64 ? p.device : 0;
+    if (!attr_set[d][pack]) {   // > 48 KiB of dynamic shared memory needs an opt-in
         cudaError_t e = pack ? cudaFuncSetAttribute(k_span<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSpanSmem)
                              : cudaFuncSetAttribute(k_span<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSpanSmem);
         if (e != cudaSuccess) return e;
-        attr_set[pack] = true;
+        attr_set[d][pack] = true;
     }
     if (pack) k_span<true><<<(unsigned)grid, kSpanWarps * 32, kSpanSmem, stream>>>(p.span, src, dst, limit);
     else k_span<false><<<(unsigned)grid, kSpanWarps * 32, kSpanSmem, stream>>>(p.span, src, dst, limit);

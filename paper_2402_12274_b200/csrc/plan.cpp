@@ -333,6 +333,20 @@ bool make_entry(const int64_t r[4], const bool cov[4], int ap, PermEntry* en) {
     return true;
 }
 
+// Append one phase variant (W entries, entry j for step word j) with the
+// words that write a byte first; returns their count.
+int push_variant(std::vector<PermEntry>& var, std::vector<PermEntry>* tab) {
+    int wc = 0;
+    for (size_t j = 0; j < var.size(); ++j) {
+        var[j].lo |= (uint32_t)j << 24;
+        if ((var[j].lo >> 16) & 0xF) tab->push_back(var[j]), ++wc;
+    }
+    PermEntry z;
+    std::memset(&z, 0, sizeof z);
+    for (size_t j = (size_t)wc; j < var.size(); ++j) tab->push_back(z);
+    return wc;
+}
+
 // Word-gather tables for one (element map, direction): output element of Eo
 // bytes, input element of Ei bytes, map[t] = input offset of output byte t
 // within its element (-1: not written).  False if the period or a word's
@@ -360,10 +374,11 @@ bool build_perm(int64_t Eo, int64_t Ei, const std::vector<int64_t>& map, PermSpe
     spec->ns = (int32_t)((W + 31) / 32);
     spec->pad = 0;
     spec->tab = reinterpret_cast<const PermEntry*>((uintptr_t)tab->size());   // patched at upload
+    int wcmax = 0;
     for (int po = 0; po < 4; ++po) {
         for (int ap = 0; ap < 4; ++ap) {
+            std::vector<PermEntry> var((size_t)W);
             for (int64_t j = 0; j < W; ++j) {
-                PermEntry en;
                 int64_t r[4];
                 bool cov[4];
                 for (int i = 0; i < 4; ++i) {
@@ -373,11 +388,14 @@ bool build_perm(int64_t Eo, int64_t Ei, const std::vector<int64_t>& map, PermSpe
                     cov[i] = map[(size_t)t] >= 0;
                     r[i] = cov[i] ? e * Ei + map[(size_t)t] - Din : 0;
                 }
-                if (!make_entry(r, cov, ap, &en)) return false;
-                tab->push_back(en);
+                if (!make_entry(r, cov, ap, &var[(size_t)j])) return false;
             }
+            const int wc = push_variant(var, tab);
+            spec->wc[po * 4 + ap] = (uint8_t)wc;
+            wcmax = std::max(wcmax, wc);
         }
     }
+    spec->ns = (wcmax + 31) / 32;
     return true;
 }
 
@@ -394,10 +412,11 @@ bool build_perm_single(int64_t Eo, const std::vector<int64_t>& map, PermSpec* sp
     spec->ns = (int32_t)((W + 31) / 32);
     spec->pad = 0;
     spec->tab = reinterpret_cast<const PermEntry*>((uintptr_t)tab->size());
+    int wcmax = 0;
     for (int po = 0; po < 4; ++po) {
         for (int ap = 0; ap < 4; ++ap) {
+            std::vector<PermEntry> var((size_t)W);
             for (int64_t j = 0; j < W; ++j) {
-                PermEntry en;
                 int64_t r[4];
                 bool cov[4];
                 for (int i = 0; i < 4; ++i) {
@@ -405,11 +424,14 @@ bool build_perm_single(int64_t Eo, const std::vector<int64_t>& map, PermSpec* sp
                     cov[i] = q >= 0 && q < Eo && map[(size_t)q] >= 0;
                     r[i] = cov[i] ? map[(size_t)q] : 0;
                 }
-                if (!make_entry(r, cov, ap, &en)) return false;
-                tab->push_back(en);
+                if (!make_entry(r, cov, ap, &var[(size_t)j])) return false;
             }
+            const int wc = push_variant(var, tab);
+            spec->wc[po * 4 + ap] = (uint8_t)wc;
+            wcmax = std::max(wcmax, wc);
         }
     }
+    spec->ns = (wcmax + 31) / 32;
     return true;
 }
 
