@@ -18,6 +18,8 @@
 
 #include <cstdint>
 
+#include <vector_types.h>
+
 namespace mpx {
 
 constexpr int kMaxChain = 4;
@@ -126,6 +128,11 @@ struct SpanPlan {
     uint64_t m_outer1;
     int32_t s_nchunks, s_outer1;
     int32_t ns_max[2];                  // most slots any spec needs, [unpack, pack]
+    // iov enumeration (k_iov_span): per chunk {segments before it within one
+    // outer element, run length if it starts a raw run (0 otherwise)}; raw
+    // pieces that continue a run add no segment
+    const longlong2* iovc;
+    int64_t segs_outer;                 // segments per outer element
 };
 
 struct DNode {

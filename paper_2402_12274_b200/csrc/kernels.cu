@@ -602,6 +602,84 @@ k_ordered_unpack(const DDesc d, const uint8_t* __restrict__ src, uint8_t* dst, i
 }
 
 // ---------------------------------------------------------------- iov
+// Chains: segment k is row k (closed form).
+__global__ void __launch_bounds__(256)
+k_iov_chain(const Chain c, int64_t k0, int64_t n, int64_t* __restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        reinterpret_cast<longlong2*>(out)[i] = make_longlong2(chain_row(c, k0 + i), c.L);
+}
+
+// Span plans: the segments of a (outer element, chunk) unit are its
+// elements' body runs in order (raw pieces of one run form one segment).  A
+// warp takes 32 units at a time: lane l loads unit l's metadata (one round
+// trip for 32 units), then the warp walks the units, broadcasting each one's
+// metadata and emitting its segments with lanes on consecutive segments --
+// coalesced 16-byte stores, no tree descent.
+__global__ void __launch_bounds__(256)
+k_iov_span(const SpanPlan sp, int64_t k0, int64_t n, int64_t* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * 8;
+    longlong2* o2 = reinterpret_cast<longlong2*>(out);
+    for (int64_t ub = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 32; ub < sp.nunits; ub += nw * 32) {
+        // lane l: metadata of unit ub + l
+        int64_t seg0 = 0, lay0 = 0, rlen = 0;
+        int32_t segs = 0, body = -1, stride = 0;
+        const int64_t u = ub + lane;
+        if (u < sp.nunits) {
+            const uint64_t o = fdiv((uint64_t)u, sp.m_nchunks, sp.s_nchunks);
+            const int64_t c = u - (int64_t)o * sp.nchunks;
+            const longlong2 ic = __ldg(sp.iovc + c);
+            const int64_t next = c + 1 < sp.nchunks ? __ldg(&sp.iovc[c + 1].x) : sp.segs_outer;
+            int64_t loff = 0;
+            if (sp.outer_depth == 1) {
+                loff = (int64_t)o * sp.outer_str[0];
+            } else if (sp.outer_depth == 2) {
+                const uint64_t o0 = fdiv(o, sp.m_outer1, sp.s_outer1);
+                loff = (int64_t)o0 * sp.outer_str[0] +
+                       (int64_t)(o - o0 * (uint64_t)sp.outer_cnt[1]) * sp.outer_str[1];
+            }
+            const SpanChunk* ch = sp.chunks + c;
+            seg0 = (int64_t)o * sp.segs_outer + ic.x;
+            segs = (int32_t)(next - ic.x);
+            lay0 = __ldg(&ch->src) + loff;
+            body = __ldg(&ch->body);
+            stride = __ldg(&ch->stride);
+            rlen = ic.y;
+            if (seg0 + segs <= k0 || seg0 >= k0 + n) segs = 0;
+        }
+        const int cnt = (int)min((int64_t)32, sp.nunits - ub);
+        for (int j = 0; j < cnt; ++j) {
+            const int32_t sg = __shfl_sync(0xffffffffu, segs, j);
+            if (sg == 0) continue;
+            const int64_t s0 = __shfl_sync(0xffffffffu, seg0, j);
+            const int64_t l0 = __shfl_sync(0xffffffffu, lay0, j);
+            const int32_t bd = __shfl_sync(0xffffffffu, body, j);
+            if (bd < 0) {   // a raw run: one segment of the whole run
+                const int64_t rl = __shfl_sync(0xffffffffu, rlen, j);
+                if (lane == 0 && s0 >= k0) o2[s0 - k0] = make_longlong2(l0, rl);
+                continue;
+            }
+            const int32_t st = __shfl_sync(0xffffffffu, stride, j);
+            const SpanBody* B = sp.bodies + bd;
+            const int nr = __ldg(&B->nruns);
+            const int q32 = 32 / nr, r32 = 32 % nr;
+            int e = lane / nr, r = lane - e * nr;
+            const int64_t lo = max((int64_t)0, k0 - s0), hi = min((int64_t)sg, k0 + n - s0);
+            for (int64_t i = lane; i < hi; i += 32) {
+                if (i >= lo)
+                    o2[s0 + i - k0] = make_longlong2(l0 + (int64_t)e * st + __ldg(&B->roff[r]), __ldg(&B->rlen[r]));
+                e += q32;
+                r += r32;
+                if (r >= nr) {
+                    r -= nr;
+                    ++e;
+                }
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256)
 k_iov(const DDesc d, int64_t k0, int64_t n, int64_t* __restrict__ out) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -722,6 +800,8 @@ cudaError_t preload_pack_kernels() {
     if ((r = cudaFuncGetAttributes(&a, k_generic<false>)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_ordered_unpack)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_iov)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_iov_chain)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_iov_span)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_span<true>)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_span<false>)) != cudaSuccess) e = r;
     if ((r = preload_perm_kernels()) != cudaSuccess) e = r;
@@ -787,7 +867,14 @@ cudaError_t launch_iov(const Plan& p, int64_t k0, int64_t n, int64_t* out, cudaS
     if (n <= 0) return cudaSuccess;
     const int64_t want = (n + 255) / 256;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count(p.device) * 16));
-    k_iov<<<(unsigned)grid, 256, 0, stream>>>(p.desc, k0, n, out);
+    if (p.kind == PLAN_CHAIN) {
+        k_iov_chain<<<(unsigned)grid, 256, 0, stream>>>(p.chain, k0, n, out);
+    } else if (p.kind == PLAN_SPAN && p.span.iovc) {
+        const int64_t g = std::max<int64_t>(1, std::min<int64_t>((p.span.nunits + 255) / 256, (int64_t)sm_count(p.device) * 8));
+        k_iov_span<<<(unsigned)g, 256, 0, stream>>>(p.span, k0, n, out);
+    } else {
+        k_iov<<<(unsigned)grid, 256, 0, stream>>>(p.desc, k0, n, out);
+    }
     return cudaGetLastError();
 }
 

@@ -533,6 +533,33 @@ bool build_span(const Node* layout, Plan* p) {
     for (const auto& c : b.chunks)
         for (int d = 0; d < 2 && sp.nperms; ++d)
             sp.ns_max[d] = std::max(sp.ns_max[d], p->perm_specs[(size_t)c.perm[d]].ns);
+    // iov segments per chunk: body chunks n * nruns; a raw piece starts a
+    // segment unless it continues the previous raw piece (one split run)
+    {
+        std::vector<int64_t> iov(2 * b.chunks.size(), 0);
+        int64_t seg = 0, first_raw = -1;
+        for (size_t i = 0; i < b.chunks.size(); ++i) {
+            const SpanChunk& c = b.chunks[i];
+            iov[2 * i] = seg;
+            if (c.body >= 0) {
+                seg += (int64_t)c.n * b.bodies[(size_t)c.body].nruns;
+                first_raw = -1;
+                continue;
+            }
+            const bool cont = first_raw >= 0 && i > 0 && b.chunks[i - 1].body < 0 &&
+                              b.chunks[i - 1].src + b.chunks[i - 1].stride == c.src &&
+                              b.chunks[i - 1].pk + b.chunks[i - 1].stride == c.pk;
+            if (cont) {
+                iov[2 * (size_t)first_raw + 1] += c.stride;
+            } else {
+                first_raw = (int64_t)i;
+                iov[2 * i + 1] = c.stride;
+                ++seg;
+            }
+        }
+        sp.segs_outer = seg;
+        p->span_iov = std::move(iov);
+    }
     p->span = sp;
     p->span_chunks = std::move(b.chunks);
     p->span_bodies = std::move(b.bodies);
@@ -614,7 +641,9 @@ std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStre
         const size_t sb = p->perm_specs.size() * sizeof(PermSpec);
         const size_t to = (so + sb + 15) & ~size_t(15);                     // perm tables
         const size_t tb = p->perm_tab.size() * sizeof(PermEntry);
-        std::vector<uint8_t> host(to + tb + 16, 0);
+        const size_t io = (to + tb + 15) & ~size_t(15);                     // iov chunk info
+        const size_t ib = p->span_iov.size() * sizeof(int64_t);
+        std::vector<uint8_t> host(io + ib + 16, 0);
         std::memcpy(host.data(), f.nodes.data(), nb);
         if (!f.kids.empty()) std::memcpy(host.data() + nb, f.kids.data(), f.kids.size() * sizeof(int32_t));
         if (pb) {
@@ -624,6 +653,7 @@ std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStre
         if (bb) std::memcpy(host.data() + bo, p->span_bodies.data(), bb);
         if (cb) std::memcpy(host.data() + co, p->span_chunks.data(), cb);
         if (tb) std::memcpy(host.data() + to, p->perm_tab.data(), tb);
+        if (ib) std::memcpy(host.data() + io, p->span_iov.data(), ib);
         (void)stream;
         void* dev = nullptr;
         cudaStream_t up = upload_stream(device);
@@ -660,6 +690,7 @@ std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStre
         p->span.bodies = (const SpanBody*)(b + bo);
         p->span.chunks = (const SpanChunk*)(b + co);
         p->span.perms = sb ? (const PermSpec*)(b + so) : nullptr;
+        p->span.iovc = ib ? (const longlong2*)(b + io) : nullptr;
         p->desc.runs = lay->runs;
         p->desc.nbytes = lay->nbytes;
     }

@@ -29,6 +29,7 @@ struct Plan {
     std::vector<SpanBody> span_bodies;
     std::vector<PermSpec> perm_specs;     // host copies; tab = offset into perm_tab until upload
     std::vector<PermEntry> perm_tab;
+    std::vector<int64_t> span_iov;        // {segment prefix, raw run length} per chunk
     void* blob = nullptr;   // device allocation backing desc
     size_t blob_bytes = 0;
     cudaEvent_t ready = nullptr;     // upload finished (recorded on an internal stream)

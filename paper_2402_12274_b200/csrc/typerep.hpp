@@ -11,6 +11,7 @@
 #pragma once
 
 #include <cstdint>
+#include <array>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -75,6 +76,7 @@ struct Datatype {
     std::mutex mu;
     std::map<std::pair<int, int64_t>, std::shared_ptr<Plan>> plans;
     std::map<int64_t, NodeP> replicated;  // layout_for(count) cache
+    std::map<int64_t, std::array<int64_t, 8>> queries;   // mpx_layout_query(count) cache
 
     NodeP layout_for(int64_t count);      // datatype.py:658-661
 };
