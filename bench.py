@@ -239,6 +239,7 @@ def _time_launch(fn, flush, reps):
     ts = []
     for _ in range(reps):
         flush.zero_()
+        torch.cuda._sleep(100000)   # GPU busy while the host enqueues: no launch gap inside the events
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         fn()
@@ -269,9 +270,16 @@ def run_extras(dev, flush, args):
         packed = torch.empty(n, dtype=torch.uint8, device=dev)
         tp = _time_launch(lambda: mp.pack_into(dt, src, packed), flush, reps)
         tu = _time_launch(lambda: mp.unpack(dt, packed, back), flush, reps)
-        out[name] = {"payload_bytes": n, "segments": dt.segment_count,
+        ti = _time_launch(lambda: mp.type_iov_tensor(dt), flush, reps)
+        peak, _ = load_peak()
+        seg = dt.segment_count
+        out[name] = {"payload_bytes": n, "segments": seg,
                      "pack_us": round(tp * 1e3, 1), "unpack_us": round(tu * 1e3, 1),
-                     "pack_GBs": round(2 * n / tp / 1e6, 1), "unpack_GBs": round(2 * n / tu / 1e6, 1)}
+                     "pack_GBs": round(2 * n / tp / 1e6, 1), "unpack_GBs": round(2 * n / tu / 1e6, 1),
+                     "pack_frac_hbm": round(2 * n / tp / 1e6 / peak, 4),
+                     "unpack_frac_hbm": round(2 * n / tu / 1e6 / peak, 4),
+                     "iov_us": round(ti * 1e3, 1), "iov_GBs": round(16 * seg / ti / 1e6, 1),
+                     "iov_frac_hbm": round(16 * seg / ti / 1e6 / peak, 4)}
         del src, back, packed
     try:
         import enqueue_bench as eb
