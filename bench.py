@@ -346,6 +346,7 @@ def gpu_arm(args):
     sampler.start()
     for i in range(args.steps):
         flush.zero_()                     # L2 flush, outside the timed events
+        torch.cuda._sleep(50000)          # keep the device busy while the host enqueues the step
         a, b, c = ev[i]
         a.record(stream)
         mp.pack_multi(dts, [arr] * len(dts), packed)
