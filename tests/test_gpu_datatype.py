@@ -217,3 +217,44 @@ def test_gpu_pinned_host_zero_copy():
         outs = [torch.empty(ref.size, dtype=torch.uint8, device=DEV)]
         mp.pack_multi([dt], [pinned], outs)
         assert np.array_equal(host(outs[0]), ref)
+
+
+SPAN_SPECS = [
+    cfg3_spec(5, hcount=3, nblocks=48),
+    ("hvector", 7, 2, 300, ("resized", 0, 36, ("struct", [2, 2, 1], [0, 5, 20],
+                                                 [("basic", 1), ("basic", 4), ("basic", 1)]))),
+    ("indexed", [5, 1, 9, 3], [0, 7, 9, 30], ("resized", 0, 12, ("struct", [1, 2], [0, 6],
+                                                                  [("basic", 4), ("basic", 1)]))),
+]
+
+
+@pytest.mark.parametrize("spec", SPAN_SPECS)
+@pytest.mark.parametrize("src_off", [0, 1, 2, 3, 5, 13])
+def test_gpu_span_plans_every_address_phase(spec, src_off):
+    """k_perm's phase tables: layout and packed buffers at every offset mod 4
+    (and mod 16), pack + full / short unpack against the oracle."""
+    dt = build_product(spec, mp)
+    ot = oracle.OracleType(spec)
+    assert dt.layout_query()["plan"] == 3    # span plan: k_perm, or k_span when a word's bytes spread > 16 B
+    span, total = ot.max_end, ot.size_bytes
+    src_h = seeded_bytes(17 + src_off, span)
+    base = torch.zeros(span + 64, dtype=torch.uint8, device=DEV)
+    src = base[src_off:src_off + span]
+    src.copy_(torch.from_numpy(src_h))
+    ref = ot.pack(src_h)
+    for pk_off in (0, 1, 2, 3, 7):
+        pbuf = torch.zeros(total + 16, dtype=torch.uint8, device=DEV)
+        out = pbuf[pk_off:pk_off + total]
+        mp.pack_into(dt, src, out)
+        assert np.array_equal(host(out), ref), (src_off, pk_off)
+        assert not host(pbuf[:pk_off]).any() and not host(pbuf[pk_off + total:]).any()
+        dbase = torch.full((span + 64,), 0xAB, dtype=torch.uint8, device=DEV)
+        dst = dbase[src_off:src_off + span]
+        for cut in (total, total // 3, 1):
+            dbase.fill_(0xAB)
+            assert mp.unpack(dt, out[:cut], dst) == cut
+            exp = np.full(span, 0xAB, np.uint8)
+            ot.unpack(ref[:cut], exp)
+            got = host(dbase)
+            assert np.array_equal(got[src_off:src_off + span], exp), (src_off, pk_off, cut)
+            assert (got[:src_off] == 0xAB).all() and (got[src_off + span:] == 0xAB).all()
