@@ -36,7 +36,10 @@ constexpr int kSlot = kFront + kBuf;
 #ifndef MPX_PERM_BPS2
 #define MPX_PERM_BPS2 4
 #endif
-template <int NS> constexpr int blocks_per_sm() { return NS <= 1 ? 4 : NS == 2 ? MPX_PERM_BPS2 : 3; }
+#ifndef MPX_PERM_BPS1
+#define MPX_PERM_BPS1 4
+#endif
+template <int NS> constexpr int blocks_per_sm() { return NS <= 1 ? MPX_PERM_BPS1 : NS == 2 ? MPX_PERM_BPS2 : 3; }
 constexpr size_t kSmem = size_t(kWarps) * 2 * kSlot;
 
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {

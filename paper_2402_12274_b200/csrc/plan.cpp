@@ -351,29 +351,15 @@ int push_variant(std::vector<PermEntry>& var, std::vector<PermEntry>* tab) {
 // bytes, input element of Ei bytes, map[t] = input offset of output byte t
 // within its element (-1: not written).  False if the period or a word's
 // input window is too wide for k_perm.
-bool build_perm(int64_t Eo, int64_t Ei, const std::vector<int64_t>& map, PermSpec* spec,
-                std::vector<PermEntry>* tab) {
-    int64_t E = 1;
-    while (((E * Eo) % 4) || ((E * Ei) % 4)) E *= 2;
-    const int64_t P = E * Eo / 4;
-    const int64_t wmax = 32 * kPermMaxSlots;
-    if (P > wmax) return false;
-    // prefer <= 3 slots per lane (4 slots cost registers), then the fullest warp
-    const int64_t wcap = P <= 96 ? 96 : wmax;
-    int64_t M = 1;
-    double best = -1;
-    for (int64_t m = 1; m * P <= wcap; ++m) {
-        const int64_t w = m * P;
-        const double eff = double(w) / double(32 * ((w + 31) / 32));
-        if (eff > best + 1e-9) { best = eff; M = m; }
-    }
-    const int64_t W = M * P;
+// Tables for M periods per step (W = M * P words) into `out`; false if a
+// word's input bytes spread over >= 16 bytes.
+bool perm_tables(int64_t Eo, int64_t Ei, int64_t E, int64_t M, const std::vector<int64_t>& map, PermSpec* spec,
+                 std::vector<PermEntry>* out) {
+    const int64_t W = M * E * Eo / 4;
     const int64_t Din = M * E * Ei;      // input bytes per step (multiple of 4)
     spec->W = (int32_t)W;
     spec->Dw = (int32_t)(Din / 4);
-    spec->ns = (int32_t)((W + 31) / 32);
     spec->pad = 0;
-    spec->tab = reinterpret_cast<const PermEntry*>((uintptr_t)tab->size());   // patched at upload
     int wcmax = 0;
     for (int po = 0; po < 4; ++po) {
         for (int ap = 0; ap < 4; ++ap) {
@@ -390,12 +376,43 @@ bool build_perm(int64_t Eo, int64_t Ei, const std::vector<int64_t>& map, PermSpe
                 }
                 if (!make_entry(r, cov, ap, &var[(size_t)j])) return false;
             }
-            const int wc = push_variant(var, tab);
+            const int wc = push_variant(var, out);
             spec->wc[po * 4 + ap] = (uint8_t)wc;
             wcmax = std::max(wcmax, wc);
         }
     }
     spec->ns = (wcmax + 31) / 32;
+    return true;
+}
+
+bool build_perm(int64_t Eo, int64_t Ei, const std::vector<int64_t>& map, PermSpec* spec,
+                std::vector<PermEntry>* tab) {
+    int64_t E = 1;
+    while (((E * Eo) % 4) || ((E * Ei) % 4)) E *= 2;
+    const int64_t P = E * Eo / 4;
+    const int64_t wmax = 32 * kPermMaxSlots;
+    if (P > wmax) return false;
+    // Periods per step: fewest slots per lane first (registers / occupancy),
+    // then the best lane use at address phase (0, 0) -- the common case of
+    // aligned buffers -- counting only words that write a byte.
+    PermSpec best{};
+    std::vector<PermEntry> best_tab;
+    double best_eff = -1;
+    for (int64_t m = 1; m * P <= wmax; ++m) {
+        PermSpec sp{};
+        std::vector<PermEntry> t;
+        if (!perm_tables(Eo, Ei, E, m, map, &sp, &t)) return false;
+        const int wc0 = sp.wc[0];
+        const double eff = wc0 ? double(wc0) / double(32 * ((wc0 + 31) / 32)) : 0.0;
+        if (best_eff < 0 || sp.ns < best.ns || (sp.ns == best.ns && eff > best_eff + 1e-9)) {
+            best = sp;
+            best_tab.swap(t);
+            best_eff = eff;
+        }
+    }
+    *spec = best;
+    spec->tab = reinterpret_cast<const PermEntry*>((uintptr_t)tab->size());   // patched at upload
+    tab->insert(tab->end(), best_tab.begin(), best_tab.end());
     return true;
 }
 
