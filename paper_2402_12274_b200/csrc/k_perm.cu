@@ -143,6 +143,36 @@ __device__ __forceinline__ Unit make_unit(const UnitIter& it, const SpanPlan& sp
     return r;
 }
 
+// Unit metadata for 32 consecutive units at once: lane l computes unit
+// ub + l (one decomposition and one round of loads for 32 units); the warp
+// then walks the batch broadcasting one unit at a time with shuffles.
+template <bool PACK>
+__device__ __forceinline__ Unit load_batch(const SpanPlan& sp, int64_t ub, int64_t u_end, const uint8_t* src,
+                                           uint8_t* dst, int64_t limit, int lane) {
+    Unit r;
+    r.in = nullptr;
+    r.out = nullptr;
+    r.in_len = r.out_len = 0;
+    r.flags = 0;
+    const int64_t u = ub + lane;
+    if (u < u_end) {
+        UnitIter it;
+        iter_init(it, sp, u, u + 1);
+        r = make_unit<PACK>(it, sp, src, dst, limit);
+    }
+    return r;
+}
+
+__device__ __forceinline__ Unit bcast(const Unit& m, int i) {
+    Unit r;
+    r.in = reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(m.in), i));
+    r.out = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(m.out), i));
+    r.in_len = __shfl_sync(0xffffffffu, m.in_len, i);
+    r.out_len = __shfl_sync(0xffffffffu, m.out_len, i);
+    r.flags = __shfl_sync(0xffffffffu, m.flags, i);
+    return r;
+}
+
 __device__ __forceinline__ void stage(uint32_t sbuf, const Unit& U, int lane) {
     const int a = (int)(reinterpret_cast<uintptr_t>(U.in) & 15);
     const uint8_t* g = U.in - a;
@@ -263,7 +293,6 @@ __global__ void __launch_bounds__(kWarps * 32, blocks_per_sm<NS>())
 k_perm(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t limit) {
     extern __shared__ __align__(16) uint8_t sm[];
     __shared__ PermSpec specs[2 * kPermMaxSpecs];
-    __shared__ Unit parked[kWarps];
     for (int i = threadIdx.x; i < sp.nperms; i += blockDim.x) specs[i] = sp.perms[i];
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -273,31 +302,58 @@ k_perm(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__
     const int64_t u0 = sp.nunits / nw * gwid + min(gwid, sp.nunits % nw);
     const int64_t u1 = u0 + sp.nunits / nw + (gwid < sp.nunits % nw ? 1 : 0);
     if (u0 >= u1) return;
-    UnitIter it;
-    iter_init(it, sp, u0, u1);
-    Unit cur = make_unit<PACK>(it, sp, src, dst, limit);
-    if (cur.flags & 1) stage(sbase, cur, lane);
-    cp_async_commit();
     uint32_t pb = 0;
-    // the next unit waits in shared memory while the current one is permuted
-    // (registers are the scarce resource inside permute)
-    Unit* park = &parked[warp];
-    for (;;) {
-        const bool more = it.left > 0;
-        if (more) {
-            iter_next(it, sp);
-            const Unit nxt = make_unit<PACK>(it, sp, src, dst, limit);
-            if (nxt.flags & 1) stage(sbase + (pb ^ kSlot), nxt, lane);
-            if (lane == 0) *park = nxt;
-        }
+    if (NS == 1) {
+        // unit metadata 32 units per batch, distributed over the lanes (one
+        // round of dependent loads per 32 units instead of per unit)
+        Unit batch = load_batch<PACK>(sp, u0, u1, src, dst, limit, lane);
+        Unit cur = bcast(batch, 0);
+        if (cur.flags & 1) stage(sbase, cur, lane);
         cp_async_commit();
-        cp_async_wait<1>();
-        __syncwarp();
-        if (cur.flags & 1) permute<PACK, NS>(specs[cur.flags >> 8], cur, sbase + pb, lane);
-        __syncwarp();
-        if (!more) break;
-        cur = *park;
-        pb ^= kSlot;
+        for (int64_t u = u0;; ++u) {
+            const bool more = u + 1 < u1;
+            Unit nxt;
+            nxt.flags = 0;
+            if (more) {
+                const int i = (int)((u + 1 - u0) & 31);
+                if (i == 0) batch = load_batch<PACK>(sp, u + 1, u1, src, dst, limit, lane);
+                nxt = bcast(batch, i);
+                if (nxt.flags & 1) stage(sbase + (pb ^ kSlot), nxt, lane);
+            }
+            cp_async_commit();
+            cp_async_wait<1>();
+            __syncwarp();
+            if (cur.flags & 1) permute<PACK, NS>(specs[cur.flags >> 8], cur, sbase + pb, lane);
+            __syncwarp();
+            if (!more) break;
+            cur = nxt;
+            pb ^= kSlot;
+        }
+    } else {
+        // more slots leave no registers for a batch: walk units one by one
+        UnitIter it;
+        iter_init(it, sp, u0, u1);
+        Unit cur = make_unit<PACK>(it, sp, src, dst, limit);
+        if (cur.flags & 1) stage(sbase, cur, lane);
+        cp_async_commit();
+        for (;;) {
+            const bool more = it.left > 0;
+            Unit nxt;
+            nxt.flags = 0;
+            if (more) {
+                iter_next(it, sp);
+                nxt = make_unit<PACK>(it, sp, src, dst, limit);
+                if (nxt.flags & 1) stage(sbase + (pb ^ kSlot), nxt, lane);
+            }
+            cp_async_commit();
+            cp_async_wait<1>();
+            __syncwarp();
+            if (cur.flags & 1) permute<PACK, NS>(specs[cur.flags >> 8], cur, sbase + pb, lane);
+            __syncwarp();
+            if (!more) break;
+            cur = nxt;
+            pb ^= kSlot;
+        }
     }
     cp_async_wait<0>();
 }
