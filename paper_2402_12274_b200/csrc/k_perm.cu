@@ -21,6 +21,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "desc.cuh"
 #include "kernels.hpp"
@@ -303,9 +305,10 @@ k_perm(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__
     const int64_t u1 = u0 + sp.nunits / nw + (gwid < sp.nunits % nw ? 1 : 0);
     if (u0 >= u1) return;
     uint32_t pb = 0;
-    if (NS == 1) {
+    if (PACK && NS == 1) {
         // unit metadata 32 units per batch, distributed over the lanes (one
-        // round of dependent loads per 32 units instead of per unit)
+        // round of dependent loads per 32 units instead of per unit; measured
+        // faster for pack, slower for unpack)
         Unit batch = load_batch<PACK>(sp, u0, u1, src, dst, limit, lane);
         Unit cur = bcast(batch, 0);
         if (cur.flags & 1) stage(sbase, cur, lane);
@@ -330,7 +333,7 @@ k_perm(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__
             pb ^= kSlot;
         }
     } else {
-        // more slots leave no registers for a batch: walk units one by one
+        // walk units one by one (more slots leave no registers for a batch)
         UnitIter it;
         iter_init(it, sp, u0, u1);
         Unit cur = make_unit<PACK>(it, sp, src, dst, limit);
@@ -360,7 +363,29 @@ k_perm(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__
 
 template <bool PACK>
 cudaError_t launch_dir(const Plan& p, const uint8_t* src, uint8_t* dst, int64_t limit, cudaStream_t stream) {
-    const int ns = p.span.ns_max[PACK ? 1 : 0];
+    // slots this launch needs: the phase variants its chunks actually take
+    // given the buffer addresses (aligned buffers touch few variants)
+    int ns = 0;
+    {
+        const int lp = (int)(reinterpret_cast<uintptr_t>(PACK ? src : dst) & 3);
+        const int pp = (int)(reinterpret_cast<uintptr_t>(PACK ? dst : src) & 3);
+        for (const int32_t u : p.perm_use[PACK ? 1 : 0]) {
+            const PermSpec& S = p.perm_specs[(size_t)(u >> 6)];
+            int wc = 0;
+            for (int v = 0; v < 16; ++v) {
+                const int po = v >> 2, ap = v & 3;
+                const int lay = PACK ? ap : po, pk = PACK ? po : ap;   // phases of this variant
+                const bool lay_ok = (u & 32) || lay == ((((u >> 2) & 3) + lp) & 3);
+                const bool pk_ok = (u & 16) || pk == (((u & 3) + pp) & 3);
+                if (lay_ok && pk_ok) wc = std::max<int>(wc, S.wc[v]);
+            }
+            ns = std::max(ns, (wc + 31) / 32);
+        }
+        ns = std::max(ns, 1);
+        static const bool dbg = getenv("MPX_DEBUG_PLAN") != nullptr;
+        if (dbg) fprintf(stderr, "[mpx k_perm] %s: %d slots (plan max %d), %zu spec/phase uses\n",
+                         PACK ? "pack" : "unpack", ns, p.span.ns_max[PACK ? 1 : 0], p.perm_use[PACK ? 1 : 0].size());
+    }
     const int64_t want = (p.span.nunits + kWarps - 1) / kWarps;
     const int64_t grid = std::max<int64_t>(
         1, std::min<int64_t>(want, (int64_t)sm_count(p.device) * (ns <= 1 ? blocks_per_sm<1>() : ns == 2 ? blocks_per_sm<2>() : blocks_per_sm<4>())));

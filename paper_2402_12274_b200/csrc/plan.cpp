@@ -6,6 +6,7 @@
 #include <cstring>
 #include <tuple>
 #include <map>
+#include <set>
 #include <mutex>
 #include <unordered_map>
 
@@ -550,6 +551,22 @@ bool build_span(const Node* layout, Plan* p) {
     for (const auto& c : b.chunks)
         for (int d = 0; d < 2 && sp.nperms; ++d)
             sp.ns_max[d] = std::max(sp.ns_max[d], p->perm_specs[(size_t)c.perm[d]].ns);
+    if (sp.nperms) {
+        // (spec, layout phase, packed phase) of every chunk; an outer stride
+        // that is not a multiple of 4 makes every phase of that side possible
+        bool lay_al = true, pk_al = true;
+        for (int i = 0; i < sp.outer_depth; ++i) {
+            lay_al = lay_al && (sp.outer_str[i] & 3) == 0;
+            pk_al = pk_al && (sp.outer_pk[i] & 3) == 0;
+        }
+        for (int d = 0; d < 2; ++d) {
+            std::set<int32_t> use;
+            for (const auto& c : b.chunks)
+                use.insert((c.perm[d] << 6) | (lay_al ? (int32_t)((c.src & 3) << 2) : 32) |
+                           (pk_al ? (int32_t)(c.pk & 3) : 16));
+            p->perm_use[d].assign(use.begin(), use.end());
+        }
+    }
     // iov segments per chunk: body chunks n * nruns; a raw piece starts a
     // segment unless it continues the previous raw piece (one split run)
     {

@@ -29,6 +29,10 @@ struct Plan {
     std::vector<SpanBody> span_bodies;
     std::vector<PermSpec> perm_specs;     // host copies; tab = offset into perm_tab until upload
     std::vector<PermEntry> perm_tab;
+    // per direction: (spec << 6 | layout phase << 2 | packed phase) of the
+    // chunks (phases mod 4 relative to the buffers; bit 5 / bit 4: any
+    // layout / packed phase)
+    std::vector<int32_t> perm_use[2];
     std::vector<int64_t> span_iov;        // {segment prefix, raw run length} per chunk
     void* blob = nullptr;   // device allocation backing desc
     size_t blob_bytes = 0;
