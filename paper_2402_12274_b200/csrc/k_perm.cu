@@ -270,9 +270,7 @@ __device__ __forceinline__ void permute(const PermSpec& S, const Unit& U, uint32
     // words past the end are clamped into the buffer and never stored.
     const int w_lo = po ? 1 : 0, w_hi = (U.out_len + po) >> 2;
     const uint32_t wmax = sbuf + (uint32_t)(kBuf - 16);
-    uint32_t kd = 0;
-#pragma unroll 2
-    for (int kw = 0; kw < words; kw += W, kd += Dw4) {
+    auto edge = [&](int kw, uint32_t kd) {
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
             if (32 * s >= wc) break;
@@ -287,7 +285,28 @@ __device__ __forceinline__ void permute(const PermSpec& S, const Unit& U, uint32
                 store_bytes(reinterpret_cast<uint8_t*>(p), r, valid_mask(cov, gw, po, U.out_len));
             }
         }
+    };
+    // interior steps (every word whole, so every window inside the staged
+    // input) need no clamp and no bounds checks
+    int kw = 0;
+    uint32_t kd = 0;
+    if (po && words > 0) {
+        edge(0, 0);
+        kw = W;
+        kd = Dw4;
     }
+    for (; kw + W <= w_hi; kw += W, kd += Dw4) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            if (32 * s >= wc) break;
+            const uint32_t r = gather_word(e[s].w + kd, e[s]);
+            const uint32_t cov = (e[s].lo >> 16) & 0xF;
+            uint32_t* p = ow + kw + (int)(e[s].lo >> 24);
+            if (cov == 0xF) *p = r;
+            else if (!PACK && cov) store_bytes(reinterpret_cast<uint8_t*>(p), r, cov);   // layout gap
+        }
+    }
+    for (; kw < words; kw += W, kd += Dw4) edge(kw, kd);
 }
 
 template <bool PACK, int NS>
