@@ -202,8 +202,33 @@ struct Slot {
     uint32_t w, lo, hi, mix;
 };
 
+// MPX_DEBUG_BOUNDS builds trap on a shared window outside the warp's two
+// staging slots (the library ships without the check)
+#ifdef MPX_DEBUG_BOUNDS
+__device__ __forceinline__ uint8_t* sm_base_dbg();
+#define MPX_CHECK_WIN(w)                                                                        \
+    do {                                                                                        \
+        const uint32_t lo_ = (uint32_t)__cvta_generic_to_shared(sm_base_dbg()) +                 \
+                             (uint32_t)((threadIdx.x >> 5) * 2 * kSlot);                          \
+        if ((w) < lo_ || (w) + 16 > lo_ + 2 * kSlot) {                                           \
+            printf("k_perm window %u outside [%u, %u)\n", (w), lo_, lo_ + 2 * kSlot);             \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+#else
+#define MPX_CHECK_WIN(w) ((void)0)
+#endif
+
 // output word of a slot whose window starts at shared address w
+#ifdef MPX_DEBUG_BOUNDS
+__device__ __forceinline__ uint8_t* sm_base_dbg() {
+    extern __shared__ __align__(16) uint8_t sm[];
+    return sm;
+}
+#endif
+
 __device__ __forceinline__ uint32_t gather_word(uint32_t w, const Slot& e) {
+    MPX_CHECK_WIN(w);
     const uint32_t a = prmt(lds32(w), lds32(w + 4), e.lo);
     const uint32_t b = prmt(lds32(w + 8), lds32(w + 12), e.hi);
     return prmt(a, b, e.mix);
