@@ -101,7 +101,8 @@ int mpx_type_iov(mpx_datatype dt, int64_t count, int64_t iov_offset, int64_t max
 int mpx_packed_size(mpx_datatype dt, int64_t count, int64_t *out);
 /* Host-side lowering summary of layout_for(count) (datatype.py:658-661):
  * out[0..7] = runs, nbytes, min_off, max_end, node_count,
- *             plan kind (0 empty, 1 chain, 2 generic), overlap, chain alignment */
+ *             plan kind (0 empty, 1 chain, 2 descriptor walk, 3 span, 4 run table),
+ *             overlap, chain alignment (span plans: word-gather spec count) */
 int mpx_layout_query(mpx_datatype dt, int64_t count, int64_t out[8]);
 
 /* ---- data movement (device buffers, asynchronous on `stream`) ----------- */

@@ -527,6 +527,8 @@ int launch_move(int dev, Datatype* d, int64_t count, bool pack, const void* src,
         e = launch_chain_batch(b, pack, dev, stream);
     } else if (plan->kind == PLAN_SPAN && !(!pack && plan->overlap)) {
         e = launch_span(*plan, pack, static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), limit, stream);
+    } else if (plan->kind == PLAN_RUNS && !(!pack && plan->overlap)) {
+        e = launch_runs(*plan, pack, static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), limit, stream);
     } else {
         e = launch_generic(*plan, pack, static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), limit,
                            stream);
@@ -627,6 +629,9 @@ int movement(int n, const mpx_datatype* dts, const int64_t* counts, const void* 
         } else if (plan->kind == PLAN_SPAN && !(!pack && plan->overlap)) {
             cudaError_t e = launch_span(*plan, pack, s, t, limit, stream);
             if (e != cudaSuccess) return cuda_fail(e, "span launch");
+        } else if (plan->kind == PLAN_RUNS && !(!pack && plan->overlap)) {
+            cudaError_t e = launch_runs(*plan, pack, s, t, limit, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "run-table launch");
         } else {
             cudaError_t e = launch_generic(*plan, pack, s, t, limit, stream);
             if (e != cudaSuccess) return cuda_fail(e, "generic launch");

@@ -537,6 +537,70 @@ k_span(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__
     }
 }
 
+// ---------------------------------------------------------------- runs
+// Flat run table (plan.hpp, RunTable): thread per run, G-byte words (G
+// divides every offset and length), consecutive runs on consecutive lanes so
+// the table loads and the packed side stay coalesced.  limit cuts the packed
+// stream (unpack prefix semantics, datatype.py:719-724).
+template <bool PACK, int G>
+__global__ void __launch_bounds__(256)
+k_runs(const RunTable t, const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t limit) {
+    using T = typename Vec<G>::T;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < t.nruns; r += stride) {
+        const int64_t so = __ldg(t.src + r), po = __ldg(t.pk + r);
+        if (po >= limit) continue;
+        const int64_t end = min(__ldg(t.pk + r + 1), limit);
+        const int len = (int)(end - po);
+        const uint8_t* s = src + (PACK ? so : po);
+        uint8_t* d = dst + (PACK ? po : so);
+        int w = 0;
+        for (; w + G <= len; w += G) *reinterpret_cast<T*>(d + w) = *reinterpret_cast<const T*>(s + w);
+        for (; w < len; ++w) d[w] = s[w];   // a run cut by the limit
+    }
+}
+
+// Longer runs (>= 16 words on average): warp per run, lanes on consecutive
+// words, so both sides move as coalesced 32 x G-byte accesses.  Lane l loads
+// the table entry of run r0 + l; the warp then walks its 32 runs.
+template <bool PACK, int G>
+__global__ void __launch_bounds__(256)
+k_runs_warp(const RunTable t, const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t limit) {
+    using T = typename Vec<G>::T;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * 8;
+    for (int64_t r0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 32; r0 < t.nruns; r0 += nw * 32) {
+        int64_t so = 0, po = limit, end = limit;
+        if (r0 + lane < t.nruns) {
+            so = __ldg(t.src + r0 + lane);
+            po = __ldg(t.pk + r0 + lane);
+            end = min(__ldg(t.pk + r0 + lane + 1), limit);
+        }
+        const int cnt = (int)min((int64_t)32, t.nruns - r0);
+        for (int j = 0; j < cnt; ++j) {
+            const int64_t p0 = __shfl_sync(0xffffffffu, po, j);
+            if (p0 >= limit) break;
+            const int64_t s0 = __shfl_sync(0xffffffffu, so, j);
+            const int len = (int)(__shfl_sync(0xffffffffu, end, j) - p0);
+            const uint8_t* s = src + (PACK ? s0 : p0);
+            uint8_t* d = dst + (PACK ? p0 : s0);
+            const int nwd = len / G;
+            for (int w = lane; w < nwd; w += 32)
+                reinterpret_cast<T*>(d)[w] = reinterpret_cast<const T*>(s)[w];
+            for (int b = nwd * G + lane; b < len; b += 32) d[b] = s[b];   // a run cut by the limit
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_iov_runs(const RunTable t, int64_t k0, int64_t n, int64_t* __restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const int64_t r = k0 + i;
+        reinterpret_cast<longlong2*>(out)[i] = make_longlong2(__ldg(t.src + r), __ldg(t.pk + r + 1) - __ldg(t.pk + r));
+    }
+}
+
 // ---------------------------------------------------------------- zipper
 // Typed -> typed transfer in one pass (datatype.py:760-797 copy_between, the
 // reference's zipper): both layouts are chains, so packed byte P maps to a
@@ -811,6 +875,13 @@ cudaError_t preload_pack_kernels() {
     if ((r = cudaFuncGetAttributes(&a, k_zip<2>)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_zip<1>)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_zip_tail)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_iov_runs)) != cudaSuccess) e = r;
+#define MPX_PRE(PK, G)                                                                     \
+    if ((r = cudaFuncGetAttributes(&a, k_runs<PK, G>)) != cudaSuccess) e = r;              \
+    if ((r = cudaFuncGetAttributes(&a, k_runs_warp<PK, G>)) != cudaSuccess) e = r
+    MPX_PRE(true, 16); MPX_PRE(true, 8); MPX_PRE(true, 4); MPX_PRE(true, 2); MPX_PRE(true, 1);
+    MPX_PRE(false, 16); MPX_PRE(false, 8); MPX_PRE(false, 4); MPX_PRE(false, 2); MPX_PRE(false, 1);
+#undef MPX_PRE
     return e;
 }
 
@@ -830,6 +901,42 @@ cudaError_t launch_span(const Plan& p, bool pack, const uint8_t* src, uint8_t* d
     }
     if (pack) k_span<true><<<(unsigned)grid, kSpanWarps * 32, kSpanSmem, stream>>>(p.span, src, dst, limit);
     else k_span<false><<<(unsigned)grid, kSpanWarps * 32, kSpanSmem, stream>>>(p.span, src, dst, limit);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_runs(const Plan& p, bool pack, const uint8_t* src, uint8_t* dst, int64_t limit,
+                        cudaStream_t stream) {
+    if (limit <= 0 || p.rt.nruns == 0) return cudaSuccess;
+    int g = p.rt.g;
+    const uintptr_t m = reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst);
+    while (g > 1 && (m & (uintptr_t)(g - 1))) g >>= 1;
+    const int64_t want = (p.rt.nruns + 255) / 256;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count(p.device) * 16));
+    const bool coop = p.rt.avg_words >= 16;
+    const int64_t wgrid = std::max<int64_t>(1, std::min<int64_t>((p.rt.nruns + 255) / 256, (int64_t)sm_count(p.device) * 8));
+#define MPX_RUNS(PK, G)                                                                     \
+    do {                                                                                    \
+        if (coop) k_runs_warp<PK, G><<<(unsigned)wgrid, 256, 0, stream>>>(p.rt, src, dst, limit); \
+        else k_runs<PK, G><<<(unsigned)grid, 256, 0, stream>>>(p.rt, src, dst, limit);     \
+    } while (0)
+    if (pack) {
+        switch (g) {
+        case 16: MPX_RUNS(true, 16); break;
+        case 8: MPX_RUNS(true, 8); break;
+        case 4: MPX_RUNS(true, 4); break;
+        case 2: MPX_RUNS(true, 2); break;
+        default: MPX_RUNS(true, 1); break;
+        }
+    } else {
+        switch (g) {
+        case 16: MPX_RUNS(false, 16); break;
+        case 8: MPX_RUNS(false, 8); break;
+        case 4: MPX_RUNS(false, 4); break;
+        case 2: MPX_RUNS(false, 2); break;
+        default: MPX_RUNS(false, 1); break;
+        }
+    }
+#undef MPX_RUNS
     return cudaGetLastError();
 }
 
@@ -869,6 +976,8 @@ cudaError_t launch_iov(const Plan& p, int64_t k0, int64_t n, int64_t* out, cudaS
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count(p.device) * 16));
     if (p.kind == PLAN_CHAIN) {
         k_iov_chain<<<(unsigned)grid, 256, 0, stream>>>(p.chain, k0, n, out);
+    } else if (p.kind == PLAN_RUNS && !p.rt.split) {
+        k_iov_runs<<<(unsigned)grid, 256, 0, stream>>>(p.rt, k0, n, out);
     } else if (p.kind == PLAN_SPAN && p.span.iovc) {
         const int64_t g = std::max<int64_t>(1, std::min<int64_t>((p.span.nunits + 255) / 256, (int64_t)sm_count(p.device) * 8));
         k_iov_span<<<(unsigned)g, 256, 0, stream>>>(p.span, k0, n, out);

@@ -45,6 +45,8 @@ cudaError_t launch_generic(const Plan& p, bool pack, const uint8_t* src, uint8_t
                            cudaStream_t stream);
 cudaError_t launch_span(const Plan& p, bool pack, const uint8_t* src, uint8_t* dst, int64_t limit,
                         cudaStream_t stream);
+cudaError_t launch_runs(const Plan& p, bool pack, const uint8_t* src, uint8_t* dst, int64_t limit,
+                        cudaStream_t stream);
 // typed -> typed in one pass for two chain plans (copy_between, datatype.py:760-797)
 cudaError_t launch_zip(const Plan& ps, const Plan& pd, const uint8_t* src, uint8_t* dst, int64_t bytes,
                        cudaStream_t stream);

@@ -644,7 +644,23 @@ void analyze(const Node* layout, Plan* p) {
         p->chain = c;
         p->chain_align = (int32_t)align;
     } else {
-        p->kind = build_span(layout, p) ? PLAN_SPAN : PLAN_GENERIC;
+        const bool span = build_span(layout, p);
+        // many small irregular runs: tiny span chunks (or no span form at
+        // all) lose to a flat run table, one thread per run
+        const int64_t units = span ? std::max<int64_t>(1, p->span.nunits) : 1;
+        const bool tiny = !span || p->perm_specs.empty() || layout->nbytes / units < 128;
+        if (tiny && layout->runs <= kMaxTableRuns && layout->nbytes / std::max<int64_t>(1, layout->runs) <= 1024) {
+            p->kind = PLAN_RUNS;
+            p->span_chunks.clear();
+            p->span_bodies.clear();
+            p->perm_specs.clear();
+            p->perm_tab.clear();
+            p->span_iov.clear();
+            p->perm_use[0].clear();
+            p->perm_use[1].clear();
+        } else {
+            p->kind = span ? PLAN_SPAN : PLAN_GENERIC;
+        }
     }
     p->overlap = may_overlap(layout);
     if (p->overlap && layout->runs <= (int64_t(1) << 22)) p->overlap = exact_overlap(layout);
@@ -661,6 +677,33 @@ std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStre
     auto p = std::make_shared<Plan>();
     p->device = device;
     analyze(lay.get(), p.get());
+    std::vector<int64_t> rt_src, rt_pk;
+    if (p->kind == PLAN_RUNS) {
+        std::vector<int64_t> flat;
+        tree::enumerate(lay.get(), 0, flat, lay->runs);
+        const size_t n = flat.size() / 2;
+        rt_src.reserve(n);
+        rt_pk.reserve(n + 1);
+        int64_t pk = 0, all = 0;
+        bool split = false;
+        for (size_t i = 0; i < n; ++i) {
+            const int64_t off = flat[2 * i], len = flat[2 * i + 1];
+            all |= off | len;
+            for (int64_t o = 0; o < len; o += kRunPiece) {
+                rt_src.push_back(off + o);
+                rt_pk.push_back(pk + o);
+                split = split || o > 0;
+            }
+            pk += len;
+        }
+        rt_pk.push_back(pk);
+        int32_t g = 16;
+        while (g > 1 && (all & (g - 1))) g >>= 1;
+        p->rt.nruns = (int64_t)rt_src.size();
+        p->rt.g = g;
+        p->rt.avg_words = p->rt.nruns ? pk / p->rt.nruns / g : 0;
+        p->rt.split = split ? 1 : 0;
+    }
     if (p->kind != PLAN_EMPTY) {
         Flattener f;
         const int32_t root = f.add(lay.get());
@@ -677,7 +720,11 @@ std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStre
         const size_t tb = p->perm_tab.size() * sizeof(PermEntry);
         const size_t io = (to + tb + 15) & ~size_t(15);                     // iov chunk info
         const size_t ib = p->span_iov.size() * sizeof(int64_t);
-        std::vector<uint8_t> host(io + ib + 16, 0);
+        const size_t ro = (io + ib + 15) & ~size_t(15);                     // run table
+        const size_t rb = rt_src.size() * sizeof(int64_t);
+        const size_t qo = (ro + rb + 15) & ~size_t(15);
+        const size_t qb = rt_pk.size() * sizeof(int64_t);
+        std::vector<uint8_t> host(qo + qb + 16, 0);
         std::memcpy(host.data(), f.nodes.data(), nb);
         if (!f.kids.empty()) std::memcpy(host.data() + nb, f.kids.data(), f.kids.size() * sizeof(int32_t));
         if (pb) {
@@ -688,6 +735,8 @@ std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStre
         if (cb) std::memcpy(host.data() + co, p->span_chunks.data(), cb);
         if (tb) std::memcpy(host.data() + to, p->perm_tab.data(), tb);
         if (ib) std::memcpy(host.data() + io, p->span_iov.data(), ib);
+        if (rb) std::memcpy(host.data() + ro, rt_src.data(), rb);
+        if (qb) std::memcpy(host.data() + qo, rt_pk.data(), qb);
         (void)stream;
         void* dev = nullptr;
         cudaStream_t up = upload_stream(device);
@@ -725,6 +774,8 @@ std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStre
         p->span.chunks = (const SpanChunk*)(b + co);
         p->span.perms = sb ? (const PermSpec*)(b + so) : nullptr;
         p->span.iovc = ib ? (const longlong2*)(b + io) : nullptr;
+        p->rt.src = rb ? (const int64_t*)(b + ro) : nullptr;
+        p->rt.pk = qb ? (const int64_t*)(b + qo) : nullptr;
         p->desc.runs = lay->runs;
         p->desc.nbytes = lay->nbytes;
     }

@@ -14,7 +14,23 @@
 
 namespace mpx {
 
-enum PlanKind : int32_t { PLAN_EMPTY = 0, PLAN_CHAIN = 1, PLAN_GENERIC = 2, PLAN_SPAN = 3 };
+enum PlanKind : int32_t { PLAN_EMPTY = 0, PLAN_CHAIN = 1, PLAN_GENERIC = 2, PLAN_SPAN = 3, PLAN_RUNS = 4 };
+
+// Flat run table for irregular layouts of many small runs (e.g. indexed types
+// with thousands of short blocks): run r = layout bytes [src[r], src[r] +
+// pk[r + 1] - pk[r]) at packed offset pk[r].  Runs longer than kRunPiece are
+// split into pieces (then `split` is set and type_iov walks the descriptor).
+constexpr int64_t kRunPiece = 512;
+constexpr int64_t kMaxTableRuns = int64_t(1) << 23;
+
+struct RunTable {
+    const int64_t* src;
+    const int64_t* pk;      // nruns + 1 entries
+    int64_t nruns;
+    int32_t g;              // largest power of two <= 16 dividing every offset and length
+    int32_t split;
+    int64_t avg_words;      // average run length in g-byte words (>= 16: warp per run)
+};
 
 struct Plan {
     int32_t kind = PLAN_EMPTY;
@@ -25,6 +41,7 @@ struct Plan {
     int32_t chain_align = 16;  // largest power of two dividing base, L and strides
     DDesc desc{};           // device descriptor (always built, used by iov + generic)
     SpanPlan span{};        // valid for PLAN_SPAN (pointers into blob)
+    RunTable rt{};          // valid for PLAN_RUNS (pointers into blob)
     std::vector<SpanChunk> span_chunks;   // host copies, uploaded with the descriptor
     std::vector<SpanBody> span_bodies;
     std::vector<PermSpec> perm_specs;     // host copies; tab = offset into perm_tab until upload

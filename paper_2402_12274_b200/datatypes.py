@@ -113,8 +113,9 @@ class Datatype:
 
     def layout_query(self, count=1):
         """Host-side lowering summary (runs, nbytes, min_off, max_end,
-        node_count, plan kind, overlap, and chain alignment -- or, for span
-        plans, the number of word-gather specs (0: k_span fallback))."""
+        node_count, plan kind (0 empty, 1 chain, 2 descriptor walk, 3 span,
+        4 run table), overlap, and chain alignment -- or, for span plans,
+        the number of word-gather specs (0: k_span fallback))."""
         out = (ctypes.c_int64 * 8)()
         check(lib.mpx_layout_query(self._h, count, out))
         keys = ("runs", "nbytes", "min_off", "max_end", "node_count", "plan",

@@ -231,11 +231,13 @@ SPAN_SPECS = [
 @pytest.mark.parametrize("spec", SPAN_SPECS)
 @pytest.mark.parametrize("src_off", [0, 1, 2, 3, 5, 13])
 def test_gpu_span_plans_every_address_phase(spec, src_off):
-    """k_perm's phase tables: layout and packed buffers at every offset mod 4
-    (and mod 16), pack + full / short unpack against the oracle."""
+    """k_perm's phase tables (and the run-table kernel): layout and packed
+    buffers at every offset mod 4 (and mod 16), pack + full / short unpack
+    against the oracle."""
     dt = build_product(spec, mp)
     ot = oracle.OracleType(spec)
-    assert dt.layout_query()["plan"] == 3    # span plan: k_perm, or k_span when a word's bytes spread > 16 B
+    # span plan (k_perm), or the flat run table when no word-gather form exists
+    assert dt.layout_query()["plan"] in (3, 4)
     span, total = ot.max_end, ot.size_bytes
     src_h = seeded_bytes(17 + src_off, span)
     base = torch.zeros(span + 64, dtype=torch.uint8, device=DEV)
@@ -258,3 +260,47 @@ def test_gpu_span_plans_every_address_phase(spec, src_off):
             got = host(dbase)
             assert np.array_equal(got[src_off:src_off + span], exp), (src_off, pk_off, cut)
             assert (got[:src_off] == 0xAB).all() and (got[src_off + span:] == 0xAB).all()
+
+
+def _irregular_indexed(seed, nblk, blmax, gapmax, elem):
+    rng = np.random.default_rng(seed)
+    bls = rng.integers(1, blmax + 1, nblk)
+    gaps = rng.integers(0, gapmax + 1, nblk)
+    displs = np.cumsum(gaps + np.concatenate([[0], bls[:-1]]))
+    return ("indexed", [int(x) for x in bls], [int(x) for x in displs], ("basic", elem))
+
+
+@pytest.mark.parametrize("spec", [
+    _irregular_indexed(1, 5000, 4, 8, 8),       # thread per run
+    _irregular_indexed(2, 3000, 16, 64, 4),
+    _irregular_indexed(3, 800, 64, 32, 8),      # warp per run (long runs)
+    _irregular_indexed(4, 4000, 3, 5, 1),       # byte runs, 1-byte words
+])
+@pytest.mark.parametrize("off", [0, 3])
+def test_gpu_run_table_plans(spec, off):
+    """Irregular indexed types (many short blocks) take the flat run table:
+    pack, full / short unpack and iov windows against the oracle, at an
+    aligned and a misaligned buffer offset."""
+    dt = build_product(spec, mp)
+    ot = oracle.OracleType(spec)
+    assert dt.layout_query()["plan"] == 4
+    span, total = ot.max_end, ot.size_bytes
+    src_h = seeded_bytes(31 + off, span)
+    base = torch.zeros(span + 32, dtype=torch.uint8, device=DEV)
+    src = base[off:off + span]
+    src.copy_(torch.from_numpy(src_h))
+    ref = ot.pack(src_h)
+    out = mp.pack(dt, src)
+    assert np.array_equal(host(out), ref)
+    for cut in (total, total // 2 + 3):
+        dbase = torch.full((span + 32,), 7, dtype=torch.uint8, device=DEV)
+        dst = dbase[off:off + span]
+        assert mp.unpack(dt, out[:cut], dst) == cut
+        exp = np.full(span, 7, np.uint8)
+        ot.unpack(ref[:cut], exp)
+        got = host(dbase)
+        assert np.array_equal(got[off:off + span], exp)
+        assert (got[:off] == 7).all() and (got[off + span:] == 7).all()
+    iov = ot.iov()
+    assert np.array_equal(host(mp.type_iov_tensor(dt)), iov)
+    assert np.array_equal(host(mp.type_iov_tensor(dt, 17, 100)), iov[17:117])
