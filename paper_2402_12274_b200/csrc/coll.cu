@@ -17,21 +17,30 @@ __device__ __forceinline__ void reduce_one(const T* const* src, T* const* dst, i
     for (int j = 0; j < n; ++j) dst[j][i] = out;
 }
 
-// 16-byte vector form: V = 16 / sizeof(T) elements per access
+// 16-byte vector form: V = 16 / sizeof(T) elements per access.  The loads of
+// up to 8 ranks are issued together (peer loads over NVLink have ~us latency),
+// then summed in rank order -- the reference's x0 + x1 + ... order.
 template <typename T, typename A>
 __device__ __forceinline__ void reduce_vec(const T* const* src, T* const* dst, int n, int64_t v) {
     constexpr int V = 16 / sizeof(T);
+    constexpr int B = 8;
     union U { uint4 q; T e[V]; };
     A acc[V];
-    U u;
-    u.q = __ldg(reinterpret_cast<const uint4*>(src[0]) + v);
 #pragma unroll
-    for (int k = 0; k < V; ++k) acc[k] = (A)u.e[k];
-    for (int j = 1; j < n; ++j) {
-        u.q = __ldg(reinterpret_cast<const uint4*>(src[j]) + v);
+    for (int k = 0; k < V; ++k) acc[k] = (A)0;
+    for (int j0 = 0; j0 < n; j0 += B) {
+        U u[B];
 #pragma unroll
-        for (int k = 0; k < V; ++k) acc[k] += (A)u.e[k];
+        for (int b = 0; b < B; ++b)
+            if (j0 + b < n) u[b].q = __ldg(reinterpret_cast<const uint4*>(src[j0 + b]) + v);
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            if (j0 + b >= n) break;
+#pragma unroll
+            for (int k = 0; k < V; ++k) acc[k] = (j0 + b == 0) ? (A)u[b].e[k] : acc[k] + (A)u[b].e[k];
+        }
     }
+    U u;
 #pragma unroll
     for (int k = 0; k < V; ++k) u.e[k] = (T)acc[k];
     for (int j = 0; j < n; ++j) reinterpret_cast<uint4*>(dst[j])[v] = u.q;
