@@ -304,3 +304,47 @@ def test_gpu_run_table_plans(spec, off):
     iov = ot.iov()
     assert np.array_equal(host(mp.type_iov_tensor(dt)), iov)
     assert np.array_equal(host(mp.type_iov_tensor(dt, 17, 100)), iov[17:117])
+
+
+def test_gpu_pack_unpack_capture_in_cuda_graph():
+    """Once its plan exists, pack/unpack is stream-capture safe: a CUDA graph
+    of the fused multi-face step replays to the same bytes."""
+    specs = [("subarray", [40, 40, 40], [38, 38, 1], [1, 1, 1], ("basic", 4)),
+             ("subarray", [40, 40, 40], [8, 38, 38], [31, 1, 1], ("basic", 4))]
+    dts = [build_product(s, mp) for s in specs]
+    src = dev_bytes(seeded_bytes(41, 40 ** 3 * 4))
+    dst = torch.zeros_like(src)
+    outs = [torch.empty(mp.packed_size(d), dtype=torch.uint8, device=DEV) for d in dts]
+    cfg3 = build_product(cfg3_spec(6, hcount=2, nblocks=32), mp)
+    csrc = dev_bytes(seeded_bytes(42, oracle.OracleType(cfg3_spec(6, hcount=2, nblocks=32)).max_end))
+    cout = torch.empty(mp.packed_size(cfg3), dtype=torch.uint8, device=DEV)
+    cback = torch.zeros_like(csrc)
+
+    def step():
+        mp.pack_multi(dts, [src] * 2, outs)
+        mp.unpack_multi(dts, outs, [dst] * 2)
+        mp.pack_into(cfg3, csrc, cout)
+        mp.unpack(cfg3, cout, cback)
+
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        step()                        # builds and uploads the plans
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            step()
+    ref = [host(o).copy() for o in outs] + [host(cout).copy()]
+    for o in outs + [cout]:
+        o.zero_()
+    dst.zero_()
+    cback.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert all(np.array_equal(host(o), r) for o, r in zip(outs + [cout], ref))
+    exp = np.zeros(40 ** 3 * 4, np.uint8)
+    for spec, r in zip(specs, ref):
+        oracle.OracleType(spec).unpack(r, exp)
+    assert np.array_equal(host(dst), exp)
+    cexp = np.zeros_like(host(csrc))
+    oracle.OracleType(cfg3_spec(6, hcount=2, nblocks=32)).unpack(ref[-1], cexp)
+    assert np.array_equal(host(cback), cexp)
