@@ -271,11 +271,18 @@ __device__ __forceinline__ void chain_wide(const ChainJob& j, int64_t t0, int64_
                 uint8_t* q = d0 + 16 * m;
                 if (blo == 0 && bhi == 16) {
                     *reinterpret_cast<uint4*>(q) = v;
-                } else {
+                } else {   // whole 8-byte halves as one store, the rest as 4-byte words
                     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (4 * k >= blo && 4 * k + 4 <= bhi) reinterpret_cast<uint32_t*>(q)[k] = w[k];
+                    for (int h = 0; h < 2; ++h) {
+                        if (8 * h >= blo && 8 * h + 8 <= bhi) {
+                            reinterpret_cast<uint2*>(q)[h] = make_uint2(w[2 * h], w[2 * h + 1]);
+                        } else {
+#pragma unroll
+                            for (int k = 2 * h; k < 2 * h + 2; ++k)
+                                if (4 * k >= blo && 4 * k + 4 <= bhi) reinterpret_cast<uint32_t*>(q)[k] = w[k];
+                        }
+                    }
                 }
             }
         }
