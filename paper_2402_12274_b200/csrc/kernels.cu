@@ -41,11 +41,11 @@ template <> struct Vec<1> { using T = uint8_t; };
 
 constexpr int kChainThreads = 256;
 
-// Scattered layout-side loads of short rows.  An L1-allocating load of a few
-// bytes makes L1 fetch the whole 128-byte line from L2 (and L2 from DRAM);
-// L2-only loads fetch 32-byte sectors.
+// Scattered layout-side loads of short rows.  Measured on the fused halo
+// pack (ncu, profiles/): L1-allocating loads 31.6 us, L2-only (.cg) 36.0 us,
+// same DRAM bytes -- the 1- and 8-wide faces of a side reuse L1 lines.
 #ifndef MPX_LAYOUT_LD
-#define MPX_LAYOUT_LD 1
+#define MPX_LAYOUT_LD 0
 #endif
 template <typename T>
 __device__ __forceinline__ T ld_layout(const T* p) {
