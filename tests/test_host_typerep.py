@@ -8,6 +8,7 @@ import ctypes
 import os
 import re
 
+import numpy as np
 import pytest
 
 import paper_2402_12274_b200 as mp
@@ -58,6 +59,13 @@ def test_config_plans():
         assert q["plan"] == 1 and not q["overlap"], name
     q = build_product(cfg3_spec(3, hcount=8), mp).layout_query()
     assert q["plan"] == 3 and not q["overlap"]      # span lowering
+    assert q["chain_align"] > 0                     # ... with word-gather specs (k_perm)
+    # irregular indexed blocks (many short runs): the flat run table
+    rng = np.random.default_rng(5)
+    bls = rng.integers(1, 5, 20000)
+    displs = np.cumsum(rng.integers(0, 9, 20000) + np.concatenate([[0], bls[:-1]]))
+    dt = mp.type_indexed([int(x) for x in bls], [int(x) for x in displs], mp.FLOAT64).commit()
+    assert dt.layout_query()["plan"] == 4
 
 
 def test_frozen_examples_host():
