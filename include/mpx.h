@@ -190,6 +190,22 @@ int mpx_stream_device(void *stream, int *device);
 /* optional: path of libnccl.so.2 when it is not already loaded */
 int mpx_nccl_load(const char *path);
 
+/* ---- passive-target read windows (onesided.py) ------------------------- */
+/* win_create (onesided.py:146-163): collective over the communicator's world;
+ * every rank exposes [base, base + bytes) with its own displacement unit;
+ * *win_id = the window number (k-th create of every rank). */
+int mpx_win_create(mpx_comm c, const void *base, int64_t bytes, int64_t disp_unit, int64_t *win_id);
+/* out = {bytes, disp_unit} of `rank`'s region of window win_id */
+int mpx_win_info(mpx_comm c, int64_t win_id, int rank, int64_t out[2]);
+/* Window.get (onesided.py:76-125): tcount x tdt at target displacement
+ * tdisp (in the target's unit) of `target`'s region -> ocount x odt into
+ * `origin`, enqueued on the communicator's stream (the target's device
+ * memory is read directly: passive target).  Signatures must agree. */
+int mpx_win_get(mpx_comm c, int64_t win_id, void *origin, int64_t origin_bytes, int64_t ocount,
+                mpx_datatype odt, int target, int64_t tdisp, int64_t tcount, mpx_datatype tdt);
+/* Window.free (onesided.py:136-144): collective */
+int mpx_win_free(mpx_comm c, int64_t win_id);
+
 #ifdef __cplusplus
 }
 #endif

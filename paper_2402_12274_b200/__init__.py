@@ -7,9 +7,12 @@ the enqueue operations, executed by hand-written sm_100a kernels in
 libmpx.so (C ABI: include/mpx.h).  Buffers are PyTorch CUDA tensors (host
 buffers are accepted and staged through the GPU).
 
+Passive-target read windows (``win_create`` / ``win_get``, onesided.py) read
+peer device memory directly with the same datatype kernels.
+
 Out of scope: socket transport and launcher,
-thread communicators, stream-multiplex communicators, one-sided windows,
-generalized requests, VCI lock studies, the message-rate benchmarks.
+thread communicators, stream-multiplex communicators, generalized requests,
+VCI lock studies, the message-rate benchmarks.
 """
 
 import os as _os
@@ -54,6 +57,11 @@ from .comms import (  # noqa: F401,E402
     send, recv, isend, irecv, wait, test, waitall,
     send_enqueue, recv_enqueue, isend_enqueue, irecv_enqueue,
     wait_enqueue, waitall_enqueue,
+)
+
+from .onesided import (  # noqa: F401,E402
+    Window, LOCK_SHARED, LOCK_EXCLUSIVE,
+    win_create, win_lock, win_unlock, win_get, win_free,
 )
 
 ANY_SOURCE = -1

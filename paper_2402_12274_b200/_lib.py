@@ -72,6 +72,10 @@ _SIGS = {
     "mpx_comm_progress": ([vp, p64], cint),
     "mpx_stream_device": ([vp, ctypes.POINTER(cint)], cint),
     "mpx_nccl_load": ([ctypes.c_char_p], cint),
+    "mpx_win_create": ([vp, vp, i64, i64, p64], cint),
+    "mpx_win_info": ([vp, i64, cint, p64], cint),
+    "mpx_win_get": ([vp, i64, vp, i64, i64, dt_t, cint, i64, i64, dt_t], cint),
+    "mpx_win_free": ([vp, i64], cint),
 }
 
 for _name, (_args, _res) in _SIGS.items():

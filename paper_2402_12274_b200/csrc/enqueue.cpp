@@ -281,6 +281,17 @@ struct World {
     std::condition_variable nccl_cv;
     std::vector<ncclComm_t> nccl;   // per rank, by ncclCommInitAll
     int nccl_state = 0;             // 0 none, 1 building, 2 ready, -1 failed
+    // passive-target read windows (onesided.py): window k = every rank's k-th
+    // mpx_win_create; created / freed collectively
+    struct Win {
+        std::vector<const void*> base;
+        std::vector<int64_t> bytes, unit;
+        int registered = 0, released = 0;
+    };
+    std::mutex win_mu;
+    std::condition_variable win_cv;
+    std::map<int64_t, Win> wins;
+    std::vector<int64_t> next_win;   // per rank
     std::mutex svc_mu;
     std::map<int, cudaStream_t> svc;  // per-device service streams (deferred frees)
     cudaStream_t service(int dev) {
@@ -754,6 +765,7 @@ int mpx_world_join(const char* group, int size, int rank, int device, int64_t ea
         w->devices.assign(size, -1);
         w->joined.assign(size, false);
         for (int i = 0; i < size; ++i) w->mbox.emplace_back(new Mailbox());
+        w->next_win.assign(size, 0);
         int rc = w->flags.init();
         if (rc) {
             delete w;
@@ -1006,6 +1018,115 @@ int mpx_allreduce_enqueue(mpx_comm h, const void* sendbuf, void* recvbuf, int64_
     if (e != cudaSuccess) return cuda_fail(e, "allreduce launch");
     for (CollRing* r : copies) MPX_RC(write_flag(c->stream, &r->finish[slot][c->rank], gen));
     for (int j = 0; j < w->size; ++j) MPX_RC(wait_flag(c->stream, &mine->finish[slot][j], gen));
+    return MPX_SUCCESS;
+}
+
+// ---------------------------------------------------------- read windows
+// onesided.py:146-163 (win_create), :76-125 (get), :136-144 (free).  Every
+// rank of the world exposes [base, base + bytes); a get moves target bytes
+// described by (target_disp * target unit, target type) into the origin
+// layout on the communicator's stream, reading the target's device memory
+// directly (peer access) -- no target-side action, as in the reference's
+// passive target.
+
+int mpx_win_create(mpx_comm h, const void* base, int64_t bytes, int64_t disp_unit, int64_t* win_id) {
+    auto c = comm_of(h);
+    if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
+    if (disp_unit < 1) return fail(MPX_ERR_ARG, "disp_unit must be a positive int");
+    if (bytes < 0 || (bytes > 0 && !base)) return fail(MPX_ERR_ARG, "bad window region");
+    World* w = c->w;
+    std::unique_lock<std::mutex> lk(w->win_mu);
+    const int64_t id = w->next_win[(size_t)c->rank]++;
+    World::Win& win = w->wins[id];
+    if (win.base.empty()) {
+        win.base.assign((size_t)w->size, nullptr);
+        win.bytes.assign((size_t)w->size, 0);
+        win.unit.assign((size_t)w->size, 1);
+    }
+    win.base[(size_t)c->rank] = base;
+    win.bytes[(size_t)c->rank] = bytes;
+    win.unit[(size_t)c->rank] = disp_unit;
+    win.registered++;
+    w->win_cv.notify_all();
+    w->win_cv.wait(lk, [&] { return w->wins[id].registered >= w->size; });   // collective
+    *win_id = id;
+    return MPX_SUCCESS;
+}
+
+// out = {bytes, disp_unit} of `rank`'s region of window `id`
+int mpx_win_info(mpx_comm h, int64_t id, int rank, int64_t out[2]) {
+    auto c = comm_of(h);
+    if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
+    World* w = c->w;
+    std::lock_guard<std::mutex> g(w->win_mu);
+    auto it = w->wins.find(id);
+    if (it == w->wins.end() || rank < 0 || rank >= w->size) return fail(MPX_ERR_ARG, "no such window / rank");
+    out[0] = it->second.bytes[(size_t)rank];
+    out[1] = it->second.unit[(size_t)rank];
+    return MPX_SUCCESS;
+}
+
+int mpx_win_get(mpx_comm h, int64_t id, void* origin, int64_t origin_bytes, int64_t ocount, mpx_datatype odt,
+                int target, int64_t tdisp, int64_t tcount, mpx_datatype tdt) {
+    auto c = comm_of(h);
+    if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
+    World* w = c->w;
+    if (target < 0 || target >= w->size) return fail(MPX_ERR_ARG, "target rank %d out of range", target);
+    Datatype* od = lookup(odt);
+    Datatype* td = lookup(tdt);
+    if (!od || !td) return fail(MPX_ERR_ARG, "bad datatype handle");
+    const void* tbase;
+    int64_t tbytes, tunit;
+    {
+        std::lock_guard<std::mutex> g(w->win_mu);
+        auto it = w->wins.find(id);
+        if (it == w->wins.end()) return fail(MPX_ERR_STATE, "window already freed");
+        tbase = it->second.base[(size_t)target];
+        tbytes = it->second.bytes[(size_t)target];
+        tunit = it->second.unit[(size_t)target];
+    }
+    MPX_RC(check_layout_region(od, ocount, origin_bytes));
+    const int64_t total = td->size * tcount;
+    if (od->size * ocount != total)
+        return fail(MPX_ERR_ARG, "origin and target type signatures disagree (%lld vs %lld bytes)",
+                    (long long)(od->size * ocount), (long long)total);
+    const int64_t off = tdisp * tunit;
+    MPX_RC(check_layout_region(td, tcount, tbytes - off));   // the target's bounds check (_serve_get)
+    if (total == 0) return MPX_SUCCESS;
+    Side s;
+    s.rank = target;
+    s.device = w->devices[(size_t)target];
+    s.dt = td;
+    s.count = tcount;
+    s.buf = const_cast<uint8_t*>(static_cast<const uint8_t*>(tbase)) + off;
+    s.bytes = total;
+    Side r;
+    r.rank = c->rank;
+    r.device = c->device;
+    r.dt = od;
+    r.count = ocount;
+    r.buf = origin;
+    r.bytes = total;
+    MPX_RC(ensure_peer(w, c->device, s.device));
+    MPX_RC(set_device(c->device));
+    return transfer(c->device, c->stream, s, r, total);
+}
+
+int mpx_win_free(mpx_comm h, int64_t id) {
+    auto c = comm_of(h);
+    if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
+    World* w = c->w;
+    std::unique_lock<std::mutex> lk(w->win_mu);
+    auto it = w->wins.find(id);
+    if (it == w->wins.end()) return fail(MPX_ERR_STATE, "window already freed");
+    it->second.released++;
+    w->win_cv.notify_all();
+    w->win_cv.wait(lk, [&] {   // collective (the reference's barrier)
+        auto j = w->wins.find(id);
+        return j == w->wins.end() || j->second.released >= w->size;
+    });
+    w->wins.erase(id);
+    w->win_cv.notify_all();
     return MPX_SUCCESS;
 }
 
