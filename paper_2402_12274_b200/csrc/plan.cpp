@@ -759,10 +759,16 @@ std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStre
         e = cudaMemcpyAsync(dev, host.data(), host.size(), cudaMemcpyHostToDevice, up);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ready, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventRecord(p->ready, up);
+        // Wait for the (private-stream) upload here, once per plan: callers'
+        // streams then never wait on it, and later calls make no event
+        // queries -- so pack / unpack of an existing plan is safe inside
+        // CUDA-graph stream capture, where such queries are refused.
+        if (e == cudaSuccess) e = cudaEventSynchronize(p->ready);
         if (e != cudaSuccess) {
             *err = std::string("descriptor upload: ") + cudaGetErrorString(e);
             return nullptr;
         }
+        p->ready_seen.store(true, std::memory_order_release);
         p->blob_bytes = host.size();
         uint8_t* b = (uint8_t*)dev;
         p->desc.nodes = (const DNode*)b;
