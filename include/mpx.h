@@ -104,6 +104,10 @@ int mpx_packed_size(mpx_datatype dt, int64_t count, int64_t *out);
  *             plan kind (0 empty, 1 chain, 2 descriptor walk, 3 span, 4 run table),
  *             overlap, chain alignment (span plans: word-gather spec count) */
 int mpx_layout_query(mpx_datatype dt, int64_t count, int64_t out[8]);
+/* Host-side span lowering of layout_for(count) as int64 words (plan kind,
+ * outer levels, chunks, word-gather specs and tables) for tests that
+ * emulate the tables on the CPU; *n = words needed. */
+int mpx_plan_dump(mpx_datatype dt, int64_t count, int64_t *out, int64_t cap, int64_t *n);
 
 /* ---- data movement (device buffers, asynchronous on `stream`) ----------- */
 /* pack: datatype.py:695-702 with _checked_view bounds (:680-692).

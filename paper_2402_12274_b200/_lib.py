@@ -51,6 +51,7 @@ _SIGS = {
     "mpx_type_iov": ([dt_t, i64, i64, i64, vp, i64, p64, vp], cint),
     "mpx_packed_size": ([dt_t, i64, p64], cint),
     "mpx_layout_query": ([dt_t, i64, p64], cint),
+    "mpx_plan_dump": ([dt_t, i64, p64, i64, p64], cint),
     "mpx_pack": ([dt_t, i64, vp, i64, vp, i64, vp], cint),
     "mpx_unpack": ([dt_t, i64, vp, i64, vp, i64, p64, vp], cint),
     "mpx_pack_multi": ([cint, pdt, p64, pvp, p64, pvp, p64, vp], cint),

@@ -444,6 +444,38 @@ int mpx_packed_size(mpx_datatype h, int64_t count, int64_t* out) {
     return MPX_SUCCESS;
 }
 
+int mpx_plan_dump(mpx_datatype h, int64_t count, int64_t* out, int64_t cap, int64_t* n) {
+    Datatype* d = lookup(h);
+    int rc = check_count(count, "count");
+    if (rc || (rc = check_usable(d, "query"))) return rc;
+    NodeP lay = d->layout_for(count);
+    Plan p;
+    analyze(lay.get(), &p);
+    std::vector<int64_t> v;
+    v.push_back(p.kind);
+    v.push_back(p.span.outer_depth);
+    for (int i = 0; i < kSpanMaxOuter; ++i) {
+        v.push_back(p.span.outer_cnt[i]);
+        v.push_back(p.span.outer_str[i]);
+        v.push_back(p.span.outer_pk[i]);
+    }
+    v.push_back((int64_t)p.span_chunks.size());
+    for (const auto& c : p.span_chunks) {
+        v.insert(v.end(), {c.src, c.pk, c.span, c.plen, c.n, c.body, c.stride, c.perm[0], c.perm[1]});
+    }
+    v.push_back((int64_t)p.perm_specs.size());
+    for (const auto& sp : p.perm_specs) {
+        v.insert(v.end(), {sp.W, sp.Dw, sp.ns, sp.pad, (int64_t) reinterpret_cast<uintptr_t>(sp.tab)});
+        for (int i = 0; i < 16; ++i) v.push_back(sp.wc[i]);
+    }
+    v.push_back((int64_t)p.perm_tab.size());
+    for (const auto& e : p.perm_tab) v.insert(v.end(), {e.wo4, (int64_t)e.lo, (int64_t)e.hi, (int64_t)e.mix});
+    *n = (int64_t)v.size();
+    if ((int64_t)v.size() > cap) return fail(MPX_ERR_ARG, "plan dump needs %lld words", (long long)v.size());
+    std::copy(v.begin(), v.end(), out);
+    return MPX_SUCCESS;
+}
+
 int mpx_layout_query(mpx_datatype h, int64_t count, int64_t out[8]) {
     Datatype* d = lookup(h);
     int rc = check_count(count, "count");

@@ -93,6 +93,9 @@ static_assert(sizeof(SpanChunk) == 48, "SpanChunk layout");
 constexpr int kPermMaxSlots = 4;     // W <= 128 words per step
 constexpr int kPermMaxSpecs = 16;
 
+// Byte form (PermSpec::pad == 1, bodies whose words spread over > 16 input
+// bytes): wo4 = input offset of byte 0, lo = cover / j as below, hi = int16
+// deltas of bytes 1 and 2, mix = int16 delta of byte 3.
 struct PermEntry {
     int32_t wo4;            // window start: byte offset from the staged input's word 0 (+ step * 4 * Dw)
     uint32_t lo;            // bits 0-15: byte_perm selector over window words (0, 1);
@@ -108,7 +111,7 @@ struct PermSpec {
     int32_t W;              // output words per warp step
     int32_t Dw;             // input words advanced per step
     int32_t ns;             // slots per lane: ceil(max(wc) / 32)
-    int32_t pad;
+    int32_t pad;            // 0: word windows; 1: per-byte gathers (PermEntry byte form)
     const PermEntry* tab;   // [16][W]: per phase variant, the words with a written byte first
     uint8_t wc[16];         // per phase variant: words with a written byte (entries used)
 };

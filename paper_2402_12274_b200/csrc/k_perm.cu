@@ -302,6 +302,20 @@ __device__ __forceinline__ uint8_t* sm_base_dbg() {
 }
 #endif
 
+// byte form: input byte i of the word at shared address w + delta_i
+__device__ __forceinline__ int byte_delta(const Slot& e, int i) {
+    return i == 0 ? 0 : i == 1 ? (int)(int16_t)(e.hi & 0xFFFF) : i == 2 ? (int)(int16_t)(e.hi >> 16)
+                                                                        : (int)(int16_t)(e.mix & 0xFFFF);
+}
+
+// byte form gather; addresses clamped into [lo, hi] (edge steps)
+__device__ __forceinline__ uint32_t gather_bytes(uint32_t w, const Slot& e, uint32_t lo, uint32_t hi) {
+    uint32_t b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) b[i] = lds8(min(max(w + (uint32_t)byte_delta(e, i), lo), hi));
+    return prmt(prmt(b[0], b[1], 0x0040u), prmt(b[2], b[3], 0x0040u), 0x5410u);
+}
+
 __device__ __forceinline__ uint32_t gather_word(uint32_t w, const Slot& e) {
     MPX_CHECK_WIN(w);
     const uint32_t a = prmt(lds32(w), lds32(w + 4), e.lo);
@@ -316,12 +330,13 @@ __device__ __forceinline__ void store_bytes(uint8_t* p, uint32_t r, uint32_t m) 
     if (m & 8) p[3] = (uint8_t)(r >> 24);
 }
 
-template <bool PACK, int NS>
+template <bool PACK, int NS, bool MIXED>
 __device__ __forceinline__ void permute(const PermSpec& S, const Unit& U, uint32_t sbuf, int lane) {
     const int a = (int)(reinterpret_cast<uintptr_t>(U.in) & 15);
     const int ap = a & 3;
     const int po = (int)(reinterpret_cast<uintptr_t>(U.out) & 3);
     const int W = S.W;
+    const bool bytes = MIXED && S.pad != 0;           // per-byte gathers (uniform per chunk)
     const int wc = S.wc[po * 4 + ap];                 // entries (words with a written byte) this phase
     const uint32_t Dw4 = 4u * (uint32_t)S.Dw;
     const uint4* tab = reinterpret_cast<const uint4*>(S.tab) + (po * 4 + ap) * W;
@@ -353,9 +368,14 @@ __device__ __forceinline__ void permute(const PermSpec& S, const Unit& U, uint32
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     if (!((vm >> i) & 1)) continue;
-                    const uint32_t pr = (e[s].lo >> (20 + i)) & 1;
-                    const uint32_t nib = ((pr ? e[s].hi : e[s].lo) >> (4 * i)) & 7;
-                    const int in_off = wb + 8 * (int)pr + 4 * (int)(nib >> 2) + (int)(nib & 3) - ap;
+                    int in_off;
+                    if (bytes) {
+                        in_off = wb + byte_delta(e[s], i) - ap;
+                    } else {
+                        const uint32_t pr = (e[s].lo >> (20 + i)) & 1;
+                        const uint32_t nib = ((pr ? e[s].hi : e[s].lo) >> (4 * i)) & 7;
+                        in_off = wb + 8 * (int)pr + 4 * (int)(nib >> 2) + (int)(nib & 3) - ap;
+                    }
                     if (in_off < U.in_len)
                         reinterpret_cast<uint8_t*>(ow + gw)[i] = (uint8_t)lds8(A + (uint32_t)(in_off + ap));
                 }
@@ -374,7 +394,8 @@ __device__ __forceinline__ void permute(const PermSpec& S, const Unit& U, uint32
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
             if (32 * s >= wc) break;
-            const uint32_t r = gather_word(min(e[s].w + kd, wmax), e[s]);
+            const uint32_t r = bytes ? gather_bytes(e[s].w + kd, e[s], sbuf - kFront, wmax + 15)
+                                     : gather_word(min(e[s].w + kd, wmax), e[s]);
             const int gw = kw + (int)(e[s].lo >> 24);
             const uint32_t cov = (e[s].lo >> 16) & 0xF;
             uint32_t* p = ow + gw;
@@ -399,7 +420,8 @@ __device__ __forceinline__ void permute(const PermSpec& S, const Unit& U, uint32
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
             if (32 * s >= wc) break;
-            const uint32_t r = gather_word(e[s].w + kd, e[s]);
+            const uint32_t r = bytes ? gather_bytes(e[s].w + kd, e[s], 0u, 0xFFFFFFFFu)
+                                     : gather_word(e[s].w + kd, e[s]);
             const uint32_t cov = (e[s].lo >> 16) & 0xF;
             uint32_t* p = ow + kw + (int)(e[s].lo >> 24);
             if (cov == 0xF) *p = r;
@@ -409,7 +431,7 @@ __device__ __forceinline__ void permute(const PermSpec& S, const Unit& U, uint32
     for (; kw < words; kw += W, kd += Dw4) edge(kw, kd);
 }
 
-template <bool PACK, int NS, bool TMA>
+template <bool PACK, int NS, bool TMA, bool MIXED>
 __global__ void __launch_bounds__(kWarps * 32, blocks_per_sm<NS>())
 k_perm(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t limit) {
     extern __shared__ __align__(16) uint8_t sm[];
@@ -447,7 +469,7 @@ k_perm(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__
             }
             pipe.commit();
             pipe.wait(pb ? 1 : 0, cur.flags & 1);
-            if (cur.flags & 1) permute<PACK, NS>(specs[cur.flags >> 8], cur, sbase + pb, lane);
+            if (cur.flags & 1) permute<PACK, NS, MIXED>(specs[cur.flags >> 8], cur, sbase + pb, lane);
             __syncwarp();
             if (!more) break;
             cur = nxt;
@@ -471,7 +493,7 @@ k_perm(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__
             }
             pipe.commit();
             pipe.wait(pb ? 1 : 0, cur.flags & 1);
-            if (cur.flags & 1) permute<PACK, NS>(specs[cur.flags >> 8], cur, sbase + pb, lane);
+            if (cur.flags & 1) permute<PACK, NS, MIXED>(specs[cur.flags >> 8], cur, sbase + pb, lane);
             __syncwarp();
             if (!more) break;
             cur = nxt;
@@ -530,10 +552,19 @@ cudaError_t launch_dir(const Plan& p, const uint8_t* src, uint8_t* dst, int64_t 
     // pack 290 us with TMA vs 299 us with cp.async; unpack -- small packed
     // chunks -- 433 vs 402-415 us, so unpack stays on cp.async.
     const bool tma = PACK && local_device_memory(src, p.device) && !disable_tma();
+    // byte-form specs need the mixed kernel; word-window-only plans get the
+    // leaner one (no byte path compiled in)
+    bool mixed = false;
+    for (const int32_t u : p.perm_use[PACK ? 1 : 0]) mixed = mixed || p.perm_specs[(size_t)(u >> 6)].pad != 0;
 #define MPX_PERM(N)                                                                              \
     do {                                                                                         \
-        if (tma) k_perm<PACK, N, true><<<(unsigned)grid, kWarps * 32, kSmem, stream>>>(p.span, src, dst, limit); \
-        else k_perm<PACK, N, false><<<(unsigned)grid, kWarps * 32, kSmem, stream>>>(p.span, src, dst, limit); \
+        if (mixed) {                                                                             \
+            if (tma) k_perm<PACK, N, true, true><<<(unsigned)grid, kWarps * 32, kSmem, stream>>>(p.span, src, dst, limit); \
+            else k_perm<PACK, N, false, true><<<(unsigned)grid, kWarps * 32, kSmem, stream>>>(p.span, src, dst, limit); \
+        } else {                                                                                 \
+            if (tma) k_perm<PACK, N, true, false><<<(unsigned)grid, kWarps * 32, kSmem, stream>>>(p.span, src, dst, limit); \
+            else k_perm<PACK, N, false, false><<<(unsigned)grid, kWarps * 32, kSmem, stream>>>(p.span, src, dst, limit); \
+        }                                                                                        \
     } while (0)
     switch (ns) {
     case 1: MPX_PERM(1); break;
@@ -564,8 +595,10 @@ cudaError_t preload_perm_kernels() {
     cudaFuncAttributes a;
     cudaError_t e = cudaSuccess, r;
 #define MPX_PRE(PK, N)                                                        \
-    if ((r = attr(k_perm<PK, N, false>, &a)) != cudaSuccess) e = r;           \
-    if ((r = attr(k_perm<PK, N, true>, &a)) != cudaSuccess) e = r
+    if ((r = attr(k_perm<PK, N, false, false>, &a)) != cudaSuccess) e = r;    \
+    if ((r = attr(k_perm<PK, N, true, false>, &a)) != cudaSuccess) e = r;     \
+    if ((r = attr(k_perm<PK, N, false, true>, &a)) != cudaSuccess) e = r;     \
+    if ((r = attr(k_perm<PK, N, true, true>, &a)) != cudaSuccess) e = r
     MPX_PRE(true, 1); MPX_PRE(true, 2); MPX_PRE(true, 3); MPX_PRE(true, 4);
     MPX_PRE(false, 1); MPX_PRE(false, 2); MPX_PRE(false, 3); MPX_PRE(false, 4);
 #undef MPX_PRE

@@ -302,12 +302,34 @@ int64_t floor_div(int64_t a, int64_t b) {   // b > 0
 
 // One table entry from the input offsets r[i] of output bytes i (cov[i]:
 // byte written) at input phase ap; false if the bytes span >= 16 input bytes.
-bool make_entry(const int64_t r[4], const bool cov[4], int ap, PermEntry* en) {
+bool make_entry(const int64_t r[4], const bool cov[4], int ap, PermEntry* en, bool bytes) {
     std::memset(en, 0, sizeof *en);
     int64_t mn = INT64_MAX;
     for (int i = 0; i < 4; ++i)
         if (cov[i]) mn = std::min(mn, ap + r[i]);
     if (mn == INT64_MAX) return true;
+    if (bytes) {   // byte gather: byte 0's offset + int16 deltas of bytes 1-3
+        int64_t first = 0;      // input offset of the first covered byte (may be negative)
+        bool have = false;
+        uint32_t cover = 0;
+        for (int i = 0; i < 4; ++i)
+            if (cov[i]) {
+                if (!have) first = ap + r[i];
+                have = true;
+                cover |= 1u << i;
+            }
+        int64_t d[4];
+        for (int i = 0; i < 4; ++i) {
+            d[i] = cov[i] ? ap + r[i] - first : 0;   // uncovered bytes re-read byte 0's address
+            if (d[i] < INT16_MIN || d[i] > INT16_MAX) return false;
+        }
+        if (first < INT32_MIN || first > INT32_MAX) return false;
+        en->wo4 = (int32_t)first;
+        en->lo = cover << 16;
+        en->hi = ((uint32_t)d[1] & 0xFFFF) | ((uint32_t)d[2] << 16);
+        en->mix = ((uint32_t)d[3] & 0xFFFF) | ((uint32_t)d[0] << 16);
+        return true;
+    }
     const int64_t wo = floor_div(mn, 4);
     if (wo < INT16_MIN || wo > INT16_MAX) return false;
     en->wo4 = (int32_t)(4 * wo);
@@ -355,12 +377,12 @@ int push_variant(std::vector<PermEntry>& var, std::vector<PermEntry>* tab) {
 // Tables for M periods per step (W = M * P words) into `out`; false if a
 // word's input bytes spread over >= 16 bytes.
 bool perm_tables(int64_t Eo, int64_t Ei, int64_t E, int64_t M, const std::vector<int64_t>& map, PermSpec* spec,
-                 std::vector<PermEntry>* out) {
+                 std::vector<PermEntry>* out, bool bytes) {
     const int64_t W = M * E * Eo / 4;
     const int64_t Din = M * E * Ei;      // input bytes per step (multiple of 4)
     spec->W = (int32_t)W;
     spec->Dw = (int32_t)(Din / 4);
-    spec->pad = 0;
+    spec->pad = bytes ? 1 : 0;
     int wcmax = 0;
     for (int po = 0; po < 4; ++po) {
         for (int ap = 0; ap < 4; ++ap) {
@@ -375,7 +397,7 @@ bool perm_tables(int64_t Eo, int64_t Ei, int64_t E, int64_t M, const std::vector
                     cov[i] = map[(size_t)t] >= 0;
                     r[i] = cov[i] ? e * Ei + map[(size_t)t] - Din : 0;
                 }
-                if (!make_entry(r, cov, ap, &var[(size_t)j])) return false;
+                if (!make_entry(r, cov, ap, &var[(size_t)j], bytes)) return false;
             }
             const int wc = push_variant(var, out);
             spec->wc[po * 4 + ap] = (uint8_t)wc;
@@ -399,10 +421,18 @@ bool build_perm(int64_t Eo, int64_t Ei, const std::vector<int64_t>& map, PermSpe
     PermSpec best{};
     std::vector<PermEntry> best_tab;
     double best_eff = -1;
+    // word windows when every output word's bytes lie within 16 input bytes,
+    // else per-byte gathers (structs with wide padding)
+    bool bytes = false;
+    {
+        PermSpec probe{};
+        std::vector<PermEntry> t;
+        if (!perm_tables(Eo, Ei, E, 1, map, &probe, &t, false)) bytes = true;
+    }
     for (int64_t m = 1; m * P <= wmax; ++m) {
         PermSpec sp{};
         std::vector<PermEntry> t;
-        if (!perm_tables(Eo, Ei, E, m, map, &sp, &t)) return false;
+        if (!perm_tables(Eo, Ei, E, m, map, &sp, &t, bytes)) return false;
         const int wc0 = sp.wc[0];
         const double eff = wc0 ? double(wc0) / double(32 * ((wc0 + 31) / 32)) : 0.0;
         if (best_eff < 0 || sp.ns < best.ns || (sp.ns == best.ns && eff > best_eff + 1e-9)) {
@@ -425,31 +455,39 @@ bool build_perm_single(int64_t Eo, const std::vector<int64_t>& map, PermSpec* sp
     const int64_t need = (Eo + 3 + 3) / 4;
     if (need > 32 * kPermMaxSlots) return false;
     const int64_t W = need;
-    spec->W = (int32_t)W;
-    spec->Dw = 0;
-    spec->ns = (int32_t)((W + 31) / 32);
-    spec->pad = 0;
-    spec->tab = reinterpret_cast<const PermEntry*>((uintptr_t)tab->size());
-    int wcmax = 0;
-    for (int po = 0; po < 4; ++po) {
-        for (int ap = 0; ap < 4; ++ap) {
-            std::vector<PermEntry> var((size_t)W);
-            for (int64_t j = 0; j < W; ++j) {
-                int64_t r[4];
-                bool cov[4];
-                for (int i = 0; i < 4; ++i) {
-                    const int64_t q = 4 * j + i - po;
-                    cov[i] = q >= 0 && q < Eo && map[(size_t)q] >= 0;
-                    r[i] = cov[i] ? map[(size_t)q] : 0;
+    auto build = [&](bool bytes, PermSpec* sp, std::vector<PermEntry>* out) {
+        sp->W = (int32_t)W;
+        sp->Dw = 0;
+        sp->pad = bytes ? 1 : 0;
+        int wcmax = 0;
+        for (int po = 0; po < 4; ++po) {
+            for (int ap = 0; ap < 4; ++ap) {
+                std::vector<PermEntry> var((size_t)W);
+                for (int64_t j = 0; j < W; ++j) {
+                    int64_t r[4];
+                    bool cov[4];
+                    for (int i = 0; i < 4; ++i) {
+                        const int64_t q = 4 * j + i - po;
+                        cov[i] = q >= 0 && q < Eo && map[(size_t)q] >= 0;
+                        r[i] = cov[i] ? map[(size_t)q] : 0;
+                    }
+                    if (!make_entry(r, cov, ap, &var[(size_t)j], bytes)) return false;
                 }
-                if (!make_entry(r, cov, ap, &var[(size_t)j])) return false;
+                const int wc = push_variant(var, out);
+                sp->wc[po * 4 + ap] = (uint8_t)wc;
+                wcmax = std::max(wcmax, wc);
             }
-            const int wc = push_variant(var, tab);
-            spec->wc[po * 4 + ap] = (uint8_t)wc;
-            wcmax = std::max(wcmax, wc);
         }
+        sp->ns = (wcmax + 31) / 32;
+        return true;
+    };
+    std::vector<PermEntry> t;
+    if (!build(false, spec, &t)) {   // word windows, else per-byte gathers
+        t.clear();
+        if (!build(true, spec, &t)) return false;
     }
-    spec->ns = (wcmax + 31) / 32;
+    spec->tab = reinterpret_cast<const PermEntry*>((uintptr_t)tab->size());
+    tab->insert(tab->end(), t.begin(), t.end());
     return true;
 }
 
