@@ -348,3 +348,30 @@ def test_gpu_pack_unpack_capture_in_cuda_graph():
     cexp = np.zeros_like(host(csrc))
     oracle.OracleType(cfg3_spec(6, hcount=2, nblocks=32)).unpack(ref[-1], cexp)
     assert np.array_equal(host(cback), cexp)
+
+
+def test_gpu_layouts_beyond_32_bit_indices():
+    """More than 2^31 rows / bytes: the chain kernels' 64-bit index paths and
+    the iov of a > 4 GiB layout, checked against strided torch views."""
+    free, _ = torch.cuda.mem_get_info()
+    if free < (24 << 30):
+        pytest.skip("needs 24 GiB of free device memory")
+    rows = (1 << 31) + 3                                     # > 2^31 rows of 1 byte, stride 2
+    dt = mp.type_vector(rows, 1, 2, mp.BYTE).commit()
+    src = torch.randint(0, 256, (2 * rows,), dtype=torch.uint8, device=DEV)
+    out = torch.empty(rows, dtype=torch.uint8, device=DEV)
+    mp.pack_into(dt, src, out)
+    assert torch.equal(out, src.view(-1, 2)[:, 0])
+    back = torch.zeros_like(src)
+    assert mp.unpack(dt, out, back) == rows
+    assert torch.equal(back.view(-1, 2)[:, 0], out) and not back.view(-1, 2)[:, 1].any()
+    iov = mp.type_iov_tensor(dt, rows - 5, 5).cpu().numpy()
+    assert [tuple(x) for x in iov] == [(2 * (rows - 5 + i), 1) for i in range(5)]
+    del src, out, back
+    # a 4-byte-word layout whose packed offsets pass 2^32
+    n = (1 << 30) + 7
+    dt4 = mp.type_vector(n, 1, 3, mp.INT32).commit()        # packed 4 GiB + 28 B, span 12 GiB
+    src = torch.arange(3 * n, dtype=torch.int32, device=DEV)
+    out = torch.empty(n, dtype=torch.int32, device=DEV)
+    mp.pack_into(dt4, src, out)
+    assert torch.equal(out, src.view(-1, 3)[:, 0])
