@@ -191,6 +191,12 @@ int mpx_comm_synchronize(mpx_comm c);
 int mpx_comm_progress(mpx_comm c, int64_t *outstanding);
 /* device owning a cudaStream_t (for wrapping a raw handle from an Info) */
 int mpx_stream_device(void *stream, int *device);
+/* a new non-blocking stream on `device`, owned by the process (never
+ * destroyed by the library).  The Python layer gives every queue,
+ * communicator and serial context its own: torch's stream pool hands out 32
+ * streams round-robin, and two ranks sharing a stream would park each other
+ * behind their stream-memop waits. */
+int mpx_stream_new(int device, void **stream);
 /* optional: path of libnccl.so.2 when it is not already loaded */
 int mpx_nccl_load(const char *path);
 

@@ -72,6 +72,7 @@ _SIGS = {
     "mpx_comm_synchronize": ([vp], cint),
     "mpx_comm_progress": ([vp, p64], cint),
     "mpx_stream_device": ([vp, ctypes.POINTER(cint)], cint),
+    "mpx_stream_new": ([cint, pvp], cint),
     "mpx_nccl_load": ([ctypes.c_char_p], cint),
     "mpx_win_create": ([vp, vp, i64, i64, p64], cint),
     "mpx_win_info": ([vp, i64, cint, p64], cint),
@@ -95,6 +96,22 @@ def check(rc):
     if rc:
         raise error_for_code(rc, last_error())
     return rc
+
+
+def own_stream(device):
+    """A dedicated CUDA stream (cudaStreamCreateWithFlags, non-blocking) for
+    one rank-side owner: a queue, a communicator or a serial context.  Never
+    one of torch's pooled streams -- torch hands its 32 out round-robin, so
+    two ranks can end up on the SAME stream and one rank's stream-memop wait
+    then parks the other rank's flag write behind it (tools/diag_alias.py).
+    The stream lives as long as the process: the C side may still order work
+    on it after the Python owner is gone, so it is never destroyed under it."""
+    import torch
+    dev = torch.device(device)
+    h = ctypes.c_void_p()
+    check(lib.mpx_stream_new(dev.index if dev.index is not None else torch.cuda.current_device(),
+                             ctypes.byref(h)))
+    return torch.cuda.ExternalStream(h.value, device=dev)
 
 
 def exported_symbols():

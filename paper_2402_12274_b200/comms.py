@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import runtime as _rt
-from ._lib import check, lib
+from ._lib import check, lib, own_stream
 from .datatypes import FLOAT32, FLOAT64, INT32, INT64, Datatype, _host_view
 from .errors import ArgError, MinimpiError, PendingError, StateError, for_status
 
@@ -191,7 +191,7 @@ class Communicator:
         self._device_queue = None
         self.local_stream = stream
         if stream is None:
-            self._stream = torch.cuda.Stream(instance.device)
+            self._stream = own_stream(instance.device)
         else:
             self._stream = stream.torch_stream
         h = ctypes.c_void_p()

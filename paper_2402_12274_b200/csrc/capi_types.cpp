@@ -580,7 +580,10 @@ int launch_zip_move(int dev, Datatype* sd, int64_t scount, const void* src, Data
     auto pd = get_plan(rd, rcount, dev, stream, &err);
     if (!pd) return fail(MPX_ERR_OTHER, "%s", err.c_str());
     if (ps->kind != PLAN_CHAIN || pd->kind != PLAN_CHAIN || pd->overlap) return MPX_ERR_PENDING;
-    cudaError_t e = launch_zip(*ps, *pd, static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), bytes, stream);
+    cudaError_t e = plan_wait(*ps, stream);
+    if (e == cudaSuccess) e = plan_wait(*pd, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "descriptor wait");
+    e = launch_zip(*ps, *pd, static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), bytes, stream);
     if (e != cudaSuccess) return cuda_fail(e, "zipper launch");
     return MPX_SUCCESS;
 }

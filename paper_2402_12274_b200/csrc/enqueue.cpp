@@ -198,6 +198,49 @@ int record_new_event(cudaStream_t s, cudaEvent_t* ev) {
     return MPX_SUCCESS;
 }
 
+// ------------------------------------------------------------ stream pool
+// Communicator side streams come from a per-device pool and go back to it
+// when the communicator dies, so the number of streams alive stays small: the
+// device spreads streams over its CUDA_DEVICE_MAX_CONNECTIONS hardware queues,
+// and two streams sharing a queue are serialised -- a stream parked in a
+// cuStreamWaitValue32 would then also park the stream that is to write the
+// flag.  (The Python layer's queue / communicator streams are torch pool
+// streams kept distinct per owner, _lib.own_stream.)
+class StreamPool {
+  public:
+    cudaError_t acquire(int dev, cudaStream_t* out) {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            auto& f = free_[dev];
+            if (!f.empty()) {
+                *out = f.back();
+                f.pop_back();
+                return cudaSuccess;
+            }
+        }
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (cur != dev) cudaSetDevice(dev);
+        cudaError_t e = cudaStreamCreateWithFlags(out, cudaStreamNonBlocking);
+        if (cur != dev && cur >= 0) cudaSetDevice(cur);
+        return e;
+    }
+    // queued work on a released stream simply runs ahead of its next owner's
+    void release(int dev, cudaStream_t s) {
+        std::lock_guard<std::mutex> g(mu_);
+        free_[dev].push_back(s);
+    }
+
+  private:
+    std::mutex mu_;
+    std::map<int, std::vector<cudaStream_t>> free_;
+};
+
+StreamPool& stream_pool() {
+    static StreamPool* p = new StreamPool();  // never destroyed: outlives late frees
+    return *p;
+}
+
 }  // namespace
 
 struct World;
@@ -311,19 +354,24 @@ struct World {
 
 struct Comm {
     ~Comm() {
-        if (side) {
-            int cur = -1;
-            cudaGetDevice(&cur);
-            cudaSetDevice(device);
-            cudaStreamSynchronize(side);
-            cudaStreamDestroy(side);
-            cudaSetDevice(cur);
-        }
+        if (side) stream_pool().release(device, side);
     }
     World* w = nullptr;
     int rank = 0, ctx = 0, device = 0;
     cudaStream_t stream = nullptr;  // the user's stream
-    cudaStream_t side = nullptr;    // internal, same device
+    cudaStream_t side = nullptr;    // internal, same device; created on first use (side_stream)
+    std::once_flag side_once;
+    cudaError_t side_err = cudaSuccess;
+    // Nonblocking operations run their deferred part here.  Created lazily:
+    // most communicators (conventional / collective contexts) never need
+    // one, and every stream spends one of the device's 32 hardware queues.
+    cudaStream_t side_stream() {
+        std::call_once(side_once, [this] {
+            side_err = stream_pool().acquire(device, &side);
+            if (side_err != cudaSuccess) side = nullptr;
+        });
+        return side;
+    }
     std::mutex err_mu;
     std::deque<std::pair<int, std::string>> deferred;
     std::atomic<int64_t> outstanding{0};
@@ -453,6 +501,7 @@ void fill_status(const std::shared_ptr<ReqState>& q, const Side& mine, int src, 
 int stage_send(const std::shared_ptr<Comm>& c, PendingSend& ps) {
     MPX_RC(set_device(c->device));
     MPX_RC(staging_alloc(c->device, (size_t)ps.s.bytes, c->stream, &ps.staging));
+    MPX_TRACE("staged %lld B", (long long)ps.s.bytes);
     MPX_RC(launch_move(c->device, ps.s.dt, ps.s.count, true, ps.s.buf, ps.staging, ps.s.bytes, c->stream));
     return MPX_SUCCESS;
 }
@@ -500,6 +549,8 @@ int do_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t buf_bytes, 
     auto it = std::find_if(mb.recvs.begin(), mb.recvs.end(), [&](const PendingRecv& pr) {
         return matches(pr.src, pr.tag, pr.ctx, c->rank, tag, c->ctx);
     });
+    MPX_TRACE("send r%d -> %d tag %d %lld B (%s) %s side", c->rank, dest, tag, (long long)s.bytes,
+              eager ? "eager" : "rndv", it == mb.recvs.end() ? "first" : "second");
     if (it == mb.recvs.end()) {
         // --- first side: publish the send -----------------------------------
         PendingSend ps{c->ctx, c->rank, tag, s, eager};
@@ -540,12 +591,13 @@ int do_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t buf_bytes, 
         MPX_RC(stage_send(c, ps));
         cudaEvent_t staged;
         MPX_RC(record_new_event(c->stream, &staged));
-        MPX_CU(cudaStreamWaitEvent(c->side, staged, 0));
-        MPX_CU(cudaStreamWaitEvent(c->side, pr.ev, 0));
-        MPX_RC(launch_move(c->device, pr.r.dt, pr.r.count, false, ps.staging, pr.r.buf, moved, c->side));
+        if (!c->side_stream()) return cuda_fail(c->side_err, "cudaStreamCreate(side)");
+        MPX_CU(cudaStreamWaitEvent(c->side_stream(), staged, 0));
+        MPX_CU(cudaStreamWaitEvent(c->side_stream(), pr.ev, 0));
+        MPX_RC(launch_move(c->device, pr.r.dt, pr.r.count, false, ps.staging, pr.r.buf, moved, c->side_stream()));
         MPX_RC(set_device(c->device));
-        MPX_CU(cudaFreeAsync(ps.staging, c->side));
-        MPX_RC(write_flag(c->side, pr.flag, pr.gen));
+        MPX_CU(cudaFreeAsync(ps.staging, c->side_stream()));
+        MPX_RC(write_flag(c->side_stream(), pr.flag, pr.gen));
         cudaEventDestroy(staged);
     } else if (blocking) {
         MPX_CU(cudaStreamWaitEvent(c->stream, pr.ev, 0));
@@ -554,17 +606,19 @@ int do_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t buf_bytes, 
     } else {
         cudaEvent_t fork;
         MPX_RC(record_new_event(c->stream, &fork));
-        MPX_CU(cudaStreamWaitEvent(c->side, fork, 0));
-        MPX_CU(cudaStreamWaitEvent(c->side, pr.ev, 0));
-        MPX_RC(transfer(c->device, c->side, s, pr.r, moved));
-        MPX_RC(write_flag(c->side, pr.flag, pr.gen));
-        MPX_RC(record_new_event(c->side, &req->done_ev));
+        if (!c->side_stream()) return cuda_fail(c->side_err, "cudaStreamCreate(side)");
+        MPX_CU(cudaStreamWaitEvent(c->side_stream(), fork, 0));
+        MPX_CU(cudaStreamWaitEvent(c->side_stream(), pr.ev, 0));
+        MPX_RC(transfer(c->device, c->side_stream(), s, pr.r, moved));
+        MPX_RC(write_flag(c->side_stream(), pr.flag, pr.gen));
+        MPX_RC(record_new_event(c->side_stream(), &req->done_ev));
         req->needs_wait = true;
         cudaEventDestroy(fork);
     }
     cudaEventDestroy(pr.ev);  // the waits above captured it
     if (req) c->outstanding++;
     if (out_req) *out_req = req;
+    MPX_TRACE("send r%d -> %d issued", c->rank, dest);
     return MPX_SUCCESS;
 }
 
@@ -594,6 +648,7 @@ int do_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t buf_bytes, int64_
     auto it = std::find_if(mb.sends.begin(), mb.sends.end(), [&](const PendingSend& ps) {
         return matches(source, tag, c->ctx, ps.src, ps.tag, ps.ctx);
     });
+    MPX_TRACE("recv r%d <- %d tag %d %s side", c->rank, source, tag, it == mb.sends.end() ? "first" : "second");
     if (it == mb.sends.end()) {
         // --- first side: post the receive ------------------------------------
         PendingRecv pr{c->ctx, source, tag, r};
@@ -631,13 +686,16 @@ int do_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t buf_bytes, int64_
     if (!blocking) {
         cudaEvent_t fork;
         MPX_RC(record_new_event(c->stream, &fork));
-        MPX_CU(cudaStreamWaitEvent(c->side, fork, 0));
+        if (!c->side_stream()) return cuda_fail(c->side_err, "cudaStreamCreate(side)");
+        MPX_CU(cudaStreamWaitEvent(c->side_stream(), fork, 0));
         cudaEventDestroy(fork);
-        st = c->side;
+        st = c->side_stream();
     }
     MPX_CU(cudaStreamWaitEvent(st, ps.ev, 0));
+    MPX_TRACE("recv r%d second side on %s stream", c->rank, blocking ? "user" : "side");
     if (ps.eager) {
         MPX_RC(consume_staging(w, c->device, st, ps, r, moved));
+        MPX_TRACE("recv r%d consumed staging", c->rank);
     } else {
         MPX_RC(transfer(c->device, st, ps.s, r, moved));
         MPX_RC(write_flag(st, ps.flag, ps.gen));
@@ -650,6 +708,7 @@ int do_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t buf_bytes, int64_
     }
     cudaEventDestroy(ps.ev);
     if (out_req) *out_req = req;
+    MPX_TRACE("recv r%d issued", c->rank);
     return MPX_SUCCESS;
 }
 
@@ -815,8 +874,7 @@ int mpx_comm_create(mpx_world h, int rank, int ctx, void* stream, mpx_comm* out)
     c->ctx = ctx;
     c->device = dev;
     c->stream = reinterpret_cast<cudaStream_t>(stream);
-    cudaError_t e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate(side)");
+    // the side stream is created on first use (Comm::side_stream)
     {   // ring index of this context (the same in every device's area)
         std::lock_guard<std::mutex> g(w->coll_mu);
         auto it = w->ring_index.find(ctx);
@@ -944,6 +1002,22 @@ int mpx_comm_progress(mpx_comm h, int64_t* outstanding) {
 
 int mpx_stream_device(void* stream, int* device) {
     MPX_CU(cudaStreamGetDevice(reinterpret_cast<cudaStream_t>(stream), device));
+    return MPX_SUCCESS;
+}
+
+int mpx_stream_new(int device, void** stream) {
+    if (!stream) return fail(MPX_ERR_ARG, "null output pointer");
+    int ndev = 0;
+    MPX_CU(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(MPX_ERR_ARG, "device %d out of range", device);
+    int cur = -1;
+    MPX_CU(cudaGetDevice(&cur));
+    if (cur != device) MPX_CU(cudaSetDevice(device));
+    cudaStream_t st = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (cur != device) cudaSetDevice(cur);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+    *stream = st;
     return MPX_SUCCESS;
 }
 

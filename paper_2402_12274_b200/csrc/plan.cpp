@@ -31,8 +31,19 @@ Plan::~Plan() {
     }
 }
 
+// Order `stream` after the plan's descriptor upload.  The host never blocks
+// on the upload: another rank of this process may hold a stream parked in a
+// stream-memop wait that this very call is about to release, and a host wait
+// on GPU work could then stall behind it (hardware queues are shared once a
+// process has more streams than CUDA_DEVICE_MAX_CONNECTIONS).
 cudaError_t plan_wait(Plan& p, cudaStream_t stream) {
     if (!p.ready || p.ready_seen.load(std::memory_order_acquire)) return cudaSuccess;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaError_t ce = cudaStreamIsCapturing(stream, &cs);
+    if (ce != cudaSuccess) return ce;
+    // inside stream capture no event may be queried: the graph waits on the
+    // (long completed) upload event as an external dependency
+    if (cs != cudaStreamCaptureStatusNone) return cudaStreamWaitEvent(stream, p.ready, cudaEventWaitExternal);
     cudaError_t q = cudaEventQuery(p.ready);
     if (q == cudaSuccess) {
         p.ready_seen.store(true, std::memory_order_release);
@@ -794,19 +805,15 @@ std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStre
         p->blob = dev;
         // pageable source: the call returns once the bytes are staged, so the
         // host vector may die; only the (private) upload stream is involved
+        MPX_TRACE("plan upload %zu B", host.size());
         e = cudaMemcpyAsync(dev, host.data(), host.size(), cudaMemcpyHostToDevice, up);
+        MPX_TRACE("plan upload issued");
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ready, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventRecord(p->ready, up);
-        // Wait for the (private-stream) upload here, once per plan: callers'
-        // streams then never wait on it, and later calls make no event
-        // queries -- so pack / unpack of an existing plan is safe inside
-        // CUDA-graph stream capture, where such queries are refused.
-        if (e == cudaSuccess) e = cudaEventSynchronize(p->ready);
         if (e != cudaSuccess) {
             *err = std::string("descriptor upload: ") + cudaGetErrorString(e);
             return nullptr;
         }
-        p->ready_seen.store(true, std::memory_order_release);
         p->blob_bytes = host.size();
         uint8_t* b = (uint8_t*)dev;
         p->desc.nodes = (const DNode*)b;

@@ -12,6 +12,25 @@
 #include "desc.cuh"
 #include "typerep.hpp"
 
+#include <cstdio>
+#include <cstdlib>
+#include <thread>
+
+// MPX_TRACE=1: host-side progress markers on stderr (diagnosing stalls)
+inline bool mpx_tracing() {
+    static const bool on = std::getenv("MPX_TRACE") != nullptr;
+    return on;
+}
+#define MPX_TRACE(...)                                                                        \
+    do {                                                                                      \
+        if (mpx_tracing()) {                                                                  \
+            std::fprintf(stderr, "[mpx %zx] ", std::hash<std::thread::id>()(std::this_thread::get_id()) & 0xffff); \
+            std::fprintf(stderr, __VA_ARGS__);                                                \
+            std::fputc('\n', stderr);                                                         \
+            std::fflush(stderr);                                                              \
+        }                                                                                     \
+    } while (0)
+
 namespace mpx {
 
 enum PlanKind : int32_t { PLAN_EMPTY = 0, PLAN_CHAIN = 1, PLAN_GENERIC = 2, PLAN_SPAN = 3, PLAN_RUNS = 4 };

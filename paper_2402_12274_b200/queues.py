@@ -15,6 +15,7 @@ import threading
 import torch
 
 from .errors import ArgError, MinimpiError, StateError
+from ._lib import own_stream
 
 _QUEUES = {}
 _lock = threading.Lock()
@@ -28,7 +29,7 @@ class DeviceQueue:
             device = instance.device if instance is not None else torch.device(
                 "cuda", torch.cuda.current_device())
         self.instance = instance
-        self.torch_stream = stream if stream is not None else torch.cuda.Stream(device)
+        self.torch_stream = stream if stream is not None else own_stream(device)
         self.device = self.torch_stream.device
         self.handle = "%016x" % self.torch_stream.cuda_stream
         self.destroyed = False

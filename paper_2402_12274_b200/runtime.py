@@ -21,7 +21,7 @@ import threading
 
 import torch
 
-from ._lib import check, lib
+from ._lib import check, lib, own_stream
 from .errors import ArgError, ExhaustedError, PendingError, StateError, UnsupportedError
 
 TRANSPORT_INPROC = "inproc"
@@ -262,7 +262,7 @@ class Instance:
                 raise ExhaustedError("VCI pool exhausted (%d in use)" % self.pool_capacity)
             self._pool_in_use += 1
             self.next_stream_id += 1
-            return Stream(sid, SERIAL_CONTEXT, self, torch.cuda.Stream(self.device))
+            return Stream(sid, SERIAL_CONTEXT, self, own_stream(self.device))
         if kind_val == "devstream":
             from .queues import queue_from_hex
             q = queue_from_hex(info.get("value"))

@@ -61,6 +61,30 @@ def on_s():
 ok = ok and probe("kernel on s (behind wait)", on_s)
 ok = ok and probe("kernel on s2 after that", on_s2)
 ok = ok and probe("torch.empty 64MB", lambda: torch.empty(64 << 20, dtype=torch.uint8, device=dev))
+from cuda.bindings import runtime as cr
+def new_stream():
+    err, h = cr.cudaStreamCreateWithFlags(1)
+    assert err == cr.cudaError_t.cudaSuccess, err
+    return torch.cuda.ExternalStream(int(h), device=dev)
+ok = ok and probe("cudaStreamCreate (new stream)", new_stream)
+ok = ok and probe("cudaEventCreate", lambda: cr.cudaEventCreate())
+def on_new():
+    ns = new_stream()
+    with torch.cuda.stream(ns):
+        torch.arange(1000, device=dev).mul_(2)
+    ev = torch.cuda.Event()
+    ev.record(ns)
+    ns.synchronize()
+ok = ok and probe("kernel on a NEW stream (+ its sync)", on_new)
+def wait_on_new():
+    ns = new_stream()
+    e = torch.cuda.Event()
+    e.record(s2)
+    ns.wait_event(e)
+    with torch.cuda.stream(ns):
+        torch.arange(1000, device=dev).mul_(2)
+    ns.synchronize()
+ok = ok and probe("event wait + kernel on a NEW stream", wait_on_new)
 print("releasing flag", flush=True)
 if mode == "host":
     flag[0] = 1
