@@ -197,6 +197,9 @@ int mpx_stream_device(void *stream, int *device);
  * streams round-robin, and two ranks sharing a stream would park each other
  * behind their stream-memop waits. */
 int mpx_stream_new(int device, void **stream);
+/* diagnostics (with MPX_TRACE set): print every recorded stream wait whose
+ * flag has not been written yet; returns how many */
+int mpx_debug_flags(void);
 /* optional: path of libnccl.so.2 when it is not already loaded */
 int mpx_nccl_load(const char *path);
 

@@ -73,6 +73,7 @@ _SIGS = {
     "mpx_comm_progress": ([vp, p64], cint),
     "mpx_stream_device": ([vp, ctypes.POINTER(cint)], cint),
     "mpx_stream_new": ([cint, pvp], cint),
+    "mpx_debug_flags": ([], cint),
     "mpx_nccl_load": ([ctypes.c_char_p], cint),
     "mpx_win_create": ([vp, vp, i64, i64, p64], cint),
     "mpx_win_info": ([vp, i64, cint, p64], cint),

@@ -122,8 +122,23 @@ int memop_fail(CUresult r, const char* what) {
     return fail(MPX_ERR_OTHER, "%s: %s", what, m ? m : "driver error");
 }
 
+// MPX_TRACE: every stream wait on a flag is remembered, so a stalled run can
+// list the waits whose flag was never written (mpx_debug_flags)
+struct FlagWait {
+    cudaStream_t s;
+    uint32_t* addr;
+    uint32_t gen;
+};
+std::mutex g_waits_mu;
+std::vector<FlagWait> g_waits;
+
 int wait_flag(cudaStream_t s, uint32_t* addr, uint32_t gen) {
     if (!memops().wait) return fail(MPX_ERR_UNSUPPORTED, "cuStreamWaitValue32 unavailable");
+    if (mpx_tracing()) {
+        std::lock_guard<std::mutex> g(g_waits_mu);
+        g_waits.push_back({s, addr, gen});
+        MPX_TRACE("wait stream %p flag %p >= %u", (void*)s, (void*)addr, gen);
+    }
     CUresult r = memops().wait(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), gen,
                                CU_STREAM_WAIT_VALUE_GEQ);
     return r == CUDA_SUCCESS ? MPX_SUCCESS : memop_fail(r, "cuStreamWaitValue32");
@@ -138,6 +153,7 @@ int write_ptr(cudaStream_t s, const void* const* addr, const void* value) {
 
 int write_flag(cudaStream_t s, uint32_t* addr, uint32_t gen) {
     if (!memops().write) return fail(MPX_ERR_UNSUPPORTED, "cuStreamWriteValue32 unavailable");
+    MPX_TRACE("write stream %p flag %p = %u", (void*)s, (void*)addr, gen);
     CUresult r = memops().write(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), gen,
                                 CU_STREAM_WRITE_VALUE_DEFAULT);
     return r == CUDA_SUCCESS ? MPX_SUCCESS : memop_fail(r, "cuStreamWriteValue32");
@@ -1019,6 +1035,21 @@ int mpx_stream_new(int device, void** stream) {
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
     *stream = st;
     return MPX_SUCCESS;
+}
+
+int mpx_debug_flags(void) {
+    std::lock_guard<std::mutex> g(mpx::g_waits_mu);
+    int n = 0;
+    for (const auto& w : mpx::g_waits) {
+        const uint32_t v = *reinterpret_cast<volatile uint32_t*>(w.addr);
+        if (v < w.gen) {
+            std::fprintf(stderr, "[mpx] unmet wait: stream %p flag %p = %u < %u (stream %s)\n", (void*)w.s,
+                         (void*)w.addr, v, w.gen, cudaStreamQuery(w.s) == cudaSuccess ? "idle" : "busy");
+            n++;
+        }
+    }
+    std::fprintf(stderr, "[mpx] %zu waits recorded, %d unmet\n", mpx::g_waits.size(), n);
+    return n;
 }
 
 int mpx_nccl_load(const char* path) {
