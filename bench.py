@@ -11,8 +11,10 @@ written per second (pack: 2 x face bytes, unpack: 2 x face bytes).
 
 N > 1 runs under torchrun, one process per GPU, each rank an independent
 replica (pack/unpack do not shard; "scaling": "weak").  L2 (126 MB) is
-flushed between timed steps by writing a 256 MiB buffer outside the timed
-events.  --impl reference times the CPU oracle port of the reference
+flushed between timed steps outside the timed events: a 256 MiB buffer is
+written, then a second 256 MiB buffer is read, so the timed kernels find L2
+cold AND clean (no write-back of the flush's dirty lines inside the timing).
+--impl reference times the CPU oracle port of the reference
 algorithm (oracle/liboracle.so) on the host cores over the same faces.
 """
 
@@ -233,12 +235,30 @@ def reference_arm(args):
 # ------------------------------------------------------------- extras
 
 
+class L2Flush:
+    """Write a 256 MiB buffer (> the 126 MB L2), then read another one: L2
+    ends up holding only clean lines of a buffer the timed work never
+    touches.  A write-only flush leaves ~126 MB of dirty lines whose
+    write-back would land inside the next timed kernel."""
+
+    def __init__(self, dev):
+        import torch
+        self.w = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        self.r = torch.zeros(32 << 20, dtype=torch.int64, device=dev)
+        self.clean = os.environ.get("MPX_FLUSH", "clean") == "clean"
+
+    def __call__(self):
+        self.w.zero_()
+        if self.clean:
+            self.r.max()
+
+
 def _time_launch(fn, flush, reps):
     import torch
     fn()
     ts = []
     for _ in range(reps):
-        flush.zero_()
+        flush()
         torch.cuda._sleep(100000)   # GPU busy while the host enqueues: no launch gap inside the events
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
@@ -321,7 +341,7 @@ def gpu_arm(args):
     dst = torch.zeros_like(arr)
     packed = [torch.empty(face_bytes(s), dtype=torch.uint8, device=dev) for _, s in faces]
     packed_host = [torch.empty(p.numel(), dtype=torch.uint8).pin_memory() for p in packed]
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = L2Flush(dev)
     stream = torch.cuda.current_stream(dev)
 
     def step():
@@ -333,7 +353,7 @@ def gpu_arm(args):
     torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        flush.zero_()
+        flush()
         step()
     torch.cuda.synchronize()
 
@@ -345,8 +365,8 @@ def gpu_arm(args):
     torch.cuda.synchronize()
     sampler.start()
     for i in range(args.steps):
-        flush.zero_()                     # L2 flush, outside the timed events
-        torch.cuda._sleep(50000)          # keep the device busy while the host enqueues the step
+        flush()                           # L2 flush, outside the timed events
+        torch.cuda._sleep(int(os.environ.get("MPX_BENCH_SLEEP", "400000")))  # ~0.2 ms: the host enqueues the whole step before event a runs
         a, b, c = ev[i]
         a.record(stream)
         mp.pack_multi(dts, [arr] * len(dts), packed)
@@ -413,7 +433,7 @@ def gpu_arm(args):
         for _ in range(max(1, args.warmup)):
             fn()
         for a, b in evs:
-            flush.zero_()
+            flush()
             a.record(stream)
             fn()
             b.record(stream)
@@ -457,7 +477,7 @@ def gpu_arm(args):
             "data": "synthetic (seeded PCG64 bytes, 514^3 f32 array)",
             "config": {"workload": WORKLOAD, "array_bytes": ARRAY_BYTES,
                        "payload_bytes_per_step": step_bytes(),
-                       "l2": "flushed between steps (256 MiB write outside the timed events)",
+                       "l2": "flushed between steps outside the timed events (256 MiB write, then 256 MiB read: L2 cold and clean)" if flush.clean else "flushed between steps (256 MiB write outside the timed events)",
                        "parallelism": "replicas x%d" % world},
             "pack_ms": round(pk, 4), "unpack_ms": round(uk, 4),
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": round(achieved, 1),

@@ -131,8 +131,29 @@ struct FlagWait {
 };
 std::mutex g_waits_mu;
 std::vector<FlagWait> g_waits;
+struct SideOp {            // a second-side transfer: runs on `side` after both events
+    cudaStream_t side;
+    cudaEvent_t fork;
+    cudaStream_t fork_on;
+    cudaEvent_t peer;
+    cudaStream_t peer_on;
+    uint32_t* flag;        // written when the transfer is done
+    int rank;
+};
+std::vector<SideOp> g_sideops;
+void note_side(const SideOp& o) {
+    std::lock_guard<std::mutex> g(g_waits_mu);
+    g_sideops.push_back(o);
+}
 
 int wait_flag(cudaStream_t s, uint32_t* addr, uint32_t gen) {
+    // MPX_SPIN_WAIT=1 (diagnosis): poll the flag from a one-warp kernel
+    // instead of parking the stream in cuStreamWaitValue32
+    static const bool spin = std::getenv("MPX_SPIN_WAIT") != nullptr;
+    if (spin) {
+        cudaError_t e = launch_flag_wait(addr, gen, s);
+        return e == cudaSuccess ? MPX_SUCCESS : cuda_fail(e, "flag wait kernel");
+    }
     if (!memops().wait) return fail(MPX_ERR_UNSUPPORTED, "cuStreamWaitValue32 unavailable");
     if (mpx_tracing()) {
         std::lock_guard<std::mutex> g(g_waits_mu);
@@ -629,9 +650,10 @@ int do_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t buf_bytes, 
         MPX_RC(write_flag(c->side_stream(), pr.flag, pr.gen));
         MPX_RC(record_new_event(c->side_stream(), &req->done_ev));
         req->needs_wait = true;
-        cudaEventDestroy(fork);
+        if (mpx_tracing()) note_side({c->side_stream(), fork, c->stream, pr.ev, pr.r.comm->stream, pr.flag, c->rank});
+        else cudaEventDestroy(fork);
     }
-    cudaEventDestroy(pr.ev);  // the waits above captured it
+    if (!mpx_tracing()) cudaEventDestroy(pr.ev);  // the waits above captured it
     if (req) c->outstanding++;
     if (out_req) *out_req = req;
     MPX_TRACE("send r%d -> %d issued", c->rank, dest);
@@ -704,7 +726,8 @@ int do_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t buf_bytes, int64_
         MPX_RC(record_new_event(c->stream, &fork));
         if (!c->side_stream()) return cuda_fail(c->side_err, "cudaStreamCreate(side)");
         MPX_CU(cudaStreamWaitEvent(c->side_stream(), fork, 0));
-        cudaEventDestroy(fork);
+        if (mpx_tracing() && !ps.eager) note_side({c->side_stream(), fork, c->stream, ps.ev, ps.s.comm->stream, ps.flag, c->rank});
+        else cudaEventDestroy(fork);
         st = c->side_stream();
     }
     MPX_CU(cudaStreamWaitEvent(st, ps.ev, 0));
@@ -722,7 +745,7 @@ int do_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t buf_bytes, int64_
         req->needs_wait = true;
         c->outstanding++;
     }
-    cudaEventDestroy(ps.ev);
+    if (!mpx_tracing()) cudaEventDestroy(ps.ev);
     if (out_req) *out_req = req;
     MPX_TRACE("recv r%d issued", c->rank);
     return MPX_SUCCESS;
@@ -1049,6 +1072,26 @@ int mpx_debug_flags(void) {
         }
     }
     std::fprintf(stderr, "[mpx] %zu waits recorded, %d unmet\n", mpx::g_waits.size(), n);
+    auto q = [](cudaEvent_t e) { return cudaEventQuery(e) == cudaSuccess ? "done" : "PENDING"; };
+    for (const auto& o : mpx::g_sideops) {
+        const uint32_t v = *reinterpret_cast<volatile uint32_t*>(o.flag);
+        std::fprintf(stderr, "[mpx] side op r%d on %p -> flag %p (=%u): fork@%p %s, peer@%p %s, side %s\n", o.rank,
+                     (void*)o.side, (void*)o.flag, v, (void*)o.fork_on, q(o.fork), (void*)o.peer_on, q(o.peer),
+                     cudaStreamQuery(o.side) == cudaSuccess ? "idle" : "busy");
+    }
+    std::lock_guard<std::mutex> gw(mpx::g_worlds_mu);
+    for (auto& kv : mpx::g_worlds) {
+        for (size_t r = 0; r < kv.second->mbox.size(); ++r) {
+            auto& mb = *kv.second->mbox[r];
+            std::lock_guard<std::mutex> gm(mb.mu);
+            for (auto& ps : mb.sends)
+                std::fprintf(stderr, "[mpx] world %s rank %zu: unmatched send from %d tag %d flag %p gen %u\n",
+                             kv.first.c_str(), r, ps.src, ps.tag, (void*)ps.flag, ps.gen);
+            for (auto& pr : mb.recvs)
+                std::fprintf(stderr, "[mpx] world %s rank %zu: unmatched recv from %d tag %d flag %p gen %u\n",
+                             kv.first.c_str(), r, pr.src, pr.tag, (void*)pr.flag, pr.gen);
+        }
+    }
     return n;
 }
 

@@ -862,6 +862,8 @@ cudaError_t launch_generic(const Plan& p, bool pack, const uint8_t* src, uint8_t
 // With CUDA lazy module loading, the first launch of a kernel loads its module
 // and that load waits behind any stream parked in a stream-memop wait (even on
 // other streams): a rank's first pack could then deadlock against a peer.
+__global__ void k_flag_wait(const uint32_t* flag, uint32_t gen);
+
 cudaError_t preload_pack_kernels() {
     cudaFuncAttributes a;
     cudaError_t e = cudaSuccess, r;
@@ -876,6 +878,7 @@ cudaError_t preload_pack_kernels() {
     if ((r = cudaFuncGetAttributes(&a, k_span<true>)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_span<false>)) != cudaSuccess) e = r;
     if ((r = preload_perm_kernels()) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_flag_wait)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_zip<16>)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_zip<8>)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_zip<4>)) != cudaSuccess) e = r;
@@ -944,6 +947,22 @@ cudaError_t launch_runs(const Plan& p, bool pack, const uint8_t* src, uint8_t* d
         }
     }
 #undef MPX_RUNS
+    return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(32) k_flag_wait(const uint32_t* flag, uint32_t gen) {
+    if (threadIdx.x != 0) return;
+    const volatile uint32_t* f = flag;
+    unsigned ns = 64;
+    while (*f < gen) {
+        __nanosleep(ns);
+        ns = ns < 2048 ? 2 * ns : ns;
+    }
+    __threadfence_system();
+}
+
+cudaError_t launch_flag_wait(const uint32_t* flag, uint32_t gen, cudaStream_t stream) {
+    k_flag_wait<<<1, 32, 0, stream>>>(flag, gen);
     return cudaGetLastError();
 }
 

@@ -55,6 +55,9 @@ cudaError_t launch_iov(const Plan& p, int64_t k0, int64_t n, int64_t* out, cudaS
 cudaError_t launch_perm(const Plan& p, bool pack, const uint8_t* src, uint8_t* dst, int64_t limit,
                         cudaStream_t stream);
 // force-load the pack/unpack/iov kernels on the current device (lazy loading)
+// one warp polls *flag >= gen (volatile, nanosleep back-off): a stream wait
+// that occupies one CTA slot instead of the stream's host-interface channel
+cudaError_t launch_flag_wait(const uint32_t* flag, uint32_t gen, cudaStream_t stream);
 cudaError_t preload_pack_kernels();
 cudaError_t preload_perm_kernels();
 int sm_count(int device);
