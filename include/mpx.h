@@ -123,7 +123,12 @@ int mpx_unpack(mpx_datatype dt, int64_t count, const void *src, int64_t src_byte
 /* Batched forms: n independent pack (unpack) operations fused into as few
  * launches as possible (one launch for up to 16 strided layouts, e.g. the
  * six faces of a halo exchange).  B200 extension; no reference equivalent
- * beyond calling pack/unpack n times. */
+ * beyond calling pack/unpack n times.  The n operations run concurrently:
+ * unpack destinations of different operations must be disjoint or carry the
+ * same bytes where they overlap (as in the halo bench, whose 1-wide faces lie
+ * inside the 8-wide faces); with conflicting overlaps which value survives
+ * is unspecified, as for concurrent MPI receives into overlapping buffers.
+ * Overlaps WITHIN one layout keep the reference's last-writer-wins order. */
 int mpx_pack_multi(int n, const mpx_datatype *dts, const int64_t *counts,
                    const void *const *srcs, const int64_t *src_bytes,
                    void *const *dsts, const int64_t *dst_bytes, void *stream);

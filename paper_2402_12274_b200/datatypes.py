@@ -516,7 +516,10 @@ def pack_multi(dts, bufs, outs, counts=None):
 
 
 def unpack_multi(dts, datas, bufs, counts=None):
-    """Fused unpack counterpart of pack_multi."""
+    """Fused unpack counterpart of pack_multi.  The unpacks run concurrently:
+    destinations of different layouts must be disjoint or agree where they
+    overlap (include/mpx.h); overlaps within one layout are last-writer-wins
+    as in unpack."""
     counts = counts or [1] * len(dts)
     check(_multi(lib.mpx_unpack_multi, dts, counts, datas, bufs))
 
