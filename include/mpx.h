@@ -196,12 +196,19 @@ int mpx_comm_synchronize(mpx_comm c);
 int mpx_comm_progress(mpx_comm c, int64_t *outstanding);
 /* device owning a cudaStream_t (for wrapping a raw handle from an Info) */
 int mpx_stream_device(void *stream, int *device);
-/* a new non-blocking stream on `device`, owned by the process (never
- * destroyed by the library).  The Python layer gives every queue,
+/* a non-blocking stream on `device` for the caller alone, owned by the
+ * process (never destroyed by the library); taken from the streams libmpx
+ * creates ahead of time at world join (creating a stream while another
+ * rank's stream is parked in a memop wait can stall in the driver).  The Python layer gives every queue,
  * communicator and serial context its own: torch's stream pool hands out 32
  * streams round-robin, and two ranks sharing a stream would park each other
  * behind their stream-memop waits. */
 int mpx_stream_new(int device, void **stream);
+/* block the calling host thread until all work queued on `stream` is done,
+ * polling cudaStreamQuery (never cudaStreamSynchronize: a thread blocked in
+ * it on a stream parked by a peer rank was seen to stall the enqueue calls
+ * of the other rank threads that would release it) */
+int mpx_stream_wait(void *stream);
 /* diagnostics (with MPX_TRACE set): print every recorded stream wait whose
  * flag has not been written yet; returns how many */
 int mpx_debug_flags(void);

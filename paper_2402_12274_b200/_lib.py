@@ -73,6 +73,7 @@ _SIGS = {
     "mpx_comm_progress": ([vp, p64], cint),
     "mpx_stream_device": ([vp, ctypes.POINTER(cint)], cint),
     "mpx_stream_new": ([cint, pvp], cint),
+    "mpx_stream_wait": ([vp], cint),
     "mpx_debug_flags": ([], cint),
     "mpx_nccl_load": ([ctypes.c_char_p], cint),
     "mpx_win_create": ([vp, vp, i64, i64, p64], cint),
@@ -113,6 +114,12 @@ def own_stream(device):
     check(lib.mpx_stream_new(dev.index if dev.index is not None else torch.cuda.current_device(),
                              ctypes.byref(h)))
     return torch.cuda.ExternalStream(h.value, device=dev)
+
+
+def stream_wait(ts):
+    """Host-wait for a torch stream through libmpx's polling wait (see
+    mpx_stream_wait); the GIL is released while waiting."""
+    check(lib.mpx_stream_wait(ts.cuda_stream))
 
 
 def exported_symbols():

@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import runtime as _rt
-from ._lib import check, lib, own_stream
+from ._lib import check, lib, own_stream, stream_wait
 from .datatypes import FLOAT32, FLOAT64, INT32, INT64, Datatype, _host_view
 from .errors import ArgError, MinimpiError, PendingError, StateError, for_status
 
@@ -122,7 +122,7 @@ class Request:
     def _complete(self):
         if self.complete:
             return
-        self.comm._stream.synchronize()
+        stream_wait(self.comm._stream)
         self.status = _status_of(self._h)
         if self._finish is not None:
             self._finish()
@@ -613,6 +613,6 @@ def allreduce(comm, sendbuf, recvbuf, count, dtype, op=SUM, algo=None):
     c = comm if comm._device_queue is None else comm
     check(lib.mpx_allreduce_enqueue(c._h, s.data_ptr(), r.data_ptr(), count, code, 0,
                                     _ALGOS.get(algo, 0)))
-    comm._stream.synchronize()
+    stream_wait(comm._stream)
     if finish is not None:
         finish()

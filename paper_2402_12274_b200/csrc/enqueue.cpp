@@ -28,6 +28,11 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <execinfo.h>
+#include <signal.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+#include <time.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -255,12 +260,35 @@ class StreamPool {
                 return cudaSuccess;
             }
         }
+        MPX_TRACE("stream pool of device %d empty: creating a stream on the data path", dev);
         int cur = -1;
         cudaGetDevice(&cur);
         if (cur != dev) cudaSetDevice(dev);
         cudaError_t e = cudaStreamCreateWithFlags(out, cudaStreamNonBlocking);
         if (cur != dev && cur >= 0) cudaSetDevice(cur);
         return e;
+    }
+    // Top the device's free list up to n streams.  Called at world join:
+    // creating a stream can stall inside the driver (holding a lock that
+    // cudaEventCreate also takes) while another rank's stream is parked in a
+    // memop wait -- measured, with native backtraces -- so streams are made
+    // ahead of time, never on the data path.
+    cudaError_t reserve(int dev, size_t n) {
+        for (;;) {
+            {
+                std::lock_guard<std::mutex> g(mu_);
+                if (free_[dev].size() >= n) return cudaSuccess;
+            }
+            int cur = -1;
+            cudaGetDevice(&cur);
+            if (cur != dev) cudaSetDevice(dev);
+            cudaStream_t s = nullptr;
+            cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+            if (cur != dev && cur >= 0) cudaSetDevice(cur);
+            if (e != cudaSuccess) return e;
+            std::lock_guard<std::mutex> g(mu_);
+            free_[dev].push_back(s);
+        }
     }
     // queued work on a released stream simply runs ahead of its next owner's
     void release(int dev, cudaStream_t s) {
@@ -399,9 +427,9 @@ struct Comm {
     cudaStream_t side = nullptr;    // internal, same device; created on first use (side_stream)
     std::once_flag side_once;
     cudaError_t side_err = cudaSuccess;
-    // Nonblocking operations run their deferred part here.  Created lazily:
-    // most communicators (conventional / collective contexts) never need
-    // one, and every stream spends one of the device's 32 hardware queues.
+    // Nonblocking operations run their deferred part here.  Taken lazily
+    // from the device's stream pool (reserved at world join, so no stream is
+    // created on the data path): most communicators never need one.
     cudaStream_t side_stream() {
         std::call_once(side_once, [this] {
             side_err = stream_pool().acquire(device, &side);
@@ -548,12 +576,15 @@ int stage_send(const std::shared_ptr<Comm>& c, PendingSend& ps) {
 // stream of the owner's device (the sender may have freed its communicator).
 int consume_staging(World* w, int dev, cudaStream_t st, const PendingSend& ps, const Side& r, int64_t moved) {
     MPX_RC(launch_move(dev, r.dt, r.count, false, ps.staging, r.buf, moved, st));
+    MPX_TRACE("consume: unpack launched");
     cudaEvent_t used;
     MPX_RC(record_new_event(st, &used));
     cudaStream_t svc = w->service(ps.s.device);
     MPX_RC(set_device(ps.s.device));
     MPX_CU(cudaStreamWaitEvent(svc, used, 0));
+    MPX_TRACE("consume: freeing staging");
     MPX_CU(cudaFreeAsync(ps.staging, svc));
+    MPX_TRACE("consume: freed");
     cudaEventDestroy(used);
     return MPX_SUCCESS;
 }
@@ -694,6 +725,7 @@ int do_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t buf_bytes, int64_
         pr.req = req;
         MPX_RC(set_device(c->device));
         MPX_RC(record_new_event(c->stream, &pr.ev));
+        MPX_TRACE("recv r%d posted", c->rank);
         w->flags.take(&pr.flag, &pr.gen);
         uint32_t* flag = pr.flag;
         const uint32_t gen = pr.gen;
@@ -724,7 +756,9 @@ int do_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t buf_bytes, int64_
     if (!blocking) {
         cudaEvent_t fork;
         MPX_RC(record_new_event(c->stream, &fork));
+        MPX_TRACE("recv r%d fork recorded", c->rank);
         if (!c->side_stream()) return cuda_fail(c->side_err, "cudaStreamCreate(side)");
+        MPX_TRACE("recv r%d side stream %p", c->rank, (void*)c->side_stream());
         MPX_CU(cudaStreamWaitEvent(c->side_stream(), fork, 0));
         if (mpx_tracing() && !ps.eager) note_side({c->side_stream(), fork, c->stream, ps.ev, ps.s.comm->stream, ps.flag, c->rank});
         else cudaEventDestroy(fork);
@@ -874,6 +908,9 @@ int mpx_world_join(const char* group, int size, int rank, int device, int64_t ea
     if (w->size != size) return fail(MPX_ERR_ARG, "world %s has %d ranks, not %d", group, w->size, size);
     if (w->joined[rank]) return fail(MPX_ERR_STATE, "rank %d already joined world %s", rank, group);
     MPX_RC(setup_device(w, device, ndev));
+    // streams for this rank's queues, communicators and side streams, made
+    // now (see StreamPool::reserve); more ranks of the world -> a deeper pool
+    MPX_CU(stream_pool().reserve(device, (size_t)std::min(64, 4 * size + 4)));
     w->joined[rank] = true;
     w->devices[rank] = device;
     w->live++;
@@ -1022,7 +1059,7 @@ int mpx_comm_synchronize(mpx_comm h) {
     auto c = comm_of(h);
     if (!c) return fail(MPX_ERR_STATE, "device queue already destroyed");
     MPX_RC(set_device(c->device));
-    MPX_CU(cudaStreamSynchronize(c->stream));
+    MPX_RC(mpx_stream_wait(c->stream));
     std::lock_guard<std::mutex> g(c->err_mu);
     if (!c->deferred.empty()) {
         auto e = c->deferred.front();
@@ -1044,21 +1081,53 @@ int mpx_stream_device(void* stream, int* device) {
     return MPX_SUCCESS;
 }
 
+// Host wait for a stream by polling cudaStreamQuery (with a short back-off)
+// instead of cudaStreamSynchronize: with several ranks of one process on a
+// device, a thread blocked in cudaStreamSynchronize on a stream parked in a
+// stream-memop wait was seen to stall other threads' enqueue calls -- the
+// very calls that would release the wait.
+int mpx_stream_wait(void* stream) {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    long ns = 1000;
+    for (;;) {
+        cudaError_t e = cudaStreamQuery(s);
+        if (e == cudaSuccess) return MPX_SUCCESS;
+        if (e != cudaErrorNotReady) return mpx::cuda_fail(e, "cudaStreamQuery");
+        struct timespec ts{0, ns};
+        nanosleep(&ts, nullptr);
+        if (ns < 100000) ns *= 2;
+    }
+}
+
 int mpx_stream_new(int device, void** stream) {
     if (!stream) return fail(MPX_ERR_ARG, "null output pointer");
     int ndev = 0;
     MPX_CU(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(MPX_ERR_ARG, "device %d out of range", device);
-    int cur = -1;
-    MPX_CU(cudaGetDevice(&cur));
-    if (cur != device) MPX_CU(cudaSetDevice(device));
     cudaStream_t st = nullptr;
-    cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-    if (cur != device) cudaSetDevice(cur);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+    cudaError_t e = mpx::stream_pool().acquire(device, &st);   // reserved at world join
+    if (e != cudaSuccess) return mpx::cuda_fail(e, "cudaStreamCreate");
     *stream = st;
     return MPX_SUCCESS;
 }
+
+// MPX_BT=1 (diagnosis): SIGUSR2 makes the receiving thread print its native
+// backtrace (with /proc/self/maps offsets resolvable by addr2line)
+namespace {
+void bt_handler(int) {
+    void* fr[64];
+    const int n = backtrace(fr, 64);
+    char head[64];
+    const int k = std::snprintf(head, sizeof head, "=== bt tid %ld\n", (long)syscall(SYS_gettid));
+    if (write(2, head, (size_t)k) < 0) return;
+    backtrace_symbols_fd(fr, n, 2);
+}
+struct BtInstall {
+    BtInstall() {
+        if (std::getenv("MPX_BT")) signal(SIGUSR2, bt_handler);
+    }
+} g_bt_install;
+}  // namespace
 
 int mpx_debug_flags(void) {
     std::lock_guard<std::mutex> g(mpx::g_waits_mu);

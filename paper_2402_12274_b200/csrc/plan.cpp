@@ -2,6 +2,7 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <deque>
 #include <climits>
 #include <cstring>
 #include <tuple>
@@ -77,6 +78,61 @@ cudaMemPool_t desc_pool(int device) {
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     pools[device] = pool;
     return pool;
+}
+
+// Pinned staging for descriptor uploads.  A cudaMemcpyAsync from pageable
+// memory may hold the calling thread until the copy engine has drained the
+// driver's bounded staging buffers -- and with several ranks of one process
+// on a device, that drain can sit behind work that only another (blocked)
+// rank thread would release.  From pinned memory the call returns at once.
+// A chunk is reused only once its latest upload has completed (checked with
+// cudaEventQuery, never waited for); otherwise another chunk is added.
+class UploadArena {
+  public:
+    cudaError_t copy(cudaStream_t up, void* dst, const void* src, size_t n) {
+        std::lock_guard<std::mutex> g(mu_);
+        Chunk* c = nullptr;
+        for (auto& k : chunks_)
+            if (k.cap - k.used >= n) { c = &k; break; }
+        if (!c)
+            for (auto& k : chunks_)
+                if (k.cap >= n && cudaEventQuery(k.last) == cudaSuccess) { k.used = 0; c = &k; break; }
+        cudaGetLastError();
+        if (!c) {
+            Chunk k;
+            k.cap = std::max<size_t>(n, size_t(8) << 20);
+            cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&k.base), k.cap, cudaHostAllocPortable);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&k.last, cudaEventDisableTiming);
+            if (e != cudaSuccess) return e;
+            chunks_.push_back(k);
+            c = &chunks_.back();
+        }
+        uint8_t* at = c->base + c->used;
+        std::memcpy(at, src, n);
+        c->used += (n + 255) & ~size_t(255);
+        if (c->used > c->cap) c->used = c->cap;
+        cudaError_t e = cudaMemcpyAsync(dst, at, n, cudaMemcpyHostToDevice, up);
+        if (e == cudaSuccess) e = cudaEventRecord(c->last, up);
+        return e;
+    }
+
+  private:
+    struct Chunk {
+        uint8_t* base = nullptr;
+        size_t cap = 0, used = 0;
+        cudaEvent_t last = nullptr;
+    };
+    std::mutex mu_;
+    std::deque<Chunk> chunks_;   // stable addresses
+};
+
+UploadArena& upload_arena(int device) {
+    static std::mutex mu;
+    static std::map<int, UploadArena*> arenas;   // never destroyed
+    std::lock_guard<std::mutex> g(mu);
+    auto& a = arenas[device];
+    if (!a) a = new UploadArena();
+    return *a;
 }
 
 // one internal upload stream per device: descriptor uploads never
@@ -788,6 +844,7 @@ std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStre
         if (qb) std::memcpy(host.data() + qo, rt_pk.data(), qb);
         (void)stream;
         void* dev = nullptr;
+        MPX_TRACE("plan create: blob %zu B", host.size());
         cudaStream_t up = upload_stream(device);
         cudaMemPool_t pool = desc_pool(device);
         cudaError_t e = pool ? cudaMallocFromPoolAsync(&dev, host.size(), pool, up) : cudaErrorMemoryAllocation;
@@ -803,10 +860,10 @@ std::shared_ptr<Plan> get_plan(Datatype* dt, int64_t count, int device, cudaStre
             std::memcpy(host.data() + so, specs.data(), sb);
         }
         p->blob = dev;
-        // pageable source: the call returns once the bytes are staged, so the
-        // host vector may die; only the (private) upload stream is involved
+        // through pinned staging: returns at once, only the (private) upload
+        // stream is involved
         MPX_TRACE("plan upload %zu B", host.size());
-        e = cudaMemcpyAsync(dev, host.data(), host.size(), cudaMemcpyHostToDevice, up);
+        e = upload_arena(device).copy(up, dev, host.data(), host.size());
         MPX_TRACE("plan upload issued");
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ready, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventRecord(p->ready, up);

@@ -24,10 +24,13 @@ inline bool mpx_tracing() {
 #define MPX_TRACE(...)                                                                        \
     do {                                                                                      \
         if (mpx_tracing()) {                                                                  \
-            std::fprintf(stderr, "[mpx %zx] ", std::hash<std::thread::id>()(std::this_thread::get_id()) & 0xffff); \
-            std::fprintf(stderr, __VA_ARGS__);                                                \
-            std::fputc('\n', stderr);                                                         \
-            std::fflush(stderr);                                                              \
+            char mpx_tb_[320];                                                                \
+            int mpx_tn_ = std::snprintf(mpx_tb_, sizeof mpx_tb_, "[mpx %04zx] ",               \
+                                        std::hash<std::thread::id>()(std::this_thread::get_id()) & 0xffff); \
+            mpx_tn_ += std::snprintf(mpx_tb_ + mpx_tn_, sizeof mpx_tb_ - mpx_tn_, __VA_ARGS__); \
+            if (mpx_tn_ > (int)sizeof mpx_tb_ - 2) mpx_tn_ = (int)sizeof mpx_tb_ - 2;         \
+            mpx_tb_[mpx_tn_++] = '\n';                                                        \
+            std::fwrite(mpx_tb_, 1, (size_t)mpx_tn_, stderr);                                  \
         }                                                                                     \
     } while (0)
 

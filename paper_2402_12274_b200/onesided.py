@@ -23,7 +23,7 @@ import ctypes
 import numpy as np
 import torch
 
-from ._lib import check, lib
+from ._lib import check, lib, stream_wait
 from .comms import CONVENTIONAL, Status
 from .datatypes import Datatype, _count, _host_view, packed_size
 from .errors import ArgError, PendingError, StateError, UnsupportedError
@@ -160,7 +160,7 @@ class Window:
         ops = self.epochs.pop(target_rank, None)
         if ops is None:
             raise StateError("no epoch open to rank %d" % target_rank)
-        self.comm._stream.synchronize()
+        stream_wait(self.comm._stream)
         first = None
         for r in ops:
             r._complete()

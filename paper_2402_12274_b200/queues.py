@@ -15,7 +15,7 @@ import threading
 import torch
 
 from .errors import ArgError, MinimpiError, StateError
-from ._lib import own_stream
+from ._lib import own_stream, stream_wait
 
 _QUEUES = {}
 _lock = threading.Lock()
@@ -56,7 +56,7 @@ class DeviceQueue:
         """Block until every enqueued operation has run; raise the first
         deferred error since the last sync, once (offload.py:111-119)."""
         self._check_live()
-        self.torch_stream.synchronize()
+        stream_wait(self.torch_stream)
         first = self._errors[0] if self._errors else None
         del self._errors[:]
         for c in list(self._comms):
@@ -74,7 +74,7 @@ class DeviceQueue:
     def destroy(self):
         """Drain, then invalidate (offload.py:121-133)."""
         self._check_live()
-        self.torch_stream.synchronize()
+        stream_wait(self.torch_stream)
         self.destroyed = True
         with _lock:
             _QUEUES.pop(self.handle, None)
