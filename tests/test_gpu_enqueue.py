@@ -602,3 +602,51 @@ def test_host_allreduce_reference_cases():   # test_comm.py:103-132
 
     out = pair(body, body)
     assert out[0] == out[1] == ([3, 30], [2.0])
+
+
+def test_queues_created_while_a_peer_stream_is_parked():
+    """Rank 0's stream is parked in a rendezvous receive (a stream-memop
+    wait) while rank 1 only then creates new queues and MPIX streams (local
+    calls) before sending: creating those streams must not stall behind the
+    parked stream (streams are reserved at world join)."""
+    import threading
+    parked = threading.Event()
+    nbytes = 1 << 20
+    payload = torch.arange(nbytes, dtype=torch.int64, device=DEV).to(torch.uint8)
+    got = {}
+
+    def rank0(inst):
+        q = mp.queue_create(inst)
+        c, s = device_comm(inst, q)                       # collective with rank 1
+        dst = torch.zeros(nbytes, dtype=torch.uint8, device=DEV)
+        mp.recv_enqueue(c, dst, nbytes, mp.BYTE, 1, 5)    # parks the stream until delivery
+        parked.set()
+        mp.queue_synchronize(q)
+        got["dst"] = dst.cpu()
+        mp.comm_free(c)
+        mp.free_stream(s)
+        mp.queue_destroy(q)
+
+    def rank1(inst):
+        q = mp.queue_create(inst)
+        c, s = device_comm(inst, q)
+        assert parked.wait(60)
+        time.sleep(0.05)
+        extra = []
+        for _ in range(3):                                # new streams while rank 0 is parked
+            eq = mp.queue_create(inst)
+            info = mp.info_create()
+            mp.info_set(info, "type", "devstream")
+            mp.info_set_hex(info, "value", bytes.fromhex(eq.handle))
+            extra.append((eq, inst.stream_create(info)))
+        mp.send_enqueue(c, payload, nbytes, mp.BYTE, 0, 5)
+        mp.queue_synchronize(q)
+        for eq, es in extra:
+            mp.free_stream(es)
+            mp.queue_destroy(eq)
+        mp.comm_free(c)
+        mp.free_stream(s)
+        mp.queue_destroy(q)
+
+    pair(rank0, rank1)
+    assert torch.equal(got["dst"], payload.cpu())
