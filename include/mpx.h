@@ -196,6 +196,19 @@ int mpx_comm_synchronize(mpx_comm c);
 int mpx_comm_progress(mpx_comm c, int64_t *outstanding);
 /* device owning a cudaStream_t (for wrapping a raw handle from an Info) */
 int mpx_stream_device(void *stream, int *device);
+/* ---- multi-process worlds (csrc/ipc.hpp) -----------------------
+ * One process per rank on one node (e.g. under torchrun): collective over
+ * the `size` processes that join job name `job`.  Matching, flags and a
+ * per-rank device staging arena of `arena_bytes` (exported with CUDA IPC)
+ * live in a shared-memory segment; every message is packed into the
+ * sender's arena at its stream position and unpacked by the receiving
+ * process straight from there.  Stream communicators and the send / recv /
+ * isend / irecv / wait enqueue calls work unchanged on such a world;
+ * allreduce_enqueue and windows return MPX_ERR_UNSUPPORTED for now. */
+int mpx_ipc_world_join(const char *job, int size, int rank, int device, int64_t eager_limit,
+                       int64_t arena_bytes, mpx_world *out);
+/* host barrier over the processes of a multi-process world */
+int mpx_world_barrier(mpx_world w);
 /* a non-blocking stream on `device` for the caller alone, owned by the
  * process (never destroyed by the library); taken from the streams libmpx
  * creates ahead of time at world join (creating a stream while another

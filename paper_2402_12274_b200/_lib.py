@@ -73,6 +73,8 @@ _SIGS = {
     "mpx_comm_progress": ([vp, p64], cint),
     "mpx_stream_device": ([vp, ctypes.POINTER(cint)], cint),
     "mpx_stream_new": ([cint, pvp], cint),
+    "mpx_ipc_world_join": ([ctypes.c_char_p, cint, cint, cint, i64, i64, pvp], cint),
+    "mpx_world_barrier": ([vp], cint),
     "mpx_stream_wait": ([vp], cint),
     "mpx_debug_flags": ([], cint),
     "mpx_nccl_load": ([ctypes.c_char_p], cint),

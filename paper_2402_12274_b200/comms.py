@@ -23,6 +23,7 @@ import torch
 
 from . import runtime as _rt
 from ._lib import check, lib, own_stream, stream_wait
+from .queues import order_after_caller
 from .datatypes import FLOAT32, FLOAT64, INT32, INT64, Datatype, _host_view
 from .errors import ArgError, MinimpiError, PendingError, StateError, for_status
 
@@ -350,6 +351,7 @@ def _queue_of(comm):
         raise ArgError("communicator is not bound to a device queue")
     q._check_live()
     comm._check_live()
+    order_after_caller(comm._stream)     # the operation follows the caller's earlier work
     return q
 
 
@@ -463,6 +465,7 @@ def _host_isend(comm, buf, count, dtype, dest, tag):
     _check_tag(tag, allow_any=False)
     _check_rank("dest", dest, comm.size)
     b, _ = _host_buffer(buf, comm.instance.device, writable=False)
+    order_after_caller(comm._stream)      # the upload above ran on the caller's stream
     h = ctypes.c_void_p()
     check(lib.mpx_isend_enqueue(comm._h, b.data_ptr(), _nbytes(b), count, dtype._h, dest, tag,
                                 ctypes.byref(h)))
@@ -479,6 +482,7 @@ def _host_irecv(comm, buf, count, dtype, source, tag):
     _check_tag(tag, allow_any=True)
     _check_rank("source", source, comm.size, allow_any=True)
     b, finish = _host_buffer(buf, comm.instance.device, writable=True)
+    order_after_caller(comm._stream)
     h = ctypes.c_void_p()
     check(lib.mpx_irecv_enqueue(comm._h, b.data_ptr(), _nbytes(b), count, dtype._h, source, tag,
                                 ctypes.byref(h)))
@@ -611,6 +615,7 @@ def allreduce(comm, sendbuf, recvbuf, count, dtype, op=SUM, algo=None):
     if _nbytes(s) < need or _nbytes(r) < need:
         raise ArgError("allreduce buffers hold %d/%d bytes, need %d" % (_nbytes(s), _nbytes(r), need))
     c = comm if comm._device_queue is None else comm
+    order_after_caller(comm._stream)      # the uploads above ran on the caller's stream
     check(lib.mpx_allreduce_enqueue(c._h, s.data_ptr(), r.data_ptr(), count, code, 0,
                                     _ALGOS.get(algo, 0)))
     stream_wait(comm._stream)

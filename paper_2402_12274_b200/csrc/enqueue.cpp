@@ -50,6 +50,7 @@
 
 #include "capi_common.hpp"
 #include "coll.hpp"
+#include "ipc.hpp"
 #include "kernels.hpp"
 #include "mpx.h"
 
@@ -368,6 +369,7 @@ struct Mailbox {
 
 struct World {
     std::string group;
+    IpcWorld* ipc = nullptr;   // multi-process job (ipc.hpp); null: ranks are threads of this process
     int size = 0;
     int64_t eager_limit = 65536;
     std::vector<int> devices;
@@ -590,9 +592,20 @@ int consume_staging(World* w, int dev, cudaStream_t st, const PendingSend& ps, c
 }
 
 // -------------------------------------------------------------- send path
+int ipc_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t count, Datatype* dt, int dest, int tag,
+             bool blocking, std::shared_ptr<ReqState>* out_req);
+int ipc_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t count, Datatype* dt, int source, int tag,
+             bool blocking, std::shared_ptr<ReqState>* out_req);
+
 int do_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t buf_bytes, int64_t count, Datatype* dt, int dest, int tag,
             bool blocking, std::shared_ptr<ReqState>* out_req) {
     World* w = c->w;
+    if (w->ipc) {
+        if (dest < 0 || dest >= w->size) return fail(MPX_ERR_ARG, "dest %d out of range for size-%d communicator", dest, w->size);
+        if (tag < 0) return fail(MPX_ERR_ARG, "tag %d out of range [0, 2147483647]", tag);
+        MPX_RC(check_layout_region(dt, count, buf_bytes));
+        return ipc_send(c, buf, count, dt, dest, tag, blocking, out_req);
+    }
     if (dest < 0 || dest >= w->size) return fail(MPX_ERR_ARG, "dest %d out of range for size-%d communicator", dest, w->size);
     if (tag < 0) return fail(MPX_ERR_ARG, "tag %d out of range [0, 2147483647]", tag);
     MPX_RC(check_layout_region(dt, count, buf_bytes));
@@ -699,6 +712,7 @@ int do_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t buf_bytes, int64_
         return fail(MPX_ERR_ARG, "source %d out of range for size-%d communicator", source, w->size);
     if (tag < 0 && tag != MPX_ANY_TAG) return fail(MPX_ERR_ARG, "tag %d out of range [0, 2147483647]", tag);
     MPX_RC(check_layout_region(dt, count, buf_bytes));  // DtypeSink check at post time (p2p.py:63-64)
+    if (w->ipc) return ipc_recv(c, buf, count, dt, source, tag, blocking, out_req);
     Side r;
     r.rank = c->rank;
     r.device = c->device;
@@ -782,6 +796,151 @@ int do_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t buf_bytes, int64_
     if (!mpx_tracing()) cudaEventDestroy(ps.ev);
     if (out_req) *out_req = req;
     MPX_TRACE("recv r%d issued", c->rank);
+    return MPX_SUCCESS;
+}
+
+// ------------------------------------------------ multi-process (ipc.hpp)
+// Every message is packed into the sender's staging arena at its stream
+// position (sends complete locally, like the reference's eager frames); the
+// receiving process unpacks from that arena after the sender's ready flag
+// and then releases the space with the consumed flag.
+struct IpcPending {          // a receive posted before its send arrived
+    std::shared_ptr<Comm> c;
+    Side r;
+    std::shared_ptr<ReqState> req;
+    cudaEvent_t ev = nullptr;   // receiver stream position (buffer ready)
+    uint32_t* flag = nullptr;   // completion, in this rank's flag range
+    uint32_t gen = 0;
+    bool blocking = false;
+};
+
+int ipc_deliver(const std::shared_ptr<Comm>& c, cudaStream_t st, const Side& r, const IpcMsg& m, int64_t* moved) {
+    MPX_RC(wait_flag(st, m.ready, m.ready_gen));
+    *moved = std::min(m.bytes, r.bytes);
+    if (*moved > 0) MPX_RC(launch_move(c->device, r.dt, r.count, false, m.data, r.buf, *moved, st));
+    MPX_RC(set_device(c->device));
+    return write_flag(st, m.consumed, m.consumed_gen);
+}
+
+bool ipc_on_match(void* cookie, const IpcMsg& m) {
+    auto* raw = static_cast<IpcPending*>(cookie);
+    set_device(raw->c->device);
+    // deliver only once the receiver's stream has reached the receive's
+    // post point: a delivery waiting for it on the side stream would hold up
+    // every later delivery queued behind it
+    const cudaError_t q = cudaEventQuery(raw->ev);
+    if (q == cudaErrorNotReady) {
+        cudaGetLastError();
+        return false;
+    }
+    std::unique_ptr<IpcPending> p(raw);
+    const auto& c = p->c;
+    int64_t moved = 0;
+    int rc = q == cudaSuccess ? MPX_SUCCESS : cuda_fail(q, "cudaEventQuery");
+    cudaStream_t st = c->side_stream();
+    if (!rc && !st) rc = cuda_fail(c->side_err, "cudaStreamCreate(side)");
+    if (!rc) rc = ipc_deliver(c, st, p->r, m, &moved);
+    if (!rc) rc = write_flag(st, p->flag, p->gen);
+    cudaEventDestroy(p->ev);
+    const bool trunc = m.bytes > p->r.bytes;
+    fill_status(p->req, p->r, m.src, m.tag, moved, trunc);
+    if (rc) defer_error(c, rc, "multi-process delivery failed: " + g_last_error);
+    else if (trunc && p->blocking)
+        defer_error(c, MPX_ERR_TRUNCATE, "message truncated: incoming data larger than the posted receive");
+    return true;
+}
+
+int ipc_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t count, Datatype* dt, int dest, int tag,
+             bool blocking, std::shared_ptr<ReqState>* out_req) {
+    IpcWorld* ipc = c->w->ipc;
+    const int64_t bytes = dt->size * count;
+    uint8_t* slot = nullptr;
+    int64_t off = 0;
+    uint32_t *ready = nullptr, rgen = 0, cidx = 0, cgen = 0;
+    MPX_RC(ipc->reserve(bytes, &slot, &off, &ready, &rgen, &cidx, &cgen));
+    MPX_RC(set_device(c->device));
+    if (bytes > 0) MPX_RC(launch_move(c->device, dt, count, true, buf, slot, bytes, c->stream));
+    MPX_RC(set_device(c->device));
+    MPX_RC(write_flag(c->stream, ready, rgen));
+    MPX_RC(ipc->post_send(dest, c->ctx, tag, bytes, off, ready, rgen, cidx, cgen));
+    MPX_TRACE("ipc send r%d -> %d tag %d %lld B", c->rank, dest, tag, (long long)bytes);
+    if (!blocking) {
+        auto req = std::make_shared<ReqState>();
+        req->comm = c;
+        req->is_send = true;
+        req->matched = true;
+        c->outstanding++;
+        if (out_req) *out_req = req;
+    }
+    return MPX_SUCCESS;
+}
+
+int ipc_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t count, Datatype* dt, int source, int tag,
+             bool blocking, std::shared_ptr<ReqState>* out_req) {
+    IpcWorld* ipc = c->w->ipc;
+    auto p = std::make_unique<IpcPending>();
+    p->c = c;
+    p->r.rank = c->rank;
+    p->r.device = c->device;
+    p->r.comm = c;
+    p->r.dt = dt;
+    p->r.count = count;
+    p->r.buf = buf;
+    p->r.bytes = dt->size * count;
+    p->blocking = blocking;
+    if (!blocking) {
+        p->req = std::make_shared<ReqState>();
+        p->req->comm = c;
+    }
+    auto req = p->req;
+    MPX_RC(set_device(c->device));
+    MPX_RC(record_new_event(c->stream, &p->ev));
+    p->flag = ipc->local_flag(&p->gen);
+    uint32_t* flag = p->flag;
+    const uint32_t gen = p->gen;
+    const Side r = p->r;
+    bool matched = false;
+    IpcMsg m;
+    IpcPending* raw = p.release();   // owned by the mailbox entry unless matched now
+    int rc = ipc->recv(c->ctx, source, tag, r.bytes, raw, &matched, &m);
+    if (rc || matched) p.reset(raw);
+    if (rc) {
+        cudaEventDestroy(p->ev);
+        return rc;
+    }
+    MPX_TRACE("ipc recv r%d <- %d tag %d %s", c->rank, source, tag, matched ? "matched" : "posted");
+    if (matched) {
+        cudaEventDestroy(p->ev);
+        cudaStream_t st = c->stream;
+        if (!blocking) {
+            cudaEvent_t fork;
+            MPX_RC(record_new_event(c->stream, &fork));
+            st = c->side_stream();
+            if (!st) return cuda_fail(c->side_err, "cudaStreamCreate(side)");
+            MPX_CU(cudaStreamWaitEvent(st, fork, 0));
+            cudaEventDestroy(fork);
+        }
+        int64_t moved = 0;
+        MPX_RC(ipc_deliver(c, st, r, m, &moved));
+        const bool trunc = m.bytes > r.bytes;
+        fill_status(req, r, m.src, m.tag, moved, trunc);
+        if (trunc && blocking)
+            defer_error(c, MPX_ERR_TRUNCATE, "message truncated: incoming data larger than the posted receive");
+        if (!blocking) {
+            MPX_RC(record_new_event(st, &req->done_ev));
+            req->needs_wait = true;
+        }
+    } else if (blocking) {
+        MPX_RC(wait_flag(c->stream, flag, gen));
+    } else {
+        req->flag = flag;
+        req->gen = gen;
+        req->needs_wait = true;
+    }
+    if (req) {
+        c->outstanding++;
+        if (out_req) *out_req = req;
+    }
     return MPX_SUCCESS;
 }
 
@@ -918,8 +1077,56 @@ int mpx_world_join(const char* group, int size, int rank, int device, int64_t ea
     return MPX_SUCCESS;
 }
 
+int mpx_ipc_world_join(const char* job, int size, int rank, int device, int64_t eager_limit, int64_t arena_bytes,
+                       mpx_world* out) {
+    if (!job || size < 1 || rank < 0 || rank >= size) return fail(MPX_ERR_ARG, "rank %d outside job of %d", rank, size);
+    if (eager_limit < 0 || arena_bytes <= 0) return fail(MPX_ERR_ARG, "eager_limit / arena size out of range");
+    int ndev = 0;
+    MPX_CU(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(MPX_ERR_ARG, "device %d not present (%d devices)", device, ndev);
+    MPX_RC(set_device(device));
+    MPX_CU(preload_pack_kernels());
+    MPX_CU(preload_coll_kernels());
+    (void)staging_pool(device);
+    IpcWorld* ipc = nullptr;
+    MPX_RC(IpcWorld::join(job, size, rank, device, arena_bytes, ipc_on_match, &ipc));
+    auto* w = new World();
+    w->group = job;
+    w->ipc = ipc;
+    w->size = size;
+    w->eager_limit = eager_limit;
+    w->joined.assign(size, false);
+    w->devices.resize(size);
+    for (int r = 0; r < size; ++r) w->devices[r] = ipc->device_of(r);
+    w->next_win.assign(size, 0);
+    int rc = setup_device(w, device, ndev);
+    if (!rc && stream_pool().reserve(device, 8) != cudaSuccess) rc = fail(MPX_ERR_OTHER, "stream reserve");
+    if (rc) return rc;
+    w->joined[rank] = true;
+    w->live = 1;
+    *out = reinterpret_cast<mpx_world>(w);
+    return MPX_SUCCESS;
+}
+
+int mpx_world_barrier(mpx_world h) {
+    auto* w = reinterpret_cast<World*>(h);
+    if (!w) return fail(MPX_ERR_STATE, "not a live world");
+    if (!w->ipc) return fail(MPX_ERR_UNSUPPORTED, "in-process worlds synchronise their rank threads in the caller");
+    return w->ipc->barrier();
+}
+
 int mpx_world_leave(mpx_world h, int rank) {
     auto* w = reinterpret_cast<World*>(h);
+    if (w && w->ipc) {
+        if (rank < 0 || rank >= w->size || !w->joined[rank]) return fail(MPX_ERR_STATE, "rank %d not in world", rank);
+        int rc = w->ipc->leave();
+        for (auto& kv : w->area) {
+            set_device(kv.first);
+            cudaFree(kv.second);
+        }
+        delete w;
+        return rc;
+    }
     std::lock_guard<std::mutex> g(g_worlds_mu);
     auto it = g_worlds.find(w ? w->group : std::string());
     if (!w || it == g_worlds.end() || it->second != w) return fail(MPX_ERR_STATE, "not a live world");
@@ -1177,6 +1384,7 @@ int mpx_allreduce_enqueue(mpx_comm h, const void* sendbuf, void* recvbuf, int64_
                           int algo) {
     auto c = comm_of(h);
     if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
+    if (c->w->ipc) return fail(MPX_ERR_UNSUPPORTED, "allreduce_enqueue across processes is not implemented yet");
     if (op != MPX_OP_SUM) return fail(MPX_ERR_ARG, "unsupported reduction op %d (only SUM)", op);
     const int es = elem_size(dtype_code);
     if (!es) return fail(MPX_ERR_ARG, "allreduce supports INT32, INT64, FLOAT32 and FLOAT64");
@@ -1252,6 +1460,7 @@ int mpx_win_create(mpx_comm h, const void* base, int64_t bytes, int64_t disp_uni
     if (disp_unit < 1) return fail(MPX_ERR_ARG, "disp_unit must be a positive int");
     if (bytes < 0 || (bytes > 0 && !base)) return fail(MPX_ERR_ARG, "bad window region");
     World* w = c->w;
+    if (w->ipc) return fail(MPX_ERR_UNSUPPORTED, "windows across processes are not implemented yet");
     std::unique_lock<std::mutex> lk(w->win_mu);
     const int64_t id = w->next_win[(size_t)c->rank]++;
     World::Win& win = w->wins[id];

@@ -116,6 +116,16 @@ def _nbytes(t):
     return t.numel() * t.element_size()
 
 
+def order_after_caller(stream):
+    """Enqueued work runs after what the calling thread already issued on its
+    current stream (program order, as the reference's serial queue gives):
+    the queue's stream waits on an event of the current stream when they
+    differ."""
+    cur = torch.cuda.current_stream(stream.device)
+    if cur.cuda_stream != stream.cuda_stream:
+        stream.wait_stream(cur)
+
+
 def memcpy_enqueue(queue, dst, src, nbytes):
     """Ordered byte copy on the queue; bounds checked at enqueue
     (offload.py:271-285)."""
@@ -127,6 +137,7 @@ def memcpy_enqueue(queue, dst, src, nbytes):
     if nbytes > _nbytes(dst) or nbytes > _nbytes(src):
         raise ArgError("memcpy of %d bytes overruns a %d/%d byte buffer"
                        % (nbytes, _nbytes(src), _nbytes(dst)))
+    order_after_caller(queue.torch_stream)
     with torch.cuda.stream(queue.torch_stream):
         dst.reshape(-1).view(torch.uint8)[:nbytes].copy_(
             src.reshape(-1).view(torch.uint8)[:nbytes], non_blocking=True)
@@ -138,6 +149,7 @@ def compute_enqueue(queue, fn, *args):
     queue._check_live()
     if not callable(fn):
         raise ArgError("compute_enqueue needs a callable")
+    order_after_caller(queue.torch_stream)
     with torch.cuda.stream(queue.torch_stream):
         try:
             fn(*args)

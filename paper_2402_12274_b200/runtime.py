@@ -26,6 +26,8 @@ from ._lib import check, lib, own_stream
 from .errors import ArgError, ExhaustedError, PendingError, StateError, UnsupportedError
 
 TRANSPORT_INPROC = "inproc"
+TRANSPORT_IPC = "ipc"          # one process per rank on one node
+DEFAULT_IPC_ARENA = 256 << 20  # per-rank staging arena of a multi-process world
 SERIAL_CONTEXT = "serial_context"
 DEVICE_QUEUE = "device_queue"
 CUDA_STREAM = "cuda_stream"
@@ -222,11 +224,27 @@ class _Group:
                 del self._groups[self.name]
 
 
+class _IpcGroup:
+    """The processes of a multi-process job: barrier through libmpx's shared
+    segment (mpx_world_barrier)."""
+
+    def __init__(self, inst):
+        self._inst = inst
+        self.barrier = self
+
+    def wait(self, timeout=None):
+        check(lib.mpx_world_barrier(self._inst._world))
+
+    def leave(self):
+        pass
+
+
 class Instance:
     """One rank of a running job (runtime.py:56-214)."""
 
-    def __init__(self, rank, size, group, device, eager_limit, vci_pool):
-        self.transport = TRANSPORT_INPROC
+    def __init__(self, rank, size, group, device, eager_limit, vci_pool, transport=TRANSPORT_INPROC,
+                 arena=DEFAULT_IPC_ARENA):
+        self.transport = transport
         self.rank = rank
         self.size = size
         self.group = group
@@ -237,6 +255,16 @@ class Instance:
         self.finalized = False
         self.next_context_id = 2
         self.next_stream_id = 0
+        if transport == TRANSPORT_IPC:
+            h = ctypes.c_void_p()
+            check(lib.mpx_ipc_world_join(group.encode(), size, rank, device, eager_limit, arena,
+                                         ctypes.byref(h)))
+            self._world = h.value
+            self._group = _IpcGroup(self)
+            from .comms import Communicator
+            self.world = Communicator(self, 0, rank, size)
+            self._comms = [self.world]
+            return
         self._group = _Group.join(group, size)
         with _Group._lock:
             on_dev = self._group.devices.setdefault(device, set())
@@ -327,8 +355,15 @@ def init(transport=None, rank=None, ranks=None, group=None, device=None,
     (the only in-scope transport: socket / multi-host bootstrap is out of
     scope)."""
     transport = _cfg(transport, "MINIMPI_TRANSPORT", TRANSPORT_INPROC, str).replace("-", "")
-    if transport != TRANSPORT_INPROC:
+    if transport not in (TRANSPORT_INPROC, TRANSPORT_IPC):
         raise UnsupportedError("transport %r is out of scope for the B200 build" % transport)
+    if transport == TRANSPORT_IPC:
+        # one process per rank: torchrun's RANK / WORLD_SIZE / LOCAL_RANK unless given
+        rank = _cfg(rank, "MINIMPI_RANK", int(os.environ.get("RANK", "0")), int)
+        size = _cfg(ranks, "MINIMPI_SIZE", int(os.environ.get("WORLD_SIZE", "1")), int)
+        group = _cfg(group, "MINIMPI_GROUP", "job%s" % os.environ.get("MASTER_PORT", ""), str)
+        if device is None and "LOCAL_RANK" in os.environ:
+            device = int(os.environ["LOCAL_RANK"]) % max(1, torch.cuda.device_count())
     rank = _cfg(rank, "MINIMPI_RANK", 0, int)
     size = _cfg(ranks, "MINIMPI_SIZE", 1, int)
     group = _cfg(group, "MINIMPI_GROUP", "default", str)
@@ -347,4 +382,5 @@ def init(transport=None, rank=None, ranks=None, group=None, device=None,
         device = rank % ndev
     if isinstance(device, torch.device):
         device = device.index or 0
-    return Instance(rank, size, group, int(device), eager_limit, vci_pool)
+    arena = int(os.environ.get("MPX_IPC_ARENA", DEFAULT_IPC_ARENA))
+    return Instance(rank, size, group, int(device), eager_limit, vci_pool, transport, arena)

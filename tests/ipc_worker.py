@@ -1,0 +1,149 @@
+"""One rank of a multi-process job (test infrastructure for
+tests/test_gpu_ipc.py): MINIMPI_TRANSPORT=ipc, rank / size / job name from
+the environment.  Runs every scenario, checks bytes against the CPU oracle
+and exits 0 on success (an assertion error exits non-zero)."""
+
+import faulthandler
+import os
+import sys
+import time
+
+faulthandler.dump_traceback_later(int(os.environ.get("IPC_WORKER_TIMEOUT", "150")), exit=True)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path[:0] = [ROOT, os.path.join(ROOT, "tests"), os.path.join(ROOT, "tests", "golden")]
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle  # noqa: E402
+import paper_2402_12274_b200 as mp  # noqa: E402
+
+
+def stream_comm(inst):
+    q = mp.queue_create(inst)
+    info = mp.info_create()
+    mp.info_set(info, "type", "devstream")
+    mp.info_set_hex(info, "value", bytes.fromhex(q.handle))
+    s = inst.stream_create(info)
+    return q, s, mp.stream_comm_create(inst.world, s)
+
+
+def data(seed, n):
+    return np.random.default_rng(seed).integers(0, 256, n, dtype=np.uint8)
+
+
+def ring(inst, q, c, nbytes, typed, order):
+    """isend -> r+1, irecv <- r-1; `order` "recv" posts the receive first on
+    every rank, "send" posts the send first and delays the receive so the
+    receiving process's progress thread never runs (send matched at post)."""
+    r, n = inst.rank, inst.size
+    dev = inst.device
+    if typed:   # vector(N/32, 4, 8) of FLOAT64 on both sides
+        spec = ("vector", nbytes // 32, 4, 8, ("basic", 8))
+        dt = mp.type_vector(nbytes // 32, 4, 8, mp.FLOAT64).commit()
+        ot = oracle.OracleType(spec)
+        span, count = ot.max_end, 1
+    else:
+        dt, ot, span, count = mp.BYTE, None, nbytes, nbytes
+    src_h = data(1000 + r, span)
+    src = torch.from_numpy(src_h).to(dev)
+    dst = torch.full((span,), 0x5A, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize(dev)
+    if order == "recv":
+        rr = mp.irecv_enqueue(c, dst, count, dt, (r - 1) % n, 7)
+        mp.barrier(inst.world)                    # every receive is posted before any send
+        sr = mp.isend_enqueue(c, src, count, dt, (r + 1) % n, 7)
+    else:
+        sr = mp.isend_enqueue(c, src, count, dt, (r + 1) % n, 7)
+        mp.barrier(inst.world)
+        rr = mp.irecv_enqueue(c, dst, count, dt, (r - 1) % n, 7)
+    mp.waitall_enqueue([rr, sr])
+    mp.queue_synchronize(q)
+    prev = data(1000 + (r - 1) % n, span)
+    if typed:
+        exp = np.full(span, 0x5A, np.uint8)
+        ot.unpack(ot.pack(prev), exp)
+    else:
+        exp = prev
+    assert np.array_equal(dst.cpu().numpy(), exp), ("ring", nbytes, typed, order)
+    assert rr.status.source == (r - 1) % n and rr.status.tag == 7, rr.status
+    if typed:
+        mp.type_free(dt)
+    mp.barrier(inst.world)
+
+
+def tags_out_of_order(inst, q, c):
+    """rank 0 sends tags 1 then 2 to rank 1, which receives 2 first (blocking
+    enqueue forms; eager semantics across processes)."""
+    dev = inst.device
+    if inst.rank == 0:
+        a = torch.full((1000,), 1, dtype=torch.uint8, device=dev)
+        b = torch.full((3000,), 2, dtype=torch.uint8, device=dev)
+        mp.send_enqueue(c, a, 1000, mp.BYTE, 1, 1)
+        mp.send_enqueue(c, b, 3000, mp.BYTE, 1, 2)
+        mp.queue_synchronize(q)
+    elif inst.rank == 1:
+        x = torch.zeros(3000, dtype=torch.uint8, device=dev)
+        y = torch.zeros(1000, dtype=torch.uint8, device=dev)
+        mp.recv_enqueue(c, x, 3000, mp.BYTE, 0, 2)
+        mp.recv_enqueue(c, y, 1000, mp.BYTE, 0, 1)
+        mp.queue_synchronize(q)
+        assert bool((x == 2).all()) and bool((y == 1).all())
+    mp.barrier(inst.world)
+
+
+def any_source_and_truncation(inst, q, c):
+    """every other rank sends to rank 0, which receives with ANY_SOURCE; then
+    a receive smaller than its message reports ERR_TRUNCATE (nonblocking)."""
+    dev, r, n = inst.device, inst.rank, inst.size
+    if r == 0:
+        got = set()
+        for _ in range(n - 1):
+            buf = torch.zeros(64, dtype=torch.uint8, device=dev)
+            req = mp.irecv_enqueue(c, buf, 64, mp.BYTE, mp.ANY_SOURCE, 3)
+            mp.wait_enqueue(req)
+            mp.queue_synchronize(q)
+            src = req.status.source
+            assert bool((buf == src).all()), (src, buf[:4])
+            got.add(src)
+        assert got == set(range(1, n))
+        small = torch.zeros(10, dtype=torch.uint8, device=dev)
+        req = mp.irecv_enqueue(c, small, 10, mp.BYTE, 1, 4)
+        mp.wait_enqueue(req)
+        mp.queue_synchronize(q)
+        assert req.status.error == "ERR_TRUNCATE", req.status
+        assert bool((small == 9).all())
+    else:
+        mp.send_enqueue(c, torch.full((64,), r, dtype=torch.uint8, device=dev), 64, mp.BYTE, 0, 3)
+        if r == 1:
+            mp.send_enqueue(c, torch.full((20,), 9, dtype=torch.uint8, device=dev), 20, mp.BYTE, 0, 4)
+        mp.queue_synchronize(q)
+    mp.barrier(inst.world)
+
+
+def main():
+    inst = mp.init(transport="ipc")
+    assert inst.transport == "ipc"
+    q, s, c = stream_comm(inst)
+    for nbytes in (8, 1 << 16, 1 << 20, 16 << 20):
+        for typed in (False, True):
+            if typed and nbytes < 32:
+                continue
+            for order in ("recv", "send"):
+                ring(inst, q, c, nbytes, typed, order)
+    tags_out_of_order(inst, q, c)
+    if inst.size >= 2:
+        any_source_and_truncation(inst, q, c)
+    t0 = time.perf_counter()
+    for _ in range(20):                       # arena reuse: many messages through the ring
+        ring(inst, q, c, 4 << 20, False, "recv")
+    mp.comm_free(c)
+    mp.free_stream(s)
+    mp.queue_destroy(q)
+    inst.finalize()
+    print("rank %d ok (%.2fs for the reuse loop)" % (inst.rank, time.perf_counter() - t0), flush=True)
+
+
+if __name__ == "__main__":
+    main()
