@@ -40,6 +40,8 @@
 #include <atomic>
 #include <condition_variable>
 #include <deque>
+#include <functional>
+#include <thread>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -241,6 +243,15 @@ int record_new_event(cudaStream_t s, cudaEvent_t* ev) {
     return MPX_SUCCESS;
 }
 
+// has the stream position recorded in `e` been reached (and passed)?
+bool ev_done(cudaEvent_t e) {
+    static const bool never_defer = std::getenv("MPX_NO_DEFER") != nullptr;   // diagnosis
+    if (never_defer) return true;
+    const cudaError_t q = cudaEventQuery(e);
+    if (q != cudaSuccess) cudaGetLastError();
+    return q != cudaErrorNotReady;
+}
+
 // ------------------------------------------------------------ stream pool
 // Communicator side streams come from a per-device pool and go back to it
 // when the communicator dies, so the number of streams alive stays small: the
@@ -404,6 +415,55 @@ struct World {
     std::vector<int64_t> next_win;   // per rank
     std::mutex svc_mu;
     std::map<int, cudaStream_t> svc;  // per-device service streams (deferred frees)
+    // Deliveries whose inputs are not reachable yet (a receive's post point,
+    // or a send's staging point, still behind earlier work on that rank's
+    // stream) wait here instead of on a side stream, where they would hold
+    // up every later, independent delivery queued behind them -- MPI lets
+    // receives complete out of posting order across tags.  One host thread
+    // per world retries them until their events have completed; it is only
+    // started when the first such delivery appears.
+    std::mutex defer_mu;
+    std::vector<std::function<bool()>> deferred_ops;
+    std::thread defer_thread;
+    bool defer_stop = false;
+    void defer(std::function<bool()> op) {
+        MPX_TRACE("delivery deferred");
+        std::lock_guard<std::mutex> g(defer_mu);
+        deferred_ops.push_back(std::move(op));
+        if (!defer_thread.joinable()) defer_thread = std::thread([this] { defer_loop(); });
+    }
+    void defer_loop() {
+        std::vector<std::function<bool()>> mine;
+        long idle = 0;
+        for (;;) {
+            {
+                std::lock_guard<std::mutex> g(defer_mu);
+                if (defer_stop && deferred_ops.empty() && mine.empty()) return;
+                for (auto& f : deferred_ops) mine.push_back(std::move(f));
+                deferred_ops.clear();
+            }
+            bool did = false;
+            for (size_t k = 0; k < mine.size();) {
+                if (mine[k]()) {
+                    MPX_TRACE("deferred delivery issued (%zu left)", mine.size() - 1);
+                    mine.erase(mine.begin() + (long)k);
+                    did = true;
+                } else {
+                    ++k;
+                }
+            }
+            if (did) idle = 0;
+            struct timespec ts{0, (mine.empty() && ++idle > 100) ? 20000L : 3000L};
+            nanosleep(&ts, nullptr);
+        }
+    }
+    void stop_deferred() {
+        {
+            std::lock_guard<std::mutex> g(defer_mu);
+            defer_stop = true;
+        }
+        if (defer_thread.joinable()) defer_thread.join();
+    }
     cudaStream_t service(int dev) {
         std::lock_guard<std::mutex> g(svc_mu);
         auto it = svc.find(dev);
@@ -673,13 +733,31 @@ int do_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t buf_bytes, 
         cudaEvent_t staged;
         MPX_RC(record_new_event(c->stream, &staged));
         if (!c->side_stream()) return cuda_fail(c->side_err, "cudaStreamCreate(side)");
-        MPX_CU(cudaStreamWaitEvent(c->side_stream(), staged, 0));
-        MPX_CU(cudaStreamWaitEvent(c->side_stream(), pr.ev, 0));
-        MPX_RC(launch_move(c->device, pr.r.dt, pr.r.count, false, ps.staging, pr.r.buf, moved, c->side_stream()));
-        MPX_RC(set_device(c->device));
-        MPX_CU(cudaFreeAsync(ps.staging, c->side_stream()));
-        MPX_RC(write_flag(c->side_stream(), pr.flag, pr.gen));
-        cudaEventDestroy(staged);
+        auto deliver = [c, staged, ev = pr.ev, r = pr.r, flag = pr.flag, gen = pr.gen, staging = ps.staging,
+                        moved]() -> int {
+            MPX_RC(set_device(c->device));
+            MPX_CU(cudaStreamWaitEvent(c->side_stream(), staged, 0));
+            MPX_CU(cudaStreamWaitEvent(c->side_stream(), ev, 0));
+            MPX_RC(launch_move(c->device, r.dt, r.count, false, staging, r.buf, moved, c->side_stream()));
+            MPX_RC(set_device(c->device));
+            MPX_CU(cudaFreeAsync(staging, c->side_stream()));
+            MPX_RC(write_flag(c->side_stream(), flag, gen));
+            cudaEventDestroy(staged);
+            cudaEventDestroy(ev);
+            return MPX_SUCCESS;
+        };
+        if (ev_done(pr.ev) && ev_done(staged)) {
+            MPX_RC(deliver());
+        } else {   // an input is behind earlier work on its stream: deliver later
+            w->defer([deliver, c, ev = pr.ev, staged]() {
+                if (!ev_done(ev) || !ev_done(staged)) return false;
+                if (int rc = deliver()) defer_error(c, rc, "deferred delivery failed: " + g_last_error);
+                return true;
+            });
+        }
+        if (req) c->outstanding++;
+        if (out_req) *out_req = req;
+        return MPX_SUCCESS;
     } else if (blocking) {
         MPX_CU(cudaStreamWaitEvent(c->stream, pr.ev, 0));
         MPX_RC(transfer(c->device, c->stream, s, pr.r, moved));
@@ -688,6 +766,34 @@ int do_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t buf_bytes, 
         cudaEvent_t fork;
         MPX_RC(record_new_event(c->stream, &fork));
         if (!c->side_stream()) return cuda_fail(c->side_err, "cudaStreamCreate(side)");
+        if (!ev_done(pr.ev) || !ev_done(fork)) {
+            // an input (the receive's post point, or this send's own stream
+            // position) is still behind earlier work: deliver from the world's
+            // deferral thread; the send request completes on a flag
+            uint32_t* done = nullptr;
+            uint32_t dgen = 0;
+            w->flags.take(&done, &dgen);
+            req->flag = done;
+            req->gen = dgen;
+            req->needs_wait = true;
+            w->defer([c, fork, ev = pr.ev, s, r = pr.r, flag = pr.flag, gen = pr.gen, moved, done, dgen]() {
+                if (!ev_done(ev) || !ev_done(fork)) return false;
+                int rc = set_device(c->device);
+                cudaStream_t side = c->side_stream();
+                if (!rc && cudaStreamWaitEvent(side, fork, 0) != cudaSuccess) rc = fail(MPX_ERR_OTHER, "wait");
+                if (!rc) rc = transfer(c->device, side, s, r, moved);
+                if (!rc) rc = set_device(c->device);
+                if (!rc) rc = write_flag(side, flag, gen);
+                if (!rc) rc = write_flag(side, done, dgen);
+                if (rc) defer_error(c, rc, "deferred delivery failed: " + g_last_error);
+                cudaEventDestroy(fork);
+                cudaEventDestroy(ev);
+                return true;
+            });
+            c->outstanding++;
+            if (out_req) *out_req = req;
+            return MPX_SUCCESS;
+        }
         MPX_CU(cudaStreamWaitEvent(c->side_stream(), fork, 0));
         MPX_CU(cudaStreamWaitEvent(c->side_stream(), pr.ev, 0));
         MPX_RC(transfer(c->device, c->side_stream(), s, pr.r, moved));
@@ -767,9 +873,49 @@ int do_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t buf_bytes, int64_
     MPX_RC(ensure_peer(w, c->device, ps.s.device));
     MPX_RC(set_device(c->device));
     cudaStream_t st = c->stream;
+    cudaEvent_t fork0 = nullptr;
+    if (!blocking) MPX_RC(record_new_event(c->stream, &fork0));
+    if (!blocking && (!ev_done(ps.ev) || !ev_done(fork0))) {
+        // an input (the send's data point, or this receive's own stream
+        // position) is still behind earlier work: deliver from the world's
+        // deferral thread, complete on a flag.  Nothing on a side stream
+        // ever waits for an unreached point, so a delivery cannot hold up a
+        // later, independent one queued behind it.
+        cudaEvent_t fork = fork0;
+        if (!c->side_stream()) return cuda_fail(c->side_err, "cudaStreamCreate(side)");
+        uint32_t* done = nullptr;
+        uint32_t dgen = 0;
+        w->flags.take(&done, &dgen);
+        req->flag = done;
+        req->gen = dgen;
+        req->needs_wait = true;
+        w->defer([w, c, fork, ps, r, moved, done, dgen]() {
+            if (!ev_done(ps.ev) || !ev_done(fork)) return false;
+            int rc = set_device(c->device);
+            cudaStream_t side = c->side_stream();
+            if (!rc && cudaStreamWaitEvent(side, fork, 0) != cudaSuccess) rc = fail(MPX_ERR_OTHER, "wait");
+            if (!rc && cudaStreamWaitEvent(side, ps.ev, 0) != cudaSuccess) rc = fail(MPX_ERR_OTHER, "wait");
+            if (!rc) {
+                if (ps.eager) {
+                    rc = consume_staging(w, c->device, side, ps, r, moved);
+                } else {
+                    rc = transfer(c->device, side, ps.s, r, moved);
+                    if (!rc) rc = write_flag(side, ps.flag, ps.gen);
+                }
+            }
+            if (!rc) rc = set_device(c->device);
+            if (!rc) rc = write_flag(side, done, dgen);
+            if (rc) defer_error(c, rc, "deferred delivery failed: " + g_last_error);
+            cudaEventDestroy(fork);
+            cudaEventDestroy(ps.ev);
+            return true;
+        });
+        c->outstanding++;
+        if (out_req) *out_req = req;
+        return MPX_SUCCESS;
+    }
     if (!blocking) {
-        cudaEvent_t fork;
-        MPX_RC(record_new_event(c->stream, &fork));
+        cudaEvent_t fork = fork0;
         MPX_TRACE("recv r%d fork recorded", c->rank);
         if (!c->side_stream()) return cuda_fail(c->side_err, "cudaStreamCreate(side)");
         MPX_TRACE("recv r%d side stream %p", c->rank, (void*)c->side_stream());
@@ -829,9 +975,9 @@ bool ipc_on_match(void* cookie, const IpcMsg& m) {
     // post point: a delivery waiting for it on the side stream would hold up
     // every later delivery queued behind it
     const cudaError_t q = cudaEventQuery(raw->ev);
-    if (q == cudaErrorNotReady) {
+    if (q == cudaErrorNotReady || *reinterpret_cast<volatile uint32_t*>(m.ready) < m.ready_gen) {
         cudaGetLastError();
-        return false;
+        return false;   // the post point or the sender's packed data is not there yet
     }
     std::unique_ptr<IpcPending> p(raw);
     const auto& c = p->c;
@@ -909,6 +1055,17 @@ int ipc_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t count, Datatype*
         return rc;
     }
     MPX_TRACE("ipc recv r%d <- %d tag %d %s", c->rank, source, tag, matched ? "matched" : "posted");
+    if (matched && !blocking && *reinterpret_cast<volatile uint32_t*>(m.ready) < m.ready_gen) {
+        // the sender has not packed it yet: a side-stream wait for that could
+        // hold up later deliveries, so the progress thread delivers it
+        req->flag = flag;
+        req->gen = gen;
+        req->needs_wait = true;
+        ipc->defer(p.release(), m);
+        c->outstanding++;
+        if (out_req) *out_req = req;
+        return MPX_SUCCESS;
+    }
     if (matched) {
         cudaEventDestroy(p->ev);
         cudaStream_t st = c->stream;
@@ -1133,6 +1290,7 @@ int mpx_world_leave(mpx_world h, int rank) {
     if (rank < 0 || rank >= w->size || !w->joined[rank]) return fail(MPX_ERR_STATE, "rank %d not in world", rank);
     w->joined[rank] = false;
     if (--w->live == 0) {
+        w->stop_deferred();
         for (auto& kv : w->area) {
             set_device(kv.first);
             cudaFree(kv.second);

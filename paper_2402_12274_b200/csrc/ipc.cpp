@@ -339,6 +339,11 @@ int IpcWorld::recv(int ctx, int src, int tag, int64_t cap, void* cookie, bool* m
     return MPX_SUCCESS;
 }
 
+void IpcWorld::defer(void* cookie, const IpcMsg& m) {
+    std::lock_guard<std::mutex> g(later_mu_);
+    later_in_.emplace_back(cookie, m);
+}
+
 void IpcWorld::progress_loop() {
     cudaSetDevice(device_);
     Box& b = sh_->box[rank_];
@@ -350,6 +355,11 @@ void IpcWorld::progress_loop() {
     long idle = 0;
     while (!stop_) {
         bool did = false;
+        {
+            std::lock_guard<std::mutex> g(later_mu_);
+            for (auto& x : later_in_) later.push_back(x);
+            later_in_.clear();
+        }
         for (size_t k = 0; k < later.size();) {
             if (cb_(later[k].first, later[k].second)) {
                 later.erase(later.begin() + (long)k);

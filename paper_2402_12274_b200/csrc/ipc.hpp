@@ -72,6 +72,9 @@ class IpcWorld {
     int recv(int ctx, int src, int tag, int64_t cap, void* cookie, bool* matched, IpcMsg* m);
     // a completion flag in this rank's range
     uint32_t* local_flag(uint32_t* gen);
+    // hand a matched receive to the progress thread (the callback is retried
+    // until it reports the delivery enqueued)
+    void defer(void* cookie, const IpcMsg& m);
 
   private:
     IpcWorld() = default;
@@ -97,6 +100,8 @@ class IpcWorld {
     uint32_t next_flag_ = 0;
     std::vector<uint32_t> shadow_;
     std::mutex mu_;             // arena ring and flag allocation
+    std::mutex later_mu_;
+    std::vector<std::pair<void*, IpcMsg>> later_in_;
     void* thread_ = nullptr;
     volatile bool stop_ = false;
 };

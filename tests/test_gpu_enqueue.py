@@ -650,3 +650,47 @@ def test_queues_created_while_a_peer_stream_is_parked():
 
     pair(rank0, rank1)
     assert torch.equal(got["dst"], payload.cpu())
+
+
+@pytest.mark.parametrize("nbytes", [1000, 1 << 20])
+def test_receives_complete_out_of_posting_order(nbytes):
+    """Rank 1 posts blocking receives for tag 2 then tag 1 before rank 0
+    sends tag 1 then tag 2 (legal MPI with eager or buffered sends): the
+    delivery of tag 1 must not sit in front of tag 2's on any stream."""
+    import threading
+    posted = threading.Event()
+    got = {}
+
+    def rank0(inst):
+        q = mp.queue_create(inst)
+        c, s = device_comm(inst, q)
+        assert posted.wait(60)
+        time.sleep(0.05)
+        a = torch.full((nbytes,), 1, dtype=torch.uint8, device=DEV)
+        b = torch.full((nbytes,), 2, dtype=torch.uint8, device=DEV)
+        reqs = [mp.isend_enqueue(c, a, nbytes, mp.BYTE, 1, 1),
+                mp.isend_enqueue(c, b, nbytes, mp.BYTE, 1, 2)]
+        mp.waitall_enqueue(reqs)
+        mp.queue_synchronize(q)
+        mp.comm_free(c)
+        mp.free_stream(s)
+        mp.queue_destroy(q)
+
+    def rank1(inst):
+        q = mp.queue_create(inst)
+        c, s = device_comm(inst, q)
+        x = torch.zeros(nbytes, dtype=torch.uint8, device=DEV)
+        y = torch.zeros(nbytes, dtype=torch.uint8, device=DEV)
+        r2 = mp.irecv_enqueue(c, x, nbytes, mp.BYTE, 0, 2)
+        mp.wait_enqueue(r2)                    # the stream reaches tag 1's post only after tag 2
+        r1 = mp.irecv_enqueue(c, y, nbytes, mp.BYTE, 0, 1)
+        mp.wait_enqueue(r1)
+        posted.set()
+        mp.queue_synchronize(q)
+        got["x"], got["y"] = x.cpu(), y.cpu()
+        mp.comm_free(c)
+        mp.free_stream(s)
+        mp.queue_destroy(q)
+
+    pair(rank0, rank1)
+    assert bool((got["x"] == 2).all()) and bool((got["y"] == 1).all())
