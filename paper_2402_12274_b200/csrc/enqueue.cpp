@@ -245,8 +245,6 @@ int record_new_event(cudaStream_t s, cudaEvent_t* ev) {
 
 // has the stream position recorded in `e` been reached (and passed)?
 bool ev_done(cudaEvent_t e) {
-    static const bool never_defer = std::getenv("MPX_NO_DEFER") != nullptr;   // diagnosis
-    if (never_defer) return true;
     const cudaError_t q = cudaEventQuery(e);
     if (q != cudaSuccess) cudaGetLastError();
     return q != cudaErrorNotReady;

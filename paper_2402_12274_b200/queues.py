@@ -10,7 +10,6 @@ MinimpiErrors it raises are deferred to the next queue_synchronize exactly
 like the reference's executor (offload.py:97-100, 111-119).
 """
 
-import os
 import threading
 
 import torch
@@ -122,8 +121,6 @@ def order_after_caller(stream):
     current stream (program order, as the reference's serial queue gives):
     the queue's stream waits on an event of the current stream when they
     differ."""
-    if os.environ.get("MPX_NO_CALLER_ORDER"):      # diagnosis
-        return
     cur = torch.cuda.current_stream(stream.device)
     if cur.cuda_stream != stream.cuda_stream:
         stream.wait_stream(cur)
