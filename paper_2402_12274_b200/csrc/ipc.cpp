@@ -12,6 +12,7 @@
 
 #include <atomic>
 #include <cerrno>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -212,26 +213,40 @@ int IpcWorld::reserve(int64_t bytes, uint8_t** dst, int64_t* off, uint32_t** rea
     if (len > arena_bytes_)
         return fail(MPX_ERR_EXHAUSTED, "message of %lld bytes exceeds the %lld-byte staging arena (MPX_IPC_ARENA)",
                     (long long)bytes, (long long)arena_bytes_);
-    // reclaim consumed slots from the head of the ring
-    size_t k = 0;
-    while (k < inflight_.size() &&
-           *reinterpret_cast<volatile uint32_t*>(&sh_->flags[rank_][inflight_[k].idx]) >= inflight_[k].gen)
-        ++k;
-    if (k) {
-        inflight_.erase(inflight_.begin(), inflight_.begin() + (long)k);
-        head_ = inflight_.empty() ? tail_ : inflight_.front().off;
-        if (inflight_.empty()) head_ = tail_ = 0;
-    }
-    // place [o, o+len): after tail_, wrapping to 0 when it does not fit
-    int64_t o = tail_;
-    const bool wrapped = !inflight_.empty() && tail_ < head_;
-    if (!wrapped) {
-        if (o + len > arena_bytes_) {
-            if (inflight_.empty() || len <= head_) o = 0;
-            else return fail(MPX_ERR_EXHAUSTED, "staging arena full: receivers have not consumed earlier messages");
+    // Room is made by receivers consuming earlier messages (they write the
+    // consumed flags from their streams).  The host runs ahead of the GPUs, so
+    // when the ring is full wait for that (polling the flags; no GPU call),
+    // up to MPX_IPC_WAIT seconds, before reporting the arena exhausted.
+    static const double limit_s = std::getenv("MPX_IPC_WAIT") ? std::atof(std::getenv("MPX_IPC_WAIT")) : 60.0;
+    int64_t o = 0;
+    for (long spins = 0;; ++spins) {
+        size_t k = 0;   // reclaim consumed slots from the head of the ring
+        while (k < inflight_.size() &&
+               *reinterpret_cast<volatile uint32_t*>(&sh_->flags[rank_][inflight_[k].idx]) >= inflight_[k].gen)
+            ++k;
+        if (k) {
+            inflight_.erase(inflight_.begin(), inflight_.begin() + (long)k);
+            head_ = inflight_.empty() ? tail_ : inflight_.front().off;
+            if (inflight_.empty()) head_ = tail_ = 0;
         }
-    } else if (o + len > head_) {
-        return fail(MPX_ERR_EXHAUSTED, "staging arena full: receivers have not consumed earlier messages");
+        // place [o, o+len): after tail_, wrapping to 0 when it does not fit
+        o = tail_;
+        bool fits;
+        const bool wrapped = !inflight_.empty() && tail_ < head_;
+        if (!wrapped) {
+            fits = o + len <= arena_bytes_;
+            if (!fits && (inflight_.empty() || len <= head_)) {
+                o = 0;
+                fits = true;
+            }
+        } else {
+            fits = o + len <= head_;
+        }
+        if (fits) break;
+        if (spins * 20e-6 > limit_s)
+            return fail(MPX_ERR_EXHAUSTED, "staging arena full for %.0f s: receivers have not consumed earlier messages",
+                        limit_s);
+        nap(20000);
     }
     tail_ = o + len;
     uint32_t cgen;
