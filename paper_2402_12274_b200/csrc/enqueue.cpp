@@ -1099,6 +1099,56 @@ int ipc_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t count, Datatype*
     return MPX_SUCCESS;
 }
 
+// Multi-process allreduce: every rank copies its contribution into the
+// collective area of its arena, then -- once every peer's contribution is in
+// place (ready counters) -- reduces ALL slices locally in rank order with the
+// native one-shot kernel reading the peers' areas, and bumps its read counter
+// so the peers may overwrite their areas for the next collective.  Ordered
+// entirely by stream memops on the caller's stream; collectives must be
+// called in the same order on every rank (MPI's rule).
+int ipc_allreduce(const std::shared_ptr<Comm>& c, const void* sendbuf, void* recvbuf, int64_t count, int dtype_code,
+                  int es) {
+    World* w = c->w;
+    IpcWorld* ipc = w->ipc;
+    const int n = w->size, me = c->rank;
+    if (n > kMaxCollRanks) return fail(MPX_ERR_UNSUPPORTED, "native allreduce supports <= %d ranks", kMaxCollRanks);
+    const int64_t bytes = count * es;
+    if (bytes > ipc->coll_bytes())
+        return fail(MPX_ERR_UNSUPPORTED, "allreduce of %lld bytes exceeds the %lld-byte collective area (1/4 of "
+                    "MPX_IPC_ARENA)", (long long)bytes, (long long)ipc->coll_bytes());
+    MPX_RC(set_device(c->device));
+    const uint32_t seq = ipc->next_coll_seq();
+    // the table of this call: send[p] = p's area (constant), recv[*] = my buffer
+    CollTable* tab = nullptr;
+    {
+        std::lock_guard<std::mutex> g(w->coll_mu);
+        auto it = w->area.find(-1 - c->device);     // per-device table of the multi-process world
+        if (it == w->area.end()) {
+            CollRing* r = nullptr;
+            MPX_CU(cudaMalloc(reinterpret_cast<void**>(&r), sizeof(CollTable)));
+            it = w->area.emplace(-1 - c->device, r).first;
+        }
+        tab = reinterpret_cast<CollTable*>(it->second);
+    }
+    cudaStream_t st = c->stream;
+    for (int q = 0; q < n; ++q)   // peers have read my previous contribution
+        if (q != me) MPX_RC(wait_flag(st, ipc->coll_read(q), seq - 1));
+    MPX_CU(cudaMemcpyAsync(ipc->my_coll_area(), sendbuf, (size_t)bytes, cudaMemcpyDeviceToDevice, st));
+    MPX_RC(write_flag(st, ipc->coll_ready(me), seq));
+    for (int q = 0; q < n; ++q)
+        if (q != me) MPX_RC(wait_flag(st, ipc->coll_ready(q), seq));
+    for (int q = 0; q < n; ++q) {
+        MPX_RC(write_ptr(st, &tab->send[q], ipc->coll_area(q)));
+        MPX_RC(write_ptr(st, (const void* const*)&tab->recv[q], recvbuf));
+    }
+    for (int s = 0; s < n; ++s) {   // every slice, rank-ordered sum, into my buffer only
+        cudaError_t e = launch_allreduce_oneshot(tab, n, s, count, dtype_code, c->device, st);
+        if (e != cudaSuccess) return cuda_fail(e, "allreduce kernel");
+    }
+    MPX_RC(write_flag(st, ipc->coll_read(me), seq));
+    return MPX_SUCCESS;
+}
+
 mpx_request publish_req(const std::shared_ptr<ReqState>& q) {
     std::lock_guard<std::mutex> g(g_handles_mu);
     g_reqs[q.get()] = q;
@@ -1540,13 +1590,13 @@ int mpx_allreduce_enqueue(mpx_comm h, const void* sendbuf, void* recvbuf, int64_
                           int algo) {
     auto c = comm_of(h);
     if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
-    if (c->w->ipc) return fail(MPX_ERR_UNSUPPORTED, "allreduce_enqueue across processes is not implemented yet");
     if (op != MPX_OP_SUM) return fail(MPX_ERR_ARG, "unsupported reduction op %d (only SUM)", op);
     const int es = elem_size(dtype_code);
     if (!es) return fail(MPX_ERR_ARG, "allreduce supports INT32, INT64, FLOAT32 and FLOAT64");
     if (count < 0) return fail(MPX_ERR_ARG, "count must be a nonnegative int");
     if (count == 0) return MPX_SUCCESS;  // comm.py:572-574
     World* w = c->w;
+    if (w->ipc) return ipc_allreduce(c, sendbuf, recvbuf, count, dtype_code, es);
     MPX_RC(set_device(c->device));
     bool distinct = true;
     {

@@ -128,6 +128,7 @@ int IpcWorld::join(const char* name, int size, int rank, int device, int64_t are
     cudaGetDevice(&cur);
     MPX_CU_RET(cudaSetDevice(device));
     w->arena_bytes_ = arena_bytes;
+    w->coll_off_ = (arena_bytes - arena_bytes / 4) & ~int64_t(255);
     MPX_CU_RET(cudaMalloc(reinterpret_cast<void**>(&w->arena_), (size_t)arena_bytes));
     MPX_CU_RET(cudaIpcGetMemHandle(&sh->arena[rank], w->arena_));
     MPX_CU_RET(cudaHostRegister(p, w->map_bytes_, cudaHostRegisterMapped | cudaHostRegisterPortable));
@@ -200,8 +201,11 @@ uint32_t* IpcWorld::local_flag(uint32_t* gen) {
     return flag_locked(gen);
 }
 
+uint32_t* IpcWorld::coll_ready(int r) { return &sh_->flags[r][kFlags - 1]; }
+uint32_t* IpcWorld::coll_read(int r) { return &sh_->flags[r][kFlags - 2]; }
+
 uint32_t* IpcWorld::flag_locked(uint32_t* gen) {
-    const uint32_t i = next_flag_++ % kFlags;
+    const uint32_t i = next_flag_++ % (kFlags - 2);   // the last two are the collective counters
     *gen = ++shadow_[i];
     return &sh_->flags[rank_][i];
 }
@@ -210,9 +214,9 @@ int IpcWorld::reserve(int64_t bytes, uint8_t** dst, int64_t* off, uint32_t** rea
                       uint32_t* cons_idx, uint32_t* cons_gen) {
     std::lock_guard<std::mutex> g(mu_);
     const int64_t len = std::max<int64_t>(256, (bytes + 255) & ~int64_t(255));
-    if (len > arena_bytes_)
-        return fail(MPX_ERR_EXHAUSTED, "message of %lld bytes exceeds the %lld-byte staging arena (MPX_IPC_ARENA)",
-                    (long long)bytes, (long long)arena_bytes_);
+    if (len > coll_off_)
+        return fail(MPX_ERR_EXHAUSTED, "message of %lld bytes exceeds the %lld-byte staging ring (3/4 of MPX_IPC_ARENA)",
+                    (long long)bytes, (long long)coll_off_);
     // Room is made by receivers consuming earlier messages (they write the
     // consumed flags from their streams).  The host runs ahead of the GPUs, so
     // when the ring is full wait for that (polling the flags; no GPU call),
@@ -234,7 +238,7 @@ int IpcWorld::reserve(int64_t bytes, uint8_t** dst, int64_t* off, uint32_t** rea
         bool fits;
         const bool wrapped = !inflight_.empty() && tail_ < head_;
         if (!wrapped) {
-            fits = o + len <= arena_bytes_;
+            fits = o + len <= coll_off_;
             if (!fits && (inflight_.empty() || len <= head_)) {
                 o = 0;
                 fits = true;

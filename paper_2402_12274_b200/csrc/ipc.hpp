@@ -76,6 +76,17 @@ class IpcWorld {
     // until it reports the delivery enqueued)
     void defer(void* cookie, const IpcMsg& m);
 
+    // collectives: the last quarter of every rank's arena is its
+    // contribution area (mapped by every peer); per rank two flags in shared
+    // memory count the collectives whose contribution is in place (ready)
+    // and whose peer contributions it has finished reading (read)
+    const uint8_t* coll_area(int r) const { return peer_[r] + coll_off_; }
+    uint8_t* my_coll_area() const { return arena_ + coll_off_; }
+    int64_t coll_bytes() const { return arena_bytes_ - coll_off_; }
+    uint32_t* coll_ready(int r);
+    uint32_t* coll_read(int r);
+    uint32_t next_coll_seq() { return ++coll_seq_; }
+
   private:
     IpcWorld() = default;
     void progress_loop();
@@ -89,6 +100,8 @@ class IpcWorld {
     size_t map_bytes_ = 0;
     uint8_t* arena_ = nullptr;
     int64_t arena_bytes_ = 0;
+    int64_t coll_off_ = 0;      // [0, coll_off_): point-to-point ring; rest: collective area
+    uint32_t coll_seq_ = 0;
     std::vector<const uint8_t*> peer_;
     IpcOnMatch cb_ = nullptr;
     struct Slot {

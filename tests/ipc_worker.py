@@ -122,6 +122,28 @@ def any_source_and_truncation(inst, q, c):
     mp.barrier(inst.world)
 
 
+def allreduce(inst, q, c):
+    """allreduce_enqueue across processes: rank-ordered sums (float32
+    accumulated in double, comm.py:582-588) and exact int64, several calls
+    back to back (the collective area is reused in stream order)."""
+    dev, n = inst.device, inst.size
+    for count in (1, 1000, 1 << 20):
+        xs = [np.random.default_rng(7 * count + r).uniform(-1, 1, count).astype(np.float32) for r in range(n)]
+        ks = [np.random.default_rng(9 * count + r).integers(-2 ** 20, 2 ** 20, count) for r in range(n)]
+        sf = torch.from_numpy(xs[inst.rank]).to(dev)
+        si = torch.from_numpy(ks[inst.rank]).to(dev)
+        rf, ri = torch.empty_like(sf), torch.empty_like(si)
+        mp.allreduce_enqueue(c, sf, rf, count, mp.FLOAT32)
+        mp.allreduce_enqueue(c, si, ri, count, mp.INT64)
+        mp.queue_synchronize(q)
+        acc = np.zeros(count, np.float64)
+        for x in xs:
+            acc += x.astype(np.float64)
+        assert np.array_equal(rf.cpu().numpy(), acc.astype(np.float32)), count
+        assert np.array_equal(ri.cpu().numpy(), np.sum(ks, axis=0)), count
+    mp.barrier(inst.world)
+
+
 def main():
     inst = mp.init(transport="ipc")
     assert inst.transport == "ipc"
@@ -133,6 +155,7 @@ def main():
             for order in ("recv", "send"):
                 ring(inst, q, c, nbytes, typed, order)
     tags_out_of_order(inst, q, c)
+    allreduce(inst, q, c)
     if inst.size >= 2:
         any_source_and_truncation(inst, q, c)
     t0 = time.perf_counter()
