@@ -313,6 +313,15 @@ def run_extras(dev, flush, args):
                                                              group="bench-ar1")
     except Exception as exc:  # report, never fail the headline
         out["enqueue_error"] = repr(exc)
+    try:   # multi-process world: 2 processes (one rank each) sharing this GPU via CUDA IPC
+        import subprocess
+        env = dict(os.environ, IPC_BENCH_LG="26")
+        p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ipc_bench.py"), "2"], env=env,
+                           capture_output=True, text=True, timeout=180)
+        rows = [json.loads(x) for x in p.stdout.splitlines() if x.startswith("{")]
+        out["ring_2processes_1gpu_64MiB"] = rows if rows else {"error": p.stderr[-300:]}
+    except Exception as exc:
+        out["ipc_error"] = repr(exc)
     return out
 
 

@@ -30,7 +30,8 @@ def worker(out_dir):
     c = mp.stream_comm_create(inst.world, s)
     r, n, dev = inst.rank, inst.size, inst.device
     res = []
-    for lg in (12, 16, 20, 24, 26):
+    sizes = [int(x) for x in os.environ.get("IPC_BENCH_LG", "12,16,20,24,26").split(",")]
+    for lg in sizes:
         for kind in ("u8", "vector"):
             nb = 1 << lg
             if kind == "u8":
