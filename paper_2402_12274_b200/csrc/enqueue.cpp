@@ -30,6 +30,7 @@
 #include <dlfcn.h>
 #include <execinfo.h>
 #include <signal.h>
+#include <sys/prctl.h>
 #include <sys/syscall.h>
 #include <unistd.h>
 #include <time.h>
@@ -431,6 +432,7 @@ struct World {
         if (!defer_thread.joinable()) defer_thread = std::thread([this] { defer_loop(); });
     }
     void defer_loop() {
+        prctl(PR_SET_TIMERSLACK, 1UL, 0, 0, 0);   // short naps really are short (default slack: 50 us)
         std::vector<std::function<bool()>> mine;
         long idle = 0;
         for (;;) {
