@@ -203,9 +203,10 @@ int mpx_stream_device(void *stream, int *device);
  * live in a shared-memory segment; every message is packed into the
  * sender's arena at its stream position and unpacked by the receiving
  * process straight from there.  Stream communicators and the send / recv /
- * isend / irecv / wait enqueue calls and allreduce_enqueue (rank-ordered,
- * through the last quarter of every arena) work unchanged on such a world;
- * windows return MPX_ERR_UNSUPPORTED for now. */
+ * isend / irecv / wait enqueue calls, allreduce_enqueue (rank-ordered,
+ * through the last quarter of every arena) and read windows (IPC handles of
+ * the exposed allocations exchanged at win_create) work unchanged on such a
+ * world. */
 int mpx_ipc_world_join(const char *job, int size, int rank, int device, int64_t eager_limit,
                        int64_t arena_bytes, mpx_world *out);
 /* host barrier over the processes of a multi-process world */

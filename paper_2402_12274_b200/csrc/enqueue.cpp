@@ -1668,7 +1668,17 @@ int mpx_win_create(mpx_comm h, const void* base, int64_t bytes, int64_t disp_uni
     if (disp_unit < 1) return fail(MPX_ERR_ARG, "disp_unit must be a positive int");
     if (bytes < 0 || (bytes > 0 && !base)) return fail(MPX_ERR_ARG, "bad window region");
     World* w = c->w;
-    if (w->ipc) return fail(MPX_ERR_UNSUPPORTED, "windows across processes are not implemented yet");
+    if (w->ipc) {   // one rank per process: exchange IPC handles through the job's segment
+        const int64_t id = w->next_win[(size_t)c->rank]++;
+        World::Win win;
+        MPX_RC(set_device(c->device));
+        MPX_RC(w->ipc->win_expose(id, base, bytes, disp_unit, &win.base, &win.bytes, &win.unit));
+        win.registered = w->size;
+        std::lock_guard<std::mutex> g(w->win_mu);
+        w->wins[id] = win;
+        *win_id = id;
+        return MPX_SUCCESS;
+    }
     std::unique_lock<std::mutex> lk(w->win_mu);
     const int64_t id = w->next_win[(size_t)c->rank]++;
     World::Win& win = w->wins[id];
@@ -1750,6 +1760,14 @@ int mpx_win_free(mpx_comm h, int64_t id) {
     auto c = comm_of(h);
     if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
     World* w = c->w;
+    if (w->ipc) {   // collective; the mappings stay cached until the world ends
+        {
+            std::lock_guard<std::mutex> g(w->win_mu);
+            if (!w->wins.count(id)) return fail(MPX_ERR_STATE, "window already freed");
+            w->wins.erase(id);
+        }
+        return w->ipc->barrier();
+    }
     std::unique_lock<std::mutex> lk(w->win_mu);
     auto it = w->wins.find(id);
     if (it == w->wins.end()) return fail(MPX_ERR_STATE, "window already freed");

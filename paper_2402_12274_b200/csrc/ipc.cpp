@@ -2,6 +2,7 @@
 // multi-process worlds (see ipc.hpp).
 #include "ipc.hpp"
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <fcntl.h>
 #include <pthread.h>
@@ -62,6 +63,14 @@ void nap(long ns) {
 }
 }  // namespace
 
+constexpr int kWins = 32;   // window slots (window id mod kWins) per job
+
+struct WinEntry {
+    cudaIpcMemHandle_t handle;
+    int64_t off, bytes, unit;
+    int64_t id;
+};
+
 struct IpcShared {
     std::atomic<uint32_t> magic;
     int32_t size;
@@ -71,6 +80,7 @@ struct IpcShared {
     int64_t arena_bytes[kMaxRanks];
     cudaIpcMemHandle_t arena[kMaxRanks];
     Box box[kMaxRanks];
+    WinEntry win[kWins][kMaxRanks];
     alignas(64) uint32_t flags[kMaxRanks][kFlags];
 };
 
@@ -186,6 +196,7 @@ int IpcWorld::leave() {
     int rc = barrier();
     for (int r = 0; r < size_; ++r)
         if (r != rank_ && peer_[r]) cudaIpcCloseMemHandle(const_cast<uint8_t*>(peer_[r]));
+    for (auto& kv : opened_) cudaIpcCloseMemHandle(kv.second);
     rc = rc ? rc : barrier();   // nobody frees its arena while a peer still maps it
     if (arena_) cudaFree(arena_);
     cudaHostUnregister(sh_);
@@ -357,6 +368,58 @@ int IpcWorld::recv(int ctx, int src, int tag, int64_t cap, void* cookie, bool* m
     pthread_mutex_unlock(&b.mu);
     *matched = false;
     return MPX_SUCCESS;
+}
+
+int IpcWorld::win_expose(int64_t id, const void* base, int64_t bytes, int64_t unit, std::vector<const void*>* bases,
+                         std::vector<int64_t>* sizes, std::vector<int64_t>* units) {
+    using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static RangeFn range = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &f, 12000, cudaEnableDefault, &q);
+        cudaGetLastError();
+        return reinterpret_cast<RangeFn>(f);
+    }();
+    if (!range) return fail(MPX_ERR_UNSUPPORTED, "cuMemGetAddressRange unavailable");
+    WinEntry& mine = sh_->win[id % kWins][rank_];
+    std::memset(static_cast<void*>(&mine), 0, sizeof mine);
+    if (bytes > 0) {
+        CUdeviceptr alloc = 0;
+        size_t len = 0;
+        if (range(&alloc, &len, reinterpret_cast<CUdeviceptr>(base)) != CUDA_SUCCESS)
+            return fail(MPX_ERR_ARG, "window region is not device memory of this process");
+        MPX_CU_RET(cudaIpcGetMemHandle(&mine.handle, reinterpret_cast<void*>(alloc)));
+        mine.off = static_cast<int64_t>(reinterpret_cast<uintptr_t>(base) - static_cast<uintptr_t>(alloc));
+    }
+    mine.bytes = bytes;
+    mine.unit = unit;
+    mine.id = id;
+    if (int rc = barrier()) return rc;   // every rank's entry is in place
+    bases->assign(size_, nullptr);
+    sizes->assign(size_, 0);
+    units->assign(size_, 1);
+    for (int r = 0; r < size_; ++r) {
+        const WinEntry& e = sh_->win[id % kWins][r];
+        if (e.id != id) return fail(MPX_ERR_STATE, "window %lld: ranks disagree on the window order", (long long)id);
+        (*sizes)[r] = e.bytes;
+        (*units)[r] = e.unit;
+        if (e.bytes == 0) continue;
+        if (r == rank_) {
+            (*bases)[r] = base;
+            continue;
+        }
+        // one mapping per (rank, allocation): a handle opens once per process
+        std::string key = std::to_string(r) + ":" + std::string(e.handle.reserved, sizeof e.handle.reserved);
+        void* mapped = nullptr;
+        for (auto& kv : opened_)
+            if (kv.first == key) mapped = kv.second;
+        if (!mapped) {
+            MPX_CU_RET(cudaIpcOpenMemHandle(&mapped, e.handle, cudaIpcMemLazyEnablePeerAccess));
+            opened_.emplace_back(key, mapped);
+        }
+        (*bases)[r] = static_cast<const uint8_t*>(mapped) + e.off;
+    }
+    return barrier();    // nobody reuses the slot before every rank has read it
 }
 
 void IpcWorld::defer(void* cookie, const IpcMsg& m) {

@@ -87,6 +87,12 @@ class IpcWorld {
     uint32_t* coll_read(int r);
     uint32_t next_coll_seq() { return ++coll_seq_; }
 
+    // windows: collective; publishes this rank's region (an IPC handle of the
+    // allocation that holds it + offset) and maps every peer's.  base[r] is
+    // rank r's region in this process (nullptr for an empty region).
+    int win_expose(int64_t id, const void* base, int64_t bytes, int64_t unit, std::vector<const void*>* bases,
+                   std::vector<int64_t>* sizes, std::vector<int64_t>* units);
+
   private:
     IpcWorld() = default;
     void progress_loop();
@@ -102,6 +108,7 @@ class IpcWorld {
     int64_t arena_bytes_ = 0;
     int64_t coll_off_ = 0;      // [0, coll_off_): point-to-point ring; rest: collective area
     uint32_t coll_seq_ = 0;
+    std::vector<std::pair<std::string, void*>> opened_;   // (rank + handle bytes) -> mapping
     std::vector<const uint8_t*> peer_;
     IpcOnMatch cb_ = nullptr;
     struct Slot {

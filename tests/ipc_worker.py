@@ -144,6 +144,47 @@ def allreduce(inst, q, c):
     mp.barrier(inst.world)
 
 
+def windows(inst):
+    """Passive-target reads across processes: every rank exposes a device
+    tensor, reads its successor's window through a strided target type into a
+    strided origin layout at a displacement (bytes checked against the
+    oracle's copy_between), then a contiguous read and an out-of-bounds read
+    rejected at unlock."""
+    dev, r, n = inst.device, inst.rank, inst.size
+    tspec = ("vector", 512, 4, 8, ("basic", 8))
+    ospec = ("vector", 256, 8, 12, ("basic", 8))
+    ts, os_ = oracle.OracleType(tspec), oracle.OracleType(ospec)
+    disp = 3
+    wbytes = ts.max_end + disp * 8 + 64
+    win_t = torch.from_numpy(data(500 + r, wbytes)).to(dev)
+    win = mp.win_create(inst.world, win_t, disp_unit=8)
+    tgt = (r + 1) % n
+    out = torch.full((os_.max_end,), 0x5A, dtype=torch.uint8, device=dev)
+    tdt = mp.type_vector(512, 4, 8, mp.FLOAT64).commit()
+    odt = mp.type_vector(256, 8, 12, mp.FLOAT64).commit()
+    mp.win_lock(win, tgt)
+    mp.win_get(win, out, 1, odt, tgt, disp, 1, tdt)
+    plain = torch.zeros(64, dtype=torch.uint8, device=dev)
+    mp.win_get(win, plain, 64, mp.BYTE, tgt, 1, 64, mp.BYTE)
+    mp.win_unlock(win, tgt)
+    src = data(500 + tgt, wbytes)
+    ref = np.full(os_.max_end, 0x5A, np.uint8)
+    assert oracle.copy_between(ts, 1, src[disp * 8:], os_, 1, ref) == ts.size_bytes
+    assert np.array_equal(out.cpu().numpy(), ref)
+    assert np.array_equal(plain.cpu().numpy(), src[8:72])
+    mp.win_lock(win, tgt)
+    mp.win_get(win, plain, 64, mp.BYTE, tgt, wbytes // 8, 64, mp.BYTE)     # beyond the target's region
+    try:
+        mp.win_unlock(win, tgt)
+        raise AssertionError("out-of-bounds read was not rejected")
+    except mp.ArgError:
+        pass
+    mp.barrier(inst.world)
+    mp.win_free(win)
+    mp.type_free(tdt)
+    mp.type_free(odt)
+
+
 def main():
     inst = mp.init(transport="ipc")
     assert inst.transport == "ipc"
@@ -156,6 +197,7 @@ def main():
                 ring(inst, q, c, nbytes, typed, order)
     tags_out_of_order(inst, q, c)
     allreduce(inst, q, c)
+    windows(inst)
     if inst.size >= 2:
         any_source_and_truncation(inst, q, c)
     t0 = time.perf_counter()

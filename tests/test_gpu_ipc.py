@@ -2,7 +2,8 @@
 processes, one rank each, sharing the box's GPU through CUDA IPC.  Each rank
 runs tests/ipc_worker.py (rings of bytes and strided FLOAT64 vectors with the
 receive or the send posted first, tags matched out of order, ANY_SOURCE,
-truncation, staging-arena reuse, allreduce_enqueue in float32 and int64)
+truncation, staging-arena reuse, allreduce_enqueue in float32 and int64,
+read windows with strided types and bounds rejection)
 and checks every byte against the CPU oracle / rank-ordered host sums."""
 
 import os
