@@ -3,7 +3,8 @@
 
 The reference ships a GET_REQ frame of flattened target segments and the
 target gathers them in its progress path (:76-125, :198-239).  Here every rank
-of the in-process world exposes device memory (peer-accessible over NVLink),
+exposes device memory -- peer-accessible over NVLink in an in-process world,
+mapped through CUDA IPC handles exchanged at win_create in a multi-process one --
 so a read is fully origin-driven: ``get`` moves the target bytes described by
 (target_disp x the target's unit, target type) straight into the origin
 layout with the datatype kernels -- the one-pass zipper when both layouts are
