@@ -185,6 +185,18 @@ def windows(inst):
     mp.type_free(odt)
 
 
+def host_buffers(inst):
+    """The reference's plain p2p surface on the world communicator with host
+    (bytes / bytearray) buffers, across processes."""
+    if inst.rank == 0:
+        mp.send(inst.world, b"across processes", 16, mp.BYTE, 1, 11)
+    elif inst.rank == 1:
+        buf = bytearray(16)
+        st = mp.recv(inst.world, buf, 16, mp.BYTE, 0, 11)
+        assert bytes(buf) == b"across processes" and st.source == 0 and st.count == 16, (buf, st)
+    mp.barrier(inst.world)
+
+
 def main():
     inst = mp.init(transport="ipc")
     assert inst.transport == "ipc"
@@ -198,6 +210,7 @@ def main():
     tags_out_of_order(inst, q, c)
     allreduce(inst, q, c)
     windows(inst)
+    host_buffers(inst)
     if inst.size >= 2:
         any_source_and_truncation(inst, q, c)
     t0 = time.perf_counter()
