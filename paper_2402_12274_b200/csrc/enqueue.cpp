@@ -482,6 +482,7 @@ struct World {
 struct Comm {
     ~Comm() {
         if (side) stream_pool().release(device, side);
+        if (late) stream_pool().release(device, late);
     }
     World* w = nullptr;
     int rank = 0, ctx = 0, device = 0;
@@ -498,6 +499,20 @@ struct Comm {
             if (side_err != cudaSuccess) side = nullptr;
         });
         return side;
+    }
+    // Deferred deliveries (World::defer) are enqueued here, and only once
+    // every stream point they depend on has been reached: they never wait,
+    // so they can never sit behind -- or hold up -- the side stream's
+    // program-ordered work.
+    cudaStream_t late = nullptr;
+    std::once_flag late_once;
+    cudaError_t late_err = cudaSuccess;
+    cudaStream_t late_stream() {
+        std::call_once(late_once, [this] {
+            late_err = stream_pool().acquire(device, &late);
+            if (late_err != cudaSuccess) late = nullptr;
+        });
+        return late;
     }
     std::mutex err_mu;
     std::deque<std::pair<int, std::string>> deferred;
@@ -734,24 +749,25 @@ int do_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t buf_bytes, 
         MPX_RC(record_new_event(c->stream, &staged));
         if (!c->side_stream()) return cuda_fail(c->side_err, "cudaStreamCreate(side)");
         auto deliver = [c, staged, ev = pr.ev, r = pr.r, flag = pr.flag, gen = pr.gen, staging = ps.staging,
-                        moved]() -> int {
+                        moved](cudaStream_t st) -> int {
             MPX_RC(set_device(c->device));
-            MPX_CU(cudaStreamWaitEvent(c->side_stream(), staged, 0));
-            MPX_CU(cudaStreamWaitEvent(c->side_stream(), ev, 0));
-            MPX_RC(launch_move(c->device, r.dt, r.count, false, staging, r.buf, moved, c->side_stream()));
+            if (!st) return cuda_fail(c->late_err, "cudaStreamCreate(late)");
+            MPX_CU(cudaStreamWaitEvent(st, staged, 0));
+            MPX_CU(cudaStreamWaitEvent(st, ev, 0));
+            MPX_RC(launch_move(c->device, r.dt, r.count, false, staging, r.buf, moved, st));
             MPX_RC(set_device(c->device));
-            MPX_CU(cudaFreeAsync(staging, c->side_stream()));
-            MPX_RC(write_flag(c->side_stream(), flag, gen));
+            MPX_CU(cudaFreeAsync(staging, st));
+            MPX_RC(write_flag(st, flag, gen));
             cudaEventDestroy(staged);
             cudaEventDestroy(ev);
             return MPX_SUCCESS;
         };
-        if (ev_done(pr.ev) && ev_done(staged)) {
-            MPX_RC(deliver());
-        } else {   // an input is behind earlier work on its stream: deliver later
+        if (ev_done(pr.ev)) {   // the side stream waits only for this rank's own staging point
+            MPX_RC(deliver(c->side_stream()));
+        } else {   // the receive's post point is behind earlier work: deliver later
             w->defer([deliver, c, ev = pr.ev, staged]() {
                 if (!ev_done(ev) || !ev_done(staged)) return false;
-                if (int rc = deliver()) defer_error(c, rc, "deferred delivery failed: " + g_last_error);
+                if (int rc = deliver(c->late_stream())) defer_error(c, rc, "deferred delivery failed: " + g_last_error);
                 return true;
             });
         }
@@ -766,10 +782,11 @@ int do_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t buf_bytes, 
         cudaEvent_t fork;
         MPX_RC(record_new_event(c->stream, &fork));
         if (!c->side_stream()) return cuda_fail(c->side_err, "cudaStreamCreate(side)");
-        if (!ev_done(pr.ev) || !ev_done(fork)) {
-            // an input (the receive's post point, or this send's own stream
-            // position) is still behind earlier work: deliver from the world's
-            // deferral thread; the send request completes on a flag
+        if (!ev_done(pr.ev)) {
+            // the receive's post point is still behind earlier work on the
+            // receiver's stream: the world's deferral thread enqueues it on the
+            // late stream once every input is reached; the send request
+            // completes on a flag
             uint32_t* done = nullptr;
             uint32_t dgen = 0;
             w->flags.take(&done, &dgen);
@@ -779,7 +796,8 @@ int do_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t buf_bytes, 
             w->defer([c, fork, ev = pr.ev, s, r = pr.r, flag = pr.flag, gen = pr.gen, moved, done, dgen]() {
                 if (!ev_done(ev) || !ev_done(fork)) return false;
                 int rc = set_device(c->device);
-                cudaStream_t side = c->side_stream();
+                cudaStream_t side = c->late_stream();
+                if (!rc && !side) rc = cuda_fail(c->late_err, "cudaStreamCreate(late)");
                 if (!rc && cudaStreamWaitEvent(side, fork, 0) != cudaSuccess) rc = fail(MPX_ERR_OTHER, "wait");
                 if (!rc) rc = transfer(c->device, side, s, r, moved);
                 if (!rc) rc = set_device(c->device);
@@ -875,12 +893,13 @@ int do_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t buf_bytes, int64_
     cudaStream_t st = c->stream;
     cudaEvent_t fork0 = nullptr;
     if (!blocking) MPX_RC(record_new_event(c->stream, &fork0));
-    if (!blocking && (!ev_done(ps.ev) || !ev_done(fork0))) {
-        // an input (the send's data point, or this receive's own stream
-        // position) is still behind earlier work: deliver from the world's
-        // deferral thread, complete on a flag.  Nothing on a side stream
-        // ever waits for an unreached point, so a delivery cannot hold up a
-        // later, independent one queued behind it.
+    if (!blocking && !ev_done(ps.ev)) {
+        // the send's data point is still behind earlier work on the
+        // sender's stream: the world's deferral thread enqueues it on the late
+        // stream once every input is reached (complete on a flag).  The side
+        // stream only ever waits for this rank's own, program-ordered stream
+        // points; nothing ever waits for a peer point that is not reached,
+        // so no delivery can hold up another queued behind it.
         cudaEvent_t fork = fork0;
         if (!c->side_stream()) return cuda_fail(c->side_err, "cudaStreamCreate(side)");
         uint32_t* done = nullptr;
@@ -892,7 +911,8 @@ int do_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t buf_bytes, int64_
         w->defer([w, c, fork, ps, r, moved, done, dgen]() {
             if (!ev_done(ps.ev) || !ev_done(fork)) return false;
             int rc = set_device(c->device);
-            cudaStream_t side = c->side_stream();
+            cudaStream_t side = c->late_stream();
+            if (!rc && !side) rc = cuda_fail(c->late_err, "cudaStreamCreate(late)");
             if (!rc && cudaStreamWaitEvent(side, fork, 0) != cudaSuccess) rc = fail(MPX_ERR_OTHER, "wait");
             if (!rc && cudaStreamWaitEvent(side, ps.ev, 0) != cudaSuccess) rc = fail(MPX_ERR_OTHER, "wait");
             if (!rc) {
