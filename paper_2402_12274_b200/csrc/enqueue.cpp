@@ -1003,8 +1003,9 @@ bool ipc_on_match(void* cookie, const IpcMsg& m) {
     const auto& c = p->c;
     int64_t moved = 0;
     int rc = q == cudaSuccess ? MPX_SUCCESS : cuda_fail(q, "cudaEventQuery");
-    cudaStream_t st = c->side_stream();
-    if (!rc && !st) rc = cuda_fail(c->side_err, "cudaStreamCreate(side)");
+    // every input is reached: the late stream (never behind a waiting op)
+    cudaStream_t st = c->late_stream();
+    if (!rc && !st) rc = cuda_fail(c->late_err, "cudaStreamCreate(late)");
     if (!rc) rc = ipc_deliver(c, st, p->r, m, &moved);
     if (!rc) rc = write_flag(st, p->flag, p->gen);
     cudaEventDestroy(p->ev);
