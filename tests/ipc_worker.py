@@ -197,6 +197,36 @@ def host_buffers(inst):
     mp.barrier(inst.world)
 
 
+def posted_first_then_matched(inst, q, c):
+    """rank 1: irecv A (posted first) and wait_enqueue(A), then irecv B that
+    matches an already-sent message; A's send arrives only afterwards.  B's
+    delivery waits (on the side stream) for rank 1's stream to pass A's wait,
+    so A's delivery -- by the progress thread -- must not queue behind it."""
+    dev = inst.device
+    if inst.rank == 0:
+        mp.send_enqueue(c, torch.full((4096,), 2, dtype=torch.uint8, device=dev), 4096, mp.BYTE, 1, 22)
+        mp.queue_synchronize(q)
+        mp.barrier(inst.world)          # 1: B is posted
+        mp.barrier(inst.world)          # 2: rank 1 has enqueued both receives
+        mp.send_enqueue(c, torch.full((4096,), 1, dtype=torch.uint8, device=dev), 4096, mp.BYTE, 1, 21)
+        mp.queue_synchronize(q)
+    elif inst.rank == 1:
+        a = torch.zeros(4096, dtype=torch.uint8, device=dev)
+        b = torch.zeros(4096, dtype=torch.uint8, device=dev)
+        ra = mp.irecv_enqueue(c, a, 4096, mp.BYTE, 0, 21)
+        mp.wait_enqueue(ra)
+        mp.barrier(inst.world)
+        rb = mp.irecv_enqueue(c, b, 4096, mp.BYTE, 0, 22)
+        mp.barrier(inst.world)
+        mp.wait_enqueue(rb)
+        mp.queue_synchronize(q)
+        assert bool((a == 1).all()) and bool((b == 2).all())
+    else:
+        mp.barrier(inst.world)
+        mp.barrier(inst.world)
+    mp.barrier(inst.world)
+
+
 def main():
     inst = mp.init(transport="ipc")
     assert inst.transport == "ipc"
@@ -208,6 +238,7 @@ def main():
             for order in ("recv", "send"):
                 ring(inst, q, c, nbytes, typed, order)
     tags_out_of_order(inst, q, c)
+    posted_first_then_matched(inst, q, c)
     allreduce(inst, q, c)
     windows(inst)
     host_buffers(inst)
