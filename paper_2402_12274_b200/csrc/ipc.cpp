@@ -143,6 +143,7 @@ int IpcWorld::join(const char* name, int size, int rank, int device, int64_t are
     MPX_CU_RET(cudaMalloc(reinterpret_cast<void**>(&w->arena_), (size_t)arena_bytes));
     MPX_CU_RET(cudaIpcGetMemHandle(&sh->arena[rank], w->arena_));
     MPX_CU_RET(cudaHostRegister(p, w->map_bytes_, cudaHostRegisterMapped | cudaHostRegisterPortable));
+    w->registered_ = true;
     sh->device[rank] = device;
     sh->arena_bytes[rank] = arena_bytes;
     w->shadow_.assign(kFlags, 0);
@@ -166,6 +167,15 @@ int IpcWorld::join(const char* name, int size, int rank, int device, int64_t are
     raw->thread_ = new std::thread([raw] { raw->progress_loop(); });
     *out = raw;
     return MPX_SUCCESS;
+}
+
+IpcWorld::~IpcWorld() {
+    for (int r = 0; r < (int)peer_.size(); ++r)
+        if (r != rank_ && peer_[r]) cudaIpcCloseMemHandle(const_cast<uint8_t*>(peer_[r]));
+    if (arena_) cudaFree(arena_);
+    if (registered_) cudaHostUnregister(sh_);
+    if (sh_) munmap(sh_, map_bytes_);
+    if (fd_ >= 0) close(fd_);
 }
 
 int IpcWorld::device_of(int r) const { return sh_->device[r]; }
@@ -204,6 +214,11 @@ int IpcWorld::leave() {
     munmap(sh_, map_bytes_);
     close(fd_);
     if (last) shm_unlink(name_.c_str());
+    peer_.clear();           // all released above: the destructor has nothing left to do
+    arena_ = nullptr;
+    registered_ = false;
+    sh_ = nullptr;
+    fd_ = -1;
     delete this;
     return rc;
 }

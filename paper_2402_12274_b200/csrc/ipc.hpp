@@ -93,6 +93,8 @@ class IpcWorld {
     int win_expose(int64_t id, const void* base, int64_t bytes, int64_t unit, std::vector<const void*>* bases,
                    std::vector<int64_t>* sizes, std::vector<int64_t>* units);
 
+    ~IpcWorld();       // frees what a failed join left behind (leave() empties it first)
+
   private:
     IpcWorld() = default;
     void progress_loop();
@@ -103,6 +105,7 @@ class IpcWorld {
     int size_ = 0, rank_ = 0, device_ = 0;
     int fd_ = -1;
     IpcShared* sh_ = nullptr;
+    bool registered_ = false;   // sh_ registered with CUDA
     size_t map_bytes_ = 0;
     uint8_t* arena_ = nullptr;
     int64_t arena_bytes_ = 0;
