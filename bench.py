@@ -44,8 +44,18 @@ WORKLOAD = ("cfg2: 12 halo faces (6 x 1-wide + 6 x 8-wide) of a 514^3 float32 ar
             "one step = fused pack of all faces + fused unpack into a second array")
 
 
+L2_NOTE = ("flushed between steps outside the timed events (256 MiB write, then 256 MiB read: "
+           "L2 cold and clean)")
+
+
 def face_specs():
     return cfg2_faces()
+
+
+def bench_config(world):
+    """The workload description both arms print (same dict => same_config)."""
+    return {"workload": WORKLOAD, "array": "514^3 float32", "faces": 12, "array_bytes": ARRAY_BYTES,
+            "payload_bytes_per_step": step_bytes(), "l2": L2_NOTE, "parallelism": "replicas x%d" % world}
 
 
 def face_bytes(spec):
@@ -219,7 +229,7 @@ def reference_arm(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded PCG64 bytes)",
-        "config": {"workload": WORKLOAD, "array": "514^3 float32", "faces": 12},
+        "config": bench_config(world),
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads,
                          "kind": "port",
                          "sample": "each step packs+unpacks all 12 cfg2 faces once with the C "
@@ -269,10 +279,36 @@ def _time_launch(fn, flush, reps):
     return float(np.median(ts))
 
 
+def _graph_batched(fn, reps, flush):
+    """Per-call time of `reps` back-to-back calls captured in one CUDA graph
+    (launch overhead amortised; L2 flushed before the replay only)."""
+    import torch
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        fn()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(reps):
+                fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(5):
+        flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts)) / reps
+
+
 def run_extras(dev, flush, args):
-    """BASELINE configs[0] and [2] (pack/unpack, L2 flushed per launch) and the
-    enqueue path (1-GPU: ranks share the device, so the ring is an HBM copy,
-    not NVLink).  Reported beside, not inside, the headline metric."""
+    """BASELINE configs[0] and [2] (pack/unpack, L2 flushed per launch), the
+    halo step split by face width, and the enqueue path on this one GPU
+    (in-process ranks share the device, so a ring is an HBM copy, not NVLink).
+    Reported beside, not inside, the headline metric."""
     import torch
     import paper_2402_12274_b200 as mp
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -281,6 +317,24 @@ def run_extras(dev, flush, args):
     from specbuild import build_product
     out = {}
     reps = max(3, min(args.steps, 10))
+    peak, _ = load_peak()
+
+    # ---- the headline step split by face width: the 1-wide faces lie inside
+    # the 8-wide ones, so the fused 12-face launch reuses lines between them
+    arr = torch.from_numpy(seeded_bytes(2, ARRAY_BYTES)).to(dev)
+    back = torch.zeros_like(arr)
+    for width in (1, 8):
+        faces = [(n, sp) for n, sp in face_specs() if min(sp[2]) == width]
+        dts = [build_product(sp, mp) for _, sp in faces]
+        pk = [torch.empty(face_bytes(sp), dtype=torch.uint8, device=dev) for _, sp in faces]
+        nb = sum(face_bytes(sp) for _, sp in faces)
+        tp = _time_launch(lambda: mp.pack_multi(dts, [arr] * len(dts), pk), flush, reps)
+        tu = _time_launch(lambda: mp.unpack_multi(dts, pk, [back] * len(dts)), flush, reps)
+        out["step_%dwide" % width] = {
+            "faces": len(dts), "payload_bytes": nb, "pack_us": round(tp * 1e3, 1), "unpack_us": round(tu * 1e3, 1),
+            "GBs": round(4 * nb / (tp + tu) / 1e6, 1), "frac_hbm": round(4 * nb / (tp + tu) / 1e6 / peak, 4)}
+    del arr, back
+
     for name, spec in (("cfg1_vector", CFG1_SPEC), ("cfg3_struct_indexed_hvector", cfg3_spec(3))):
         dt = build_product(spec, mp)
         span = dt.layout_query()["max_end"]
@@ -291,37 +345,175 @@ def run_extras(dev, flush, args):
         tp = _time_launch(lambda: mp.pack_into(dt, src, packed), flush, reps)
         tu = _time_launch(lambda: mp.unpack(dt, packed, back), flush, reps)
         ti = _time_launch(lambda: mp.type_iov_tensor(dt), flush, reps)
-        peak, _ = load_peak()
         seg = dt.segment_count
-        out[name] = {"payload_bytes": n, "segments": seg,
-                     "pack_us": round(tp * 1e3, 1), "unpack_us": round(tu * 1e3, 1),
-                     "pack_GBs": round(2 * n / tp / 1e6, 1), "unpack_GBs": round(2 * n / tu / 1e6, 1),
-                     "pack_frac_hbm": round(2 * n / tp / 1e6 / peak, 4),
-                     "unpack_frac_hbm": round(2 * n / tu / 1e6 / peak, 4),
-                     "iov_us": round(ti * 1e3, 1), "iov_GBs": round(16 * seg / ti / 1e6, 1),
-                     "iov_frac_hbm": round(16 * seg / ti / 1e6 / peak, 4)}
+        row = {"payload_bytes": n, "segments": seg,
+               "pack_us": round(tp * 1e3, 1), "unpack_us": round(tu * 1e3, 1),
+               "pack_GBs": round(2 * n / tp / 1e6, 1), "unpack_GBs": round(2 * n / tu / 1e6, 1),
+               "pack_frac_hbm": round(2 * n / tp / 1e6 / peak, 4),
+               "unpack_frac_hbm": round(2 * n / tu / 1e6 / peak, 4),
+               "iov_us": round(ti * 1e3, 1), "iov_GBs": round(16 * seg / ti / 1e6, 1),
+               "iov_frac_hbm": round(16 * seg / ti / 1e6 / peak, 4)}
+        if name == "cfg1_vector":
+            # 128 KiB is launch-latency bound: also 100 packs / unpacks
+            # replayed from one CUDA graph (L2 warm after the first)
+            try:
+                bp = _graph_batched(lambda: mp.pack_into(dt, src, packed), 100, flush)
+                bu = _graph_batched(lambda: mp.unpack(dt, packed, back), 100, flush)
+                row["batched"] = {"calls": 100, "via": "one CUDA graph replay",
+                                  "pack_us_per_call": round(bp * 1e3, 2), "unpack_us_per_call": round(bu * 1e3, 2),
+                                  "pack_GBs": round(2 * n / bp / 1e6, 1), "unpack_GBs": round(2 * n / bu / 1e6, 1)}
+            except Exception as exc:
+                row["batched"] = {"error": repr(exc)[:200]}
+        out[name] = row
         del src, back, packed
     try:
         import enqueue_bench as eb
-        out["ring_2ranks_1gpu_64MiB"] = eb.ring(2, 64 << 20, iters=reps)
-        out["ring_2ranks_1gpu_64MiB_vector"] = eb.ring(2, 64 << 20, iters=reps, kind="vector",
-                                                       group="bench-ring-v")
-        out["ring_2ranks_1gpu_64MiB_vector_noscale"] = eb.ring(2, 64 << 20, iters=reps, kind="vector",
-                                                               group="bench-ring-vn", scale=False)
-        out["allreduce_native_2ranks_1gpu_64MiB_f32"] = eb.allreduce(2, 16 << 20, iters=reps, algo="native")
+        for nb in (64 << 20, 1 << 30):
+            it = reps if nb <= (64 << 20) else 3
+            tag = "64MiB" if nb == 64 << 20 else "1GiB"
+            out["ring_2ranks_1gpu_%s" % tag] = eb.ring(2, nb, iters=it, group="bench-ring-%s" % tag)
+            out["ring_2ranks_1gpu_%s_vector" % tag] = eb.ring(2, nb, iters=it, kind="vector",
+                                                              group="bench-ring-v-%s" % tag)
+            out["ring_2ranks_1gpu_%s_vector_noscale" % tag] = eb.ring(2, nb, iters=it, kind="vector", scale=False,
+                                                                      group="bench-ring-vn-%s" % tag)
+            out["allreduce_native_2ranks_1gpu_%s_f32" % tag] = eb.allreduce(2, nb // 4, iters=it, algo="native",
+                                                                            group="bench-ar-%s" % tag)
         out["allreduce_nccl_1rank_64MiB_f32"] = eb.allreduce(1, 16 << 20, iters=reps, algo="nccl",
                                                              group="bench-ar1")
     except Exception as exc:  # report, never fail the headline
         out["enqueue_error"] = repr(exc)
     try:   # multi-process world: 2 processes (one rank each) sharing this GPU via CUDA IPC
         import subprocess
-        env = dict(os.environ, IPC_BENCH_LG="26")
+        env = dict(os.environ, IPC_BENCH_LG="26,30")
         p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ipc_bench.py"), "2"], env=env,
-                           capture_output=True, text=True, timeout=180)
+                           capture_output=True, text=True, timeout=240)
         rows = [json.loads(x) for x in p.stdout.splitlines() if x.startswith("{")]
-        out["ring_2processes_1gpu_64MiB"] = rows if rows else {"error": p.stderr[-300:]}
+        out["ring_2processes_1gpu"] = rows if rows else {"error": p.stderr[-300:]}
     except Exception as exc:
         out["ipc_error"] = repr(exc)
+    return out
+
+
+NVLINK_GBS = 900.0   # NVLink 5, per direction per GPU (north_star)
+
+
+def multi_gpu_enqueue(args, dev, world):
+    """BASELINE configs[3] / [4] over the N GPUs of this torchrun job: every
+    process joins the multi-process world (transport "ipc": one rank per GPU,
+    CUDA IPC peer mappings), then (a) a ring of isend_enqueue ->(r+1) /
+    irecv_enqueue <-(r-1) + waitall_enqueue at 64 MiB and 1 GiB, bytes and the
+    vector(N/32, 4, 8) FLOAT64 type (with and without the dependent scale
+    kernels), rendezvous = one peer pull over NVLink per message; (b)
+    allreduce_enqueue of float32 and int64 at 64 MiB and 1 GiB through NCCL
+    (ncclCommInitRank) and the native kernel.  Times: CUDA events on each
+    rank's queue stream, max over ranks.  busbw: ring N/t (every GPU sends N
+    and receives N at once, one direction each); allreduce S/t * 2(n-1)/n."""
+    import torch
+    import torch.distributed as dist
+    import paper_2402_12274_b200 as mp
+    inst = mp.init(transport="ipc", group="bench%s" % os.environ.get("MASTER_PORT", "0"))
+    q = mp.queue_create(inst)
+    info = mp.info_create()
+    mp.info_set(info, "type", "devstream")
+    mp.info_set_hex(info, "value", bytes.fromhex(q.handle))
+    st = inst.stream_create(info)
+    c = mp.stream_comm_create(inst.world, st)
+    r, n = inst.rank, inst.size
+    out = {"ranks": n, "transport": "ipc: one process per GPU, CUDA IPC peer mappings",
+           "nvlink_GBs_per_direction": NVLINK_GBS, "ring": [], "allreduce": []}
+
+    def all_min(ok):
+        t = torch.tensor([1.0 if ok else 0.0], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return bool(t.item() > 0)
+
+    def timed(one, iters):
+        for _ in range(2):
+            one()
+        mp.queue_synchronize(q)
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(q.torch_stream)
+        for _ in range(iters):
+            one()
+        e1.record(q.torch_stream)
+        mp.queue_synchronize(q)
+        return max_over_ranks(e0.elapsed_time(e1) / iters, dev)
+
+    g = torch.Generator(device=dev)
+    for nb in (64 << 20, 1 << 30):
+        iters = 10 if nb <= (64 << 20) else 3
+        for kind, scale in (("u8", False), ("vector", True), ("vector", False)):
+            vec = kind == "vector"
+            span = 2 * nb - 32 if vec else nb
+            g.manual_seed(1000 + r)
+            src = torch.randint(0, 256, (span,), generator=g, device=dev, dtype=torch.uint8)
+            dst = torch.zeros_like(src)
+            dt, count = (mp.type_vector(nb // 32, 4, 8, mp.FLOAT64).commit(), 1) if vec else (mp.BYTE, nb)
+            f64 = span // 8
+
+            def one():
+                if scale:
+                    with torch.cuda.stream(q.torch_stream):
+                        src.view(torch.float64)[:f64].mul_(1.0)      # dependent kernel before the send
+                rr = mp.irecv_enqueue(c, dst, count, dt, (r - 1) % n, 0)
+                sr = mp.isend_enqueue(c, src, count, dt, (r + 1) % n, 0)
+                mp.waitall_enqueue([rr, sr])
+                if scale:
+                    with torch.cuda.stream(q.torch_stream):
+                        dst.view(torch.float64)[:f64].mul_(1.0)      # dependent kernel after the receive
+
+            ms = timed(one, iters)
+            g.manual_seed(1000 + (r - 1) % n)
+            exp = torch.randint(0, 256, (span,), generator=g, device=dev, dtype=torch.uint8)
+            if vec:
+                pad = torch.zeros(32, dtype=torch.uint8, device=dev)
+                ok = bool((torch.cat([dst, pad]).view(-1, 64)[:, :32] ==
+                           torch.cat([exp, pad]).view(-1, 64)[:, :32]).all())
+            else:
+                ok = bool((dst == exp).all())
+            bw = nb / (ms / 1e3) / 1e9
+            out["ring"].append({"kind": kind, "scale_kernels": scale, "bytes": nb, "iters": iters,
+                                "ms_per_iter": round(ms, 4), "busbw_GBps": round(bw, 1),
+                                "nvlink_frac": round(bw / NVLINK_GBS, 4), "correct": all_min(ok)})
+            if vec:
+                mp.type_free(dt)
+            del src, dst, exp
+    for nb in (64 << 20, 1 << 30):
+        iters = 10 if nb <= (64 << 20) else 3
+        for kind in ("float32", "int64"):
+            es = 4 if kind == "float32" else 8
+            count = nb // es
+            g.manual_seed(2000 + r)
+            if kind == "float32":
+                x = torch.rand(count, generator=g, device=dev) * 2 - 1
+            else:
+                x = torch.randint(-2 ** 20, 2 ** 20, (count,), generator=g, device=dev, dtype=torch.int64)
+            y = torch.empty_like(x)
+            code = mp.FLOAT32 if kind == "float32" else mp.INT64
+            for algo in ("nccl", "native"):
+                try:
+                    ms = timed(lambda: mp.allreduce_enqueue(c, x, y, count, code, algo=algo), iters)
+                except Exception as exc:
+                    out["allreduce"].append({"kind": kind, "bytes": nb, "algo": algo, "error": repr(exc)[:200]})
+                    continue
+                ref = x.clone()
+                dist.all_reduce(ref)                       # torch's NCCL as the checker
+                if kind == "int64":
+                    ok = bool((y == ref).all())
+                else:
+                    ok = bool(((y.double() - ref.double()).abs() <= 1e-6 * n * (1 + ref.double().abs())).all())
+                alg = nb / (ms / 1e3) / 1e9
+                bus = alg * 2 * (n - 1) / n
+                out["allreduce"].append({"kind": kind, "bytes": nb, "algo": algo, "iters": iters,
+                                         "ms_per_iter": round(ms, 4), "algbw_GBps": round(alg, 1),
+                                         "busbw_GBps": round(bus, 1), "nvlink_frac": round(bus / NVLINK_GBS, 4),
+                                         "correct": all_min(ok)})
+            del x, y
+    mp.comm_free(c)
+    mp.free_stream(st)
+    mp.queue_destroy(q)
+    inst.finalize()
     return out
 
 
@@ -478,16 +670,14 @@ def gpu_arm(args):
     if rank == 0 and world == 1 and not args.no_extras:
         extras = run_extras(dev, flush, args)
 
+    line = None
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seeded PCG64 bytes, 514^3 f32 array)",
-            "config": {"workload": WORKLOAD, "array_bytes": ARRAY_BYTES,
-                       "payload_bytes_per_step": step_bytes(),
-                       "l2": "flushed between steps outside the timed events (256 MiB write, then 256 MiB read: L2 cold and clean)" if flush.clean else "flushed between steps (256 MiB write outside the timed events)",
-                       "parallelism": "replicas x%d" % world},
+            "config": bench_config(world),
             "pack_ms": round(pk, 4), "unpack_ms": round(uk, 4),
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": round(achieved, 1),
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
@@ -509,6 +699,28 @@ def gpu_arm(args):
             "cpu_baseline": cpu,
             "extras": extras,
         }
+    if world > 1 and not args.no_extras:
+        # ring / allreduce over the N GPUs; a watchdog prints the line without
+        # them if the job does not finish in time (never lose the headline)
+        budget = float(os.environ.get("MPX_BENCH_MULTI_TIMEOUT", "420"))
+
+        def expire():
+            if line is not None:
+                line["multi_gpu"] = {"error": "timed out after %.0f s" % budget}
+                emit(line)
+            os._exit(0)
+
+        timer = threading.Timer(budget, expire)
+        timer.daemon = True
+        timer.start()
+        try:
+            mg = multi_gpu_enqueue(args, dev, world)
+        except Exception as exc:
+            mg = {"error": repr(exc)[:300]}
+        timer.cancel()
+        if line is not None:
+            line["multi_gpu"] = mg
+    if line is not None:
         emit(line)
     if world > 1:
         dist.destroy_process_group()

@@ -46,6 +46,23 @@ __device__ __forceinline__ void reduce_vec(const T* const* src, T* const* dst, i
     for (int j = 0; j < n; ++j) reinterpret_cast<uint4*>(dst[j])[v] = u.q;
 }
 
+// slice [lo, hi) of the n buffers whose pointers are in shared memory
+template <typename T, typename A>
+__device__ __forceinline__ void reduce_slice(const T* const* src, T* const* dst, int n, int aligned, int64_t lo,
+                                             int64_t hi) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    constexpr int V = 16 / sizeof(T);
+    if (aligned) {
+        const int64_t vlo = (lo + V - 1) / V, vhi = hi / V;
+        for (int64_t v = vlo + t0; v < vhi; v += stride) reduce_vec<T, A>(src, dst, n, v);
+        for (int64_t i = lo + t0; i < min(hi, vlo * V); i += stride) reduce_one<T, A>(src, dst, n, i);
+        for (int64_t i = max(lo, vhi * V) + t0; i < hi; i += stride) reduce_one<T, A>(src, dst, n, i);
+    } else {
+        for (int64_t i = lo + t0; i < hi; i += stride) reduce_one<T, A>(src, dst, n, i);
+    }
+}
+
 template <typename T, typename A>
 __global__ void __launch_bounds__(256)
 k_allreduce_oneshot(const CollTable* __restrict__ tab, int n, int64_t lo, int64_t hi) {
@@ -62,17 +79,30 @@ k_allreduce_oneshot(const CollTable* __restrict__ tab, int n, int64_t lo, int64_
             aligned = 0;
     }
     __syncthreads();
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    constexpr int V = 16 / sizeof(T);
-    if (aligned) {
-        const int64_t vlo = (lo + V - 1) / V, vhi = hi / V;
-        for (int64_t v = vlo + t0; v < vhi; v += stride) reduce_vec<T, A>(src, dst, n, v);
-        for (int64_t i = lo + t0; i < min(hi, vlo * V); i += stride) reduce_one<T, A>(src, dst, n, i);
-        for (int64_t i = max(lo, vhi * V) + t0; i < hi; i += stride) reduce_one<T, A>(src, dst, n, i);
-    } else {
-        for (int64_t i = lo + t0; i < hi; i += stride) reduce_one<T, A>(src, dst, n, i);
+    reduce_slice<T, A>(src, dst, n, aligned, lo, hi);
+}
+
+struct DirectPtrs {
+    const void* send[kMaxDirectRanks];
+    void* recv[kMaxDirectRanks];
+};
+
+template <typename T, typename A>
+__global__ void __launch_bounds__(256)
+k_allreduce_direct(const DirectPtrs p, int n, int64_t lo, int64_t hi) {
+    __shared__ const T* src[kMaxDirectRanks];
+    __shared__ T* dst[kMaxDirectRanks];
+    __shared__ int aligned;
+    if (threadIdx.x == 0) aligned = 1;
+    __syncthreads();
+    if (threadIdx.x < n) {
+        src[threadIdx.x] = static_cast<const T*>(p.send[threadIdx.x]);
+        dst[threadIdx.x] = static_cast<T*>(p.recv[threadIdx.x]);
+        if (((reinterpret_cast<uintptr_t>(src[threadIdx.x]) | reinterpret_cast<uintptr_t>(dst[threadIdx.x])) & 15) != 0)
+            aligned = 0;
     }
+    __syncthreads();
+    reduce_slice<T, A>(src, dst, n, aligned, lo, hi);
 }
 
 int sms(int device) {
@@ -90,6 +120,10 @@ cudaError_t preload_coll_kernels() {
     if ((r = cudaFuncGetAttributes(&a, k_allreduce_oneshot<long long, unsigned long long>)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_allreduce_oneshot<float, double>)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_allreduce_oneshot<double, double>)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_allreduce_direct<int32_t, uint32_t>)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_allreduce_direct<long long, unsigned long long>)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_allreduce_direct<float, double>)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_allreduce_direct<double, double>)) != cudaSuccess) e = r;
     return e;
 }
 
@@ -113,6 +147,37 @@ cudaError_t launch_allreduce_oneshot(const CollTable* table, int n, int rank, in
         break;
     default:
         k_allreduce_oneshot<double, double><<<grid, 256, 0, stream>>>(table, n, lo, hi);
+        break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_allreduce_direct(const void* const* send, void* const* recv, int n, int rank, int64_t count,
+                                    int dtype_code, int device, cudaStream_t stream) {
+    if (n > kMaxDirectRanks) return cudaErrorInvalidValue;
+    DirectPtrs p{};
+    for (int j = 0; j < n; ++j) {
+        p.send[j] = send[j];
+        p.recv[j] = recv[j];
+    }
+    const int64_t chunk = (count + n - 1) / n;
+    const int64_t lo = std::min<int64_t>(count, (int64_t)rank * chunk);
+    const int64_t hi = std::min<int64_t>(count, lo + chunk);
+    if (hi <= lo) return cudaSuccess;
+    const int64_t want = (hi - lo + 255) / 256;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms(device) * 8));
+    switch (dtype_code) {
+    case MPX_INT32:
+        k_allreduce_direct<int32_t, uint32_t><<<grid, 256, 0, stream>>>(p, n, lo, hi);
+        break;
+    case MPX_INT64:
+        k_allreduce_direct<long long, unsigned long long><<<grid, 256, 0, stream>>>(p, n, lo, hi);
+        break;
+    case MPX_FLOAT32:
+        k_allreduce_direct<float, double><<<grid, 256, 0, stream>>>(p, n, lo, hi);
+        break;
+    default:
+        k_allreduce_direct<double, double><<<grid, 256, 0, stream>>>(p, n, lo, hi);
         break;
     }
     return cudaGetLastError();

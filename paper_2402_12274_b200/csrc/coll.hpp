@@ -34,6 +34,13 @@ struct CollRing {
 cudaError_t launch_allreduce_oneshot(const CollTable* table, int n, int rank, int64_t count, int dtype_code,
                                      int device, cudaStream_t stream);
 
+// Same reduction with the n buffer pairs passed by value (multi-process
+// worlds: the pointers are this process's mappings of the peers' buffers,
+// known on the host at enqueue time).
+constexpr int kMaxDirectRanks = 16;
+cudaError_t launch_allreduce_direct(const void* const* send, void* const* recv, int n, int rank, int64_t count,
+                                    int dtype_code, int device, cudaStream_t stream);
+
 cudaError_t preload_coll_kernels();
 
 }  // namespace mpx

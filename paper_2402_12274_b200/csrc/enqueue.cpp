@@ -401,6 +401,7 @@ struct World {
     std::condition_variable nccl_cv;
     std::vector<ncclComm_t> nccl;   // per rank, by ncclCommInitAll
     int nccl_state = 0;             // 0 none, 1 building, 2 ready, -1 failed
+    std::map<int, ncclComm_t> nccl_ctx;   // multi-process: this rank's communicator per context
     // passive-target read windows (onesided.py): window k = every rank's k-th
     // mpx_win_create; created / freed collectively
     struct Win {
@@ -464,6 +465,21 @@ struct World {
         }
         if (defer_thread.joinable()) defer_thread.join();
     }
+    std::mutex late_mu;
+    std::map<int, cudaStream_t> late;   // device -> the world's late stream there
+    cudaError_t take_late(int dev) {
+        std::lock_guard<std::mutex> g(late_mu);
+        if (late.count(dev)) return cudaSuccess;
+        cudaStream_t st = nullptr;
+        cudaError_t e = stream_pool().acquire(dev, &st);
+        if (e == cudaSuccess) late[dev] = st;
+        return e;
+    }
+    cudaStream_t late_on(int dev) {
+        std::lock_guard<std::mutex> g(late_mu);
+        auto it = late.find(dev);
+        return it == late.end() ? nullptr : it->second;
+    }
     cudaStream_t service(int dev) {
         std::lock_guard<std::mutex> g(svc_mu);
         auto it = svc.find(dev);
@@ -482,7 +498,6 @@ struct World {
 struct Comm {
     ~Comm() {
         if (side) stream_pool().release(device, side);
-        if (late) stream_pool().release(device, late);
     }
     World* w = nullptr;
     int rank = 0, ctx = 0, device = 0;
@@ -504,22 +519,27 @@ struct Comm {
     // every stream point they depend on has been reached: they never wait,
     // so they can never sit behind -- or hold up -- the side stream's
     // program-ordered work.
-    cudaStream_t late = nullptr;
-    std::once_flag late_once;
-    cudaError_t late_err = cudaSuccess;
-    cudaStream_t late_stream() {
-        std::call_once(late_once, [this] {
-            late_err = stream_pool().acquire(device, &late);
-            if (late_err != cudaSuccess) late = nullptr;
-        });
-        return late;
-    }
+    // One per (world, device), shared by the device's communicators -- safe
+    // because nothing on it ever waits -- and taken at world join (never on
+    // the deferral / progress thread), so the streams alive per device stay
+    // few: more streams than the device's CUDA_DEVICE_MAX_CONNECTIONS
+    // hardware queues put two streams on one queue, and a stream parked in a
+    // wait then parks the other (measured: tools/stall_probe.py, 4 ranks with
+    // 4 queues stall every time, with 8+ queues never).
+    cudaError_t late_err = cudaErrorNotReady;
+    cudaStream_t late_stream();
     std::mutex err_mu;
     std::deque<std::pair<int, std::string>> deferred;
     std::atomic<int64_t> outstanding{0};
     int64_t coll_seq = 0;
     int ring = -1;                  // index into every device's ring area
 };
+
+cudaStream_t Comm::late_stream() {
+    cudaStream_t st = w->late_on(device);
+    late_err = st ? cudaSuccess : cudaErrorInvalidResourceHandle;
+    return st;
+}
 
 namespace {
 
@@ -575,6 +595,7 @@ int setup_device(World* w, int dev, int ndev) {
         done.insert(dev);
     }
     w->service(dev);
+    MPX_CU(w->take_late(dev));
     {
         std::lock_guard<std::mutex> g2(w->coll_mu);
         if (!w->area.count(dev)) {
@@ -966,10 +987,16 @@ int do_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t buf_bytes, int64_
 }
 
 // ------------------------------------------------ multi-process (ipc.hpp)
-// Every message is packed into the sender's staging arena at its stream
-// position (sends complete locally, like the reference's eager frames); the
-// receiving process unpacks from that arena after the sender's ready flag
-// and then releases the space with the consumed flag.
+// Eager messages (<= eager_limit, self-sends, and layouts a peer cannot
+// rebuild) are packed into the sender's staging arena at its stream
+// position; the receiving process unpacks from that arena and releases the
+// space with the consumed flag (sends complete locally, like the reference's
+// eager frames).  Larger messages whose layout is contiguous or a strided
+// chain go rendezvous (transport.py:355-375,548-602): the sender publishes a
+// cached IPC handle of its buffer's allocation plus its layout, the receiver
+// pulls the bytes straight from the sender's buffer in ONE transfer kernel
+// (typed -> typed through the zipper) over NVLink and writes the done flag
+// the send completes on.  No staging copy, no size cap.
 struct IpcPending {          // a receive posted before its send arrived
     std::shared_ptr<Comm> c;
     Side r;
@@ -980,10 +1007,69 @@ struct IpcPending {          // a receive posted before its send arrived
     bool blocking = false;
 };
 
-int ipc_deliver(const std::shared_ptr<Comm>& c, cudaStream_t st, const Side& r, const IpcMsg& m, int64_t* moved) {
-    MPX_RC(wait_flag(st, m.ready, m.ready_gen));
+// the sender's layout in a form the receiving process can rebuild (chains)
+bool ipc_layout_of(Datatype* dt, int64_t count, IpcLayout* out) {
+    NodeP lay = dt->layout_for(count);
+    const Node* n = lay.get();
+    IpcLayout L;
+    L.nrep = 0;
+    while (n->kind == Kind::Rep) {
+        if (L.nrep == kIpcMaxRep) return false;
+        L.rep[L.nrep][0] = n->count;
+        L.rep[L.nrep][1] = n->stride;
+        L.rep[L.nrep][2] = n->base;
+        L.nrep++;
+        n = n->body.get();
+    }
+    if (n->kind != Kind::Run) return false;
+    L.run_off = n->off;
+    L.run_len = n->len;
+    *out = L;
+    return true;
+}
+
+// a datatype with exactly a peer sender's layout (receiving side; cached for
+// the process lifetime -- its plans may be in use by queued transfers)
+Datatype* ipc_layout_type(const IpcLayout& L) {
+    static std::mutex mu;
+    static std::map<std::string, std::unique_ptr<Datatype>>* cache =
+        new std::map<std::string, std::unique_ptr<Datatype>>();
+    const std::string key(reinterpret_cast<const char*>(&L), sizeof L);
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache->find(key);
+    if (it != cache->end()) return it->second.get();
+    NodeP n = tree::run(L.run_off, L.run_len);
+    for (int i = L.nrep - 1; i >= 0; --i) n = tree::rep(L.rep[i][0], L.rep[i][1], n, L.rep[i][2]);
+    auto d = std::make_unique<Datatype>();
+    d->layout = n;
+    d->size = n->nbytes;
+    d->lb = n->min_off;
+    d->ub = n->max_end;
+    d->committed = true;
+    d->desc = "peer-layout";
+    Datatype* raw = d.get();
+    cache->emplace(key, std::move(d));
+    return raw;
+}
+
+int ipc_deliver(const std::shared_ptr<Comm>& c, cudaStream_t st, const Side& r, IpcMsg m, int64_t* moved) {
     *moved = std::min(m.bytes, r.bytes);
-    if (*moved > 0) MPX_RC(launch_move(c->device, r.dt, r.count, false, m.data, r.buf, *moved, st));
+    if (m.rndv) MPX_RC(c->w->ipc->resolve(&m));   // map the sender's allocation (cached)
+    MPX_RC(wait_flag(st, m.ready, m.ready_gen));
+    if (*moved > 0) {
+        if (m.rndv) {   // pull from the sender's buffer
+            Side s;
+            s.rank = m.src;
+            s.device = c->w->devices[(size_t)m.src];
+            s.dt = ipc_layout_type(m.layout);
+            s.count = 1;
+            s.buf = const_cast<uint8_t*>(m.data);
+            s.bytes = m.bytes;
+            MPX_RC(transfer(c->device, st, s, r, *moved));
+        } else {
+            MPX_RC(launch_move(c->device, r.dt, r.count, false, m.data, r.buf, *moved, st));
+        }
+    }
     MPX_RC(set_device(c->device));
     return write_flag(st, m.consumed, m.consumed_gen);
 }
@@ -997,7 +1083,7 @@ bool ipc_on_match(void* cookie, const IpcMsg& m) {
     const cudaError_t q = cudaEventQuery(raw->ev);
     if (q == cudaErrorNotReady || *reinterpret_cast<volatile uint32_t*>(m.ready) < m.ready_gen) {
         cudaGetLastError();
-        return false;   // the post point or the sender's packed data is not there yet
+        return false;   // the post point or the sender's data is not there yet
     }
     std::unique_ptr<IpcPending> p(raw);
     const auto& c = p->c;
@@ -1021,21 +1107,43 @@ int ipc_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t count, Dat
              bool blocking, std::shared_ptr<ReqState>* out_req) {
     IpcWorld* ipc = c->w->ipc;
     const int64_t bytes = dt->size * count;
-    uint8_t* slot = nullptr;
-    int64_t off = 0;
-    uint32_t *ready = nullptr, rgen = 0, cidx = 0, cgen = 0;
-    MPX_RC(ipc->reserve(bytes, &slot, &off, &ready, &rgen, &cidx, &cgen));
+    IpcSend s;
+    s.dest = dest;
+    s.ctx = c->ctx;
+    s.tag = tag;
+    s.bytes = bytes;
+    const bool rndv = bytes > c->w->eager_limit && dest != c->rank && ipc_layout_of(dt, count, &s.layout) &&
+                      ipc->export_buffer(buf, &s.handle, &s.bufid, &s.buf_off) == MPX_SUCCESS;
     MPX_RC(set_device(c->device));
-    if (bytes > 0) MPX_RC(launch_move(c->device, dt, count, true, buf, slot, bytes, c->stream));
-    MPX_RC(set_device(c->device));
-    MPX_RC(write_flag(c->stream, ready, rgen));
-    MPX_RC(ipc->post_send(dest, c->ctx, tag, bytes, off, ready, rgen, cidx, cgen));
-    MPX_TRACE("ipc send r%d -> %d tag %d %lld B", c->rank, dest, tag, (long long)bytes);
+    uint32_t* done = nullptr;
+    uint32_t dgen = 0;
+    if (rndv) {
+        s.rndv = 1;
+        s.ready = ipc->local_flag(&s.ready_gen);
+        done = ipc->local_flag(&dgen);
+        s.cons_idx = ipc->flag_index(done);
+        s.cons_gen = dgen;
+        MPX_RC(write_flag(c->stream, s.ready, s.ready_gen));   // the buffer is ready at this stream position
+    } else {
+        uint8_t* slot = nullptr;
+        MPX_RC(ipc->reserve(bytes, &slot, &s.off, &s.ready, &s.ready_gen, &s.cons_idx, &s.cons_gen));
+        if (bytes > 0) MPX_RC(launch_move(c->device, dt, count, true, buf, slot, bytes, c->stream));
+        MPX_RC(set_device(c->device));
+        MPX_RC(write_flag(c->stream, s.ready, s.ready_gen));
+    }
+    MPX_RC(ipc->post_send(s));
+    MPX_TRACE("ipc send r%d -> %d tag %d %lld B (%s)", c->rank, dest, tag, (long long)bytes, rndv ? "rndv" : "eager");
+    if (rndv && blocking) MPX_RC(wait_flag(c->stream, done, dgen));   // complete once the receiver has pulled it
     if (!blocking) {
         auto req = std::make_shared<ReqState>();
         req->comm = c;
         req->is_send = true;
         req->matched = true;
+        if (rndv) {
+            req->flag = done;
+            req->gen = dgen;
+            req->needs_wait = true;
+        }
         c->outstanding++;
         if (out_req) *out_req = req;
     }
@@ -1077,8 +1185,8 @@ int ipc_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t count, Datatype*
     }
     MPX_TRACE("ipc recv r%d <- %d tag %d %s", c->rank, source, tag, matched ? "matched" : "posted");
     if (matched && !blocking && *reinterpret_cast<volatile uint32_t*>(m.ready) < m.ready_gen) {
-        // the sender has not packed it yet: a side-stream wait for that could
-        // hold up later deliveries, so the progress thread delivers it
+        // the sender's data point is not reached yet: a side-stream wait for
+        // that could hold up later deliveries, so the progress thread delivers it
         req->flag = flag;
         req->gen = gen;
         req->needs_wait = true;
@@ -1122,53 +1230,37 @@ int ipc_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t count, Datatype*
     return MPX_SUCCESS;
 }
 
-// Multi-process allreduce: every rank copies its contribution into the
-// collective area of its arena, then -- once every peer's contribution is in
-// place (ready counters) -- reduces ALL slices locally in rank order with the
-// native one-shot kernel reading the peers' areas, and bumps its read counter
-// so the peers may overwrite their areas for the next collective.  Ordered
-// entirely by stream memops on the caller's stream; collectives must be
-// called in the same order on every rank (MPI's rule).
-int ipc_allreduce(const std::shared_ptr<Comm>& c, const void* sendbuf, void* recvbuf, int64_t count, int dtype_code,
-                  int es) {
+// Multi-process native allreduce: every rank publishes IPC handles of its
+// send and receive buffers on the host (cached mappings; the call is
+// collective), then on its stream: "arrived" (my buffers are ready), wait
+// for every rank's arrival, reduce MY slice of every rank's send buffer in
+// rank order and store it into every rank's receive buffer (peer loads and
+// stores over NVLink), "finished", wait for every rank to finish (my receive
+// buffer is complete and nobody reads my send buffer any more).  Flags and
+// sequence numbers are per communicator context, so collectives of
+// different communicators never alias.
+int ipc_allreduce_native(const std::shared_ptr<Comm>& c, const void* sendbuf, void* recvbuf, int64_t count,
+                         int dtype_code) {
     World* w = c->w;
     IpcWorld* ipc = w->ipc;
     const int n = w->size, me = c->rank;
-    if (n > kMaxCollRanks) return fail(MPX_ERR_UNSUPPORTED, "native allreduce supports <= %d ranks", kMaxCollRanks);
-    const int64_t bytes = count * es;
-    if (bytes > ipc->coll_bytes())
-        return fail(MPX_ERR_UNSUPPORTED, "allreduce of %lld bytes exceeds the %lld-byte collective area (1/4 of "
-                    "MPX_IPC_ARENA)", (long long)bytes, (long long)ipc->coll_bytes());
+    if (n > kMaxDirectRanks) return fail(MPX_ERR_UNSUPPORTED, "native allreduce supports <= %d ranks", kMaxDirectRanks);
+    const int cs = (c->ctx >> 1) % IpcWorld::kCollCtx;
+    const int64_t seq = ++c->coll_seq;
+    std::vector<const void*> sends;
+    std::vector<void*> recvs;
+    MPX_RC(ipc->coll_exchange(cs, seq, sendbuf, recvbuf, count, dtype_code, &sends, &recvs));
     MPX_RC(set_device(c->device));
-    const uint32_t seq = ipc->next_coll_seq();
-    // the table of this call: send[p] = p's area (constant), recv[*] = my buffer
-    CollTable* tab = nullptr;
-    {
-        std::lock_guard<std::mutex> g(w->coll_mu);
-        auto it = w->area.find(-1 - c->device);     // per-device table of the multi-process world
-        if (it == w->area.end()) {
-            CollRing* r = nullptr;
-            MPX_CU(cudaMalloc(reinterpret_cast<void**>(&r), sizeof(CollTable)));
-            it = w->area.emplace(-1 - c->device, r).first;
-        }
-        tab = reinterpret_cast<CollTable*>(it->second);
-    }
     cudaStream_t st = c->stream;
-    for (int q = 0; q < n; ++q)   // peers have read my previous contribution
-        if (q != me) MPX_RC(wait_flag(st, ipc->coll_read(q), seq - 1));
-    MPX_CU(cudaMemcpyAsync(ipc->my_coll_area(), sendbuf, (size_t)bytes, cudaMemcpyDeviceToDevice, st));
-    MPX_RC(write_flag(st, ipc->coll_ready(me), seq));
+    const uint32_t g = static_cast<uint32_t>(seq);
+    MPX_RC(write_flag(st, ipc->coll_arrive(me, cs), g));
     for (int q = 0; q < n; ++q)
-        if (q != me) MPX_RC(wait_flag(st, ipc->coll_ready(q), seq));
-    for (int q = 0; q < n; ++q) {
-        MPX_RC(write_ptr(st, &tab->send[q], ipc->coll_area(q)));
-        MPX_RC(write_ptr(st, (const void* const*)&tab->recv[q], recvbuf));
-    }
-    for (int s = 0; s < n; ++s) {   // every slice, rank-ordered sum, into my buffer only
-        cudaError_t e = launch_allreduce_oneshot(tab, n, s, count, dtype_code, c->device, st);
-        if (e != cudaSuccess) return cuda_fail(e, "allreduce kernel");
-    }
-    MPX_RC(write_flag(st, ipc->coll_read(me), seq));
+        if (q != me) MPX_RC(wait_flag(st, ipc->coll_arrive(q, cs), g));
+    cudaError_t e = launch_allreduce_direct(sends.data(), recvs.data(), n, me, count, dtype_code, c->device, st);
+    if (e != cudaSuccess) return cuda_fail(e, "allreduce kernel");
+    MPX_RC(write_flag(st, ipc->coll_finish(me, cs), g));
+    for (int q = 0; q < n; ++q)
+        if (q != me) MPX_RC(wait_flag(st, ipc->coll_finish(q, cs), g));
     return MPX_SUCCESS;
 }
 
@@ -1205,6 +1297,9 @@ struct Nccl {
                               cudaStream_t) = nullptr;
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
     const char* (*errStr)(ncclResult_t) = nullptr;
+    // multi-process worlds: one communicator per context, id through the segment
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
 };
 Nccl g_nccl;
 std::mutex g_nccl_mu;
@@ -1214,6 +1309,8 @@ bool nccl_bind(void* h) {
     g_nccl.allReduce = (decltype(g_nccl.allReduce))dlsym(h, "ncclAllReduce");
     g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(h, "ncclCommDestroy");
     g_nccl.errStr = (decltype(g_nccl.errStr))dlsym(h, "ncclGetErrorString");
+    g_nccl.getUniqueId = (decltype(g_nccl.getUniqueId))dlsym(h, "ncclGetUniqueId");
+    g_nccl.commInitRank = (decltype(g_nccl.commInitRank))dlsym(h, "ncclCommInitRank");
     return g_nccl.commInitAll && g_nccl.allReduce && g_nccl.commDestroy && g_nccl.errStr;
 }
 
@@ -1246,6 +1343,40 @@ int nccl_comm_for(const std::shared_ptr<Comm>& c, ncclComm_t* out) {
     if (w->nccl_state != 2) return fail(MPX_ERR_TRANSPORT, "NCCL communicator creation failed");
     *out = w->nccl[c->rank];
     return MPX_SUCCESS;
+}
+
+// multi-process worlds: the communicator of this context, created on its
+// first allreduce (collective: every rank makes the same calls in the same
+// order); rank 0's unique id reaches the others through the job's segment
+int nccl_comm_ipc(const std::shared_ptr<Comm>& c, ncclComm_t* out) {
+    World* w = c->w;
+    std::lock_guard<std::mutex> g(w->nccl_mu);
+    auto it = w->nccl_ctx.find(c->ctx);
+    if (it != w->nccl_ctx.end()) {
+        *out = it->second;
+        return MPX_SUCCESS;
+    }
+    if (!g_nccl.getUniqueId || !g_nccl.commInitRank)
+        return fail(MPX_ERR_UNSUPPORTED, "libnccl lacks ncclGetUniqueId / ncclCommInitRank");
+    ncclUniqueId id;
+    std::memset(&id, 0, sizeof id);
+    if (c->rank == 0) {
+        ncclResult_t r = g_nccl.getUniqueId(&id);
+        if (r != ncclSuccess) return fail(MPX_ERR_TRANSPORT, "ncclGetUniqueId: %s", g_nccl.errStr(r));
+    }
+    MPX_RC(w->ipc->share_blob(c->ctx >> 1, c->ctx, &id, sizeof id));
+    MPX_RC(set_device(c->device));
+    ncclComm_t nc = nullptr;
+    ncclResult_t r = g_nccl.commInitRank(&nc, w->size, id, c->rank);
+    if (r != ncclSuccess) return fail(MPX_ERR_TRANSPORT, "ncclCommInitRank: %s", g_nccl.errStr(r));
+    w->nccl_ctx[c->ctx] = nc;
+    *out = nc;
+    return MPX_SUCCESS;
+}
+
+ncclDataType_t nccl_type(int code) {
+    return code == MPX_INT32 ? ncclInt32 : code == MPX_INT64 ? ncclInt64 : code == MPX_FLOAT32 ? ncclFloat32
+                                                                                             : ncclFloat64;
 }
 
 int elem_size(int code) {
@@ -1295,9 +1426,10 @@ int mpx_world_join(const char* group, int size, int rank, int device, int64_t ea
     if (w->size != size) return fail(MPX_ERR_ARG, "world %s has %d ranks, not %d", group, w->size, size);
     if (w->joined[rank]) return fail(MPX_ERR_STATE, "rank %d already joined world %s", rank, group);
     MPX_RC(setup_device(w, device, ndev));
-    // streams for this rank's queues, communicators and side streams, made
-    // now (see StreamPool::reserve); more ranks of the world -> a deeper pool
-    MPX_CU(stream_pool().reserve(device, (size_t)std::min(64, 4 * size + 4)));
+    // streams for this rank's queue, world communicator and side stream (+ the
+    // device's late stream), made now (see StreamPool::reserve) -- and no
+    // more: every extra stream shares a hardware queue sooner
+    MPX_CU(stream_pool().reserve(device, (size_t)std::min(64, 3 * size + 2)));
     w->joined[rank] = true;
     w->devices[rank] = device;
     w->live++;
@@ -1347,11 +1479,14 @@ int mpx_world_leave(mpx_world h, int rank) {
     auto* w = reinterpret_cast<World*>(h);
     if (w && w->ipc) {
         if (rank < 0 || rank >= w->size || !w->joined[rank]) return fail(MPX_ERR_STATE, "rank %d not in world", rank);
+        for (auto& kv : w->nccl_ctx) g_nccl.commDestroy(kv.second);
+        w->nccl_ctx.clear();
         int rc = w->ipc->leave();
         for (auto& kv : w->area) {
             set_device(kv.first);
             cudaFree(kv.second);
         }
+        for (auto& kv : w->late) stream_pool().release(kv.first, kv.second);
         delete w;
         return rc;
     }
@@ -1369,6 +1504,7 @@ int mpx_world_leave(mpx_world h, int rank) {
         if (w->nccl_state == 2)
             for (auto cm : w->nccl)
                 if (cm) g_nccl.commDestroy(cm);
+        for (auto& kv : w->late) stream_pool().release(kv.first, kv.second);
         g_worlds.erase(it);
         delete w;
     }
@@ -1618,8 +1754,8 @@ int mpx_allreduce_enqueue(mpx_comm h, const void* sendbuf, void* recvbuf, int64_
     if (!es) return fail(MPX_ERR_ARG, "allreduce supports INT32, INT64, FLOAT32 and FLOAT64");
     if (count < 0) return fail(MPX_ERR_ARG, "count must be a nonnegative int");
     if (count == 0) return MPX_SUCCESS;  // comm.py:572-574
+    (void)es;
     World* w = c->w;
-    if (w->ipc) return ipc_allreduce(c, sendbuf, recvbuf, count, dtype_code, es);
     MPX_RC(set_device(c->device));
     bool distinct = true;
     {
@@ -1631,13 +1767,14 @@ int mpx_allreduce_enqueue(mpx_comm h, const void* sendbuf, void* recvbuf, int64_
         if (!distinct) return fail(MPX_ERR_UNSUPPORTED, "NCCL allreduce needs one device per rank");
         if (!nccl_available()) return fail(MPX_ERR_UNSUPPORTED, "libnccl.so.2 not available");
         ncclComm_t nc;
-        MPX_RC(nccl_comm_for(c, &nc));
-        ncclDataType_t t = dtype_code == MPX_INT32 ? ncclInt32 : dtype_code == MPX_INT64 ? ncclInt64
-                         : dtype_code == MPX_FLOAT32 ? ncclFloat32 : ncclFloat64;
-        ncclResult_t r = g_nccl.allReduce(sendbuf, recvbuf, (size_t)count, t, ncclSum, nc, c->stream);
+        MPX_RC(w->ipc ? nccl_comm_ipc(c, &nc) : nccl_comm_for(c, &nc));
+        MPX_RC(set_device(c->device));
+        ncclResult_t r = g_nccl.allReduce(sendbuf, recvbuf, (size_t)count, nccl_type(dtype_code), ncclSum, nc,
+                                          c->stream);
         if (r != ncclSuccess) return fail(MPX_ERR_TRANSPORT, "ncclAllReduce: %s", g_nccl.errStr(r));
         return MPX_SUCCESS;
     }
+    if (w->ipc) return ipc_allreduce_native(c, sendbuf, recvbuf, count, dtype_code);
     // native one-shot: every rank's stream publishes its buffers and arrives
     // (memops into every participating device's ring copy), waits for all on
     // its own device's copy, reduces its slice into every rank, meets again

@@ -1,5 +1,5 @@
-// ipc.cpp -- shared segment, matching, flags, arenas and progress thread of
-// multi-process worlds (see ipc.hpp).
+// ipc.cpp -- shared segment, matching, flags, arenas, buffer export/import
+// and progress thread of multi-process worlds (see ipc.hpp).
 #include "ipc.hpp"
 
 #include <cuda.h>
@@ -25,10 +25,13 @@
 namespace mpx {
 
 namespace {
-constexpr uint32_t kMagic = 0x4d505849;   // "MPXI"
+constexpr uint32_t kMagic = 0x4d505832;   // "MPX2"
 constexpr int kMaxRanks = 16;
 constexpr int kSlots = 512;               // mailbox entries per receiving rank
 constexpr int kFlags = 1 << 16;           // completion flags per rank
+constexpr int kCollFlags = 2 * IpcWorld::kCollCtx;   // the last flags of each rank: collective counters
+constexpr int kCollDepth = 4;             // collective calls in flight per context slot
+constexpr int kBlobs = 16;
 
 enum : int32_t { FREE = 0, SEND = 1, RECV = 2, MATCHED = 3 };
 
@@ -37,18 +40,36 @@ struct Entry {
     int32_t ctx, src, tag;      // RECV: patterns; SEND/MATCHED: the send's
     int64_t seq;
     int64_t bytes;              // SEND: message bytes; RECV: capacity
-    int64_t off;                // sender's arena offset
+    int64_t off;                // eager: sender's arena offset
     uint32_t ready_idx, ready_gen;   // in the sender's flag range
     uint32_t cons_idx, cons_gen;
     int32_t sender;
-    int32_t pad;
+    int32_t rndv;
     uint64_t cookie;            // RECV / MATCHED: receiver-process pointer
+    cudaIpcMemHandle_t handle;  // rendezvous: the sender's allocation
+    uint64_t bufid;
+    int64_t buf_off;
+    IpcLayout layout;
 };
 
 struct Box {
     pthread_mutex_t mu;
     int64_t next_seq;
     Entry e[kSlots];
+};
+
+struct CollPost {
+    std::atomic<int64_t> seq;   // call number published (+1; 0 = none)
+    cudaIpcMemHandle_t h[2];    // send, recv allocations
+    uint64_t id[2];
+    int64_t off[2];
+    int64_t count;
+    int32_t code, pad;
+};
+
+struct Blob {
+    std::atomic<int64_t> key;   // key + 1 once written
+    unsigned char data[128];
 };
 
 #define MPX_CU_RET(x)                                      \
@@ -61,12 +82,34 @@ void nap(long ns) {
     struct timespec ts{0, ns};
     nanosleep(&ts, nullptr);
 }
+
+// restores the calling thread's device on every exit path
+struct DeviceGuard {
+    int cur = -1;
+    DeviceGuard() { cudaGetDevice(&cur); }
+    ~DeviceGuard() {
+        if (cur >= 0) cudaSetDevice(cur);
+    }
+};
+
+using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+using AttrFn = CUresult (*)(void*, CUpointer_attribute, CUdeviceptr);
+
+template <typename F>
+F driver_fn(const char* name) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPointByVersion(name, &f, 12000, cudaEnableDefault, &q);
+    cudaGetLastError();
+    return reinterpret_cast<F>(f);
+}
 }  // namespace
 
 constexpr int kWins = 32;   // window slots (window id mod kWins) per job
 
 struct WinEntry {
     cudaIpcMemHandle_t handle;
+    uint64_t bufid;
     int64_t off, bytes, unit;
     int64_t id;
 };
@@ -74,13 +117,15 @@ struct WinEntry {
 struct IpcShared {
     std::atomic<uint32_t> magic;
     int32_t size;
-    std::atomic<int32_t> joined, mapped, left;
+    std::atomic<int32_t> joined, mapped, left, failed;
     std::atomic<int64_t> bar_count, bar_gen;
     int32_t device[kMaxRanks];
     int64_t arena_bytes[kMaxRanks];
     cudaIpcMemHandle_t arena[kMaxRanks];
     Box box[kMaxRanks];
     WinEntry win[kWins][kMaxRanks];
+    CollPost coll[kMaxRanks][IpcWorld::kCollCtx][kCollDepth];
+    Blob blob[kBlobs];
     alignas(64) uint32_t flags[kMaxRanks][kFlags];
 };
 
@@ -88,6 +133,7 @@ int IpcWorld::join(const char* name, int size, int rank, int device, int64_t are
                    IpcWorld** out) {
     if (size < 1 || size > kMaxRanks) return fail(MPX_ERR_ARG, "multi-process worlds hold 1..%d ranks", kMaxRanks);
     if (rank < 0 || rank >= size) return fail(MPX_ERR_ARG, "rank %d outside job of %d", rank, size);
+    DeviceGuard guard;
     std::unique_ptr<IpcWorld> w(new IpcWorld());
     w->name_ = std::string("/mpx-") + name;
     for (auto& ch : w->name_)
@@ -97,11 +143,19 @@ int IpcWorld::join(const char* name, int size, int rank, int device, int64_t are
     w->device_ = device;
     w->cb_ = cb;
     w->map_bytes_ = (sizeof(IpcShared) + 4095) & ~size_t(4095);
-    // rank 0 creates and initialises the segment; the others wait for it
+    // rank 0 creates and initialises the segment (and removes it again if its
+    // own join fails); the others wait for it
+    struct Unlinker {
+        const std::string* name = nullptr;
+        ~Unlinker() {
+            if (name) shm_unlink(name->c_str());
+        }
+    } unlink_on_fail;
     if (rank == 0) {
         shm_unlink(w->name_.c_str());   // a stale segment of a crashed job
         w->fd_ = shm_open(w->name_.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
         if (w->fd_ < 0) return fail(MPX_ERR_TRANSPORT, "shm_open(%s): %s", w->name_.c_str(), strerror(errno));
+        unlink_on_fail.name = &w->name_;
         if (ftruncate(w->fd_, (off_t)w->map_bytes_) != 0)
             return fail(MPX_ERR_TRANSPORT, "ftruncate: %s", strerror(errno));
     } else {
@@ -134,12 +188,17 @@ int IpcWorld::join(const char* name, int size, int rank, int device, int64_t are
         if (sh->magic.load() != kMagic) return fail(MPX_ERR_TRANSPORT, "job %s: segment never initialised", name);
         if (sh->size != size) return fail(MPX_ERR_ARG, "job %s has %d ranks, not %d", name, sh->size, size);
     }
+    // a rank that fails from here on tells the others, so they fail fast
+    struct FailFlag {
+        IpcShared* sh;
+        bool ok = false;
+        ~FailFlag() {
+            if (!ok) sh->failed.fetch_add(1);
+        }
+    } failed{sh};
     // this rank's arena, exported; the whole segment registered with CUDA
-    int cur = -1;
-    cudaGetDevice(&cur);
     MPX_CU_RET(cudaSetDevice(device));
     w->arena_bytes_ = arena_bytes;
-    w->coll_off_ = (arena_bytes - arena_bytes / 4) & ~int64_t(255);
     MPX_CU_RET(cudaMalloc(reinterpret_cast<void**>(&w->arena_), (size_t)arena_bytes));
     MPX_CU_RET(cudaIpcGetMemHandle(&sh->arena[rank], w->arena_));
     MPX_CU_RET(cudaHostRegister(p, w->map_bytes_, cudaHostRegisterMapped | cudaHostRegisterPortable));
@@ -148,7 +207,7 @@ int IpcWorld::join(const char* name, int size, int rank, int device, int64_t are
     sh->arena_bytes[rank] = arena_bytes;
     w->shadow_.assign(kFlags, 0);
     sh->joined.fetch_add(1);
-    for (int t = 0; t < 1200000 && sh->joined.load() < size; ++t) nap(100000);
+    for (int t = 0; t < 1200000 && sh->joined.load() < size && !sh->failed.load(); ++t) nap(100000);
     if (sh->joined.load() < size) return fail(MPX_ERR_TRANSPORT, "job %s: not every rank joined", name);
     w->peer_.assign(size, nullptr);
     for (int r = 0; r < size; ++r) {
@@ -161,17 +220,27 @@ int IpcWorld::join(const char* name, int size, int rank, int device, int64_t are
         w->peer_[r] = static_cast<const uint8_t*>(q);
     }
     sh->mapped.fetch_add(1);
-    for (int t = 0; t < 1200000 && sh->mapped.load() < size; ++t) nap(100000);
-    if (cur >= 0) cudaSetDevice(cur);
+    for (int t = 0; t < 1200000 && sh->mapped.load() < size && !sh->failed.load(); ++t) nap(100000);
+    if (sh->mapped.load() < size)
+        return fail(MPX_ERR_TRANSPORT, "job %s: a peer failed to map the staging arenas", name);
+    failed.ok = true;
+    unlink_on_fail.name = nullptr;
     IpcWorld* raw = w.release();
     raw->thread_ = new std::thread([raw] { raw->progress_loop(); });
     *out = raw;
     return MPX_SUCCESS;
 }
 
-IpcWorld::~IpcWorld() {
+void IpcWorld::release_all() {
     for (int r = 0; r < (int)peer_.size(); ++r)
         if (r != rank_ && peer_[r]) cudaIpcCloseMemHandle(const_cast<uint8_t*>(peer_[r]));
+    peer_.clear();
+    for (auto& kv : imported_) cudaIpcCloseMemHandle(kv.second);
+    imported_.clear();
+}
+
+IpcWorld::~IpcWorld() {
+    release_all();
     if (arena_) cudaFree(arena_);
     if (registered_) cudaHostUnregister(sh_);
     if (sh_) munmap(sh_, map_bytes_);
@@ -203,10 +272,10 @@ int IpcWorld::leave() {
         delete t;
         thread_ = nullptr;
     }
+    DeviceGuard guard;
+    cudaSetDevice(device_);
     int rc = barrier();
-    for (int r = 0; r < size_; ++r)
-        if (r != rank_ && peer_[r]) cudaIpcCloseMemHandle(const_cast<uint8_t*>(peer_[r]));
-    for (auto& kv : opened_) cudaIpcCloseMemHandle(kv.second);
+    release_all();
     rc = rc ? rc : barrier();   // nobody frees its arena while a peer still maps it
     if (arena_) cudaFree(arena_);
     cudaHostUnregister(sh_);
@@ -214,8 +283,7 @@ int IpcWorld::leave() {
     munmap(sh_, map_bytes_);
     close(fd_);
     if (last) shm_unlink(name_.c_str());
-    peer_.clear();           // all released above: the destructor has nothing left to do
-    arena_ = nullptr;
+    arena_ = nullptr;           // all released above: the destructor has nothing left to do
     registered_ = false;
     sh_ = nullptr;
     fd_ = -1;
@@ -228,11 +296,13 @@ uint32_t* IpcWorld::local_flag(uint32_t* gen) {
     return flag_locked(gen);
 }
 
-uint32_t* IpcWorld::coll_ready(int r) { return &sh_->flags[r][kFlags - 1]; }
-uint32_t* IpcWorld::coll_read(int r) { return &sh_->flags[r][kFlags - 2]; }
+uint32_t IpcWorld::flag_index(const uint32_t* f) const { return static_cast<uint32_t>(f - &sh_->flags[rank_][0]); }
+
+uint32_t* IpcWorld::coll_arrive(int r, int cs) { return &sh_->flags[r][kFlags - 1 - 2 * cs]; }
+uint32_t* IpcWorld::coll_finish(int r, int cs) { return &sh_->flags[r][kFlags - 2 - 2 * cs]; }
 
 uint32_t* IpcWorld::flag_locked(uint32_t* gen) {
-    const uint32_t i = next_flag_++ % (kFlags - 2);   // the last two are the collective counters
+    const uint32_t i = next_flag_++ % (kFlags - kCollFlags);   // the last ones are the collective counters
     *gen = ++shadow_[i];
     return &sh_->flags[rank_][i];
 }
@@ -241,9 +311,9 @@ int IpcWorld::reserve(int64_t bytes, uint8_t** dst, int64_t* off, uint32_t** rea
                       uint32_t* cons_idx, uint32_t* cons_gen) {
     std::lock_guard<std::mutex> g(mu_);
     const int64_t len = std::max<int64_t>(256, (bytes + 255) & ~int64_t(255));
-    if (len > coll_off_)
-        return fail(MPX_ERR_EXHAUSTED, "message of %lld bytes exceeds the %lld-byte staging ring (3/4 of MPX_IPC_ARENA)",
-                    (long long)bytes, (long long)coll_off_);
+    if (len > arena_bytes_)
+        return fail(MPX_ERR_EXHAUSTED, "staged message of %lld bytes exceeds the %lld-byte staging arena "
+                    "(MPX_IPC_ARENA)", (long long)bytes, (long long)arena_bytes_);
     // Room is made by receivers consuming earlier messages (they write the
     // consumed flags from their streams).  The host runs ahead of the GPUs, so
     // when the ring is full wait for that (polling the flags; no GPU call),
@@ -257,15 +327,18 @@ int IpcWorld::reserve(int64_t bytes, uint8_t** dst, int64_t* off, uint32_t** rea
             ++k;
         if (k) {
             inflight_.erase(inflight_.begin(), inflight_.begin() + (long)k);
-            head_ = inflight_.empty() ? tail_ : inflight_.front().off;
             if (inflight_.empty()) head_ = tail_ = 0;
+            else head_ = inflight_.front().off;
         }
-        // place [o, o+len): after tail_, wrapping to 0 when it does not fit
+        // place [o, o+len): after tail_, wrapping to 0 when it does not fit.
+        // Used space is [head_, tail_) when tail_ > head_, and wraps past the
+        // end when tail_ <= head_ with messages in flight (tail_ == head_:
+        // completely full -- the wrapped message exactly filled the gap).
         o = tail_;
         bool fits;
-        const bool wrapped = !inflight_.empty() && tail_ < head_;
+        const bool wrapped = !inflight_.empty() && tail_ <= head_;
         if (!wrapped) {
-            fits = o + len <= coll_off_;
+            fits = o + len <= arena_bytes_;
             if (!fits && (inflight_.empty() || len <= head_)) {
                 o = 0;
                 fits = true;
@@ -307,45 +380,54 @@ void IpcWorld::msg_of(int box, int slot, IpcMsg* m) {
     m->src = e.sender;
     m->tag = e.tag;
     m->bytes = e.bytes;
-    m->data = peer_[e.sender] + e.off;
+    m->rndv = e.rndv;
+    m->data = e.rndv ? nullptr : peer_[e.sender] + e.off;
     m->ready = &sh_->flags[e.sender][e.ready_idx];
     m->ready_gen = e.ready_gen;
     m->consumed = &sh_->flags[e.sender][e.cons_idx];
     m->consumed_gen = e.cons_gen;
+    m->handle = e.handle;
+    m->bufid = e.bufid;
+    m->buf_off = e.buf_off;
+    m->layout = e.layout;
 }
 
-int IpcWorld::post_send(int dest, int ctx, int tag, int64_t bytes, int64_t off, uint32_t* ready, uint32_t ready_gen,
-                        uint32_t cons_idx, uint32_t cons_gen) {
-    if (dest < 0 || dest >= size_) return fail(MPX_ERR_ARG, "dest %d out of range", dest);
-    Box& b = sh_->box[dest];
+int IpcWorld::post_send(const IpcSend& s) {
+    if (s.dest < 0 || s.dest >= size_) return fail(MPX_ERR_ARG, "dest %d out of range", s.dest);
+    Box& b = sh_->box[s.dest];
     pthread_mutex_lock(&b.mu);
     // the oldest posted receive this send matches
     int best = -1;
     for (int i = 0; i < kSlots; ++i) {
         const Entry& e = b.e[i];
-        if (e.state == RECV && matches(e.src, e.tag, e.ctx, rank_, tag, ctx) && (best < 0 || e.seq < b.e[best].seq))
+        if (e.state == RECV && matches(e.src, e.tag, e.ctx, rank_, s.tag, s.ctx) && (best < 0 || e.seq < b.e[best].seq))
             best = i;
     }
     int i = best >= 0 ? best : free_slot(b);
     if (i < 0) {
         pthread_mutex_unlock(&b.mu);
-        return fail(MPX_ERR_EXHAUSTED, "mailbox of rank %d full", dest);
+        return fail(MPX_ERR_EXHAUSTED, "mailbox of rank %d full", s.dest);
     }
     Entry& e = b.e[i];
     if (best < 0) {
         e.seq = b.next_seq++;
-        e.ctx = ctx;
+        e.ctx = s.ctx;
         e.src = rank_;
         e.cookie = 0;
     }
-    e.tag = tag;
-    e.bytes = bytes;
-    e.off = off;
-    e.ready_idx = static_cast<uint32_t>(ready - &sh_->flags[rank_][0]);
-    e.ready_gen = ready_gen;
-    e.cons_idx = cons_idx;
-    e.cons_gen = cons_gen;
+    e.tag = s.tag;
+    e.bytes = s.bytes;
+    e.off = s.off;
+    e.ready_idx = flag_index(s.ready);
+    e.ready_gen = s.ready_gen;
+    e.cons_idx = s.cons_idx;
+    e.cons_gen = s.cons_gen;
     e.sender = rank_;
+    e.rndv = s.rndv;
+    e.handle = s.handle;
+    e.bufid = s.bufid;
+    e.buf_off = s.buf_off;
+    e.layout = s.layout;
     e.state = best >= 0 ? MATCHED : SEND;
     pthread_mutex_unlock(&b.mu);
     return MPX_SUCCESS;
@@ -385,26 +467,116 @@ int IpcWorld::recv(int ctx, int src, int tag, int64_t cap, void* cookie, bool* m
     return MPX_SUCCESS;
 }
 
+int IpcWorld::resolve(IpcMsg* m) {
+    if (!m->rndv || m->data) return MPX_SUCCESS;
+    uint8_t* base = nullptr;
+    if (int rc = import_buffer(m->src, m->handle, m->bufid, &base)) return rc;
+    m->data = base + m->buf_off;
+    return MPX_SUCCESS;
+}
+
+int IpcWorld::export_buffer(const void* p, cudaIpcMemHandle_t* h, uint64_t* id, int64_t* off) {
+    static RangeFn range = driver_fn<RangeFn>("cuMemGetAddressRange");
+    static AttrFn attr = driver_fn<AttrFn>("cuPointerGetAttribute");
+    if (!range || !attr) return fail(MPX_ERR_UNSUPPORTED, "cuMemGetAddressRange / cuPointerGetAttribute unavailable");
+    unsigned long long bid = 0;
+    if (attr(&bid, CU_POINTER_ATTRIBUTE_BUFFER_ID, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS)
+        return fail(MPX_ERR_UNSUPPORTED, "buffer is not device memory of this process");
+    CUdeviceptr alloc = 0;
+    size_t len = 0;
+    if (range(&alloc, &len, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS)
+        return fail(MPX_ERR_UNSUPPORTED, "buffer is not device memory of this process");
+    *id = bid;
+    *off = static_cast<int64_t>(reinterpret_cast<uintptr_t>(p) - static_cast<uintptr_t>(alloc));
+    std::lock_guard<std::mutex> g(buf_mu_);
+    auto it = exported_.find(bid);
+    if (it != exported_.end()) {
+        *h = it->second;
+        return MPX_SUCCESS;
+    }
+    cudaError_t e = cudaIpcGetMemHandle(h, reinterpret_cast<void*>(alloc));
+    if (e != cudaSuccess) {   // e.g. stream-ordered pool memory: not exportable this way
+        cudaGetLastError();
+        return fail(MPX_ERR_UNSUPPORTED, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    }
+    exported_[bid] = *h;
+    return MPX_SUCCESS;
+}
+
+int IpcWorld::import_buffer(int rank, const cudaIpcMemHandle_t& h, uint64_t id, uint8_t** base) {
+    if (rank == rank_) return fail(MPX_ERR_ARG, "a process cannot import its own allocation");
+    std::lock_guard<std::mutex> g(buf_mu_);
+    auto key = std::make_pair(rank, id);
+    auto it = imported_.find(key);
+    if (it != imported_.end()) {
+        *base = it->second;
+        return MPX_SUCCESS;
+    }
+    DeviceGuard guard;
+    MPX_CU_RET(cudaSetDevice(device_));
+    void* q = nullptr;
+    MPX_CU_RET(cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess));
+    imported_[key] = static_cast<uint8_t*>(q);
+    *base = static_cast<uint8_t*>(q);
+    return MPX_SUCCESS;
+}
+
+int IpcWorld::coll_exchange(int cs, int64_t seq, const void* send, void* recv, int64_t count, int code,
+                            std::vector<const void*>* sends, std::vector<void*>* recvs) {
+    CollPost& mine = sh_->coll[rank_][cs][seq % kCollDepth];
+    if (int rc = export_buffer(send, &mine.h[0], &mine.id[0], &mine.off[0])) return rc;
+    if (int rc = export_buffer(recv, &mine.h[1], &mine.id[1], &mine.off[1])) return rc;
+    mine.count = count;
+    mine.code = code;
+    mine.seq.store(seq + 1, std::memory_order_release);
+    sends->assign(size_, nullptr);
+    recvs->assign(size_, nullptr);
+    for (int r = 0; r < size_; ++r) {
+        if (r == rank_) {
+            (*sends)[r] = send;
+            (*recvs)[r] = recv;
+            continue;
+        }
+        CollPost& p = sh_->coll[r][cs][seq % kCollDepth];
+        for (long t = 0; p.seq.load(std::memory_order_acquire) != seq + 1; ++t) {
+            if (t > 6000000) return fail(MPX_ERR_TRANSPORT, "collective %lld: rank %d never arrived", (long long)seq, r);
+            if (t > 1000) nap(20000);
+        }
+        if (p.count != count || p.code != code)
+            return fail(MPX_ERR_ARG, "collective %lld: rank %d passed count %lld / type %d, this rank %lld / %d",
+                        (long long)seq, r, (long long)p.count, p.code, (long long)count, code);
+        uint8_t* b = nullptr;
+        if (int rc = import_buffer(r, p.h[0], p.id[0], &b)) return rc;
+        (*sends)[r] = b + p.off[0];
+        if (int rc = import_buffer(r, p.h[1], p.id[1], &b)) return rc;
+        (*recvs)[r] = b + p.off[1];
+    }
+    return MPX_SUCCESS;
+}
+
+int IpcWorld::share_blob(int slot, int64_t key, void* blob, size_t n) {
+    if (n > sizeof(Blob::data)) return fail(MPX_ERR_ARG, "blob too large");
+    Blob& b = sh_->blob[slot % kBlobs];
+    if (rank_ == 0) {
+        std::memcpy(b.data, blob, n);
+        b.key.store(key + 1, std::memory_order_release);
+        return MPX_SUCCESS;
+    }
+    for (long t = 0; b.key.load(std::memory_order_acquire) != key + 1; ++t) {
+        if (t > 6000000) return fail(MPX_ERR_TRANSPORT, "rank 0 never published blob %lld", (long long)key);
+        nap(20000);
+    }
+    std::memcpy(blob, b.data, n);
+    return MPX_SUCCESS;
+}
+
 int IpcWorld::win_expose(int64_t id, const void* base, int64_t bytes, int64_t unit, std::vector<const void*>* bases,
                          std::vector<int64_t>* sizes, std::vector<int64_t>* units) {
-    using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
-    static RangeFn range = [] {
-        void* f = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &f, 12000, cudaEnableDefault, &q);
-        cudaGetLastError();
-        return reinterpret_cast<RangeFn>(f);
-    }();
-    if (!range) return fail(MPX_ERR_UNSUPPORTED, "cuMemGetAddressRange unavailable");
     WinEntry& mine = sh_->win[id % kWins][rank_];
     std::memset(static_cast<void*>(&mine), 0, sizeof mine);
     if (bytes > 0) {
-        CUdeviceptr alloc = 0;
-        size_t len = 0;
-        if (range(&alloc, &len, reinterpret_cast<CUdeviceptr>(base)) != CUDA_SUCCESS)
+        if (export_buffer(base, &mine.handle, &mine.bufid, &mine.off))
             return fail(MPX_ERR_ARG, "window region is not device memory of this process");
-        MPX_CU_RET(cudaIpcGetMemHandle(&mine.handle, reinterpret_cast<void*>(alloc)));
-        mine.off = static_cast<int64_t>(reinterpret_cast<uintptr_t>(base) - static_cast<uintptr_t>(alloc));
     }
     mine.bytes = bytes;
     mine.unit = unit;
@@ -423,16 +595,9 @@ int IpcWorld::win_expose(int64_t id, const void* base, int64_t bytes, int64_t un
             (*bases)[r] = base;
             continue;
         }
-        // one mapping per (rank, allocation): a handle opens once per process
-        std::string key = std::to_string(r) + ":" + std::string(e.handle.reserved, sizeof e.handle.reserved);
-        void* mapped = nullptr;
-        for (auto& kv : opened_)
-            if (kv.first == key) mapped = kv.second;
-        if (!mapped) {
-            MPX_CU_RET(cudaIpcOpenMemHandle(&mapped, e.handle, cudaIpcMemLazyEnablePeerAccess));
-            opened_.emplace_back(key, mapped);
-        }
-        (*bases)[r] = static_cast<const uint8_t*>(mapped) + e.off;
+        uint8_t* mapped = nullptr;   // one mapping per (rank, allocation)
+        if (int rc = import_buffer(r, e.handle, e.bufid, &mapped)) return rc;
+        (*bases)[r] = mapped + e.off;
     }
     return barrier();    // nobody reuses the slot before every rank has read it
 }

@@ -18,7 +18,6 @@ a private CUDA stream used for host-blocking communication.
 import ctypes
 import os
 import threading
-import warnings
 
 import torch
 
@@ -188,11 +187,6 @@ def free_stream(stream):
 # -------------------------------------------------------------- instance
 
 
-# in-process ranks per device validated by the test-suite and the enqueue
-# sweeps; beyond it init warns (known limit)
-MAX_RANKS_PER_DEVICE = 6
-
-
 class _Group:
     """In-process job: ranks of one world joined by name."""
 
@@ -204,7 +198,6 @@ class _Group:
         self.size = size
         self.barrier = threading.Barrier(size)
         self.members = 0
-        self.devices = {}            # device index -> ranks of this world on it
 
     @classmethod
     def join(cls, name, size):
@@ -266,15 +259,6 @@ class Instance:
             self._comms = [self.world]
             return
         self._group = _Group.join(group, size)
-        with _Group._lock:
-            on_dev = self._group.devices.setdefault(device, set())
-            on_dev.add(rank)
-            crowded = len(on_dev) == MAX_RANKS_PER_DEVICE + 1
-        if crowded:
-            warnings.warn("more than %d ranks of world %r share cuda:%d; large nonblocking "
-                          "exchanges between that many in-process ranks on one GPU are known "
-                          "to stall (DESIGN.md section 6)" % (MAX_RANKS_PER_DEVICE, group, device),
-                          RuntimeWarning, stacklevel=3)
         h = ctypes.c_void_p()
         check(lib.mpx_world_join(group.encode(), size, rank, device, eager_limit,
                                  ctypes.byref(h)))

@@ -125,23 +125,34 @@ def any_source_and_truncation(inst, q, c):
 def allreduce(inst, q, c):
     """allreduce_enqueue across processes: rank-ordered sums (float32
     accumulated in double, comm.py:582-588) and exact int64, several calls
-    back to back (the collective area is reused in stream order)."""
+    back to back (the flags and handle slots are reused in stream order)."""
     dev, n = inst.device, inst.size
-    for count in (1, 1000, 1 << 20):
-        xs = [np.random.default_rng(7 * count + r).uniform(-1, 1, count).astype(np.float32) for r in range(n)]
-        ks = [np.random.default_rng(9 * count + r).integers(-2 ** 20, 2 ** 20, count) for r in range(n)]
-        sf = torch.from_numpy(xs[inst.rank]).to(dev)
-        si = torch.from_numpy(ks[inst.rank]).to(dev)
-        rf, ri = torch.empty_like(sf), torch.empty_like(si)
-        mp.allreduce_enqueue(c, sf, rf, count, mp.FLOAT32)
-        mp.allreduce_enqueue(c, si, ri, count, mp.INT64)
-        mp.queue_synchronize(q)
-        acc = np.zeros(count, np.float64)
-        for x in xs:
-            acc += x.astype(np.float64)
-        assert np.array_equal(rf.cpu().numpy(), acc.astype(np.float32)), count
-        assert np.array_equal(ri.cpu().numpy(), np.sum(ks, axis=0)), count
+    for algo in algos():
+        for count in (1, 1000, 1 << 20):
+            xs = [np.random.default_rng(7 * count + r).uniform(-1, 1, count).astype(np.float32) for r in range(n)]
+            ks = [np.random.default_rng(9 * count + r).integers(-2 ** 20, 2 ** 20, count) for r in range(n)]
+            sf = torch.from_numpy(xs[inst.rank]).to(dev)
+            si = torch.from_numpy(ks[inst.rank]).to(dev)
+            rf, ri = torch.empty_like(sf), torch.empty_like(si)
+            mp.allreduce_enqueue(c, sf, rf, count, mp.FLOAT32, algo=algo)
+            mp.allreduce_enqueue(c, si, ri, count, mp.INT64, algo=algo)
+            mp.queue_synchronize(q)
+            acc = np.zeros(count, np.float64)
+            for x in xs:
+                acc += x.astype(np.float64)
+            got = rf.cpu().numpy()
+            if algo == "native":   # rank order, double accumulation: bit-exact
+                assert np.array_equal(got, acc.astype(np.float32)), count
+            else:                  # NCCL's order: |got - ref| <= 1e-6 * sum_r |x_r| (SURVEY 8c)
+                bound = 1e-6 * np.sum([np.abs(x.astype(np.float64)) for x in xs], axis=0)
+                assert np.all(np.abs(got.astype(np.float64) - acc) <= bound), count
+            assert np.array_equal(ri.cpu().numpy(), np.sum(ks, axis=0)), (algo, count)
     mp.barrier(inst.world)
+
+
+def algos():
+    """native always; NCCL when every rank has its own GPU (one rank per device)."""
+    return ["native", "nccl"] if "LOCAL_RANK" in os.environ else ["native"]
 
 
 def windows(inst):
@@ -227,10 +238,126 @@ def posted_first_then_matched(inst, q, c):
     mp.barrier(inst.world)
 
 
+def arena_wrap(inst, q, c, iters=40):
+    """Staged (eager-path) messages wrapping the staging arena several times
+    without any host synchronisation: a non-chain layout (irregular indexed
+    blocks, so no rendezvous) of ~3 MiB per message through the 64 MiB arena
+    of the test job, a distinct payload per iteration, every received message
+    checked (an arena slot overwritten before it was consumed, or a message
+    delivered to the wrong receive, shows up as a wrong payload)."""
+    dev, r, n = inst.device, inst.rank, inst.size
+    rng = np.random.default_rng(77)
+    nblk = 1 << 16
+    displs = np.cumsum(rng.integers(1, 4, nblk)).astype(np.int64) - 1
+    spec = ("indexed_block", 6, [int(x) for x in displs], ("basic", 1))
+    dt = mp.type_indexed_block(6, [int(x) for x in displs], mp.INT8).commit()
+    ot = oracle.OracleType(spec)
+    span = ot.max_end
+    srcs = [torch.from_numpy(data(7000 + 97 * i + r, span)).to(dev) for i in range(iters)]
+    dsts = [torch.zeros(span, dtype=torch.uint8, device=dev) for _ in range(iters)]
+    torch.cuda.synchronize(dev)
+    mp.barrier(inst.world)
+    reqs = []
+    for i in range(iters):
+        reqs.append(mp.irecv_enqueue(c, dsts[i], 1, dt, (r - 1) % n, 100 + i))
+        reqs.append(mp.isend_enqueue(c, srcs[i], 1, dt, (r + 1) % n, 100 + i))
+    mp.waitall_enqueue(reqs)
+    mp.queue_synchronize(q)
+    for i in range(iters):
+        exp = np.zeros(span, np.uint8)
+        ot.unpack(ot.pack(data(7000 + 97 * i + (r - 1) % n, span)), exp)
+        assert np.array_equal(dsts[i].cpu().numpy(), exp), ("arena wrap", i)
+    mp.type_free(dt)
+    mp.barrier(inst.world)
+
+
+def big(inst, q, c):
+    """BASELINE configs[3]/[4] at their largest size: 1 GiB messages (bytes,
+    and the vector(N/32, 4, 8) FLOAT64 type over a 2 GiB span) around the
+    ring through the rendezvous pull, and 1 GiB allreduce_enqueue in float32
+    (rank-ordered double accumulation, bit-exact) and int64 (exact).  Data is
+    generated and checked on the device (seeded torch generators)."""
+    dev, r, n = inst.device, inst.rank, inst.size
+    nb = 1 << 30
+    prev = (r - 1) % n
+
+    def gen(seed, numel, dtype=torch.uint8):
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed)
+        if dtype == torch.uint8:
+            return torch.randint(0, 256, (numel,), generator=g, device=dev, dtype=torch.uint8)
+        if dtype == torch.int64:
+            return torch.randint(-2 ** 20, 2 ** 20, (numel,), generator=g, device=dev, dtype=torch.int64)
+        return torch.rand(numel, generator=g, device=dev, dtype=torch.float32) * 2 - 1
+
+    for typed in (False, True):
+        span = 2 * nb - 32 if typed else nb
+        src = gen(31 + r, span)
+        dst = torch.full((span,), 0x5A, dtype=torch.uint8, device=dev)
+        if typed:
+            dt, count = mp.type_vector(nb // 32, 4, 8, mp.FLOAT64).commit(), 1
+        else:
+            dt, count = mp.BYTE, nb
+        torch.cuda.synchronize(dev)
+        mp.barrier(inst.world)
+        rr = mp.irecv_enqueue(c, dst, count, dt, prev, 5)
+        sr = mp.isend_enqueue(c, src, count, dt, (r + 1) % n, 5)
+        mp.waitall_enqueue([rr, sr])
+        mp.queue_synchronize(q)
+        exp = gen(31 + prev, span)
+        if typed:
+            d = torch.cat([dst, torch.zeros(32, dtype=torch.uint8, device=dev)]).view(-1, 64)
+            e = torch.cat([exp, torch.zeros(32, dtype=torch.uint8, device=dev)]).view(-1, 64)
+            assert bool((d[:, :32] == e[:, :32]).all()), "1 GiB vector ring payload"
+            assert bool((d[:-1, 32:] == 0x5A).all()), "1 GiB vector ring wrote outside the layout"
+            mp.type_free(dt)
+        else:
+            assert bool((dst == exp).all()), "1 GiB byte ring"
+        assert rr.status.count == count and rr.status.source == prev, rr.status
+        del src, dst, exp
+        mp.barrier(inst.world)
+    for algo in algos():
+        count = nb // 4
+        xs = gen(51 + r, count, torch.float32)
+        out = torch.empty_like(xs)
+        mp.allreduce_enqueue(c, xs, out, count, mp.FLOAT32, algo=algo)
+        mp.queue_synchronize(q)
+        acc = torch.zeros(count, dtype=torch.float64, device=dev)
+        mag = torch.zeros(count, dtype=torch.float64, device=dev)
+        for k in range(n):
+            x = gen(51 + k, count, torch.float32).double()
+            acc += x
+            mag += x.abs()
+        if algo == "native":
+            assert bool((out == acc.float()).all()), "1 GiB float32 allreduce (rank-ordered, double accumulation)"
+        else:
+            assert bool(((out.double() - acc).abs() <= 1e-6 * mag).all()), "1 GiB float32 NCCL allreduce"
+        del xs, out, acc, mag
+        count = nb // 8
+        ks = gen(61 + r, count, torch.int64)
+        out = torch.empty_like(ks)
+        mp.allreduce_enqueue(c, ks, out, count, mp.INT64, algo=algo)
+        mp.queue_synchronize(q)
+        ref = torch.zeros_like(ks)
+        for k in range(n):
+            ref += gen(61 + k, count, torch.int64)
+        assert bool((out == ref).all()), "1 GiB int64 allreduce (%s)" % algo
+        del ks, out, ref
+    mp.barrier(inst.world)
+
+
 def main():
     inst = mp.init(transport="ipc")
     assert inst.transport == "ipc"
     q, s, c = stream_comm(inst)
+    if os.environ.get("IPC_WORKER_MODE") == "big":
+        big(inst, q, c)
+        mp.comm_free(c)
+        mp.free_stream(s)
+        mp.queue_destroy(q)
+        inst.finalize()
+        print("rank %d ok" % inst.rank, flush=True)
+        return
     for nbytes in (8, 1 << 16, 1 << 20, 16 << 20):
         for typed in (False, True):
             if typed and nbytes < 32:
@@ -244,6 +371,7 @@ def main():
     host_buffers(inst)
     if inst.size >= 2:
         any_source_and_truncation(inst, q, c)
+    arena_wrap(inst, q, c)
     t0 = time.perf_counter()
     for _ in range(20):                       # arena reuse: many messages through the ring
         ring(inst, q, c, 4 << 20, False, "recv")

@@ -197,7 +197,7 @@ def test_cross_rank_device_pipeline():
     def rank0(inst):
         q = mp.queue_create(inst)
         c, s = device_comm(inst, q)
-        x = torch.ones(count, dtype=torch.float64, device=DEV)
+        x = torch.ones(count, dtype=torch.float64, device=inst.device)
         mp.send(c, x, count, mp.FLOAT64, 1, 2)
         mp.queue_synchronize(q)
         mp.comm_free(c)
@@ -207,8 +207,8 @@ def test_cross_rank_device_pipeline():
     def rank1(inst):
         q = mp.queue_create(inst)
         c, s = device_comm(inst, q)
-        x = torch.zeros(count, dtype=torch.float64, device=DEV)
-        y = torch.full((count,), 2.0, dtype=torch.float64, device=DEV)
+        x = torch.zeros(count, dtype=torch.float64, device=inst.device)
+        y = torch.full((count,), 2.0, dtype=torch.float64, device=inst.device)
         mp.recv(c, x, count, mp.FLOAT64, 0, 2)
         mp.compute_enqueue(q, mp.saxpy, 2.0, x, y, count)
         mp.queue_synchronize(q)
@@ -227,8 +227,8 @@ def test_criterion_09a_saxpy_pipeline_without_host_sync():
     def device_rank(inst):
         q = mp.queue_create(inst)
         dc, s = device_comm(inst, q)
-        x = torch.zeros(n, dtype=torch.float64, device=DEV)
-        y = torch.full((n,), 2.0, dtype=torch.float64, device=DEV)
+        x = torch.zeros(n, dtype=torch.float64, device=inst.device)
+        y = torch.full((n,), 2.0, dtype=torch.float64, device=inst.device)
         mp.recv(dc, x, n, mp.FLOAT64, 1, 11)
         mp.compute_enqueue(q, mp.saxpy, 2.0, x, y, n)
         mp.queue_synchronize(q)
@@ -258,7 +258,7 @@ def test_criterion_09b_compute_overlaps_pending_receive():
     def device_rank(inst):
         q = mp.queue_create(inst)
         dc, s = device_comm(inst, q)
-        buf = torch.zeros(1024, dtype=torch.float64, device=DEV)
+        buf = torch.zeros(1024, dtype=torch.float64, device=inst.device)
         rreq = mp.irecv(dc, buf, 1024, mp.FLOAT64, 1, 3)
         e_compute = torch.cuda.Event(enable_timing=True)
         e_done = torch.cuda.Event(enable_timing=True)
@@ -279,7 +279,7 @@ def test_criterion_09b_compute_overlaps_pending_receive():
         sc = mp.stream_comm_create(inst.world, hs)
         gate.wait()
         time.sleep(0.3)
-        data = torch.full((1024,), 2.5, dtype=torch.float64, device=DEV)
+        data = torch.full((1024,), 2.5, dtype=torch.float64, device=inst.device)
         mp.send(sc, data, 1024, mp.FLOAT64, 0, 3)
         mp.comm_free(sc)
         mp.free_stream(hs)
@@ -301,14 +301,14 @@ def test_criterion_10_stream_resource_semantics():
         for _ in range(10 * cap):
             mp.free_stream(inst.stream_create())
         # the reference refuses cudaStream_t (UnsupportedError); here it works
-        ts = torch.cuda.Stream(DEV)
+        ts = torch.cuda.Stream(inst.device)
         info = mp.info_create()
         mp.info_set_hex(info, "value", ts.cuda_stream)
         info.set("type", "cudaStream_t")
         s = inst.stream_create(info)
         assert s.kind == mp.CUDA_STREAM and s.cuda_stream == ts.cuda_stream
         c = mp.stream_comm_create(inst.world, s)
-        buf = torch.zeros(3, dtype=torch.uint8, device=DEV)
+        buf = torch.zeros(3, dtype=torch.uint8, device=inst.device)
         mp.send(c, u8(b"abc"), 3, mp.BYTE, 0, 0)
         mp.recv(c, buf, 3, mp.BYTE, 0, 0)
         ts.synchronize()
@@ -323,8 +323,9 @@ def test_criterion_10_stream_resource_semantics():
 
 
 def _ring(n, nbytes, dtype_kind, blocking=False, eager_limit=None):
-    """ring r -> r+1 on n in-process ranks sharing cuda:0, scale kernels
-    before the send and after the receive on the same stream."""
+    """ring r -> r+1 on n in-process ranks (rank r on cuda:(r % devices):
+    one GPU -> they share it; 2+ GPUs -> NVLink peer transfers), scale
+    kernels before the send and after the receive on the same stream."""
     results = [None] * n
 
     def body(inst):
@@ -333,12 +334,12 @@ def _ring(n, nbytes, dtype_kind, blocking=False, eager_limit=None):
         c, s = device_comm(inst, q)
         g = torch.Generator(device="cpu").manual_seed(100 + r)
         if dtype_kind == "u8":
-            src = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, generator=g).to(DEV)
+            src = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, generator=g).to(inst.device)
             dst = torch.zeros_like(src)
             dt, count = mp.BYTE, nbytes
         else:   # vector(N/32, 4, 8) of FLOAT64 over 2N bytes
             nv = nbytes // 32
-            src = torch.rand(nv * 8, dtype=torch.float64, generator=g).to(DEV)
+            src = torch.rand(nv * 8, dtype=torch.float64, generator=g).to(inst.device)
             dst = torch.zeros_like(src)
             dt, count = mp.type_vector(nv, 4, 8, mp.FLOAT64).commit(), 1
         with torch.cuda.stream(q.torch_stream):
@@ -405,7 +406,7 @@ def test_any_source_any_tag_and_fifo_order():
     def rank1(inst):
         q = mp.queue_create(inst)
         c, s = device_comm(inst, q)
-        got = [torch.zeros(1, dtype=torch.uint8, device=DEV) for _ in range(3)]
+        got = [torch.zeros(1, dtype=torch.uint8, device=inst.device) for _ in range(3)]
         r0 = mp.irecv(c, got[0], 1, mp.BYTE, mp.ANY_SOURCE, 9)
         r1 = mp.irecv(c, got[1], 1, mp.BYTE, 0, mp.ANY_TAG)
         r2 = mp.irecv(c, got[2], 1, mp.BYTE, mp.ANY_SOURCE, mp.ANY_TAG)
@@ -424,10 +425,10 @@ def test_typed_transfer_vector_to_contiguous():   # test_p2p.py:114-132
     def rank0(inst):
         q = mp.queue_create(inst)
         c, s = device_comm(inst, q)
-        src = torch.arange(12, dtype=torch.int32, device=DEV)
+        src = torch.arange(12, dtype=torch.int32, device=inst.device)
         vt = mp.type_vector(4, 1, 3, mp.INT32).commit()
         mp.send(c, src, 1, vt, 1, 0)
-        back = torch.zeros(12, dtype=torch.int32, device=DEV)
+        back = torch.zeros(12, dtype=torch.int32, device=inst.device)
         mp.recv(c, back, 1, vt, 1, 1)
         mp.queue_synchronize(q)
         assert back.cpu().tolist() == [0, 0, 0, 3, 0, 0, 6, 0, 0, 9, 0, 0]
@@ -437,7 +438,7 @@ def test_typed_transfer_vector_to_contiguous():   # test_p2p.py:114-132
     def rank1(inst):
         q = mp.queue_create(inst)
         c, s = device_comm(inst, q)
-        dst = torch.zeros(4, dtype=torch.int32, device=DEV)
+        dst = torch.zeros(4, dtype=torch.int32, device=inst.device)
         rr = mp.irecv(c, dst, 4, mp.INT32, 0, 0)
         mp.wait_enqueue(rr)
         mp.send(c, dst, 4, mp.INT32, 0, 1)
@@ -460,7 +461,7 @@ def test_zipper_typed_to_typed_rendezvous():
     def rank0(inst):
         q = mp.queue_create(inst)
         c, s = device_comm(inst, q)
-        src = torch.arange(4096 * 5, dtype=torch.float64, device=DEV)
+        src = torch.arange(4096 * 5, dtype=torch.float64, device=inst.device)
         mp.send(c, src, 1, mp.type_vector(4096, 3, 5, mp.FLOAT64).commit(), 1, 3)
         mp.queue_synchronize(q)
         mp.comm_free(c)
@@ -469,7 +470,7 @@ def test_zipper_typed_to_typed_rendezvous():
     def rank1(inst):
         q = mp.queue_create(inst)
         c, s = device_comm(inst, q)
-        dst = torch.zeros(2048 * 8, dtype=torch.float64, device=DEV)
+        dst = torch.zeros(2048 * 8, dtype=torch.float64, device=inst.device)
         mp.recv(c, dst, 1, mp.type_hvector(2048, 6, 64, mp.FLOAT64).commit(), 0, 3)
         mp.queue_synchronize(q)
         ref = np.zeros(2048 * 8, np.float64)
@@ -504,7 +505,7 @@ def test_zipper_chain_to_chain_matches_copy_between(st, rt, elem):
     def rank0(inst):
         q = mp.queue_create(inst)
         c, s = device_comm(inst, q)
-        src = torch.from_numpy(src_h).to(DEV)
+        src = torch.from_numpy(src_h).to(inst.device)
         mp.send(c, src, 1, build_product(st, mp), 1, 5)
         mp.queue_synchronize(q)
         mp.comm_free(c)
@@ -513,7 +514,7 @@ def test_zipper_chain_to_chain_matches_copy_between(st, rt, elem):
     def rank1(inst):
         q = mp.queue_create(inst)
         c, s = device_comm(inst, q)
-        dst = torch.zeros(ot_r.max_end, dtype=torch.uint8, device=DEV)
+        dst = torch.zeros(ot_r.max_end, dtype=torch.uint8, device=inst.device)
         mp.recv(c, dst, 1, build_product(rt, mp), 0, 5)
         mp.queue_synchronize(q)
         ref = np.zeros(ot_r.max_end, np.uint8)
@@ -548,7 +549,7 @@ def test_allreduce_enqueue_native_matches_rank_ordered_oracle(n, kind):
     def body(inst):
         q = mp.queue_create(inst)
         c, s = device_comm(inst, q)
-        sb = torch.from_numpy(bufs[inst.rank]).to(DEV)
+        sb = torch.from_numpy(bufs[inst.rank]).to(inst.device)
         rb = torch.zeros_like(sb)
         with torch.cuda.stream(q.torch_stream):
             sb.mul_(1)                                  # compute before
@@ -573,7 +574,7 @@ def test_allreduce_enqueue_nccl_single_rank():
     try:
         q = mp.queue_create(inst)
         c, s = device_comm(inst, q)
-        x = torch.randn(1 << 16, device=DEV)
+        x = torch.randn(1 << 16, device=inst.device)
         y = torch.zeros_like(x)
         mp.allreduce_enqueue(c, x, y, x.numel(), mp.FLOAT32, algo="nccl")
         mp.queue_synchronize(q)
@@ -587,11 +588,11 @@ def test_allreduce_enqueue_nccl_single_rank():
 def test_host_allreduce_reference_cases():   # test_comm.py:103-132
     def body(inst):
         r = inst.rank
-        ib = torch.tensor([1 + r, 10 + 10 * r], dtype=torch.int64, device=DEV)
-        io = torch.zeros(2, dtype=torch.int64, device=DEV)
+        ib = torch.tensor([1 + r, 10 + 10 * r], dtype=torch.int64, device=inst.device)
+        io = torch.zeros(2, dtype=torch.int64, device=inst.device)
         mp.allreduce(inst.world, ib, io, 2, mp.INT64)
-        fb = torch.tensor([1.0], dtype=torch.float64, device=DEV)
-        fo = torch.zeros(1, dtype=torch.float64, device=DEV)
+        fb = torch.tensor([1.0], dtype=torch.float64, device=inst.device)
+        fo = torch.zeros(1, dtype=torch.float64, device=inst.device)
         mp.allreduce(inst.world, fb, fo, 1, mp.FLOAT64)
         mp.allreduce(inst.world, fb, fo, 0, mp.FLOAT64)          # count 0: no-op
         with pytest.raises(ArgError):
@@ -612,13 +613,13 @@ def test_queues_created_while_a_peer_stream_is_parked():
     import threading
     parked = threading.Event()
     nbytes = 1 << 20
-    payload = torch.arange(nbytes, dtype=torch.int64, device=DEV).to(torch.uint8)
+    payload = torch.arange(nbytes, dtype=torch.int64).to(torch.uint8)
     got = {}
 
     def rank0(inst):
         q = mp.queue_create(inst)
         c, s = device_comm(inst, q)                       # collective with rank 1
-        dst = torch.zeros(nbytes, dtype=torch.uint8, device=DEV)
+        dst = torch.zeros(nbytes, dtype=torch.uint8, device=inst.device)
         mp.recv_enqueue(c, dst, nbytes, mp.BYTE, 1, 5)    # parks the stream until delivery
         parked.set()
         mp.queue_synchronize(q)
@@ -639,7 +640,7 @@ def test_queues_created_while_a_peer_stream_is_parked():
             mp.info_set(info, "type", "devstream")
             mp.info_set_hex(info, "value", bytes.fromhex(eq.handle))
             extra.append((eq, inst.stream_create(info)))
-        mp.send_enqueue(c, payload, nbytes, mp.BYTE, 0, 5)
+        mp.send_enqueue(c, payload.to(inst.device), nbytes, mp.BYTE, 0, 5)
         mp.queue_synchronize(q)
         for eq, es in extra:
             mp.free_stream(es)
@@ -666,8 +667,8 @@ def test_receives_complete_out_of_posting_order(nbytes):
         c, s = device_comm(inst, q)
         assert posted.wait(60)
         time.sleep(0.05)
-        a = torch.full((nbytes,), 1, dtype=torch.uint8, device=DEV)
-        b = torch.full((nbytes,), 2, dtype=torch.uint8, device=DEV)
+        a = torch.full((nbytes,), 1, dtype=torch.uint8, device=inst.device)
+        b = torch.full((nbytes,), 2, dtype=torch.uint8, device=inst.device)
         reqs = [mp.isend_enqueue(c, a, nbytes, mp.BYTE, 1, 1),
                 mp.isend_enqueue(c, b, nbytes, mp.BYTE, 1, 2)]
         mp.waitall_enqueue(reqs)
@@ -679,8 +680,8 @@ def test_receives_complete_out_of_posting_order(nbytes):
     def rank1(inst):
         q = mp.queue_create(inst)
         c, s = device_comm(inst, q)
-        x = torch.zeros(nbytes, dtype=torch.uint8, device=DEV)
-        y = torch.zeros(nbytes, dtype=torch.uint8, device=DEV)
+        x = torch.zeros(nbytes, dtype=torch.uint8, device=inst.device)
+        y = torch.zeros(nbytes, dtype=torch.uint8, device=inst.device)
         r2 = mp.irecv_enqueue(c, x, nbytes, mp.BYTE, 0, 2)
         mp.wait_enqueue(r2)                    # the stream reaches tag 1's post only after tag 2
         r1 = mp.irecv_enqueue(c, y, nbytes, mp.BYTE, 0, 1)
@@ -694,3 +695,42 @@ def test_receives_complete_out_of_posting_order(nbytes):
 
     pair(rank0, rank1)
     assert bool((got["x"] == 2).all()) and bool((got["y"] == 1).all())
+
+
+# ---------------------------------------- BASELINE sizes (configs[3], [4])
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("n,nbytes", [(2, 64 << 20), (4, 64 << 20), (2, 1 << 30)])
+@pytest.mark.parametrize("kind", ["u8", "vector"])
+def test_ring_baseline_sizes(n, nbytes, kind):
+    """64 MiB and 1 GiB rings (rendezvous; typed -> typed through the zipper),
+    data generated and checked on the device (tests/ringkit.py)."""
+    import ringkit
+    ringkit.ring(n, nbytes, kind, iters=2 if nbytes < (1 << 30) else 1)
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("nbytes", [1 << 10, 64 << 20, 1 << 30])
+@pytest.mark.parametrize("kind", ["int64", "float32"])
+def test_allreduce_baseline_sizes_native(nbytes, kind):
+    import ringkit
+    ringkit.allreduce(2, nbytes, kind, "native")
+
+
+@pytest.mark.timeout(900)
+def test_eight_ranks_on_one_gpu_vector_ring_20_runs():
+    """8 in-process ranks sharing one GPU, nonblocking 64 MiB vector(N/32,4,8)
+    ring with the dependent scale kernels (tools/enqueue_bench.py), 20 fresh
+    worlds in a row.  Streams per device stay below the hardware queue count
+    (one shared late stream per device, a pool reserve of 3 per rank): with
+    more streams than queues a stream parked in a wait parks its queue-mate
+    (tools/stall_probe.py: 4 ranks on 4 queues stall every run)."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import enqueue_bench as eb
+    for k in range(20):
+        res = eb.ring(8, 64 << 20, iters=5, warmup=3, kind="vector", group=unique_group("r8-%d" % k),
+                      device=lambda r: 0)
+        assert res["correct"], (k, res)

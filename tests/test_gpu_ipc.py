@@ -17,12 +17,14 @@ pytestmark = [pytest.mark.gpu, pytest.mark.timeout(600)]
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def run_job(n):
+def run_job(n, mode="all", devices=None):
     job = "t%s" % uuid.uuid4().hex[:10]
     procs = []
     for r in range(n):
         env = dict(os.environ, MINIMPI_TRANSPORT="ipc", MINIMPI_RANK=str(r), MINIMPI_SIZE=str(n),
-                   MINIMPI_GROUP=job, MPX_IPC_ARENA=str(64 << 20))
+                   MINIMPI_GROUP=job, MPX_IPC_ARENA=str(64 << 20), IPC_WORKER_MODE=mode)
+        if devices:
+            env["LOCAL_RANK"] = str(r % devices)     # one rank per device (init(transport="ipc"))
         procs.append(subprocess.Popen([sys.executable, os.path.join(HERE, "ipc_worker.py")], env=env,
                                       stdout=subprocess.PIPE, stderr=subprocess.STDOUT))
     outs = []
@@ -41,3 +43,25 @@ def run_job(n):
 @pytest.mark.parametrize("n", [2, 3])
 def test_multi_process_world(n):
     run_job(n)
+
+
+def test_multi_process_1gib_ring_and_allreduce():
+    """1 GiB rendezvous rings (bytes and the strided vector type) and 1 GiB
+    allreduce, 2 processes on this box's GPU (BASELINE configs[3]/[4] top size)."""
+    run_job(2, mode="big")
+
+
+def _ndev():
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_multi_process_one_rank_per_gpu(n):
+    """The deployment shape: one process per GPU (peer mappings over NVLink,
+    NCCL allreduce through ncclCommInitRank with the id shared in the job's
+    segment).  Needs n devices; skipped on smaller boxes."""
+    if _ndev() < n:
+        pytest.skip("needs %d GPUs, %d visible" % (n, _ndev()))
+    run_job(n, devices=n)
+    run_job(n, mode="big", devices=n)

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def _run_ranks(n, body, group):
+def _run_ranks(n, body, group, device=None):
     import paper_2402_12274_b200 as mp
     import torch
     ndev = torch.cuda.device_count()
@@ -28,7 +28,7 @@ def _run_ranks(n, body, group):
     def runner(r):
         inst = None
         try:
-            inst = mp.init(rank=r, ranks=n, group=group, device=r % ndev)
+            inst = mp.init(rank=r, ranks=n, group=group, device=device(r) if device else r % ndev)
             out[r] = body(inst, bar)
         except BaseException as e:  # noqa: B902
             errs.append(e)
@@ -50,7 +50,7 @@ def _run_ranks(n, body, group):
     return out
 
 
-def ring(n=2, nbytes=64 << 20, iters=20, warmup=3, group="bench-ring", kind="u8", scale=True):
+def ring(n=2, nbytes=64 << 20, iters=20, warmup=3, group="bench-ring", kind="u8", scale=True, device=None):
     """kind "u8": contiguous bytes; "vector": vector(N/32, 4, 8) of float64
     on both sides (BASELINE configs[3]: payload N bytes over a 2N - 32 byte
     span; typed -> typed, so the rendezvous path runs the one-pass zipper),
@@ -111,7 +111,7 @@ def ring(n=2, nbytes=64 << 20, iters=20, warmup=3, group="bench-ring", kind="u8"
         mp.free_stream(s)
         return dev_ms, wall, ok
 
-    res = _run_ranks(n, body, group)
+    res = _run_ranks(n, body, group, device)
     ms = max(x[0] for x in res) / iters
     wall = max(x[1] for x in res)
     return {"ranks": n, "kind": kind, "scale_kernels": bool(kind != "u8" and scale), "bytes": nbytes, "iters": iters, "ms_per_iter": ms,
