@@ -67,6 +67,38 @@ def step_bytes():
     return 4 * sum(face_bytes(s) for _, s in face_specs())
 
 
+def step_floor(dts, dev):
+    """DRAM floor of one step from the layouts themselves: every face's bytes
+    are marked in a coverage copy of the array (unpack of 0xFF, i.e. the
+    library's own scatter), then counted per DRAM unit.  Reads of the layout
+    (pack) cost whole 128-byte lines -- the granularity measured on this B200
+    (profiles/r01_l2probe.csv, tools/l2probe.py: an isolated 4-byte read per 2 KB row moves 128 B
+    of DRAM) -- writes (unpack) whole 32-byte sectors, plus one 32-byte fill
+    read per partially written sector; the packed side is contiguous.  The
+    union over the 12 faces is taken (a 1-wide face lies inside the 8-wide
+    face of its side), so this is a lower bound for the fused step."""
+    import torch
+    import paper_2402_12274_b200 as mp
+    n = (ARRAY_BYTES + 127) // 128 * 128
+    cov = torch.zeros(n, dtype=torch.uint8, device=dev)
+    payload = 0
+    for dt in dts:
+        k = mp.packed_size(dt)
+        payload += k
+        mp.unpack(dt, torch.full((k,), 0xFF, dtype=torch.uint8, device=dev), cov[:ARRAY_BYTES])
+    hit = cov != 0
+    per32 = hit.view(-1, 32).sum(1)
+    sectors = int((per32 > 0).sum())
+    partial = int(((per32 > 0) & (per32 < 32)).sum())
+    lines = int(hit.view(-1, 128).any(1).sum())
+    del cov, hit, per32
+    pack_floor = lines * 128 + payload
+    unpack_floor = payload + sectors * 32 + partial * 32
+    return {"payload_bytes": payload, "layout_lines_128B": lines, "layout_sectors_32B": sectors,
+            "partial_sectors": partial, "pack_floor_bytes": pack_floor, "unpack_floor_bytes": unpack_floor,
+            "step_floor_bytes": pack_floor + unpack_floor}
+
+
 def dist_env():
     return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
             int(os.environ.get("LOCAL_RANK", "0")))
@@ -448,6 +480,8 @@ def multi_gpu_enqueue(args, dev, world):
             span = 2 * nb - 32 if vec else nb
             g.manual_seed(1000 + r)
             src = torch.randint(0, 256, (span,), generator=g, device=dev, dtype=torch.uint8)
+            if vec:   # finite doubles: the scale kernels must not change a NaN's payload bits
+                src.view(torch.float64).copy_(torch.rand(span // 8, generator=g, device=dev, dtype=torch.float64))
             dst = torch.zeros_like(src)
             dt, count = (mp.type_vector(nb // 32, 4, 8, mp.FLOAT64).commit(), 1) if vec else (mp.BYTE, nb)
             f64 = span // 8
@@ -455,7 +489,7 @@ def multi_gpu_enqueue(args, dev, world):
             def one():
                 if scale:
                     with torch.cuda.stream(q.torch_stream):
-                        src.view(torch.float64)[:f64].mul_(1.0)      # dependent kernel before the send
+                        src.view(torch.float64)[:f64].mul_(1.0)      # dependent kernel before the send (finite data)
                 rr = mp.irecv_enqueue(c, dst, count, dt, (r - 1) % n, 0)
                 sr = mp.isend_enqueue(c, src, count, dt, (r + 1) % n, 0)
                 mp.waitall_enqueue([rr, sr])
@@ -466,6 +500,8 @@ def multi_gpu_enqueue(args, dev, world):
             ms = timed(one, iters)
             g.manual_seed(1000 + (r - 1) % n)
             exp = torch.randint(0, 256, (span,), generator=g, device=dev, dtype=torch.uint8)
+            if vec:
+                exp.view(torch.float64).copy_(torch.rand(span // 8, generator=g, device=dev, dtype=torch.float64))
             if vec:
                 pad = torch.zeros(32, dtype=torch.uint8, device=dev)
                 ok = bool((torch.cat([dst, pad]).view(-1, 64)[:, :32] ==
@@ -544,6 +580,7 @@ def gpu_arm(args):
     packed_host = [torch.empty(p.numel(), dtype=torch.uint8).pin_memory() for p in packed]
     flush = L2Flush(dev)
     stream = torch.cuda.current_stream(dev)
+    floor = step_floor(dts, dev)
 
     def step():
         mp.pack_multi(dts, [arr] * len(dts), packed)
@@ -683,7 +720,13 @@ def gpu_arm(args):
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
                          "traffic": traffic.get("bytes_per_launch") if traffic else None,
-                         "algorithmic_bytes_per_launch": launch_bytes},
+                         "traffic_source": traffic.get("source") if traffic else None,
+                         "algorithmic_bytes_per_launch": launch_bytes,
+                         "floor_bytes_per_launch": floor["unpack_floor_bytes" if uk >= pk else "pack_floor_bytes"],
+                         "frac_of_floor": round(floor["unpack_floor_bytes" if uk >= pk else "pack_floor_bytes"]
+                                                / (dom_ms / 1e3) / 1e9 / peak, 4)},
+            "step_floor": dict(floor, frac_of_floor=round(floor["step_floor_bytes"] / (ms_per_step / 1e3) / 1e9
+                                                          / peak, 4)),
             "e2e": {"value": round(job_value(step_bytes(), world, e2e_ms), 3), "unit": "GB/s",
                     "ms_per_step": round(e2e_ms, 3),
                     "mode": "halo step: array resident in HBM; received packed faces H2D "

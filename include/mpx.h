@@ -194,19 +194,26 @@ int mpx_comm_synchronize(mpx_comm c);
 /* explicit progress (runtime.py:141-146): reclaim staging buffers and events
  * of completed operations; never blocks.  *outstanding = live requests. */
 int mpx_comm_progress(mpx_comm c, int64_t *outstanding);
+/* order `stream` after the work already issued on `after` (same device):
+ * one pooled event recorded on `after`, waited on by `stream`; no host wait */
+int mpx_stream_order(void *after, void *stream);
 /* device owning a cudaStream_t (for wrapping a raw handle from an Info) */
 int mpx_stream_device(void *stream, int *device);
 /* ---- multi-process worlds (csrc/ipc.hpp) -----------------------
  * One process per rank on one node (e.g. under torchrun): collective over
- * the `size` processes that join job name `job`.  Matching, flags and a
- * per-rank device staging arena of `arena_bytes` (exported with CUDA IPC)
- * live in a shared-memory segment; every message is packed into the
- * sender's arena at its stream position and unpacked by the receiving
- * process straight from there.  Stream communicators and the send / recv /
- * isend / irecv / wait enqueue calls, allreduce_enqueue (rank-ordered,
- * through the last quarter of every arena) and read windows (IPC handles of
- * the exposed allocations exchanged at win_create) work unchanged on such a
- * world. */
+ * the `size` processes that join job name `job`.  Matching and flags live in
+ * a shared-memory segment.  Eager messages (<= eager_limit, self-sends, and
+ * layouts that are not strided chains) are packed into the sender's device
+ * staging arena of `arena_bytes` (exported with CUDA IPC) at its stream
+ * position and unpacked by the receiving process straight from there;
+ * larger contiguous / chain-layout messages are pulled by the receiver
+ * directly from the sender's buffer (cached IPC mapping of its allocation)
+ * in one transfer kernel, and the send completes when it has been read
+ * (transport.py:355-375,548-602).  Stream communicators and the send / recv
+ * / isend / irecv / wait enqueue calls, allreduce_enqueue (NCCL through
+ * ncclCommInitRank when every rank has its own GPU, else the rank-ordered
+ * native kernel over the peers' mapped buffers) and read windows work
+ * unchanged on such a world. */
 int mpx_ipc_world_join(const char *job, int size, int rank, int device, int64_t eager_limit,
                        int64_t arena_bytes, mpx_world *out);
 /* host barrier over the processes of a multi-process world */

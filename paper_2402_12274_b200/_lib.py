@@ -11,7 +11,8 @@ import os
 from .errors import error_for_code
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libmpx.so")
+# MPX_LIB_PATH: an A/B build of the same sources (experiments only)
+SO_PATH = os.environ.get("MPX_LIB_PATH") or os.path.join(_HERE, "libmpx.so")
 
 if not os.path.exists(SO_PATH):
     raise ImportError(
@@ -56,6 +57,7 @@ _SIGS = {
     "mpx_unpack": ([dt_t, i64, vp, i64, vp, i64, p64, vp], cint),
     "mpx_pack_multi": ([cint, pdt, p64, pvp, p64, pvp, p64, vp], cint),
     "mpx_unpack_multi": ([cint, pdt, p64, pvp, p64, pvp, p64, vp], cint),
+    "mpx_stream_order": ([vp, vp], cint),
     "mpx_world_join": ([ctypes.c_char_p, cint, cint, cint, i64, pvp], cint),
     "mpx_world_leave": ([vp, cint], cint),
     "mpx_comm_create": ([vp, cint, cint, vp, pvp], cint),

@@ -15,7 +15,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INC = os.path.join(os.path.dirname(HERE), "include")
-SO = os.path.join(HERE, "libmpx.so")
+SO = os.environ.get("MPX_SO_OUT") or os.path.join(HERE, "libmpx.so")   # MPX_SO_OUT: A/B builds
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -41,7 +41,7 @@ def _stale():
 def build(force=False, verbose=False):
     if not force and not _stale():
         return SO
-    objdir = os.path.join(HERE, "_obj")
+    objdir = os.path.join(HERE, "_obj") if SO.endswith(os.path.join(HERE, "libmpx.so")) else SO + ".obj"
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []

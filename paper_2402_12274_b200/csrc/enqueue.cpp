@@ -238,8 +238,58 @@ int staging_alloc(int dev, size_t bytes, cudaStream_t st, void** out) {
     return MPX_SUCCESS;
 }
 
+// Events are recycled through a per-device free list: creating and
+// destroying one per stream point cost ~2 us of host time per operation.
+// An event goes back to the list only when its last user is done with it
+// (every wait on it enqueued, every query done) -- the points where the code
+// used to destroy it -- so re-recording it later cannot be observed.
+class EventPool {
+  public:
+    cudaError_t get(cudaEvent_t* ev) {
+        int dev = -1;
+        cudaGetDevice(&dev);
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            auto& f = free_[dev];
+            if (!f.empty()) {
+                *ev = f.back();
+                f.pop_back();
+                return cudaSuccess;
+            }
+        }
+        cudaError_t e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+        if (e == cudaSuccess) {
+            std::lock_guard<std::mutex> g(mu_);
+            dev_of_[*ev] = dev;
+        }
+        return e;
+    }
+    void put(cudaEvent_t ev) {
+        if (!ev) return;
+        std::lock_guard<std::mutex> g(mu_);
+        auto it = dev_of_.find(ev);
+        if (it == dev_of_.end()) {   // not one of ours
+            cudaEventDestroy(ev);
+            return;
+        }
+        free_[it->second].push_back(ev);
+    }
+
+  private:
+    std::mutex mu_;
+    std::unordered_map<int, std::vector<cudaEvent_t>> free_;
+    std::unordered_map<cudaEvent_t, int> dev_of_;
+};
+
+EventPool& event_pool() {
+    static EventPool* p = new EventPool();   // never destroyed: events outlive late users
+    return *p;
+}
+
+void release_event(cudaEvent_t ev) { event_pool().put(ev); }
+
 int record_new_event(cudaStream_t s, cudaEvent_t* ev) {
-    MPX_CU(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+    MPX_CU(event_pool().get(ev));
     MPX_CU(cudaEventRecord(*ev, s));
     return MPX_SUCCESS;
 }
@@ -335,6 +385,11 @@ struct ReqState {
     uint32_t* flag = nullptr;  // wait flag >= gen (first side)
     uint32_t gen = 0;
     cudaEvent_t done_ev = nullptr;  // or wait this event (second side, side stream)
+    // or run this delivery on the waiting stream: a nonblocking receive
+    // matched at initiation moves its data when its stream reaches the wait
+    // (the stream then waits only for the sender's data point, which the
+    // wait has to anyway -- no side stream, no deferral thread)
+    std::function<int(cudaStream_t)> at_wait;
     bool needs_wait = false;
     bool waited = false;
     std::mutex mu;
@@ -683,7 +738,7 @@ int consume_staging(World* w, int dev, cudaStream_t st, const PendingSend& ps, c
     MPX_TRACE("consume: freeing staging");
     MPX_CU(cudaFreeAsync(ps.staging, svc));
     MPX_TRACE("consume: freed");
-    cudaEventDestroy(used);
+    release_event(used);
     return MPX_SUCCESS;
 }
 
@@ -768,6 +823,29 @@ int do_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t buf_bytes, 
         MPX_RC(stage_send(c, ps));
         cudaEvent_t staged;
         MPX_RC(record_new_event(c->stream, &staged));
+        ps.ev = staged;
+        if (pr.req) {   // a nonblocking receive not waited yet: it unpacks at its wait
+            std::unique_lock<std::mutex> rl(pr.req->mu);
+            if (!pr.req->waited) {
+                World* wd = w;
+                Side rr = pr.r;
+                cudaEvent_t post = pr.ev;
+                pr.req->at_wait = [wd, ps, rr, moved, post](cudaStream_t ws) -> int {
+                    MPX_RC(set_device(rr.device));
+                    MPX_CU(cudaStreamWaitEvent(ws, ps.ev, 0));
+                    MPX_RC(consume_staging(wd, rr.device, ws, ps, rr, moved));
+                    MPX_RC(set_device(rr.device));
+                    release_event(ps.ev);
+                    release_event(post);
+                    return MPX_SUCCESS;
+                };
+                rl.unlock();
+                MPX_TRACE("send r%d -> %d: eager, delivered at the receiver's wait", c->rank, dest);
+                if (req) c->outstanding++;
+                if (out_req) *out_req = req;
+                return MPX_SUCCESS;
+            }
+        }
         if (!c->side_stream()) return cuda_fail(c->side_err, "cudaStreamCreate(side)");
         auto deliver = [c, staged, ev = pr.ev, r = pr.r, flag = pr.flag, gen = pr.gen, staging = ps.staging,
                         moved](cudaStream_t st) -> int {
@@ -779,8 +857,8 @@ int do_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t buf_bytes, 
             MPX_RC(set_device(c->device));
             MPX_CU(cudaFreeAsync(staging, st));
             MPX_RC(write_flag(st, flag, gen));
-            cudaEventDestroy(staged);
-            cudaEventDestroy(ev);
+            release_event(staged);
+            release_event(ev);
             return MPX_SUCCESS;
         };
         if (ev_done(pr.ev)) {   // the side stream waits only for this rank's own staging point
@@ -825,8 +903,8 @@ int do_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t buf_bytes, 
                 if (!rc) rc = write_flag(side, flag, gen);
                 if (!rc) rc = write_flag(side, done, dgen);
                 if (rc) defer_error(c, rc, "deferred delivery failed: " + g_last_error);
-                cudaEventDestroy(fork);
-                cudaEventDestroy(ev);
+                release_event(fork);
+                release_event(ev);
                 return true;
             });
             c->outstanding++;
@@ -840,9 +918,9 @@ int do_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t buf_bytes, 
         MPX_RC(record_new_event(c->side_stream(), &req->done_ev));
         req->needs_wait = true;
         if (mpx_tracing()) note_side({c->side_stream(), fork, c->stream, pr.ev, pr.r.comm->stream, pr.flag, c->rank});
-        else cudaEventDestroy(fork);
+        else release_event(fork);
     }
-    if (!mpx_tracing()) cudaEventDestroy(pr.ev);  // the waits above captured it
+    if (!mpx_tracing()) release_event(pr.ev);  // the waits above captured it
     if (req) c->outstanding++;
     if (out_req) *out_req = req;
     MPX_TRACE("send r%d -> %d issued", c->rank, dest);
@@ -912,6 +990,27 @@ int do_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t buf_bytes, int64_
     MPX_RC(ensure_peer(w, c->device, ps.s.device));
     MPX_RC(set_device(c->device));
     cudaStream_t st = c->stream;
+    if (!blocking && ps.eager) {
+        // an eager message (its sender never waits for it) matched at
+        // initiation: the data moves when this stream reaches wait_enqueue,
+        // waiting there only for the sender's staging point -- no side
+        // stream, no deferral thread.  (Not for rendezvous: the sender's
+        // completion would then hang on this rank's wait, which MPI lets
+        // depend on the sender's later operations.)
+        req->at_wait = [w, c, ps, r, moved](cudaStream_t ws) -> int {
+            MPX_RC(set_device(c->device));
+            MPX_CU(cudaStreamWaitEvent(ws, ps.ev, 0));
+            MPX_RC(consume_staging(w, c->device, ws, ps, r, moved));
+            MPX_RC(set_device(c->device));
+            release_event(ps.ev);
+            return MPX_SUCCESS;
+        };
+        req->needs_wait = true;
+        c->outstanding++;
+        if (out_req) *out_req = req;
+        MPX_TRACE("recv r%d matched an eager send at initiation: delivery at wait", c->rank);
+        return MPX_SUCCESS;
+    }
     cudaEvent_t fork0 = nullptr;
     if (!blocking) MPX_RC(record_new_event(c->stream, &fork0));
     if (!blocking && !ev_done(ps.ev)) {
@@ -922,51 +1021,41 @@ int do_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t buf_bytes, int64_
         // points; nothing ever waits for a peer point that is not reached,
         // so no delivery can hold up another queued behind it.
         cudaEvent_t fork = fork0;
-        if (!c->side_stream()) return cuda_fail(c->side_err, "cudaStreamCreate(side)");
         uint32_t* done = nullptr;
         uint32_t dgen = 0;
         w->flags.take(&done, &dgen);
         req->flag = done;
         req->gen = dgen;
         req->needs_wait = true;
-        w->defer([w, c, fork, ps, r, moved, done, dgen]() {
+        w->defer([c, fork, ps, r, moved, done, dgen]() {
             if (!ev_done(ps.ev) || !ev_done(fork)) return false;
             int rc = set_device(c->device);
             cudaStream_t side = c->late_stream();
-            if (!rc && !side) rc = cuda_fail(c->late_err, "cudaStreamCreate(late)");
+            if (!rc && !side) rc = cuda_fail(c->late_err, "late stream");
             if (!rc && cudaStreamWaitEvent(side, fork, 0) != cudaSuccess) rc = fail(MPX_ERR_OTHER, "wait");
             if (!rc && cudaStreamWaitEvent(side, ps.ev, 0) != cudaSuccess) rc = fail(MPX_ERR_OTHER, "wait");
-            if (!rc) {
-                if (ps.eager) {
-                    rc = consume_staging(w, c->device, side, ps, r, moved);
-                } else {
-                    rc = transfer(c->device, side, ps.s, r, moved);
-                    if (!rc) rc = write_flag(side, ps.flag, ps.gen);
-                }
-            }
+            if (!rc) rc = transfer(c->device, side, ps.s, r, moved);
+            if (!rc) rc = write_flag(side, ps.flag, ps.gen);
             if (!rc) rc = set_device(c->device);
             if (!rc) rc = write_flag(side, done, dgen);
             if (rc) defer_error(c, rc, "deferred delivery failed: " + g_last_error);
-            cudaEventDestroy(fork);
-            cudaEventDestroy(ps.ev);
+            release_event(fork);
+            release_event(ps.ev);
             return true;
         });
         c->outstanding++;
         if (out_req) *out_req = req;
         return MPX_SUCCESS;
     }
-    if (!blocking) {
-        cudaEvent_t fork = fork0;
-        MPX_TRACE("recv r%d fork recorded", c->rank);
+    if (!blocking) {   // rendezvous, the sender's data point reached: the side stream
         if (!c->side_stream()) return cuda_fail(c->side_err, "cudaStreamCreate(side)");
-        MPX_TRACE("recv r%d side stream %p", c->rank, (void*)c->side_stream());
-        MPX_CU(cudaStreamWaitEvent(c->side_stream(), fork, 0));
-        if (mpx_tracing() && !ps.eager) note_side({c->side_stream(), fork, c->stream, ps.ev, ps.s.comm->stream, ps.flag, c->rank});
-        else cudaEventDestroy(fork);
+        MPX_CU(cudaStreamWaitEvent(c->side_stream(), fork0, 0));
+        if (mpx_tracing()) note_side({c->side_stream(), fork0, c->stream, ps.ev, ps.s.comm->stream, ps.flag, c->rank});
+        else release_event(fork0);
         st = c->side_stream();
     }
     MPX_CU(cudaStreamWaitEvent(st, ps.ev, 0));
-    MPX_TRACE("recv r%d second side on %s stream", c->rank, blocking ? "user" : "side");
+    MPX_TRACE("recv r%d second side on the %s stream", c->rank, blocking ? "user" : "side");
     if (ps.eager) {
         MPX_RC(consume_staging(w, c->device, st, ps, r, moved));
         MPX_TRACE("recv r%d consumed staging", c->rank);
@@ -980,7 +1069,7 @@ int do_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t buf_bytes, int64_
         req->needs_wait = true;
         c->outstanding++;
     }
-    if (!mpx_tracing()) cudaEventDestroy(ps.ev);
+    if (!mpx_tracing()) release_event(ps.ev);
     if (out_req) *out_req = req;
     MPX_TRACE("recv r%d issued", c->rank);
     return MPX_SUCCESS;
@@ -1076,6 +1165,29 @@ int ipc_deliver(const std::shared_ptr<Comm>& c, cudaStream_t st, const Side& r, 
 
 bool ipc_on_match(void* cookie, const IpcMsg& m) {
     auto* raw = static_cast<IpcPending*>(cookie);
+    if (!m.rndv && raw->req) {
+        // an eager message for a nonblocking receive not waited yet: it
+        // unpacks when the receiver's stream reaches the wait
+        std::unique_lock<std::mutex> rl(raw->req->mu);
+        if (!raw->req->waited) {
+            std::unique_ptr<IpcPending> p(raw);
+            const int64_t moved = std::min(m.bytes, p->r.bytes);
+            auto& q = p->req;
+            q->matched = true;
+            q->source = m.src;
+            q->tag = m.tag;
+            q->count = p->r.dt->size ? moved / p->r.dt->size : 0;
+            q->err = m.bytes > p->r.bytes ? MPX_ERR_TRUNCATE : MPX_SUCCESS;
+            auto c = p->c;
+            const Side r = p->r;
+            q->at_wait = [c, r, m](cudaStream_t ws) -> int {
+                int64_t mv = 0;
+                return ipc_deliver(c, ws, r, m, &mv);
+            };
+            release_event(p->ev);
+            return true;
+        }
+    }
     set_device(raw->c->device);
     // deliver only once the receiver's stream has reached the receive's
     // post point: a delivery waiting for it on the side stream would hold up
@@ -1094,7 +1206,7 @@ bool ipc_on_match(void* cookie, const IpcMsg& m) {
     if (!rc && !st) rc = cuda_fail(c->late_err, "cudaStreamCreate(late)");
     if (!rc) rc = ipc_deliver(c, st, p->r, m, &moved);
     if (!rc) rc = write_flag(st, p->flag, p->gen);
-    cudaEventDestroy(p->ev);
+    release_event(p->ev);
     const bool trunc = m.bytes > p->r.bytes;
     fill_status(p->req, p->r, m.src, m.tag, moved, trunc);
     if (rc) defer_error(c, rc, "multi-process delivery failed: " + g_last_error);
@@ -1180,13 +1292,32 @@ int ipc_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t count, Datatype*
     int rc = ipc->recv(c->ctx, source, tag, r.bytes, raw, &matched, &m);
     if (rc || matched) p.reset(raw);
     if (rc) {
-        cudaEventDestroy(p->ev);
+        release_event(p->ev);
         return rc;
     }
     MPX_TRACE("ipc recv r%d <- %d tag %d %s", c->rank, source, tag, matched ? "matched" : "posted");
+    if (matched && !blocking && !m.rndv) {
+        // an eager message matched at initiation: the data moves when this
+        // stream reaches wait_enqueue (waiting there for the sender's ready
+        // flag, which the wait needs anyway; the sender never waits for it)
+        release_event(p->ev);
+        const int64_t moved = std::min(m.bytes, r.bytes);
+        fill_status(req, r, m.src, m.tag, moved, m.bytes > r.bytes);
+        req->at_wait = [c, r, m](cudaStream_t ws) -> int {
+            int64_t mv = 0;
+            MPX_RC(ipc_deliver(c, ws, r, m, &mv));
+            return MPX_SUCCESS;
+        };
+        req->needs_wait = true;
+        c->outstanding++;
+        if (out_req) *out_req = req;
+        return MPX_SUCCESS;
+    }
     if (matched && !blocking && *reinterpret_cast<volatile uint32_t*>(m.ready) < m.ready_gen) {
-        // the sender's data point is not reached yet: a side-stream wait for
-        // that could hold up later deliveries, so the progress thread delivers it
+        // rendezvous whose sender has not reached its data point: a
+        // side-stream wait for that could hold up later deliveries (and the
+        // sender's completion must not hang on this rank's wait), so the
+        // progress thread delivers it once the ready flag is written
         req->flag = flag;
         req->gen = gen;
         req->needs_wait = true;
@@ -1196,15 +1327,15 @@ int ipc_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t count, Datatype*
         return MPX_SUCCESS;
     }
     if (matched) {
-        cudaEventDestroy(p->ev);
+        release_event(p->ev);
         cudaStream_t st = c->stream;
-        if (!blocking) {
+        if (!blocking) {   // rendezvous with the sender's data point reached: the side stream
             cudaEvent_t fork;
             MPX_RC(record_new_event(c->stream, &fork));
             st = c->side_stream();
             if (!st) return cuda_fail(c->side_err, "cudaStreamCreate(side)");
             MPX_CU(cudaStreamWaitEvent(st, fork, 0));
-            cudaEventDestroy(fork);
+            release_event(fork);
         }
         int64_t moved = 0;
         MPX_RC(ipc_deliver(c, st, r, m, &moved));
@@ -1276,10 +1407,18 @@ int wait_one(const std::shared_ptr<ReqState>& q) {
     if (q->waited) return MPX_SUCCESS;
     q->waited = true;
     MPX_RC(set_device(c->device));
-    if (q->needs_wait) {
+    if (q->at_wait) {
+        auto f = std::move(q->at_wait);
+        q->at_wait = nullptr;
+        int rc = f(c->stream);
+        if (rc) {
+            c->outstanding--;
+            return rc;
+        }
+    } else if (q->needs_wait) {
         if (q->done_ev) {
             MPX_CU(cudaStreamWaitEvent(c->stream, q->done_ev, 0));
-            cudaEventDestroy(q->done_ev);
+            release_event(q->done_ev);
             q->done_ev = nullptr;
         } else {
             MPX_RC(wait_flag(c->stream, q->flag, q->gen));
@@ -1669,6 +1808,19 @@ int mpx_stream_wait(void* stream) {
         nanosleep(&ts, nullptr);
         if (ns < 100000) ns *= 2;
     }
+}
+
+int mpx_stream_order(void* after, void* stream) {
+    if (after == stream) return MPX_SUCCESS;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int dev = 0;
+    MPX_CU(cudaStreamGetDevice(s, &dev));
+    MPX_RC(mpx::set_device(dev));
+    cudaEvent_t ev;
+    MPX_RC(mpx::record_new_event(reinterpret_cast<cudaStream_t>(after), &ev));
+    cudaError_t e = cudaStreamWaitEvent(s, ev, 0);
+    mpx::release_event(ev);
+    return e == cudaSuccess ? MPX_SUCCESS : mpx::cuda_fail(e, "cudaStreamWaitEvent");
 }
 
 int mpx_stream_new(int device, void** stream) {

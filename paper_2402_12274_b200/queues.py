@@ -15,7 +15,7 @@ import threading
 import torch
 
 from .errors import ArgError, MinimpiError, StateError
-from ._lib import own_stream, stream_wait
+from ._lib import check, lib, own_stream, stream_wait
 
 _QUEUES = {}
 _lock = threading.Lock()
@@ -121,9 +121,10 @@ def order_after_caller(stream):
     current stream (program order, as the reference's serial queue gives):
     the queue's stream waits on an event of the current stream when they
     differ."""
-    cur = torch.cuda.current_stream(stream.device)
-    if cur.cuda_stream != stream.cuda_stream:
-        stream.wait_stream(cur)
+    dev = stream.device.index
+    cur = torch._C._cuda_getCurrentRawStream(dev if dev is not None else torch.cuda.current_device())
+    if cur != stream.cuda_stream:
+        check(lib.mpx_stream_order(cur, stream.cuda_stream))   # one pooled event, no Python objects
 
 
 def memcpy_enqueue(queue, dst, src, nbytes):

@@ -51,18 +51,20 @@ def ring(n, nbytes, kind, iters=2, device=default_device, scale=True):
             dt, count = mp.BYTE, nbytes
         prev = (r - 1) % n
         for it in range(iters):
-            src = gen(dev, 7919 * it + r, span)
-            dst = torch.full((span,), 0x5A, dtype=torch.uint8, device=dev)
-            torch.cuda.synchronize(dev)
+            # everything on the queue's stream, no torch.cuda.synchronize(): a
+            # device-wide sync would also wait for peer ranks' streams parked
+            # on this rank's future sends (ranks sharing a GPU)
             with torch.cuda.stream(q.torch_stream):
+                src = gen(dev, 7919 * it + r, span)
+                dst = torch.full((span,), 0x5A, dtype=torch.uint8, device=dev)
                 if scale and vector:
-                    src.view(torch.float64)[: span // 8].mul_(1.0)   # dependent kernel before the send
+                    src.mul_(1)        # dependent elementwise kernel before the send (bytes: NaN-safe)
             rr = mp.irecv_enqueue(c, dst, count, dt, prev, it)
             sr = mp.isend_enqueue(c, src, count, dt, (r + 1) % n, it)
             mp.waitall_enqueue([rr, sr])
             with torch.cuda.stream(q.torch_stream):
                 if scale and vector:
-                    dst.view(torch.float64)[: span // 8].mul_(1.0)   # dependent kernel after the receive
+                    dst.mul_(1)        # dependent elementwise kernel after the receive
             mp.queue_synchronize(q)
             exp = gen(dev, 7919 * it + prev, span)
             if vector:
@@ -92,10 +94,9 @@ def allreduce(n, nbytes, kind, algo, device=default_device):
         q, s, c = stream_comm(inst)
         es = 8 if kind == "int64" else 4
         count = nbytes // es
-        x = gen(dev, 104729 * (r + 1), count, kind)
-        y = torch.empty_like(x)
-        torch.cuda.synchronize(dev)
         with torch.cuda.stream(q.torch_stream):
+            x = gen(dev, 104729 * (r + 1), count, kind)
+            y = torch.empty_like(x)
             x.mul_(1)                                   # compute before
         mp.allreduce_enqueue(c, x, y, count, mp.INT64 if kind == "int64" else mp.FLOAT32, algo=algo)
         with torch.cuda.stream(q.torch_stream):
