@@ -194,6 +194,12 @@ int mpx_comm_synchronize(mpx_comm c);
 /* explicit progress (runtime.py:141-146): reclaim staging buffers and events
  * of completed operations; never blocks.  *outstanding = live requests. */
 int mpx_comm_progress(mpx_comm c, int64_t *outstanding);
+/* give a stream from mpx_stream_new back to libmpx once its owner is done
+ * with it and it is drained (queue destroyed, communicator freed): the
+ * number of streams per device then stays that of the live owners -- more
+ * streams than CUDA_DEVICE_MAX_CONNECTIONS hardware queues let a stream
+ * parked in a wait park its queue-mates.  Unknown streams are ignored. */
+int mpx_stream_release(void *stream);
 /* order `stream` after the work already issued on `after` (same device):
  * one pooled event recorded on `after`, waited on by `stream`; no host wait */
 int mpx_stream_order(void *after, void *stream);

@@ -58,6 +58,7 @@ _SIGS = {
     "mpx_pack_multi": ([cint, pdt, p64, pvp, p64, pvp, p64, vp], cint),
     "mpx_unpack_multi": ([cint, pdt, p64, pvp, p64, pvp, p64, vp], cint),
     "mpx_stream_order": ([vp, vp], cint),
+    "mpx_stream_release": ([vp], cint),
     "mpx_world_join": ([ctypes.c_char_p, cint, cint, cint, i64, pvp], cint),
     "mpx_world_leave": ([vp, cint], cint),
     "mpx_comm_create": ([vp, cint, cint, vp, pvp], cint),
@@ -110,14 +111,22 @@ def own_stream(device):
     one of torch's pooled streams -- torch hands its 32 out round-robin, so
     two ranks can end up on the SAME stream and one rank's stream-memop wait
     then parks the other rank's flag write behind it (tools/diag_alias.py).
-    The stream lives as long as the process: the C side may still order work
-    on it after the Python owner is gone, so it is never destroyed under it."""
+    The stream is never destroyed (the C side may still order work on it
+    after the Python owner is gone); owners that end explicitly and drained
+    hand it back with release_stream, so a later owner reuses it."""
     import torch
     dev = torch.device(device)
     h = ctypes.c_void_p()
     check(lib.mpx_stream_new(dev.index if dev.index is not None else torch.cuda.current_device(),
                              ctypes.byref(h)))
     return torch.cuda.ExternalStream(h.value, device=dev)
+
+
+def release_stream(ts):
+    """Drain a stream from own_stream and give it back to libmpx's pool (the
+    owner is done with it): streams per device stay those of live owners."""
+    check(lib.mpx_stream_wait(ts.cuda_stream))
+    check(lib.mpx_stream_release(ts.cuda_stream))
 
 
 def stream_wait(ts):

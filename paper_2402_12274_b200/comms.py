@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import runtime as _rt
-from ._lib import check, lib, own_stream, stream_wait
+from ._lib import check, lib, own_stream, release_stream, stream_wait
 from .queues import order_after_caller
 from .datatypes import FLOAT32, FLOAT64, INT32, INT64, Datatype, _host_view
 from .errors import ArgError, MinimpiError, PendingError, StateError, for_status
@@ -191,6 +191,7 @@ class Communicator:
         self.freed = False
         self._device_queue = None
         self.local_stream = stream
+        self._owns_stream = stream is None
         if stream is None:
             self._stream = own_stream(instance.device)
         else:
@@ -255,6 +256,9 @@ class Communicator:
                 check(lib.mpx_comm_free(c._h))
                 c._h = None
         self.freed = True
+        if getattr(self, "_owns_stream", False):
+            self._owns_stream = False
+            release_stream(self._stream)
 
     # p2p surface (comm.py:129-155)
     def send(self, buf, count, dtype, dest, tag):

@@ -327,6 +327,10 @@ class StreamPool {
         if (cur != dev) cudaSetDevice(dev);
         cudaError_t e = cudaStreamCreateWithFlags(out, cudaStreamNonBlocking);
         if (cur != dev && cur >= 0) cudaSetDevice(cur);
+        if (e == cudaSuccess) {
+            std::lock_guard<std::mutex> g(mu_);
+            made_.insert(*out);
+        }
         return e;
     }
     // Top the device's free list up to n streams.  Called at world join:
@@ -349,6 +353,7 @@ class StreamPool {
             if (e != cudaSuccess) return e;
             std::lock_guard<std::mutex> g(mu_);
             free_[dev].push_back(s);
+            made_.insert(s);
         }
     }
     // queued work on a released stream simply runs ahead of its next owner's
@@ -356,10 +361,22 @@ class StreamPool {
         std::lock_guard<std::mutex> g(mu_);
         free_[dev].push_back(s);
     }
+    // a stream handed out by mpx_stream_new, returned by its owner once
+    // drained (queue destroyed, communicator freed); false if not ours or
+    // already free
+    bool give_back(int dev, cudaStream_t s) {
+        std::lock_guard<std::mutex> g(mu_);
+        if (!made_.count(s)) return false;
+        auto& f = free_[dev];
+        if (std::find(f.begin(), f.end(), s) != f.end()) return false;
+        f.push_back(s);
+        return true;
+    }
 
   private:
     std::mutex mu_;
     std::map<int, std::vector<cudaStream_t>> free_;
+    std::set<cudaStream_t> made_;
 };
 
 StreamPool& stream_pool() {
@@ -551,9 +568,7 @@ struct World {
 };
 
 struct Comm {
-    ~Comm() {
-        if (side) stream_pool().release(device, side);
-    }
+    ~Comm();
     World* w = nullptr;
     int rank = 0, ctx = 0, device = 0;
     cudaStream_t stream = nullptr;  // the user's stream
@@ -583,12 +598,57 @@ struct Comm {
     // 4 queues stall every time, with 8+ queues never).
     cudaError_t late_err = cudaErrorNotReady;
     cudaStream_t late_stream();
+    // Host run-ahead bound: a mark (pooled event) is recorded on the user
+    // stream every kMarkEvery enqueue calls, and a call finding more than
+    // kMaxMarks marks outstanding first polls the oldest until the GPU has
+    // passed it.  Without it a loop of thousands of enqueue calls fills the
+    // CUDA work queues; a rank thread then blocks INSIDE a CUDA call while
+    // the work its queue is parked on needs that very thread's later calls
+    // (measured: a 2000-iteration 8-byte ring of 2 in-process ranks hung in
+    // cuLaunchKernel / cuEventRecord).  Waiting for the own stream is safe
+    // for any program that is deadlock-free executed in order.
+    static constexpr int kMarkEvery = 16;
+    static constexpr size_t kMaxMarks = 4;
+    std::mutex mark_mu;
+    std::deque<cudaEvent_t> marks;
+    int since_mark = 0;
+    int throttle();
     std::mutex err_mu;
     std::deque<std::pair<int, std::string>> deferred;
     std::atomic<int64_t> outstanding{0};
     int64_t coll_seq = 0;
     int ring = -1;                  // index into every device's ring area
 };
+
+Comm::~Comm() {
+    if (side) stream_pool().release(device, side);
+    for (cudaEvent_t e : marks) release_event(e);
+}
+
+int Comm::throttle() {
+    std::unique_lock<std::mutex> g(mark_mu);
+    if (++since_mark >= kMarkEvery) {
+        since_mark = 0;
+        MPX_RC(set_device(device));
+        cudaEvent_t ev;
+        MPX_RC(record_new_event(stream, &ev));
+        marks.push_back(ev);
+    }
+    long ns = 500;
+    while (marks.size() > kMaxMarks) {
+        const cudaError_t q = cudaEventQuery(marks.front());
+        if (q == cudaErrorNotReady) {
+            struct timespec ts{0, ns};
+            nanosleep(&ts, nullptr);
+            if (ns < 50000) ns *= 2;
+            continue;
+        }
+        if (q != cudaSuccess) cudaGetLastError();
+        release_event(marks.front());
+        marks.pop_front();
+    }
+    return MPX_SUCCESS;
+}
 
 cudaStream_t Comm::late_stream() {
     cudaStream_t st = w->late_on(device);
@@ -727,18 +787,31 @@ int stage_send(const std::shared_ptr<Comm>& c, PendingSend& ps) {
 // Consume an eager staging buffer on stream `st` (device of st = `dev`):
 // unpack into the receiver, then free the staging on the world's service
 // stream of the owner's device (the sender may have freed its communicator).
+// The free never parks a stream: on the consuming stream itself when the
+// staging lives on that device, else (a peer device's pool) by the world's
+// deferral thread once the unpack has run.  (A service stream waiting for the
+// unpack would sit parked -- possibly thousands of operations ahead of the
+// GPU when the host runs ahead -- and a parked stream also parks every stream
+// that shares its hardware queue: measured as a ring deadlock.)
 int consume_staging(World* w, int dev, cudaStream_t st, const PendingSend& ps, const Side& r, int64_t moved) {
     MPX_RC(launch_move(dev, r.dt, r.count, false, ps.staging, r.buf, moved, st));
     MPX_TRACE("consume: unpack launched");
+    if (ps.s.device == dev) {
+        MPX_RC(set_device(dev));
+        MPX_CU(cudaFreeAsync(ps.staging, st));
+        return MPX_SUCCESS;
+    }
     cudaEvent_t used;
     MPX_RC(record_new_event(st, &used));
-    cudaStream_t svc = w->service(ps.s.device);
-    MPX_RC(set_device(ps.s.device));
-    MPX_CU(cudaStreamWaitEvent(svc, used, 0));
-    MPX_TRACE("consume: freeing staging");
-    MPX_CU(cudaFreeAsync(ps.staging, svc));
-    MPX_TRACE("consume: freed");
-    release_event(used);
+    const int sdev = ps.s.device;
+    void* staging = ps.staging;
+    w->defer([w, sdev, staging, used]() {
+        if (!ev_done(used)) return false;
+        set_device(sdev);
+        cudaFreeAsync(staging, w->service(sdev));
+        release_event(used);
+        return true;
+    });
     return MPX_SUCCESS;
 }
 
@@ -1691,6 +1764,7 @@ int mpx_comm_free(mpx_comm h) {
 int mpx_send_enqueue(mpx_comm h, const void* buf, int64_t bb, int64_t count, mpx_datatype dt, int dest, int tag) {
     auto c = comm_of(h);
     if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
+    MPX_RC(c->throttle());
     Datatype* d = lookup(dt);
     if (!d) return fail(MPX_ERR_ARG, "not a datatype handle");
     return do_send(c, buf, bb, count, d, dest, tag, true, nullptr);
@@ -1699,6 +1773,7 @@ int mpx_send_enqueue(mpx_comm h, const void* buf, int64_t bb, int64_t count, mpx
 int mpx_recv_enqueue(mpx_comm h, void* buf, int64_t bb, int64_t count, mpx_datatype dt, int source, int tag) {
     auto c = comm_of(h);
     if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
+    MPX_RC(c->throttle());
     Datatype* d = lookup(dt);
     if (!d) return fail(MPX_ERR_ARG, "not a datatype handle");
     return do_recv(c, buf, bb, count, d, source, tag, true, nullptr);
@@ -1708,6 +1783,7 @@ int mpx_isend_enqueue(mpx_comm h, const void* buf, int64_t bb, int64_t count, mp
                       mpx_request* out) {
     auto c = comm_of(h);
     if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
+    MPX_RC(c->throttle());
     Datatype* d = lookup(dt);
     if (!d) return fail(MPX_ERR_ARG, "not a datatype handle");
     std::shared_ptr<ReqState> q;
@@ -1720,6 +1796,7 @@ int mpx_irecv_enqueue(mpx_comm h, void* buf, int64_t bb, int64_t count, mpx_data
                       mpx_request* out) {
     auto c = comm_of(h);
     if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
+    MPX_RC(c->throttle());
     Datatype* d = lookup(dt);
     if (!d) return fail(MPX_ERR_ARG, "not a datatype handle");
     std::shared_ptr<ReqState> q;
@@ -1731,6 +1808,7 @@ int mpx_irecv_enqueue(mpx_comm h, void* buf, int64_t bb, int64_t count, mpx_data
 int mpx_wait_enqueue(mpx_request h) {
     auto q = req_of(h);
     if (!q) return fail(MPX_ERR_ARG, "wait_enqueue needs a request produced by an _enqueue operation");
+    MPX_RC(q->comm->throttle());
     return wait_one(q);
 }
 
@@ -1744,6 +1822,7 @@ int mpx_waitall_enqueue(int n, const mpx_request* hs) {
     for (auto& q : qs)
         if (q->comm->stream != qs[0]->comm->stream)
             return fail(MPX_ERR_ARG, "waitall_enqueue cannot mix device queues");
+    if (!qs.empty()) MPX_RC(qs[0]->comm->throttle());
     for (auto& q : qs) MPX_RC(wait_one(q));
     return MPX_SUCCESS;
 }
@@ -1821,6 +1900,14 @@ int mpx_stream_order(void* after, void* stream) {
     cudaError_t e = cudaStreamWaitEvent(s, ev, 0);
     mpx::release_event(ev);
     return e == cudaSuccess ? MPX_SUCCESS : mpx::cuda_fail(e, "cudaStreamWaitEvent");
+}
+
+int mpx_stream_release(void* stream) {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int dev = 0;
+    MPX_CU(cudaStreamGetDevice(s, &dev));
+    mpx::stream_pool().give_back(dev, s);
+    return MPX_SUCCESS;
 }
 
 int mpx_stream_new(int device, void** stream) {
@@ -1906,6 +1993,7 @@ int mpx_allreduce_enqueue(mpx_comm h, const void* sendbuf, void* recvbuf, int64_
     if (!es) return fail(MPX_ERR_ARG, "allreduce supports INT32, INT64, FLOAT32 and FLOAT64");
     if (count < 0) return fail(MPX_ERR_ARG, "count must be a nonnegative int");
     if (count == 0) return MPX_SUCCESS;  // comm.py:572-574
+    MPX_RC(c->throttle());
     (void)es;
     World* w = c->w;
     MPX_RC(set_device(c->device));

@@ -15,7 +15,7 @@ import threading
 import torch
 
 from .errors import ArgError, MinimpiError, StateError
-from ._lib import check, lib, own_stream, stream_wait
+from ._lib import check, lib, own_stream, release_stream, stream_wait
 
 _QUEUES = {}
 _lock = threading.Lock()
@@ -29,6 +29,7 @@ class DeviceQueue:
             device = instance.device if instance is not None else torch.device(
                 "cuda", torch.cuda.current_device())
         self.instance = instance
+        self._owned = stream is None
         self.torch_stream = stream if stream is not None else own_stream(device)
         self.device = self.torch_stream.device
         self.handle = "%016x" % self.torch_stream.cuda_stream
@@ -78,6 +79,8 @@ class DeviceQueue:
         self.destroyed = True
         with _lock:
             _QUEUES.pop(self.handle, None)
+        if self._owned:
+            release_stream(self.torch_stream)
 
     def stream_info(self):
         return {"type": "devstream", "value": self.handle}

@@ -21,7 +21,7 @@ import threading
 
 import torch
 
-from ._lib import check, lib, own_stream
+from ._lib import check, lib, own_stream, release_stream
 from .errors import ArgError, ExhaustedError, PendingError, StateError, UnsupportedError
 
 TRANSPORT_INPROC = "inproc"
@@ -182,6 +182,7 @@ def free_stream(stream):
     stream.freed = True
     if stream.kind == SERIAL_CONTEXT:
         stream.instance._pool_in_use -= 1
+        release_stream(stream.torch_stream)     # its own CUDA stream goes back to libmpx
 
 
 # -------------------------------------------------------------- instance

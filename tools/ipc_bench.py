@@ -43,6 +43,30 @@ def worker(out_dir):
                 dst = torch.zeros_like(src)
                 dt, count = mp.type_vector(nb // 32, 4, 8, mp.FLOAT64).commit(), 1
             iters = 20 if nb <= (1 << 24) else 10
+            # correctness first (untimed): distinct payloads per iteration into
+            # per-iteration receive buffers, no sync until all are posted, every
+            # message checked -- an overwritten staging slot or a misdelivered
+            # message shows up as a wrong payload
+            if nb <= (1 << 26):
+                k = 4
+                srcs = [src.clone().fill_((r * 16 + i) % 256) if kind == "u8" else
+                        src.clone().fill_(float(r * 16 + i)) for i in range(k)]
+                dsts = [torch.zeros_like(dst) for _ in range(k)]
+                reqs = []
+                for i in range(k):
+                    reqs.append(mp.irecv_enqueue(c, dsts[i], count, dt, (r - 1) % n, 100 + i))
+                    reqs.append(mp.isend_enqueue(c, srcs[i], count, dt, (r + 1) % n, 100 + i))
+                mp.waitall_enqueue(reqs)
+                mp.queue_synchronize(q)
+                p = (r - 1) % n
+                for i in range(k):
+                    if kind == "u8":
+                        good = bool((dsts[i] == (p * 16 + i) % 256).all())
+                    else:
+                        good = bool((dsts[i].view(-1, 8)[:, :4] == float(p * 16 + i)).all())
+                    assert good, ("ipc ring payload", nb, kind, i)
+                del srcs, dsts
+                mp.barrier(inst.world)
 
             def one():
                 rr = mp.irecv_enqueue(c, dst, count, dt, (r - 1) % n, 0)
