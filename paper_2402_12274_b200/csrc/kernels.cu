@@ -689,17 +689,6 @@ k_iov_chain(const Chain c, int64_t k0, int64_t n, int64_t* __restrict__ out) {
 // coalesced 16-byte stores, no tree descent.
 __global__ void __launch_bounds__(256)
 k_iov_span(const SpanPlan sp, int64_t k0, int64_t n, int64_t* __restrict__ out) {
-    // The 32 units of a warp produce one contiguous range of output pairs.
-    // Pairs go through a 64-entry shared-memory ring and leave in 32-pair
-    // (512-byte) blocks aligned to even output indices, so every 32-byte
-    // sector of the output is written whole by one store instruction --
-    // except at the two ends of the warp's range.  (Writing each unit's
-    // pairs straight from the lanes split the sectors at every unit boundary
-    // between two store instructions: the L2 then filled them from DRAM,
-    // 322 MB of reads for the 537 MB write-only cfg3 list.)
-    constexpr int kRing = 64;
-    __shared__ longlong2 ring_all[8][kRing];
-    longlong2* ring = ring_all[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     const int64_t nw = (int64_t)gridDim.x * 8;
     longlong2* o2 = reinterpret_cast<longlong2*>(out);
@@ -730,21 +719,6 @@ k_iov_span(const SpanPlan sp, int64_t k0, int64_t n, int64_t* __restrict__ out) 
             rlen = ic.y;
             if (seg0 + segs <= k0 || seg0 >= k0 + n) segs = 0;
         }
-        const unsigned live = __ballot_sync(0xffffffffu, segs > 0);
-        if (!live) continue;
-        const int64_t first_seg = __shfl_sync(0xffffffffu, seg0, __ffs(live) - 1);
-        const int64_t obase0 = max(first_seg, k0) - k0;   // first output pair of this warp
-        const int64_t oring = obase0 & ~int64_t(1);        // ring origin: even (sector-aligned)
-        int64_t flushed = oring;                           // pairs < flushed have been written
-        int64_t fill = obase0;                             // next pair to be produced
-        auto flush_full = [&]() {
-            while (fill - flushed >= 32) {
-                const int64_t oi = flushed + lane;
-                if (oi >= obase0) o2[oi] = ring[(oi - oring) & (kRing - 1)];
-                __syncwarp();
-                flushed += 32;
-            }
-        };
         const int cnt = (int)min((int64_t)32, sp.nunits - ub);
         for (int j = 0; j < cnt; ++j) {
             const int32_t sg = __shfl_sync(0xffffffffu, segs, j);
@@ -754,32 +728,18 @@ k_iov_span(const SpanPlan sp, int64_t k0, int64_t n, int64_t* __restrict__ out) 
             const int32_t bd = __shfl_sync(0xffffffffu, body, j);
             if (bd < 0) {   // a raw run: one segment of the whole run
                 const int64_t rl = __shfl_sync(0xffffffffu, rlen, j);
-                if (s0 >= k0) {
-                    if (lane == 0) ring[(s0 - k0 - oring) & (kRing - 1)] = make_longlong2(l0, rl);
-                    __syncwarp();
-                    fill = s0 - k0 + 1;
-                    flush_full();
-                }
+                if (lane == 0 && s0 >= k0) o2[s0 - k0] = make_longlong2(l0, rl);
                 continue;
             }
             const int32_t st = __shfl_sync(0xffffffffu, stride, j);
             const SpanBody* B = sp.bodies + bd;
             const int nr = __ldg(&B->nruns);
             const int q32 = 32 / nr, r32 = 32 % nr;
+            int e = lane / nr, r = lane - e * nr;
             const int64_t lo = max((int64_t)0, k0 - s0), hi = min((int64_t)sg, k0 + n - s0);
-            // element / run of the first pair this lane produces (index lo + lane)
-            int64_t i = lo + lane;
-            int e = (int)(i / nr), r = (int)(i - (int64_t)e * nr);
-            for (int64_t i0 = lo; i0 < hi; i0 += 32) {
-                if (i < hi) {
-                    const int64_t oi = s0 + i - k0;
-                    ring[(oi - oring) & (kRing - 1)] =
-                        make_longlong2(l0 + (int64_t)e * st + __ldg(&B->roff[r]), __ldg(&B->rlen[r]));
-                }
-                __syncwarp();
-                fill = s0 + min(i0 + 32, hi) - k0;
-                flush_full();
-                i += 32;
+            for (int64_t i = lane; i < hi; i += 32) {
+                if (i >= lo)
+                    o2[s0 + i - k0] = make_longlong2(l0 + (int64_t)e * st + __ldg(&B->roff[r]), __ldg(&B->rlen[r]));
                 e += q32;
                 r += r32;
                 if (r >= nr) {
@@ -788,10 +748,6 @@ k_iov_span(const SpanPlan sp, int64_t k0, int64_t n, int64_t* __restrict__ out) 
                 }
             }
         }
-        // the tail of the warp's range
-        const int64_t oi = flushed + lane;
-        if (oi >= obase0 && oi < fill) o2[oi] = ring[(oi - oring) & (kRing - 1)];
-        __syncwarp();
     }
 }
 
