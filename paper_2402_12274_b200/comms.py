@@ -64,12 +64,12 @@ class Status:
 
 
 def _check_count(count):
-    if not isinstance(count, int) or isinstance(count, bool) or count < 0:
+    if type(count) is not int and (not isinstance(count, int) or isinstance(count, bool)) or count < 0:
         raise ArgError("count must be a nonnegative int, got %r" % (count,))
 
 
 def _check_tag(tag, allow_any):
-    if not isinstance(tag, int) or isinstance(tag, bool):
+    if type(tag) is not int and (not isinstance(tag, int) or isinstance(tag, bool)):
         raise ArgError("tag must be an int, got %r" % (tag,))
     if allow_any and tag == ANY_TAG:
         return
@@ -80,7 +80,7 @@ def _check_tag(tag, allow_any):
 def _check_rank(name, value, size, allow_any=False):
     if allow_any and value == ANY:
         return
-    if not isinstance(value, int) or isinstance(value, bool) or not 0 <= value < size:
+    if type(value) is not int and (not isinstance(value, int) or isinstance(value, bool)) or not 0 <= value < size:
         raise ArgError("%s %r out of range for size-%d communicator" % (name, value, size))
 
 
@@ -89,9 +89,12 @@ def _check_dtype(dtype):
         raise ArgError("expected a Datatype, got %r" % (dtype,))
 
 
+_Tensor = torch.Tensor
+
+
 def _dev_buffer(buf):
     """Enqueue operations need device-addressable memory."""
-    if isinstance(buf, torch.Tensor) and (buf.is_cuda or buf.is_pinned()):
+    if isinstance(buf, _Tensor) and (buf.is_cuda or buf.is_pinned()):
         if not buf.is_contiguous():
             raise ArgError("buffer must be C-contiguous")
         return buf
@@ -100,7 +103,7 @@ def _dev_buffer(buf):
 
 
 def _nbytes(t):
-    return t.numel() * t.element_size()
+    return t.nbytes
 
 
 # ---------------------------------------------------------------- requests
@@ -145,7 +148,12 @@ class EnqueuedRequest(Request):
     enqueued = True
 
     def __init__(self, comm, handle, keep=()):
-        super().__init__(comm, handle, keep=keep)
+        # hot path (one per isend/irecv_enqueue): plain attribute stores
+        self.comm = comm
+        self._h = handle
+        self._finish = None
+        self._keep = keep
+        self.complete = False
         self.queue = comm._device_queue
 
     @property
@@ -353,8 +361,10 @@ def _queue_of(comm):
     q = comm._device_queue
     if q is None:
         raise ArgError("communicator is not bound to a device queue")
-    q._check_live()
-    comm._check_live()
+    if q.destroyed:
+        raise StateError("device queue already destroyed")
+    if comm.freed:
+        raise StateError("communicator already freed")
     order_after_caller(comm._stream)     # the operation follows the caller's earlier work
     return q
 

@@ -17,6 +17,7 @@ import torch
 from .errors import ArgError, MinimpiError, StateError
 from ._lib import check, lib, own_stream, release_stream, stream_wait
 
+_raw_stream = torch._C._cuda_getCurrentRawStream
 _QUEUES = {}
 _lock = threading.Lock()
 
@@ -125,9 +126,12 @@ def order_after_caller(stream):
     the queue's stream waits on an event of the current stream when they
     differ."""
     dev = stream.device.index
-    cur = torch._C._cuda_getCurrentRawStream(dev if dev is not None else torch.cuda.current_device())
-    if cur != stream.cuda_stream:
-        check(lib.mpx_stream_order(cur, stream.cuda_stream))   # one pooled event, no Python objects
+    cur = _raw_stream(dev if dev is not None else torch.cuda.current_device())
+    s = stream.cuda_stream
+    if cur != s:
+        rc = lib.mpx_stream_order(cur, s)   # one pooled event, no Python objects
+        if rc:
+            check(rc)
 
 
 def memcpy_enqueue(queue, dst, src, nbytes):
