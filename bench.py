@@ -104,6 +104,16 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
+# torchrun jobs use NCCL; MPX_BENCH_DIST_BACKEND=gloo lets the N > 1 code path
+# run with several processes on ONE GPU (NCCL refuses duplicate GPUs) -- a
+# functional check of the multi-GPU section, not a measurement
+DIST_BACKEND = os.environ.get("MPX_BENCH_DIST_BACKEND", "nccl")
+
+
+def _coll_device(device):
+    return device if DIST_BACKEND == "nccl" else "cpu"
+
+
 def max_over_ranks(value, device=None):
     """Max of a per-rank float over the job (the contract's timing rule).
     Works with NCCL (device tensor) and gloo (CPU tensor)."""
@@ -111,7 +121,7 @@ def max_over_ranks(value, device=None):
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return float(value)
-    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=_coll_device(device))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -443,7 +453,10 @@ def multi_gpu_enqueue(args, dev, world):
     import torch
     import torch.distributed as dist
     import paper_2402_12274_b200 as mp
-    inst = mp.init(transport="ipc", group="bench%s" % os.environ.get("MASTER_PORT", "0"))
+    import uuid
+    name = [uuid.uuid4().hex[:12]]
+    dist.broadcast_object_list(name, src=0)      # a job name no stale segment can carry
+    inst = mp.init(transport="ipc", group="bench-" + name[0])
     q = mp.queue_create(inst)
     info = mp.info_create()
     mp.info_set(info, "type", "devstream")
@@ -455,7 +468,7 @@ def multi_gpu_enqueue(args, dev, world):
            "nvlink_GBs_per_direction": NVLINK_GBS, "ring": [], "allreduce": []}
 
     def all_min(ok):
-        t = torch.tensor([1.0 if ok else 0.0], device=dev)
+        t = torch.tensor([1.0 if ok else 0.0], device=_coll_device(dev))
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         return bool(t.item() > 0)
 
@@ -533,8 +546,9 @@ def multi_gpu_enqueue(args, dev, world):
                 except Exception as exc:
                     out["allreduce"].append({"kind": kind, "bytes": nb, "algo": algo, "error": repr(exc)[:200]})
                     continue
-                ref = x.clone()
-                dist.all_reduce(ref)                       # torch's NCCL as the checker
+                ref = x.clone() if DIST_BACKEND == "nccl" else x.cpu()
+                dist.all_reduce(ref)                       # torch.distributed as the checker
+                ref = ref.to(dev)
                 if kind == "int64":
                     ok = bool((y == ref).all())
                 else:
@@ -561,10 +575,14 @@ def gpu_arm(args):
     import torch.distributed as dist
 
     rank, world, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())   # one GPU per rank (several only in the gloo check)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if DIST_BACKEND == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(DIST_BACKEND)
 
     import paper_2402_12274_b200 as mp
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -761,7 +779,9 @@ def gpu_arm(args):
         try:
             mg = multi_gpu_enqueue(args, dev, world)
         except Exception as exc:
-            mg = {"error": repr(exc)[:300]}
+            import traceback
+            traceback.print_exc()              # stderr, every rank
+            mg = {"error": "rank %d: %r" % (rank, exc)}
         timer.cancel()
         if line is not None:
             line["multi_gpu"] = mg

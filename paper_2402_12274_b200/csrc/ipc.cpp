@@ -184,9 +184,37 @@ int IpcWorld::join(const char* name, int size, int rank, int device, int64_t are
         pthread_mutexattr_destroy(&a);
         sh->magic.store(kMagic, std::memory_order_release);
     } else {
-        for (int t = 0; t < 120000 && sh->magic.load(std::memory_order_acquire) != kMagic; ++t) nap(1000000);
-        if (sh->magic.load() != kMagic) return fail(MPX_ERR_TRANSPORT, "job %s: segment never initialised", name);
-        if (sh->size != size) return fail(MPX_ERR_ARG, "job %s has %d ranks, not %d", name, sh->size, size);
+        // A segment left behind by a crashed job of the same name may be found
+        // before rank 0 replaces it (unlink + create): one whose size differs,
+        // that is already full, or that a failed rank marked, is stale -- drop
+        // it and open the name again.
+        for (int t = 0;; ++t) {
+            const bool ready = sh->magic.load(std::memory_order_acquire) == kMagic;
+            const bool stale = ready && (sh->size != size || sh->joined.load() >= size || sh->failed.load() > 0);
+            if (ready && !stale) break;
+            if (t >= 120000) {
+                if (stale) return fail(MPX_ERR_ARG, "job %s has %d ranks, not %d (or is a dead job's segment)", name,
+                                       sh->size, size);
+                return fail(MPX_ERR_TRANSPORT, "job %s: segment never initialised", name);
+            }
+            nap(1000000);
+            if (stale || t % 1000 == 999) {   // reopen the name: rank 0 may have replaced the segment
+                int fd = shm_open(w->name_.c_str(), O_RDWR, 0600);
+                struct stat st{};
+                if (fd >= 0 && fstat(fd, &st) == 0 && (size_t)st.st_size >= w->map_bytes_) {
+                    void* q = mmap(nullptr, w->map_bytes_, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+                    if (q != MAP_FAILED) {
+                        munmap(w->sh_, w->map_bytes_);
+                        close(w->fd_);
+                        w->fd_ = fd;
+                        w->sh_ = sh = static_cast<IpcShared*>(q);
+                        p = q;
+                        fd = -1;
+                    }
+                }
+                if (fd >= 0) close(fd);
+            }
+        }
     }
     // a rank that fails from here on tells the others, so they fail fast
     struct FailFlag {

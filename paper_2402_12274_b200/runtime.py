@@ -345,8 +345,9 @@ def init(transport=None, rank=None, ranks=None, group=None, device=None,
     if transport == TRANSPORT_IPC:
         # one process per rank: torchrun's RANK / WORLD_SIZE / LOCAL_RANK unless given
         rank = _cfg(rank, "MINIMPI_RANK", int(os.environ.get("RANK", "0")), int)
-        size = _cfg(ranks, "MINIMPI_SIZE", int(os.environ.get("WORLD_SIZE", "1")), int)
-        group = _cfg(group, "MINIMPI_GROUP", "job%s" % os.environ.get("MASTER_PORT", ""), str)
+        ranks = _cfg(ranks, "MINIMPI_SIZE", int(os.environ.get("WORLD_SIZE", "1")), int)
+        group = _cfg(group, "MINIMPI_GROUP", "job%s%s" % (os.environ.get("MASTER_PORT", ""),
+                                                         os.environ.get("TORCHELASTIC_RUN_ID", "")), str)
         if device is None and "LOCAL_RANK" in os.environ:
             device = int(os.environ["LOCAL_RANK"]) % max(1, torch.cuda.device_count())
     rank = _cfg(rank, "MINIMPI_RANK", 0, int)

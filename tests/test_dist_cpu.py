@@ -83,3 +83,28 @@ def test_reference_arm_json_contract():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_ipc_init_takes_rank_and_size_from_torchrun(monkeypatch):
+    """init(transport="ipc") under torchrun: RANK / WORLD_SIZE / LOCAL_RANK /
+    MASTER_PORT (no MINIMPI_* variables) give the rank, size, device and job
+    name (a torchrun job of 2 once came out as size 1)."""
+    import paper_2402_12274_b200 as mp
+    from paper_2402_12274_b200 import runtime
+    seen = {}
+
+    class FakeInstance:
+        def __init__(self, rank, size, group, device, eager, pool, transport, arena):
+            seen.update(rank=rank, size=size, group=group, device=device, transport=transport)
+
+    for k in ("MINIMPI_RANK", "MINIMPI_SIZE", "MINIMPI_GROUP", "MINIMPI_TRANSPORT"):
+        monkeypatch.delenv(k, raising=False)
+    monkeypatch.setenv("RANK", "1")
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    monkeypatch.setenv("LOCAL_RANK", "1")
+    monkeypatch.setenv("MASTER_PORT", "29533")
+    monkeypatch.setenv("TORCHELASTIC_RUN_ID", "none")
+    monkeypatch.setattr(runtime, "Instance", FakeInstance)
+    monkeypatch.setattr(runtime.torch.cuda, "device_count", lambda: 8)
+    mp.init(transport="ipc")
+    assert seen == {"rank": 1, "size": 2, "group": "job29533none", "device": 1, "transport": "ipc"}
