@@ -705,8 +705,8 @@ def gpu_arm(args):
     # ---- roofline of the dominant kernel ----
     pk, uk = float(np.mean(pack_ms)), float(np.mean(unpack_ms))
     launch_bytes = step_bytes() // 2          # one fused launch moves half the step
-    dom_name, dom_ms = ("unpack_multi (k_chain<false>)", uk) if uk >= pk else \
-        ("pack_multi (k_chain<true>)", pk)
+    dom_name, dom_ms = ("unpack_multi (k_chain_unpack)", uk) if uk >= pk else \
+        ("pack_multi (k_chain_pack)", pk)
     achieved = launch_bytes / (dom_ms / 1e3) / 1e9
     peak, peak_kind = load_peak()
     traffic = load_traffic()

@@ -53,7 +53,8 @@ def main():
         name = r["Kernel Name"]
         if "k_chain" not in name:
             continue
-        kind = "pack" if ("k_chain<1>" in name or "(bool)1" in name or "k_chain<true>" in name) else "unpack"
+        kind = "pack" if ("k_chain<1>" in name or "(bool)1" in name or "k_chain<true>" in name
+                          or "k_chain_pack" in name) else "unpack"
         lid = (kind, r["ID"])
         grid = r.get("Grid Size", "(0")
         launches.setdefault(lid, {"grid": int(grid.strip("()").split(",")[0] or 0)})[r["Metric Name"]] = metric(r)
