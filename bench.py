@@ -280,11 +280,71 @@ def reference_arm(args):
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    try:
+        line["python_reference"] = python_reference_sample()
+    except Exception as exc:
+        line["python_reference"] = {"error": repr(exc)[:300]}
     emit(line)
     return 0
 
 
 # ------------------------------------------------------------- extras
+
+
+def python_reference_sample(dev=None):
+    """The unmodified reference itself (minimpi, pure Python, installed into
+    baseline/_ref with pip --target) on this box's host, one core: pack and
+    unpack of BASELINE configs[0] (vector(4096,4,8) of FLOAT64, best of 3) and
+    of one cfg2 1-wide x-face (262,144 four-byte segments, once) -- the same
+    bytes as the GPU path, whose output is compared when `dev` is given.
+    Reported beside the C-port reference arm (~100x faster than this)."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "minimpi")):
+        return {"unavailable": "baseline/_ref/minimpi not installed"}
+    sys.path.insert(0, ref_dir)
+    try:
+        import minimpi as ref
+    finally:
+        sys.path.remove(ref_dir)
+    out = {"impl": "minimpi (the reference, pure Python) from baseline/_ref", "cores": 1, "cpu": cpu_model()}
+    cfg1 = ref.type_vector(4096, 4, 8, ref.FLOAT64)
+    cfg1.commit()
+    src = seeded_bytes(11, 32768 * 8)
+    best_p, best_u, packed = 1e9, 1e9, None
+    for _ in range(3):
+        t0 = time.perf_counter()
+        packed = ref.pack(cfg1, memoryview(src))
+        best_p = min(best_p, time.perf_counter() - t0)
+        back = bytearray(len(src))
+        t0 = time.perf_counter()
+        ref.unpack(cfg1, packed, back)
+        best_u = min(best_u, time.perf_counter() - t0)
+    n = len(packed)
+    out["cfg1_vector"] = {"payload_bytes": n, "pack_ms": round(best_p * 1e3, 3), "unpack_ms": round(best_u * 1e3, 3),
+                          "pack_GBs": round(2 * n / best_p / 1e9, 4), "unpack_GBs": round(2 * n / best_u / 1e9, 4)}
+    xface = ref.type_create_subarray([N3] * 3, [512, 512, 1], [1, 1, 1], ref.FLOAT32)
+    xface.commit()
+    arr = seeded_bytes(2, ARRAY_BYTES)
+    t0 = time.perf_counter()
+    xp = ref.pack(xface, memoryview(arr))
+    tp = time.perf_counter() - t0
+    dst = bytearray(ARRAY_BYTES)
+    t0 = time.perf_counter()
+    ref.unpack(xface, xp, dst)
+    tu = time.perf_counter() - t0
+    del dst
+    out["cfg2_xlo_w1"] = {"payload_bytes": len(xp), "segments": 262144, "pack_ms": round(tp * 1e3, 1),
+                          "unpack_ms": round(tu * 1e3, 1), "pack_GBs": round(2 * len(xp) / tp / 1e9, 4),
+                          "unpack_GBs": round(2 * len(xp) / tu / 1e9, 4)}
+    if dev is not None:   # the GPU path's bytes against the reference's own, same inputs
+        import torch
+        import paper_2402_12274_b200 as mp
+        g1 = mp.type_vector(4096, 4, 8, mp.FLOAT64).commit()
+        gx = mp.type_create_subarray([N3] * 3, [512, 512, 1], [1, 1, 1], mp.FLOAT32).commit()
+        a1 = mp.pack(g1, torch.from_numpy(src).to(dev)).cpu().numpy().tobytes()
+        ax = mp.pack(gx, torch.from_numpy(arr).to(dev)).cpu().numpy().tobytes()
+        out["gpu_pack_equals_reference"] = bool(a1 == bytes(packed) and ax == bytes(xp))
+    return out
 
 
 class L2Flush:
@@ -424,6 +484,10 @@ def run_extras(dev, flush, args):
                                                              group="bench-ar1")
     except Exception as exc:  # report, never fail the headline
         out["enqueue_error"] = repr(exc)
+    try:
+        out["python_reference"] = python_reference_sample(dev)
+    except Exception as exc:
+        out["python_reference"] = {"error": repr(exc)[:300]}
     try:   # multi-process world: 2 processes (one rank each) sharing this GPU via CUDA IPC
         import subprocess
         env = dict(os.environ, IPC_BENCH_LG="26,30")

@@ -339,6 +339,21 @@ class StreamPool {
     // memop wait -- measured, with native backtraces -- so streams are made
     // ahead of time, never on the data path.
     cudaError_t reserve(int dev, size_t n) {
+        {   // the first reserve of a device creates one batch covering every
+            // hardware queue but two (the legacy default stream and one spare):
+            // the driver hands queues out round-robin at stream creation, so
+            // streams created together sit on distinct queues -- a stream
+            // parked in a wait then never parks another of ours, whatever
+            // stream (re)use later brings (tools/stall_probe.py: a shared queue
+            // deadlocks the 8-ranks-per-GPU ring)
+            std::lock_guard<std::mutex> g(mu_);
+            if (!batched_.count(dev)) {
+                batched_.insert(dev);
+                const char* env = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+                const int conn = env ? std::max(1, std::min(32, std::atoi(env))) : 8;
+                n = std::max(n, (size_t)std::max(1, conn - 2));
+            }
+        }
         for (;;) {
             {
                 std::lock_guard<std::mutex> g(mu_);
@@ -377,6 +392,7 @@ class StreamPool {
     std::mutex mu_;
     std::map<int, std::vector<cudaStream_t>> free_;
     std::set<cudaStream_t> made_;
+    std::set<int> batched_;
 };
 
 StreamPool& stream_pool() {
@@ -557,11 +573,10 @@ struct World {
         auto it = svc.find(dev);
         if (it != svc.end()) return it->second;
         cudaStream_t st = nullptr;
-        int cur = -1;
-        cudaGetDevice(&cur);
-        cudaSetDevice(dev);
-        cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-        cudaSetDevice(cur);
+        if (stream_pool().acquire(dev, &st) != cudaSuccess) {
+            cudaGetLastError();
+            st = nullptr;
+        }
         svc[dev] = st;
         return st;
     }
@@ -1637,11 +1652,11 @@ int mpx_world_join(const char* group, int size, int rank, int device, int64_t ea
     }
     if (w->size != size) return fail(MPX_ERR_ARG, "world %s has %d ranks, not %d", group, w->size, size);
     if (w->joined[rank]) return fail(MPX_ERR_STATE, "rank %d already joined world %s", rank, group);
-    MPX_RC(setup_device(w, device, ndev));
     // streams for this rank's queue, world communicator and side stream (+ the
-    // device's late stream), made now (see StreamPool::reserve) -- and no
-    // more: every extra stream shares a hardware queue sooner
+    // device's late and service streams), made now (see StreamPool::reserve)
+    // -- and no more: every extra stream shares a hardware queue sooner
     MPX_CU(stream_pool().reserve(device, (size_t)std::min(64, 3 * size + 2)));
+    MPX_RC(setup_device(w, device, ndev));
     w->joined[rank] = true;
     w->devices[rank] = device;
     w->live++;
@@ -1671,8 +1686,8 @@ int mpx_ipc_world_join(const char* job, int size, int rank, int device, int64_t 
     w->devices.resize(size);
     for (int r = 0; r < size; ++r) w->devices[r] = ipc->device_of(r);
     w->next_win.assign(size, 0);
-    int rc = setup_device(w, device, ndev);
-    if (!rc && stream_pool().reserve(device, 8) != cudaSuccess) rc = fail(MPX_ERR_OTHER, "stream reserve");
+    int rc = stream_pool().reserve(device, 8) != cudaSuccess ? fail(MPX_ERR_OTHER, "stream reserve") : MPX_SUCCESS;
+    if (!rc) rc = setup_device(w, device, ndev);
     if (rc) return rc;
     w->joined[rank] = true;
     w->live = 1;
@@ -1699,6 +1714,8 @@ int mpx_world_leave(mpx_world h, int rank) {
             cudaFree(kv.second);
         }
         for (auto& kv : w->late) stream_pool().release(kv.first, kv.second);
+        for (auto& kv : w->svc)
+            if (kv.second) stream_pool().release(kv.first, kv.second);
         delete w;
         return rc;
     }
@@ -1717,6 +1734,8 @@ int mpx_world_leave(mpx_world h, int rank) {
             for (auto cm : w->nccl)
                 if (cm) g_nccl.commDestroy(cm);
         for (auto& kv : w->late) stream_pool().release(kv.first, kv.second);
+        for (auto& kv : w->svc)
+            if (kv.second) stream_pool().release(kv.first, kv.second);
         g_worlds.erase(it);
         delete w;
     }

@@ -722,15 +722,21 @@ def test_allreduce_baseline_sizes_native(nbytes, kind):
 def test_eight_ranks_on_one_gpu_vector_ring_20_runs():
     """8 in-process ranks sharing one GPU, nonblocking 64 MiB vector(N/32,4,8)
     ring with the dependent scale kernels (tools/enqueue_bench.py), 20 fresh
-    worlds in a row.  Streams per device stay below the hardware queue count
-    (one shared late stream per device, a pool reserve of 3 per rank): with
-    more streams than queues a stream parked in a wait parks its queue-mate
-    (tools/stall_probe.py: 4 ranks on 4 queues stall every run)."""
+    worlds in a row -- in a fresh process, the way a job starts: libmpx's
+    first stream batch then covers the hardware queues with distinct streams
+    (csrc/enqueue.cpp StreamPool::reserve).  With more streams than queues a
+    stream parked in a wait parks its queue-mate (tools/stall_probe.py: 4
+    ranks on 4 queues stall every run)."""
     import os
+    import subprocess
     import sys
-    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
-    import enqueue_bench as eb
-    for k in range(20):
-        res = eb.ring(8, 64 << 20, iters=5, warmup=3, kind="vector", group=unique_group("r8-%d" % k),
-                      device=lambda r: 0)
-        assert res["correct"], (k, res)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path[:0] = [%r, %r]\n"
+            "import enqueue_bench as eb\n"
+            "for k in range(20):\n"
+            "    res = eb.ring(8, 64 << 20, iters=5, warmup=3, kind='vector', group='r8-%%d' %% k,\n"
+            "                  device=lambda r: 0)\n"
+            "    assert res['correct'], (k, res)\n"
+            "print('20 ok')\n") % (root, os.path.join(root, "tools"))
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0 and "20 ok" in p.stdout, p.stdout[-2000:] + p.stderr[-3000:]
