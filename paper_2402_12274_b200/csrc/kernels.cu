@@ -102,6 +102,33 @@ __device__ __forceinline__ void store_partial16(uint8_t* p, const uint4& v, int 
     }
 }
 
+// Unpack threads ask L2 for the destination line of a row (prefetch.global.L2)
+// BEFORE loading the packed bytes: a partially written sector needs a DRAM
+// fill, and issued this way the fill overlaps the load instead of trailing
+// the store.  Measured on the bench step (A/B, round 2): fused unpack of the
+// 12 halo faces 62.3 -> 52.1 us, same DRAM bytes.  MPX_UNPACK_PREFETCH=0 turns
+// it off (experiments).
+#ifndef MPX_UNPACK_PREFETCH
+#define MPX_UNPACK_PREFETCH 1
+#endif
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+#if MPX_UNPACK_PREFETCH
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+#else
+    (void)p;
+#endif
+}
+// only the partially covered 32-byte sectors at the two ends of [d, d + len)
+// need a fill; whole-sector writes never do (a prefetch there only costs:
+// the vector(N/32,4,8) zipper, 32-byte aligned rows, slowed 0.146 -> 0.159 ms)
+__device__ __forceinline__ void prefetch_partial(const uint8_t* d, int64_t len) {
+    if (len <= 0) return;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(d), e = a + (uintptr_t)len;
+    const bool head = (a & 31) != 0, tail = (e & 31) != 0;
+    if (head) prefetch_l2(d);
+    if (tail && (!head || ((e - 1) >> 5) != (a >> 5))) prefetch_l2(d + len - 1);
+}
+
 // Warp per row, 16-byte vectors on both sides.  The packed side is 16-byte
 // aligned (L % 16 == 0); the layout side may start at any byte: aligned
 // 16-byte loads (pack) or stores (unpack) are realigned with funnel shifts
@@ -155,6 +182,8 @@ __device__ __forceinline__ void chain_rows(const ChainJob& j, int64_t warp0, int
             const int a = (int)(reinterpret_cast<uintptr_t>(drow) & 15);
             uint8_t* d16 = drow - a;
             const int64_t nout = a ? nch + 1 : nch;
+            if (a && lane == 0 && k0 == 0) prefetch_l2(d16);                       // partial first chunk
+            if (a && lane == 31 && k0 + kRowPieceChunks >= nout) prefetch_l2(d16 + 16 * nch);   // partial last
             uint4 v[kRowU];
 #pragma unroll
             for (int u = 0; u < kRowU; ++u) {
@@ -210,6 +239,7 @@ __device__ __forceinline__ void chain_elems(const ChainJob& j, int64_t t0, int64
             ok[q] = r < j.rows;
             lo[q] = ok[q] ? chain_row(c, r) : 0;
             po[q] = r * c.L;
+            if (!PACK && ok[q]) prefetch_partial(j.dst + lo[q], c.L);
         }
         for (int w = 0; w < nw; ++w) {
             T v[R];
@@ -251,6 +281,7 @@ __device__ __forceinline__ void chain_wide(const ChainJob& j, int64_t t0, int64_
             for (int m = 0; m < 4; ++m)
                 if (m < nq) d16[m] = funnel16(v[m], v[m + 1], a);
         } else {
+            prefetch_partial(j.dst + off, c.L);
             const uint4* p16 = reinterpret_cast<const uint4*>(j.src + r * c.L);
             uint8_t* d = j.dst + off;
             const int a = (int)(reinterpret_cast<uintptr_t>(d) & 15);
@@ -568,6 +599,7 @@ k_runs(const RunTable t, const uint8_t* __restrict__ src, uint8_t* __restrict__ 
         const int len = (int)(end - po);
         const uint8_t* s = src + (PACK ? so : po);
         uint8_t* d = dst + (PACK ? po : so);
+        if (!PACK) prefetch_partial(d, len);   // destination fill before the load (see prefetch_l2)
         int w = 0;
         for (; w + G <= len; w += G) *reinterpret_cast<T*>(d + w) = *reinterpret_cast<const T*>(s + w);
         for (; w < len; ++w) d[w] = s[w];   // a run cut by the limit
@@ -638,6 +670,7 @@ k_zip(const Chain cs, const Chain cd, const uint8_t* __restrict__ src, uint8_t* 
             ok[q] = p < npieces;
             so[q] = ok[q] ? chain_off(cs, p * g) : 0;
             dof[q] = ok[q] ? chain_off(cd, p * g) : 0;
+            if (ok[q]) prefetch_partial(dst + dof[q], g);
         }
         for (int w = 0; w < g; w += W) {
             T v[2];
@@ -803,6 +836,9 @@ void chain_setup(const Plan& p, bool pack, ChainJob* j) {
     j->w = (int32_t)w;
 }
 
+#ifndef MPX_ELEM_RPT
+#define MPX_ELEM_RPT 2
+#endif
 cudaError_t launch_chain_batch(ChainBatch& b, bool pack, int device, cudaStream_t stream) {
     if (b.njobs == 0) return cudaSuccess;
     (void)pack;
@@ -819,7 +855,10 @@ cudaError_t launch_chain_batch(ChainBatch& b, bool pack, int device, cudaStream_
             const int64_t items = j.rows * ((nch + kRowPieceChunks - 1) / kRowPieceChunks);
             want = (items + kChainThreads / 32 - 1) / (kChainThreads / 32);
         } else {
-            want = (j.rows + kChainThreads - 1) / kChainThreads;
+            // element-mode unpack: MPX_ELEM_RPT rows per thread (their
+            // destination lines prefetched together); 1 = a thread per row
+            const int64_t per = (!pack && j.mode == CHAIN_ELEM) ? MPX_ELEM_RPT : 1;
+            want = (j.rows + per * kChainThreads - 1) / (per * kChainThreads);
         }
         j.nblk = (int32_t)std::max<int64_t>(1, std::min<int64_t>(want, cap));
         j.gsize = 1;
