@@ -363,10 +363,17 @@ __device__ __forceinline__ void chain_body(const ChainBatch& b) {
 
 // Separate entry points so each direction gets its own register budget
 // (A/B on the bench step, round 2): pack at 6 CTAs/SM (40 registers) 33.8 ->
-// 32.0 us, while the unpack keeps 64 registers (at 6 CTAs/SM it slows from
-// 62.3 to 66.6 us).
+// 32.0 us; unpack (with the destination prefetches) at 4 CTAs/SM (64
+// registers) 52.1 -> 48.5 us -- 5 CTAs 48.2 (spills), 6 CTAs 49.4.
 __global__ void __launch_bounds__(kChainThreads, 6) k_chain_pack(const ChainBatch b) { chain_body<true>(b); }
+#ifndef MPX_UNPACK_MINB
+#define MPX_UNPACK_MINB 4
+#endif
+#if MPX_UNPACK_MINB
+__global__ void __launch_bounds__(kChainThreads, MPX_UNPACK_MINB) k_chain_unpack(const ChainBatch b) { chain_body<false>(b); }
+#else
 __global__ void __launch_bounds__(kChainThreads) k_chain_unpack(const ChainBatch b) { chain_body<false>(b); }
+#endif
 
 // ---------------------------------------------------------------- generic
 constexpr int kGenWarps = 8;
@@ -857,7 +864,8 @@ cudaError_t launch_chain_batch(ChainBatch& b, bool pack, int device, cudaStream_
         } else {
             // element-mode unpack: MPX_ELEM_RPT rows per thread (their
             // destination lines prefetched together); 1 = a thread per row
-            const int64_t per = (!pack && j.mode == CHAIN_ELEM) ? MPX_ELEM_RPT : 1;
+            const int64_t per = (!pack && j.mode == CHAIN_ELEM &&
+                                 j.rows >= (int64_t)kChainThreads * sm_count(device) * 4) ? MPX_ELEM_RPT : 1;
             want = (j.rows + per * kChainThreads - 1) / (per * kChainThreads);
         }
         j.nblk = (int32_t)std::max<int64_t>(1, std::min<int64_t>(want, cap));

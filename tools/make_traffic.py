@@ -58,9 +58,11 @@ def main():
         lid = (kind, r["ID"])
         grid = r.get("Grid Size", "(0")
         launches.setdefault(lid, {"grid": int(grid.strip("()").split(",")[0] or 0)})[r["Metric Name"]] = metric(r)
-    # the fused 12-face launches of the timed step: the largest grid
-    big = max(m["grid"] for m in launches.values())
-    launches = {k: m for k, m in launches.items() if m["grid"] == big}
+    # the fused 12-face launches of the timed step: the largest grid of each direction
+    big = {}
+    for (kind, _), m in launches.items():
+        big[kind] = max(big.get(kind, 0), m["grid"])
+    launches = {k: m for k, m in launches.items() if m["grid"] == big[k[0]]}
     kernels = {}
     for (kind, _), m in launches.items():
         m = dict(m)
