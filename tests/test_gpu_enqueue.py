@@ -375,7 +375,7 @@ def _ring(n, nbytes, dtype_kind, blocking=False, eager_limit=None):
             assert torch.equal(got, exp)
 
 
-@pytest.mark.parametrize("n", [2, 3])
+@pytest.mark.parametrize("n", [2, 3, 8])
 @pytest.mark.parametrize("nbytes", [8, 1 << 16, 1 << 20])
 @pytest.mark.parametrize("kind", ["u8", "vector"])
 def test_ring_nonblocking(n, nbytes, kind):
@@ -530,7 +530,7 @@ def test_zipper_chain_to_chain_matches_copy_between(st, rt, elem):
 # ------------------------------------------------------------- allreduce
 
 
-@pytest.mark.parametrize("n", [1, 2, 4])
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
 @pytest.mark.parametrize("kind", ["int64", "float64", "float32"])
 def test_allreduce_enqueue_native_matches_rank_ordered_oracle(n, kind):
     count = 100_003
