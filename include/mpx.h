@@ -29,6 +29,7 @@ extern "C" {
 #define MPX_ERR_EXHAUSTED    6   /* ExhaustedError  "ERR_EXHAUSTED"   */
 #define MPX_ERR_TRANSPORT    7   /* TransportError  "ERR_TRANSPORT"   */
 #define MPX_ERR_OTHER        8   /* MinimpiError    "ERR_OTHER" (CUDA failures) */
+#define MPX_WOULD_BLOCK      9   /* not an error: see mpx_comm_set_host_wait */
 
 /* builtin datatypes (datatype.py:410-422; INT8 is new) */
 #define MPX_BYTE     0
@@ -200,6 +201,13 @@ int mpx_comm_progress(mpx_comm c, int64_t *outstanding);
  * streams than CUDA_DEVICE_MAX_CONNECTIONS hardware queues let a stream
  * parked in a wait park its queue-mates.  Unknown streams are ignored. */
 int mpx_stream_release(void *stream);
+/* Host run-ahead bound: every communicator keeps its host thread at most
+ * ~64 enqueue calls ahead of its stream, waiting (polling) when further.
+ * mpx_comm_set_host_wait(c, 0): such a call instead returns MPX_WOULD_BLOCK
+ * before it has any effect; the caller then runs mpx_comm_throttle_wait(c)
+ * (with its own locks released, e.g. Python's GIL) and repeats the call. */
+int mpx_comm_set_host_wait(mpx_comm c, int may_wait);
+int mpx_comm_throttle_wait(mpx_comm c);
 /* order `stream` after the work already issued on `after` (same device):
  * one pooled event recorded on `after`, waited on by `stream`; no host wait */
 int mpx_stream_order(void *after, void *stream);

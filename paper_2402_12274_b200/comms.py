@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import runtime as _rt
-from ._lib import check, lib, own_stream, release_stream, stream_wait
+from ._lib import GIL_FASTPATH, WOULD_BLOCK, check, fast, lib, own_stream, release_stream, stream_wait
 from .queues import order_after_caller
 from .datatypes import FLOAT32, FLOAT64, INT32, INT64, Datatype, _host_view
 from .errors import ArgError, MinimpiError, PendingError, StateError, for_status
@@ -104,6 +104,29 @@ def _dev_buffer(buf):
 
 def _nbytes(t):
     return t.nbytes
+
+
+def _call_blocking(comm, name, *args):
+    """A call that may wait on the host (collectives: peers, NCCL set-up):
+    always with the GIL released."""
+    f = getattr(lib, name)
+    rc = f(*args)
+    while rc == WOULD_BLOCK:
+        check(lib.mpx_comm_throttle_wait(comm._h))
+        rc = f(*args)
+    return check(rc)
+
+
+def _call(comm, name, *args):
+    """One enqueue call on `comm`; when its host thread is too far ahead of
+    the stream the call returns MPX_WOULD_BLOCK untouched: wait with the GIL
+    released, then repeat it."""
+    f = getattr(getattr(comm, "_lib", lib), name)
+    rc = f(*args)
+    while rc == WOULD_BLOCK:
+        check(lib.mpx_comm_throttle_wait(comm._h))
+        rc = f(*args)
+    return check(rc)
 
 
 # ---------------------------------------------------------------- requests
@@ -208,6 +231,12 @@ class Communicator:
         check(lib.mpx_comm_create(instance._world, rank, context_id, self._stream.cuda_stream,
                                   ctypes.byref(h)))
         self._h = h.value
+        # in-process ranks share one GIL: short enqueue calls keep it held
+        # (_lib.fast) and a throttled call hands back MPX_WOULD_BLOCK instead
+        # of waiting inside (see _call)
+        self._lib = fast if (GIL_FASTPATH and instance.transport == _rt.TRANSPORT_INPROC) else lib
+        if self._lib is fast:
+            check(lib.mpx_comm_set_host_wait(self._h, 0))
         self._live = []           # requests / buffers kept alive until completion
         self._coll = None
 
@@ -377,7 +406,7 @@ def send_enqueue(comm, buf, count, dtype, dest, tag):
     _check_tag(tag, allow_any=False)
     _check_rank("dest", dest, comm.size)
     b = _dev_buffer(buf)
-    check(lib.mpx_send_enqueue(comm._h, b.data_ptr(), _nbytes(b), count, dtype._h, dest, tag))
+    _call(comm, "mpx_send_enqueue", comm._h, b.data_ptr(), _nbytes(b), count, dtype._h, dest, tag)
     comm._live.append(b)
 
 
@@ -390,7 +419,7 @@ def recv_enqueue(comm, buf, count, dtype, source=ANY_SOURCE, tag=ANY_TAG):
     _check_tag(tag, allow_any=True)
     _check_rank("source", source, comm.size, allow_any=True)
     b = _dev_buffer(buf)
-    check(lib.mpx_recv_enqueue(comm._h, b.data_ptr(), _nbytes(b), count, dtype._h, source, tag))
+    _call(comm, "mpx_recv_enqueue", comm._h, b.data_ptr(), _nbytes(b), count, dtype._h, source, tag)
     comm._live.append(b)
 
 
@@ -403,8 +432,8 @@ def isend_enqueue(comm, buf, count, dtype, dest, tag):
     _check_rank("dest", dest, comm.size)
     b = _dev_buffer(buf)
     h = ctypes.c_void_p()
-    check(lib.mpx_isend_enqueue(comm._h, b.data_ptr(), _nbytes(b), count, dtype._h, dest, tag,
-                                ctypes.byref(h)))
+    _call(comm, "mpx_isend_enqueue", comm._h, b.data_ptr(), _nbytes(b), count, dtype._h, dest, tag,
+          ctypes.byref(h))
     r = EnqueuedRequest(comm, h.value, keep=(b,))
     comm._live.append(r)
     return r
@@ -419,8 +448,8 @@ def irecv_enqueue(comm, buf, count, dtype, source=ANY_SOURCE, tag=ANY_TAG):
     _check_rank("source", source, comm.size, allow_any=True)
     b = _dev_buffer(buf)
     h = ctypes.c_void_p()
-    check(lib.mpx_irecv_enqueue(comm._h, b.data_ptr(), _nbytes(b), count, dtype._h, source, tag,
-                                ctypes.byref(h)))
+    _call(comm, "mpx_irecv_enqueue", comm._h, b.data_ptr(), _nbytes(b), count, dtype._h, source, tag,
+          ctypes.byref(h))
     r = EnqueuedRequest(comm, h.value, keep=(b,))
     comm._live.append(r)
     return r
@@ -430,7 +459,7 @@ def wait_enqueue(request):
     """Put the completion wait on the request's own queue (offload.py:241-248)."""
     if not isinstance(request, EnqueuedRequest):
         raise ArgError("wait_enqueue needs a request produced by an _enqueue operation")
-    check(lib.mpx_wait_enqueue(request._h))
+    _call(request.comm, "mpx_wait_enqueue", request._h)
 
 
 def waitall_enqueue(requests):
@@ -446,7 +475,7 @@ def waitall_enqueue(requests):
         if r.queue is not q:
             raise ArgError("waitall_enqueue cannot mix device queues")
     hs = (ctypes.c_void_p * len(requests))(*[r._h for r in requests])
-    check(lib.mpx_waitall_enqueue(len(requests), hs))
+    _call(requests[0].comm, "mpx_waitall_enqueue", len(requests), hs)
 
 
 # ------------------------------------------------------ host p2p surface
@@ -481,9 +510,9 @@ def _host_isend(comm, buf, count, dtype, dest, tag):
     b, _ = _host_buffer(buf, comm.instance.device, writable=False)
     order_after_caller(comm._stream)      # the upload above ran on the caller's stream
     h = ctypes.c_void_p()
-    check(lib.mpx_isend_enqueue(comm._h, b.data_ptr(), _nbytes(b), count, dtype._h, dest, tag,
-                                ctypes.byref(h)))
-    check(lib.mpx_wait_enqueue(h.value))
+    _call(comm, "mpx_isend_enqueue", comm._h, b.data_ptr(), _nbytes(b), count, dtype._h, dest, tag,
+          ctypes.byref(h))
+    _call(comm, "mpx_wait_enqueue", h.value)
     r = Request(comm, h.value, keep=(b,))
     comm._live.append(r)
     return r
@@ -498,9 +527,9 @@ def _host_irecv(comm, buf, count, dtype, source, tag):
     b, finish = _host_buffer(buf, comm.instance.device, writable=True)
     order_after_caller(comm._stream)
     h = ctypes.c_void_p()
-    check(lib.mpx_irecv_enqueue(comm._h, b.data_ptr(), _nbytes(b), count, dtype._h, source, tag,
-                                ctypes.byref(h)))
-    check(lib.mpx_wait_enqueue(h.value))
+    _call(comm, "mpx_irecv_enqueue", comm._h, b.data_ptr(), _nbytes(b), count, dtype._h, source, tag,
+          ctypes.byref(h))
+    _call(comm, "mpx_wait_enqueue", h.value)
     r = Request(comm, h.value, finish=finish, keep=(b,))
     comm._live.append(r)
     return r
@@ -611,8 +640,8 @@ def allreduce_enqueue(comm, sendbuf, recvbuf, count, dtype, op=SUM, algo=None):
     need = count * dtype.size_bytes
     if _nbytes(s) < need or _nbytes(r) < need:
         raise ArgError("allreduce buffers hold %d/%d bytes, need %d" % (_nbytes(s), _nbytes(r), need))
-    check(lib.mpx_allreduce_enqueue(comm._h, s.data_ptr(), r.data_ptr(), count, code, 0,
-                                    _ALGOS.get(algo, 0)))
+    _call_blocking(comm, "mpx_allreduce_enqueue", comm._h, s.data_ptr(), r.data_ptr(), count, code, 0,
+                   _ALGOS.get(algo, 0))
     comm._live.extend((s, r))
 
 
@@ -630,8 +659,8 @@ def allreduce(comm, sendbuf, recvbuf, count, dtype, op=SUM, algo=None):
         raise ArgError("allreduce buffers hold %d/%d bytes, need %d" % (_nbytes(s), _nbytes(r), need))
     c = comm if comm._device_queue is None else comm
     order_after_caller(comm._stream)      # the uploads above ran on the caller's stream
-    check(lib.mpx_allreduce_enqueue(c._h, s.data_ptr(), r.data_ptr(), count, code, 0,
-                                    _ALGOS.get(algo, 0)))
+    _call_blocking(c, "mpx_allreduce_enqueue", c._h, s.data_ptr(), r.data_ptr(), count, code, 0,
+                   _ALGOS.get(algo, 0))
     stream_wait(comm._stream)
     if finish is not None:
         finish()

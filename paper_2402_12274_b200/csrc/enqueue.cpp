@@ -627,7 +627,13 @@ struct Comm {
     std::mutex mark_mu;
     std::deque<cudaEvent_t> marks;
     int since_mark = 0;
+    // false (mpx_comm_set_host_wait): throttle returns MPX_WOULD_BLOCK instead
+    // of waiting, before the call has any effect -- a binding that holds a
+    // language lock across its calls (Python's GIL, ctypes.PyDLL) waits with
+    // the lock released (mpx_comm_throttle_wait) and repeats the call
+    std::atomic<bool> host_may_wait{true};
     int throttle();
+    int throttle_wait();
     std::mutex err_mu;
     std::deque<std::pair<int, std::string>> deferred;
     std::atomic<int64_t> outstanding{0};
@@ -653,9 +659,30 @@ int Comm::throttle() {
     while (marks.size() > kMaxMarks) {
         const cudaError_t q = cudaEventQuery(marks.front());
         if (q == cudaErrorNotReady) {
+            if (!host_may_wait.load(std::memory_order_relaxed)) return MPX_WOULD_BLOCK;
             struct timespec ts{0, ns};
             nanosleep(&ts, nullptr);
             if (ns < 50000) ns *= 2;
+            continue;
+        }
+        if (q != cudaSuccess) cudaGetLastError();
+        release_event(marks.front());
+        marks.pop_front();
+    }
+    return MPX_SUCCESS;
+}
+
+int Comm::throttle_wait() {
+    std::unique_lock<std::mutex> g(mark_mu);
+    long ns = 500;
+    while (marks.size() > kMaxMarks) {
+        const cudaError_t q = cudaEventQuery(marks.front());
+        if (q == cudaErrorNotReady) {
+            g.unlock();
+            struct timespec ts{0, ns};
+            nanosleep(&ts, nullptr);
+            if (ns < 50000) ns *= 2;
+            g.lock();
             continue;
         }
         if (q != cudaSuccess) cudaGetLastError();
@@ -1876,6 +1903,19 @@ int mpx_comm_synchronize(mpx_comm h) {
         return fail(e.first, "%s", e.second.c_str());
     }
     return MPX_SUCCESS;
+}
+
+int mpx_comm_set_host_wait(mpx_comm h, int may_wait) {
+    auto c = comm_of(h);
+    if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
+    c->host_may_wait.store(may_wait != 0);
+    return MPX_SUCCESS;
+}
+
+int mpx_comm_throttle_wait(mpx_comm h) {
+    auto c = comm_of(h);
+    if (!c) return fail(MPX_ERR_STATE, "communicator already freed");
+    return c->throttle_wait();
 }
 
 int mpx_comm_progress(mpx_comm h, int64_t* outstanding) {
