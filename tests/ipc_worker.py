@@ -17,6 +17,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import oracle  # noqa: E402
+from specbuild import build_product  # noqa: E402
 import paper_2402_12274_b200 as mp  # noqa: E402
 
 
@@ -238,6 +239,42 @@ def posted_first_then_matched(inst, q, c):
     mp.barrier(inst.world)
 
 
+def rendezvous_layouts(inst, q, c):
+    """Rendezvous (above the eager limit) with sender layouts the receiver must
+    rebuild from their 64-byte description: a replicated vector (count > 1),
+    a 3-level subarray face and an hvector of contiguous blocks, each received
+    into a different layout; every byte checked against the oracle's
+    copy_between (datatype.py:760-797)."""
+    r, n, dev = inst.rank, inst.size, inst.device
+    cases = [
+        (("vector", 1024, 4, 8, ("basic", 8)), 8, ("contiguous", 32768, ("basic", 8)), 1),
+        (("subarray", [40, 60, 70], [30, 50, 16], [5, 4, 3], ("basic", 4)), 1,
+         ("vector", 12000, 2, 3, ("basic", 4)), 1),
+        (("hvector", 300, 1, 1000, ("contiguous", 64, ("basic", 4))), 1, ("contiguous", 300 * 256, ("basic", 1)), 1),
+    ]
+    for k, (sspec, scount, rspec, rcount) in enumerate(cases):
+        st, rt = oracle.OracleType(sspec), oracle.OracleType(rspec)
+        sdt = build_product(sspec, mp)
+        rdt = build_product(rspec, mp)
+        sspan = st.max_end + (scount - 1) * st.extent_bytes if scount > 1 else st.max_end
+        src_h = data(3000 + 10 * k + r, sspan)
+        src = torch.from_numpy(src_h).to(dev)
+        rspan = rt.max_end
+        dst = torch.full((rspan,), 0x5A, dtype=torch.uint8, device=dev)
+        torch.cuda.synchronize(dev)
+        rr = mp.irecv_enqueue(c, dst, rcount, rdt, (r - 1) % n, 200 + k)
+        sr = mp.isend_enqueue(c, src, scount, sdt, (r + 1) % n, 200 + k)
+        mp.waitall_enqueue([rr, sr])
+        mp.queue_synchronize(q)
+        prev = data(3000 + 10 * k + (r - 1) % n, sspan)
+        exp = np.full(rspan, 0x5A, np.uint8)
+        moved = oracle.copy_between(st, scount, prev, rt, rcount, exp)
+        assert moved == st.size_bytes * scount, (k, moved)
+        assert np.array_equal(dst.cpu().numpy(), exp), ("rendezvous layout", k)
+        assert rr.status.count == rcount, rr.status
+    mp.barrier(inst.world)
+
+
 def arena_wrap(inst, q, c, iters=40):
     """Staged (eager-path) messages wrapping the staging arena several times
     without any host synchronisation: a non-chain layout (irregular indexed
@@ -372,6 +409,7 @@ def main():
     if inst.size >= 2:
         any_source_and_truncation(inst, q, c)
     arena_wrap(inst, q, c)
+    rendezvous_layouts(inst, q, c)
     t0 = time.perf_counter()
     for _ in range(20):                       # arena reuse: many messages through the ring
         ring(inst, q, c, 4 << 20, False, "recv")
