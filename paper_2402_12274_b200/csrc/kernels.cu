@@ -266,8 +266,14 @@ template <bool PACK>
 __device__ __forceinline__ void chain_wide(const ChainJob& j, int64_t t0, int64_t nthr) {
     const Chain& c = j.c;
     const int nq = (int)(c.L >> 4);
+    int64_t next_off = t0 < j.rows ? chain_row(c, t0) : 0;
+    if (!PACK && t0 < j.rows) prefetch_partial(j.dst + next_off, c.L);
     for (int64_t r = t0; r < j.rows; r += nthr) {
-        const int64_t off = chain_row(c, r);
+        const int64_t off = next_off;
+        if (r + nthr < j.rows) {   // the row this thread takes next: its fill starts now
+            next_off = chain_row(c, r + nthr);
+            if (!PACK) prefetch_partial(j.dst + next_off, c.L);
+        }
         if (PACK) {
             const uint8_t* s = j.src + off;
             const int a = (int)(reinterpret_cast<uintptr_t>(s) & 15);
@@ -281,7 +287,6 @@ __device__ __forceinline__ void chain_wide(const ChainJob& j, int64_t t0, int64_
             for (int m = 0; m < 4; ++m)
                 if (m < nq) d16[m] = funnel16(v[m], v[m + 1], a);
         } else {
-            prefetch_partial(j.dst + off, c.L);
             const uint4* p16 = reinterpret_cast<const uint4*>(j.src + r * c.L);
             uint8_t* d = j.dst + off;
             const int a = (int)(reinterpret_cast<uintptr_t>(d) & 15);
@@ -846,6 +851,10 @@ void chain_setup(const Plan& p, bool pack, ChainJob* j) {
 #ifndef MPX_ELEM_RPT
 #define MPX_ELEM_RPT 2
 #endif
+#ifndef MPX_WIDE_RPT
+#define MPX_WIDE_RPT 2
+#endif
+
 cudaError_t launch_chain_batch(ChainBatch& b, bool pack, int device, cudaStream_t stream) {
     if (b.njobs == 0) return cudaSuccess;
     (void)pack;
@@ -864,8 +873,12 @@ cudaError_t launch_chain_batch(ChainBatch& b, bool pack, int device, cudaStream_
         } else {
             // element-mode unpack: MPX_ELEM_RPT rows per thread (their
             // destination lines prefetched together); 1 = a thread per row
-            const int64_t per = (!pack && j.mode == CHAIN_ELEM &&
-                                 j.rows >= (int64_t)kChainThreads * sm_count(device) * 4) ? MPX_ELEM_RPT : 1;
+            const bool big = j.rows >= (int64_t)kChainThreads * sm_count(device) * 4;
+            // unpack of large faces: 2 rows per thread, the next row's
+            // destination prefetched while the current one is stored (wide
+            // mode 48.3 -> 44.6 us on the bench step); pack keeps a thread per
+            // row (2 per thread measured 32.1 -> 35.6 us)
+            const int64_t per = (!pack && big) ? (j.mode == CHAIN_ELEM ? MPX_ELEM_RPT : MPX_WIDE_RPT) : 1;
             want = (j.rows + per * kChainThreads - 1) / (per * kChainThreads);
         }
         j.nblk = (int32_t)std::max<int64_t>(1, std::min<int64_t>(want, cap));
