@@ -275,6 +275,32 @@ def rendezvous_layouts(inst, q, c):
     mp.barrier(inst.world)
 
 
+def rendezvous_truncation_and_empty(inst, q, c):
+    """A 1 MiB rendezvous message into a 512 KiB receive: the prefix lands,
+    the receive reports ERR_TRUNCATE, the send completes (the receiver still
+    writes the done flag); then a zero-byte message (count 0) both ways."""
+    r, n, dev = inst.rank, inst.size, inst.device
+    nb = 1 << 20
+    src_h = data(4000 + r, nb)
+    src = torch.from_numpy(src_h).to(dev)
+    dst = torch.full((nb // 2,), 0x5A, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize(dev)
+    rr = mp.irecv_enqueue(c, dst, nb // 2, mp.BYTE, (r - 1) % n, 300)
+    sr = mp.isend_enqueue(c, src, nb, mp.BYTE, (r + 1) % n, 300)
+    mp.waitall_enqueue([rr, sr])
+    mp.queue_synchronize(q)
+    prev = data(4000 + (r - 1) % n, nb)
+    assert rr.status.error == "ERR_TRUNCATE", rr.status
+    assert np.array_equal(dst.cpu().numpy(), prev[: nb // 2])
+    empty = torch.zeros(1, dtype=torch.uint8, device=dev)
+    rr = mp.irecv_enqueue(c, empty, 0, mp.BYTE, (r - 1) % n, 301)
+    sr = mp.isend_enqueue(c, empty, 0, mp.BYTE, (r + 1) % n, 301)
+    mp.waitall_enqueue([rr, sr])
+    mp.queue_synchronize(q)
+    assert rr.status.count == 0 and rr.status.error is None and rr.status.source == (r - 1) % n, rr.status
+    mp.barrier(inst.world)
+
+
 def arena_wrap(inst, q, c, iters=40):
     """Staged (eager-path) messages wrapping the staging arena several times
     without any host synchronisation: a non-chain layout (irregular indexed
@@ -410,6 +436,7 @@ def main():
         any_source_and_truncation(inst, q, c)
     arena_wrap(inst, q, c)
     rendezvous_layouts(inst, q, c)
+    rendezvous_truncation_and_empty(inst, q, c)
     t0 = time.perf_counter()
     for _ in range(20):                       # arena reuse: many messages through the ring
         ring(inst, q, c, 4 << 20, False, "recv")
