@@ -813,6 +813,8 @@ def gpu_arm(args):
                                                           / peak, 4)) if floor else None,
             "e2e": {"value": round(job_value(step_bytes(), world, e2e_ms), 3), "unit": "GB/s",
                     "ms_per_step": round(e2e_ms, 3),
+                    "bound": "PCIe: the step's 56.6 MB H2D + 56.6 MB D2H take ~%.0f %% of it; the kernels %.0f %%"
+                             % (100.0 * (e2e_ms - ms_per_step) / e2e_ms, 100.0 * ms_per_step / e2e_ms),
                     "mode": "halo step: array resident in HBM; received packed faces H2D "
                             "(overlapped with the fused pack) and packed faces D2H (overlapped "
                             "with the fused unpack), pinned host buffers",

@@ -514,11 +514,13 @@ struct World {
     std::vector<std::function<bool()>> deferred_ops;
     std::thread defer_thread;
     bool defer_stop = false;
+    std::condition_variable defer_cv;
     void defer(std::function<bool()> op) {
         MPX_TRACE("delivery deferred");
         std::lock_guard<std::mutex> g(defer_mu);
         deferred_ops.push_back(std::move(op));
         if (!defer_thread.joinable()) defer_thread = std::thread([this] { defer_loop(); });
+        defer_cv.notify_one();   // an idle thread sleeps on the cv: no wake-up latency
     }
     void defer_loop() {
         prctl(PR_SET_TIMERSLACK, 1UL, 0, 0, 0);   // short naps really are short (default slack: 50 us)
@@ -526,7 +528,9 @@ struct World {
         long idle = 0;
         for (;;) {
             {
-                std::lock_guard<std::mutex> g(defer_mu);
+                std::unique_lock<std::mutex> g(defer_mu);
+                if (mine.empty())   // nothing pending: sleep until a delivery is deferred
+                    defer_cv.wait(g, [&] { return defer_stop || !deferred_ops.empty(); });
                 if (defer_stop && deferred_ops.empty() && mine.empty()) return;
                 for (auto& f : deferred_ops) mine.push_back(std::move(f));
                 deferred_ops.clear();
@@ -542,7 +546,8 @@ struct World {
                 }
             }
             if (did) idle = 0;
-            struct timespec ts{0, (mine.empty() && ++idle > 100) ? 20000L : 3000L};
+            if (mine.empty()) continue;
+            struct timespec ts{0, ++idle > 1000 ? 20000L : 2000L};   // inputs pending on the GPU: poll
             nanosleep(&ts, nullptr);
         }
     }
@@ -551,6 +556,7 @@ struct World {
             std::lock_guard<std::mutex> g(defer_mu);
             defer_stop = true;
         }
+        defer_cv.notify_one();
         if (defer_thread.joinable()) defer_thread.join();
     }
     std::mutex late_mu;
