@@ -291,6 +291,91 @@ def reference_arm(args):
 # ------------------------------------------------------------- extras
 
 
+def _python_reference_enqueue(ref):
+    """The reference's own enqueue ring and allreduce: 2
+    in-process ranks on threads (its tests/_twin.py pattern), a DeviceQueue
+    (executor thread) per rank; isend/irecv_enqueue + waitall_enqueue of 64 KiB
+    of bytes around the ring (its blocking form deadlocks above the eager
+    limit), and the host allreduce of 1 MiB of INT64 and FLOAT64 (its only
+    types).  Wall time per iteration, max over ranks."""
+    import itertools
+    res = {}
+    n = 2
+    tag = itertools.count()
+
+    def host(body):
+        group = "benchref-%d" % next(tag)
+        outs, errs = [None] * n, []
+
+        def runner(r):
+            inst = None
+            try:
+                inst = ref.init(transport="inproc", rank=r, ranks=n, group=group)
+                outs[r] = body(inst)
+            except BaseException as exc:  # noqa: B902
+                errs.append(exc)
+            finally:
+                if inst is not None and not inst.finalized:
+                    try:
+                        inst.finalize()
+                    except Exception:
+                        pass
+        th = [threading.Thread(target=runner, args=(r,), daemon=True) for r in range(n)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(120)
+        if errs:
+            raise errs[0]
+        return outs
+
+    nb, iters = 64 << 10, 20
+
+    def ring(inst):
+        q = ref.queue_create(inst)
+        info = ref.info_create()
+        ref.info_set(info, "type", "devstream")
+        ref.info_set_hex(info, "value", bytes.fromhex(q.handle))
+        c = ref.stream_comm_create(inst.world, inst.stream_create(info))
+        r = inst.rank
+        src, dst = bytearray([r]) * nb, bytearray(nb)
+
+        def one():
+            rr = ref.irecv_enqueue(c, dst, nb, ref.BYTE, (r - 1) % n, 0)
+            sr = ref.isend_enqueue(c, src, nb, ref.BYTE, (r + 1) % n, 0)
+            ref.waitall_enqueue([rr, sr])
+        one()
+        ref.queue_synchronize(q)
+        t0 = time.perf_counter()
+        for _ in range(iters):
+            one()
+        ref.queue_synchronize(q)
+        dt = (time.perf_counter() - t0) / iters
+        ok = dst == bytearray([(r - 1) % n]) * nb
+        ref.queue_destroy(q)
+        return dt, ok
+
+    rs = host(ring)
+    dt = max(x[0] for x in rs)
+    res["ring_2ranks_64KiB"] = {"ms_per_iter": round(dt * 1e3, 3), "GBps_per_rank": round(nb / dt / 1e9, 4),
+                                "correct": all(x[1] for x in rs)}
+    count = (1 << 20) // 8
+    for kind, dtype in (("int64", ref.INT64), ("float64", ref.FLOAT64)):
+        def ar(inst):
+            import array
+            fmt = "q" if kind == "int64" else "d"
+            s_ = array.array(fmt, [inst.rank + 1] * count)
+            r_ = array.array(fmt, [0] * count)
+            t0 = time.perf_counter()
+            ref.allreduce(inst.world, s_, r_, count, dtype)
+            return time.perf_counter() - t0, r_[0] == 3
+        rs = host(ar)
+        dt = max(x[0] for x in rs)
+        res["allreduce_2ranks_1MiB_" + kind] = {"ms": round(dt * 1e3, 2), "algbw_GBps": round((1 << 20) / dt / 1e9, 5),
+                                                "correct": all(x[1] for x in rs)}
+    return res
+
+
 def python_reference_sample(dev=None):
     """The unmodified reference itself (minimpi, pure Python, installed into
     baseline/_ref with pip --target) on this box's host, one core: pack and
@@ -336,6 +421,7 @@ def python_reference_sample(dev=None):
     out["cfg2_xlo_w1"] = {"payload_bytes": len(xp), "segments": 262144, "pack_ms": round(tp * 1e3, 1),
                           "unpack_ms": round(tu * 1e3, 1), "pack_GBs": round(2 * len(xp) / tp / 1e9, 4),
                           "unpack_GBs": round(2 * len(xp) / tu / 1e9, 4)}
+    out.update(_python_reference_enqueue(ref))
     if dev is not None:   # the GPU path's bytes against the reference's own, same inputs
         import torch
         import paper_2402_12274_b200 as mp
