@@ -61,6 +61,43 @@ namespace mpx {
 
 namespace {
 
+// MPX_PROF=1 (diagnosis): host time spent in selected CUDA calls of the
+// enqueue path, per category, printed at exit
+struct ProfCat {
+    std::atomic<int64_t> ns{0}, n{0};
+};
+enum { P_ORDER, P_RECORD, P_MALLOC, P_FREE, P_LAUNCH, P_WAITEV, P_MEMOP, P_QUERY, P_NCAT };
+ProfCat g_prof[P_NCAT];
+const char* const g_prof_name[P_NCAT] = {"stream_order", "event_record", "malloc_async", "free_async",
+                                         "launch_move", "stream_wait_event", "memop", "event_query"};
+inline bool profiling() {
+    static const bool on = std::getenv("MPX_PROF") != nullptr;
+    return on;
+}
+struct ProfScope {
+    int cat;
+    struct timespec t0;
+    explicit ProfScope(int c) : cat(c) {
+        if (profiling()) clock_gettime(CLOCK_MONOTONIC, &t0);
+    }
+    ~ProfScope() {
+        if (!profiling()) return;
+        struct timespec t1;
+        clock_gettime(CLOCK_MONOTONIC, &t1);
+        g_prof[cat].ns += (t1.tv_sec - t0.tv_sec) * 1000000000LL + (t1.tv_nsec - t0.tv_nsec);
+        g_prof[cat].n += 1;
+    }
+};
+struct ProfReport {
+    ~ProfReport() {
+        if (!profiling()) return;
+        for (int i = 0; i < P_NCAT; ++i)
+            if (g_prof[i].n.load())
+                std::fprintf(stderr, "[mpx prof] %-18s %9lld calls %8.2f us/call\n", g_prof_name[i],
+                             (long long)g_prof[i].n.load(), g_prof[i].ns.load() / 1e3 / (double)g_prof[i].n.load());
+    }
+} g_prof_report;
+
 // ------------------------------------------------------------------ flags
 // Completion flags live in pinned, mapped host memory (device address = host
 // address under UVA).  Slot values only grow, so a waiter on (slot, gen) with
@@ -182,6 +219,7 @@ int write_ptr(cudaStream_t s, const void* const* addr, const void* value) {
 }
 
 int write_flag(cudaStream_t s, uint32_t* addr, uint32_t gen) {
+    ProfScope ps(P_MEMOP);
     if (!memops().write) return fail(MPX_ERR_UNSUPPORTED, "cuStreamWriteValue32 unavailable");
     MPX_TRACE("write stream %p flag %p = %u", (void*)s, (void*)addr, gen);
     CUresult r = memops().write(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), gen,
@@ -234,6 +272,7 @@ cudaMemPool_t staging_pool(int dev) {
 int staging_alloc(int dev, size_t bytes, cudaStream_t st, void** out) {
     cudaMemPool_t pool = staging_pool(dev);
     if (!pool) return fail(MPX_ERR_OTHER, "cannot create the staging memory pool on device %d", dev);
+    ProfScope ps(P_MALLOC);
     MPX_CU(cudaMallocFromPoolAsync(out, bytes ? bytes : 1, pool, st));
     return MPX_SUCCESS;
 }
@@ -289,6 +328,7 @@ EventPool& event_pool() {
 void release_event(cudaEvent_t ev) { event_pool().put(ev); }
 
 int record_new_event(cudaStream_t s, cudaEvent_t* ev) {
+    ProfScope ps(P_RECORD);
     MPX_CU(event_pool().get(ev));
     MPX_CU(cudaEventRecord(*ev, s));
     return MPX_SUCCESS;
@@ -296,6 +336,7 @@ int record_new_event(cudaStream_t s, cudaEvent_t* ev) {
 
 // has the stream position recorded in `e` been reached (and passed)?
 bool ev_done(cudaEvent_t e) {
+    ProfScope ps(P_QUERY);
     const cudaError_t q = cudaEventQuery(e);
     if (q != cudaSuccess) cudaGetLastError();
     return q != cudaErrorNotReady;
@@ -828,6 +869,7 @@ int stage_send(const std::shared_ptr<Comm>& c, PendingSend& ps) {
     MPX_RC(set_device(c->device));
     MPX_RC(staging_alloc(c->device, (size_t)ps.s.bytes, c->stream, &ps.staging));
     MPX_TRACE("staged %lld B", (long long)ps.s.bytes);
+    ProfScope pl(P_LAUNCH);
     MPX_RC(launch_move(c->device, ps.s.dt, ps.s.count, true, ps.s.buf, ps.staging, ps.s.bytes, c->stream));
     return MPX_SUCCESS;
 }
@@ -842,10 +884,14 @@ int stage_send(const std::shared_ptr<Comm>& c, PendingSend& ps) {
 // GPU when the host runs ahead -- and a parked stream also parks every stream
 // that shares its hardware queue: measured as a ring deadlock.)
 int consume_staging(World* w, int dev, cudaStream_t st, const PendingSend& ps, const Side& r, int64_t moved) {
-    MPX_RC(launch_move(dev, r.dt, r.count, false, ps.staging, r.buf, moved, st));
+    {
+        ProfScope pl(P_LAUNCH);
+        MPX_RC(launch_move(dev, r.dt, r.count, false, ps.staging, r.buf, moved, st));
+    }
     MPX_TRACE("consume: unpack launched");
     if (ps.s.device == dev) {
         MPX_RC(set_device(dev));
+        ProfScope pf(P_FREE);
         MPX_CU(cudaFreeAsync(ps.staging, st));
         return MPX_SUCCESS;
     }
@@ -953,7 +999,10 @@ int do_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t buf_bytes, 
                 cudaEvent_t post = pr.ev;
                 pr.req->at_wait = [wd, ps, rr, moved, post](cudaStream_t ws) -> int {
                     MPX_RC(set_device(rr.device));
-                    MPX_CU(cudaStreamWaitEvent(ws, ps.ev, 0));
+                    {
+                        ProfScope pw(P_WAITEV);
+                        MPX_CU(cudaStreamWaitEvent(ws, ps.ev, 0));
+                    }
                     MPX_RC(consume_staging(wd, rr.device, ws, ps, rr, moved));
                     MPX_RC(set_device(rr.device));
                     release_event(ps.ev);
@@ -1956,6 +2005,7 @@ int mpx_stream_wait(void* stream) {
 
 int mpx_stream_order(void* after, void* stream) {
     if (after == stream) return MPX_SUCCESS;
+    mpx::ProfScope ps(mpx::P_ORDER);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     int dev = 0;
     MPX_CU(cudaStreamGetDevice(s, &dev));

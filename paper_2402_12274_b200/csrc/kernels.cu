@@ -326,6 +326,9 @@ __device__ __forceinline__ void chain_wide(const ChainJob& j, int64_t t0, int64_
 }
 
 template <bool PACK>
+__device__ __forceinline__ void chain_job_body(const ChainJob& j, int64_t blk);
+
+template <bool PACK>
 __device__ __forceinline__ void chain_body(const ChainBatch& b) {
     // jobs with equal block counts are interleaved block by block, so e.g. the
     // lo and hi x-faces touch the same DRAM pages at the same time
@@ -343,8 +346,11 @@ __device__ __forceinline__ void chain_body(const ChainBatch& b) {
             break;
         }
     }
-    const ChainJob& j = b.job[ji];
-    const int64_t blk = blk32;
+    chain_job_body<PACK>(b.job[ji], blk32);
+}
+
+template <bool PACK>
+__device__ __forceinline__ void chain_job_body(const ChainJob& j, int64_t blk) {
     if (j.mode == CHAIN_ROW) {
         chain_rows<PACK>(j, blk * (kChainThreads / 32) + (threadIdx.x >> 5),
                          (int64_t)j.nblk * (kChainThreads / 32));
@@ -371,13 +377,22 @@ __device__ __forceinline__ void chain_body(const ChainBatch& b) {
 // 32.0 us; unpack (with the destination prefetches) at 4 CTAs/SM (64
 // registers) 52.1 -> 48.5 us -- 5 CTAs 48.2 (spills), 6 CTAs 49.4.
 __global__ void __launch_bounds__(kChainThreads, 6) k_chain_pack(const ChainBatch b) { chain_body<true>(b); }
+// one layout: the job by value (~250 B of parameters instead of the batch's
+// ~4 KB: MPX_PROF measured 4.3-4.9 us of host time per single-layout launch)
+__global__ void __launch_bounds__(kChainThreads, 6) k_chain1_pack(const ChainJob j) {
+    chain_job_body<true>(j, blockIdx.x);
+}
 #ifndef MPX_UNPACK_MINB
 #define MPX_UNPACK_MINB 4
 #endif
 #if MPX_UNPACK_MINB
 __global__ void __launch_bounds__(kChainThreads, MPX_UNPACK_MINB) k_chain_unpack(const ChainBatch b) { chain_body<false>(b); }
+__global__ void __launch_bounds__(kChainThreads, MPX_UNPACK_MINB) k_chain1_unpack(const ChainJob j) {
+    chain_job_body<false>(j, blockIdx.x);
+}
 #else
 __global__ void __launch_bounds__(kChainThreads) k_chain_unpack(const ChainBatch b) { chain_body<false>(b); }
+__global__ void __launch_bounds__(kChainThreads) k_chain1_unpack(const ChainJob j) { chain_job_body<false>(j, blockIdx.x); }
 #endif
 
 // ---------------------------------------------------------------- generic
@@ -905,8 +920,14 @@ cudaError_t launch_chain_batch(ChainBatch& b, bool pack, int device, cudaStream_
         }
         total += (int64_t)j.nblk * g;
     }
-    if (pack) k_chain_pack<<<(unsigned)total, kChainThreads, 0, stream>>>(b);
-    else k_chain_unpack<<<(unsigned)total, kChainThreads, 0, stream>>>(b);
+    if (b.njobs == 1) {   // blocks map 1:1 onto the job (blk0 = 0, one-job group)
+        if (pack) k_chain1_pack<<<(unsigned)total, kChainThreads, 0, stream>>>(b.job[0]);
+        else k_chain1_unpack<<<(unsigned)total, kChainThreads, 0, stream>>>(b.job[0]);
+    } else if (pack) {
+        k_chain_pack<<<(unsigned)total, kChainThreads, 0, stream>>>(b);
+    } else {
+        k_chain_unpack<<<(unsigned)total, kChainThreads, 0, stream>>>(b);
+    }
     return cudaGetLastError();
 }
 
@@ -936,6 +957,8 @@ cudaError_t preload_pack_kernels() {
     cudaError_t e = cudaSuccess, r;
     if ((r = cudaFuncGetAttributes(&a, k_chain_pack)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_chain_unpack)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_chain1_pack)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_chain1_unpack)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_generic<true>)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_generic<false>)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_ordered_unpack)) != cudaSuccess) e = r;
