@@ -301,6 +301,50 @@ def rendezvous_truncation_and_empty(inst, q, c):
     mp.barrier(inst.world)
 
 
+def stress(inst, q, c, seed=11):
+    """tests/test_gpu_enqueue_stress.py's random nonblocking schedules across
+    processes: eager (arena) and rendezvous (pull) messages, exact source and
+    ANY_SOURCE, random posting order per rank, typed and byte sends."""
+    import random
+    from test_gpu_enqueue_stress import payload, schedule
+    r, n, dev = inst.rank, inst.size, inst.device
+    rng = random.Random(seed * 7919 + r)
+    vec = {}
+    for msgs in schedule(seed, n, phases=4, per_pair=2):
+        ops = [("send", m) for m in msgs if m[0] == r] + [("recv", m) for m in msgs if m[1] == r]
+        rng.shuffle(ops)
+        reqs, checks, keep = [], [], []
+        for kind, (s_, d_, tag, nb, typed, anys) in ops:
+            if kind == "send":
+                data_ = payload(dev, s_, tag, nb)
+                if typed:
+                    if nb not in vec:
+                        vec[nb] = mp.type_vector(nb // 32, 4, 8, mp.FLOAT64).commit()
+                    buf = torch.zeros(2 * nb, dtype=torch.uint8, device=dev)
+                    buf.view(-1, 64)[:, :32] = data_.view(-1, 32)
+                    reqs.append(mp.isend_enqueue(c, buf, 1, vec[nb], d_, 1000 + tag))
+                else:
+                    buf = data_ if nb else torch.zeros(1, dtype=torch.uint8, device=dev)
+                    reqs.append(mp.isend_enqueue(c, buf, nb, mp.BYTE, d_, 1000 + tag))
+                keep.append(buf)
+            else:
+                dst = torch.full((max(nb, 1),), 0x5A, dtype=torch.uint8, device=dev)
+                rq = mp.irecv_enqueue(c, dst, nb, mp.BYTE, mp.ANY_SOURCE if anys else s_, 1000 + tag)
+                reqs.append(rq)
+                checks.append((rq, dst, s_, tag, nb))
+        mp.waitall_enqueue(reqs)
+        mp.queue_synchronize(q)
+        for rq, dst, s_, tag, nb in checks:
+            st = rq.status
+            assert st.source == s_ and st.tag == 1000 + tag and st.count == nb and st.error is None, (s_, tag, st)
+            if nb:
+                assert torch.equal(dst[:nb], payload(dev, s_, tag, nb)), ("stress", s_, tag, nb)
+        del keep
+        mp.barrier(inst.world)
+    for t in vec.values():
+        mp.type_free(t)
+
+
 def arena_wrap(inst, q, c, iters=40):
     """Staged (eager-path) messages wrapping the staging arena several times
     without any host synchronisation: a non-chain layout (irregular indexed
@@ -437,6 +481,7 @@ def main():
     arena_wrap(inst, q, c)
     rendezvous_layouts(inst, q, c)
     rendezvous_truncation_and_empty(inst, q, c)
+    stress(inst, q, c)
     t0 = time.perf_counter()
     for _ in range(20):                       # arena reuse: many messages through the ring
         ring(inst, q, c, 4 << 20, False, "recv")
