@@ -648,6 +648,10 @@ def multi_gpu_enqueue(args, dev, world):
             dst = torch.zeros_like(src)
             dt, count = (mp.type_vector(nb // 32, 4, 8, mp.FLOAT64).commit(), 1) if vec else (mp.BYTE, nb)
             f64 = span // 8
+            # the scale kernels run on the queue's stream: order it after the
+            # buffers' initialisation on the current stream (the enqueue calls
+            # order themselves, a kernel launched under torch.cuda.stream does not)
+            q.torch_stream.wait_stream(torch.cuda.current_stream(dev))
 
             def one():
                 if scale:

@@ -77,6 +77,11 @@ def ring(n=2, nbytes=64 << 20, iters=20, warmup=3, group="bench-ring", kind="u8"
             dst = torch.zeros_like(src)
             count, dt = 1, mp.type_vector(nbytes // 32, 4, 8, mp.FLOAT64).commit()
 
+        # the scale kernels run on the queue's stream: order it after the
+        # buffers' initialisation on the current stream (a device-wide sync
+        # would also wait for peer ranks' parked streams)
+        q.torch_stream.wait_stream(torch.cuda.current_stream(inst.device))
+
         def one():
             if kind != "u8" and scale:
                 with torch.cuda.stream(q.torch_stream):
