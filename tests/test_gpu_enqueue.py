@@ -740,3 +740,51 @@ def test_eight_ranks_on_one_gpu_vector_ring_20_runs():
             "print('20 ok')\n") % (root, os.path.join(root, "tools"))
     p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
     assert p.returncode == 0 and "20 ok" in p.stdout, p.stdout[-2000:] + p.stderr[-3000:]
+
+
+def test_throttled_enqueue_releases_the_gil():
+    """Host run-ahead bound: with the queue's stream held up by a long kernel,
+    a loop of eager self-sends soon finds 4 marks outstanding; the call then
+    returns MPX_WOULD_BLOCK untouched and the binding waits in
+    mpx_comm_throttle_wait WITH THE GIL RELEASED (the enqueue calls themselves
+    keep it, ctypes.PyDLL) -- another Python thread keeps running meanwhile,
+    and every message still arrives."""
+    import threading
+    inst = mp.init(group=unique_group("gil"), device=0)
+    try:
+        q = mp.queue_create(inst)
+        c, s = device_comm(inst, q)
+        ticks = [0]
+        stop = threading.Event()
+
+        def ticker():
+            while not stop.is_set():
+                ticks[0] += 1
+                time.sleep(0)
+
+        t = threading.Thread(target=ticker, daemon=True)
+        t.start()
+        n = 160
+        src = torch.arange(n, dtype=torch.int64, device=inst.device).to(torch.uint8)
+        dst = torch.zeros(n, dtype=torch.uint8, device=inst.device)
+        with torch.cuda.stream(q.torch_stream):
+            torch.cuda._sleep(200_000_000)          # ~0.1 s: the stream cannot pass the first mark
+        before = ticks[0]
+        t0 = time.perf_counter()
+        for i in range(n):
+            rr = mp.irecv_enqueue(c, dst[i:i + 1], 1, mp.BYTE, 0, i)
+            sr = mp.isend_enqueue(c, src[i:i + 1], 1, mp.BYTE, 0, i)
+            mp.waitall_enqueue([rr, sr])
+        waited = time.perf_counter() - t0
+        during = ticks[0] - before
+        mp.queue_synchronize(q)
+        stop.set()
+        t.join(5)
+        assert torch.equal(dst, src)
+        assert waited > 0.02, waited                 # the loop really was throttled
+        assert during > 100, during                  # ... and the other thread ran meanwhile
+        mp.comm_free(c)
+        mp.free_stream(s)
+        mp.queue_destroy(q)
+    finally:
+        inst.finalize()
