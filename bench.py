@@ -150,9 +150,9 @@ def load_traffic():
 
 
 class ClockSampler:
-    """SM clock + throttle reasons sampled through NVML every ~0.5 ms while
-    the timed region runs (nvidia-smi's 100 ms period is longer than the
-    whole region)."""
+    """SM clock + throttle reasons sampled through NVML (every ~0.2 ms plus
+    the NVML call time) from the warm-up through the timed region
+    (nvidia-smi's 100 ms period is longer than the whole region)."""
 
     REASONS = (("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20),
                ("hw_thermal_slowdown", 0x40), ("hw_power_brake", 0x80),
@@ -182,7 +182,7 @@ class ClockSampler:
                     self.reasons |= pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
                 except Exception:
                     pass
-                time.sleep(0.0005)
+                time.sleep(0.0002)
 
         self.thread = threading.Thread(target=run, daemon=True)
         self.thread.start()
@@ -763,6 +763,10 @@ def gpu_arm(args):
     step()
     torch.cuda.synchronize()
 
+    # clocks are sampled from the warm-up through the end of the timed steps
+    # (same load; the timed region alone is ~10 ms, a few NVML samples)
+    sampler = ClockSampler(local)
+    sampler.start()
     for _ in range(args.warmup):
         flush()
         step()
@@ -770,11 +774,9 @@ def gpu_arm(args):
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    sampler = ClockSampler(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler.start()
     for i in range(args.steps):
         flush()                           # L2 flush, outside the timed events
         torch.cuda._sleep(int(os.environ.get("MPX_BENCH_SLEEP", "400000")))  # ~0.2 ms: the host enqueues the whole step before event a runs
