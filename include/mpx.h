@@ -232,6 +232,15 @@ int mpx_ipc_world_join(const char *job, int size, int rank, int device, int64_t 
                        int64_t arena_bytes, mpx_world *out);
 /* host barrier over the processes of a multi-process world */
 int mpx_world_barrier(mpx_world w);
+/* Matching mode of an in-process world (csrc/dmatch.hpp), set
+ * by every rank right after mpx_world_join, before any point-to-point call:
+ * 0 = on the host when an operation is enqueued (default), 1 = on the GPU
+ * when each rank's stream reaches the operation (posted / unexpected queues
+ * in the receiver's device memory, every message buffered).  The ranks must
+ * agree (MPX_ERR_ARG otherwise); multi-process worlds: host only
+ * (MPX_ERR_UNSUPPORTED).  Replaces the matching of transport.py:191-201,
+ * 399-428 (executor-thread order, offload.py:87-102). */
+int mpx_world_set_matching(mpx_world w, int device_side);
 /* a non-blocking stream on `device` for the caller alone, owned by the
  * process (never destroyed by the library); taken from the streams libmpx
  * creates ahead of time at world join (creating a stream while another

@@ -80,6 +80,7 @@ _SIGS = {
     "mpx_stream_new": ([cint, pvp], cint),
     "mpx_ipc_world_join": ([ctypes.c_char_p, cint, cint, cint, i64, i64, pvp], cint),
     "mpx_world_barrier": ([vp], cint),
+    "mpx_world_set_matching": ([vp, cint], cint),
     "mpx_stream_wait": ([vp], cint),
     "mpx_debug_flags": ([], cint),
     "mpx_nccl_load": ([ctypes.c_char_p], cint),

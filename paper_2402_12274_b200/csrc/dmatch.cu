@@ -1,0 +1,342 @@
+// dmatch.cu -- device-resident matching kernels (see dmatch.hpp).
+//
+// Matching rules: transport.py:191-201 (a receive pattern matches a message
+// when the contexts are equal and source / tag are equal or ANY_*), the
+// earliest candidate wins (posting order for receives, arrival order for
+// messages: transport.py:399-428, :509-516).  Box entries are read with
+// volatile (L1-bypassing) loads: a box is written by kernels of several
+// ranks, possibly on peer GPUs over NVLink, and published under its lock
+// with system-scope fences.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+
+#include "dmatch.hpp"
+#include "kernels.hpp"
+#include "mpx.h"
+
+namespace mpx {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr unsigned long long kNone = ~0ull;
+constexpr uint64_t kGiveUpNs = 20ull * 1000000000ull;   // a full queue for 20 s: report and drop
+
+__device__ __forceinline__ uint64_t now_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ void lock(DmBox* b) {
+    while (atomicCAS_system(&b->lock, 0, 1) != 0) __nanosleep(64);
+    __threadfence_system();
+}
+
+__device__ __forceinline__ void unlock(DmBox* b) {
+    __threadfence_system();
+    atomicExch_system(&b->lock, 0);
+}
+
+__device__ __forceinline__ bool pat_match(int psrc, int ptag, int pctx, int src, int tag, int ctx) {
+    return pctx == ctx && (psrc == MPX_ANY_SOURCE || psrc == src) && (ptag == MPX_ANY_TAG || ptag == tag);
+}
+
+// block-wide: the key (seq << 12 | index) of the earliest live entry accepted
+// by `ok`, or kNone
+template <typename F>
+__device__ __forceinline__ unsigned long long earliest(int hw, F ok, unsigned long long* sh) {
+    if (threadIdx.x == 0) *sh = kNone;
+    __syncthreads();
+    unsigned long long mine = kNone;
+    for (int i = threadIdx.x; i < hw; i += blockDim.x) {
+        const unsigned long long k = ok(i);
+        mine = k < mine ? k : mine;
+    }
+    if (mine != kNone) atomicMin(sh, mine);
+    __syncthreads();
+    const unsigned long long r = *sh;
+    __syncthreads();
+    return r;
+}
+
+// block-wide: the lowest free index below min(hw + 1, kDmSlots), or -1
+template <typename F>
+__device__ __forceinline__ int first_free(int hw, F is_free, int* sh) {
+    if (threadIdx.x == 0) *sh = INT_MAX;
+    __syncthreads();
+    const int lim = hw + 1 < kDmSlots ? hw + 1 : kDmSlots;
+    for (int i = threadIdx.x; i < lim; i += blockDim.x)
+        if (is_free(i)) {
+            atomicMin(sh, i);
+            break;
+        }
+    __syncthreads();
+    const int r = *sh;
+    __syncthreads();
+    return r == INT_MAX ? -1 : r;
+}
+
+__device__ __forceinline__ void publish(DmResult* res, int src, int tag, int64_t bytes, const uint8_t* data,
+                                        uint32_t* consumed, uint32_t cgen) {
+    volatile DmResult* r = res;
+    r->src = src;
+    r->tag = tag;
+    r->bytes = bytes;
+    r->data = data;
+    r->consumed = consumed;
+    r->cgen = cgen;
+    __threadfence_system();
+    r->ready = 1;
+}
+
+struct SendArgs {
+    DmBox* box;
+    int32_t src, tag, ctx;
+    uint32_t cgen;
+    const uint8_t* data;
+    int64_t bytes;
+    uint32_t* consumed;
+};
+
+// a message arrives at the receiving rank's box
+__global__ void __launch_bounds__(kThreads) k_dm_send(const SendArgs a) {
+    __shared__ unsigned long long best;
+    __shared__ int slot;
+    DmBox* b = a.box;
+    volatile DmBox* vb = b;
+    const uint64_t t0 = now_ns();
+    for (;;) {
+        if (threadIdx.x == 0) lock(b);
+        __syncthreads();
+        const int hw = vb->hw_recv;
+        const unsigned long long k = earliest(hw, [&](int i) -> unsigned long long {
+            volatile const DmRecv& r = vb->recv[i];
+            if (r.state != 1 || !pat_match(r.src, r.tag, r.ctx, a.src, a.tag, a.ctx)) return kNone;
+            return ((unsigned long long)r.seq << 12) | (unsigned)i;
+        }, &best);
+        bool done = true;
+        if (k != kNone) {   // the earliest posted receive takes it
+            if (threadIdx.x == 0) {
+                const int i = (int)(k & 0xFFF);
+                publish(&b->result[vb->recv[i].result], a.src, a.tag, a.bytes, a.data, a.consumed, a.cgen);
+                vb->recv[i].state = 0;
+                int h = hw;
+                while (h > 0 && vb->recv[h - 1].state == 0) --h;
+                vb->hw_recv = h;
+            }
+        } else {            // unexpected: queue it
+            const int hm = vb->hw_msg;
+            const int f = first_free(hm, [&](int i) { return vb->msg[i].state == 0; }, &slot);
+            if (threadIdx.x == 0) {
+                if (f >= 0) {
+                    volatile DmMsg& m = vb->msg[f];
+                    m.src = a.src;
+                    m.tag = a.tag;
+                    m.ctx = a.ctx;
+                    m.seq = vb->next_seq;
+                    vb->next_seq = vb->next_seq + 1;
+                    m.data = a.data;
+                    m.bytes = a.bytes;
+                    m.consumed = a.consumed;
+                    m.cgen = a.cgen;
+                    __threadfence_system();
+                    m.state = 1;
+                    if (f + 1 > hm) vb->hw_msg = f + 1;
+                } else if (now_ns() - t0 < kGiveUpNs) {
+                    done = false;   // full: let receivers drain it, retry
+                } else {
+                    vb->err = MPX_ERR_EXHAUSTED;
+                }
+            }
+        }
+        if (threadIdx.x == 0) {
+            unlock(b);
+            slot = done ? 1 : 0;
+        }
+        __syncthreads();
+        if (slot) return;
+        __nanosleep(1000);
+    }
+}
+
+struct PostArgs {
+    DmBox* box;
+    int32_t src, tag, ctx;   // patterns
+    int32_t result;
+};
+
+// a receive is posted at its stream position
+__global__ void __launch_bounds__(kThreads) k_dm_post(const PostArgs a) {
+    __shared__ unsigned long long best;
+    __shared__ int slot;
+    DmBox* b = a.box;
+    volatile DmBox* vb = b;
+    const uint64_t t0 = now_ns();
+    for (;;) {
+        if (threadIdx.x == 0) {
+            lock(b);
+            volatile DmResult* r = &b->result[a.result];
+            r->ready = 0;
+            r->ndone = 0;
+        }
+        __syncthreads();
+        const int hm = vb->hw_msg;
+        const unsigned long long k = earliest(hm, [&](int i) -> unsigned long long {
+            volatile const DmMsg& m = vb->msg[i];
+            if (m.state != 1 || !pat_match(a.src, a.tag, a.ctx, m.src, m.tag, m.ctx)) return kNone;
+            return ((unsigned long long)m.seq << 12) | (unsigned)i;
+        }, &best);
+        bool done = true;
+        if (k != kNone) {   // the earliest unexpected message
+            if (threadIdx.x == 0) {
+                const int i = (int)(k & 0xFFF);
+                volatile DmMsg& m = vb->msg[i];
+                publish(&b->result[a.result], m.src, m.tag, m.bytes, m.data, m.consumed, m.cgen);
+                m.state = 0;
+                int h = hm;
+                while (h > 0 && vb->msg[h - 1].state == 0) --h;
+                vb->hw_msg = h;
+            }
+        } else {
+            const int hr = vb->hw_recv;
+            const int f = first_free(hr, [&](int i) { return vb->recv[i].state == 0; }, &slot);
+            if (threadIdx.x == 0) {
+                if (f >= 0) {
+                    volatile DmRecv& r = vb->recv[f];
+                    r.src = a.src;
+                    r.tag = a.tag;
+                    r.ctx = a.ctx;
+                    r.result = a.result;
+                    r.seq = vb->next_seq;
+                    vb->next_seq = vb->next_seq + 1;
+                    __threadfence_system();
+                    r.state = 1;
+                    if (f + 1 > hr) vb->hw_recv = f + 1;
+                } else if (now_ns() - t0 < kGiveUpNs) {
+                    done = false;
+                } else {
+                    vb->err = MPX_ERR_EXHAUSTED;
+                }
+            }
+        }
+        if (threadIdx.x == 0) {
+            unlock(b);
+            slot = done ? 1 : 0;
+        }
+        __syncthreads();
+        if (slot) return;
+        __nanosleep(1000);
+    }
+}
+
+// wait for a receive's match (one thread spins; the GPU stays free for the
+// senders' kernels) and record its status
+__global__ void __launch_bounds__(32) k_dm_wait(DmBox* b, int res, DmStatus* st, int64_t cap) {
+    if (threadIdx.x) return;
+    volatile DmResult* r = &b->result[res];
+    volatile DmBox* vb = b;
+    unsigned ns = 32;
+    while (r->ready == 0) {
+        if (vb->err) {
+            volatile DmStatus* s = st;
+            s->err = vb->err;
+            s->src = -1;
+            s->tag = -1;
+            s->bytes = 0;
+            return;
+        }
+        __nanosleep(ns);
+        ns = ns < 1024 ? 2 * ns : ns;
+    }
+    __threadfence_system();
+    volatile DmStatus* s = st;
+    s->src = r->src;
+    s->tag = r->tag;
+    s->bytes = r->bytes;
+    s->err = r->bytes > cap ? MPX_ERR_TRUNCATE : MPX_SUCCESS;
+}
+
+// copy the part of the message that fits; the last CTA releases the bounce
+// buffer and completes the status
+__global__ void __launch_bounds__(kThreads) k_dm_copy(DmBox* b, int res, uint8_t* __restrict__ dst, int64_t cap,
+                                                      DmStatus* st) {
+    volatile DmResult* r = &b->result[res];
+    const bool ok = r->ready != 0;
+    const uint8_t* src = ok ? (const uint8_t*)r->data : nullptr;
+    const int64_t n = ok ? (r->bytes < cap ? r->bytes : cap) : 0;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    if (n > 0) {
+        const uintptr_t mis = (reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst));
+        int64_t head = 0;
+        if ((mis & 15) == 0) {
+            const int64_t nv = n >> 4;
+            const uint4* s4 = reinterpret_cast<const uint4*>(src);
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+            for (int64_t i = tid; i < nv; i += nth) d4[i] = s4[i];
+            head = nv << 4;
+        } else if ((mis & 3) == 0) {
+            const int64_t nv = n >> 2;
+            const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
+            uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
+            for (int64_t i = tid; i < nv; i += nth) d4[i] = s4[i];
+            head = nv << 2;
+        }
+        for (int64_t i = head + tid; i < n; i += nth) dst[i] = src[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        if (atomicAdd((unsigned*)&b->result[res].ndone, 1u) == gridDim.x - 1) {
+            if (ok) {
+                uint32_t* c = r->consumed;
+                *reinterpret_cast<volatile uint32_t*>(c) = r->cgen;
+            }
+            __threadfence_system();
+            reinterpret_cast<volatile DmStatus*>(st)->done = 1;
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t dm_send(DmBox* box, int src, int tag, int ctx, const uint8_t* data, int64_t bytes, uint32_t* consumed,
+                    uint32_t cgen, cudaStream_t stream) {
+    SendArgs a{box, src, tag, ctx, cgen, data, bytes, consumed};
+    k_dm_send<<<1, kThreads, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t dm_post(DmBox* box, int src, int tag, int ctx, int result, cudaStream_t stream) {
+    PostArgs a{box, src, tag, ctx, result};
+    k_dm_post<<<1, kThreads, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t dm_wait(DmBox* box, int result, DmStatus* status, int64_t cap, cudaStream_t stream) {
+    k_dm_wait<<<1, 32, 0, stream>>>(box, result, status, cap);
+    return cudaGetLastError();
+}
+
+cudaError_t dm_copy(DmBox* box, int result, uint8_t* dst, int64_t cap, DmStatus* status, int device,
+                    cudaStream_t stream) {
+    const int64_t want = (cap + (int64_t)kThreads * 64 - 1) / ((int64_t)kThreads * 64);
+    const int64_t grid = want < 1 ? 1 : (want > (int64_t)sm_count(device) * 4 ? (int64_t)sm_count(device) * 4 : want);
+    k_dm_copy<<<(unsigned)grid, kThreads, 0, stream>>>(box, result, dst, cap, status);
+    return cudaGetLastError();
+}
+
+cudaError_t preload_dm_kernels() {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaSuccess, r;
+    if ((r = cudaFuncGetAttributes(&a, k_dm_send)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_dm_post)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_dm_wait)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_dm_copy)) != cudaSuccess) e = r;
+    return e;
+}
+
+}  // namespace mpx

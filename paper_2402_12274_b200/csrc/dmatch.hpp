@@ -1,0 +1,103 @@
+// dmatch.hpp -- device-resident message matching.
+//
+// In a world joined with device matching (mpx_world_set_matching), the MPI
+// matching of stream-communicator point-to-point traffic happens on the GPU,
+// at the moment each rank's STREAM reaches the operation -- the B200 form of
+// the reference's executor-thread matching (offload.py:87-102 ->
+// transport.py:399-428 for receives, :191-201 / :509-516 for arriving
+// frames): every receiving rank owns a DmBox in its device memory holding the
+// two MPI queues,
+//
+//   msg[]  -- the unexpected queue: messages that arrived before a matching
+//             receive was posted (transport.py `_unexpected`);
+//   recv[] -- the posted-receive queue (transport.py `_posted`);
+//
+// each entry stamped with a box-wide sequence number, so "earliest" is
+// arrival / posting order.  One single-CTA kernel per operation, serialised
+// by a spin lock in the box (system-scope atomics: senders on peer GPUs
+// reach the box over NVLink):
+//
+//   k_dm_send  (sender's stream, after packing the message into its bounce
+//              buffer): earliest posted receive that matches (source / tag /
+//              context, ANY_SOURCE / ANY_TAG on the receive) -> hand the
+//              message to its result slot; none -> append to msg[];
+//   k_dm_post  (receiver's stream, at the receive's position): earliest
+//              unexpected message that matches -> result slot; none ->
+//              append to recv[];
+//   k_dm_wait  (receiver's stream, at wait / blocking receive): spin until
+//              the result slot is filled (a single CTA: never starves the
+//              sender's kernels of SMs), write the status;
+//   k_dm_copy  grid-wide copy of the message prefix that fits out of the
+//              bounce buffer; its last CTA marks the bounce buffer consumed
+//              (the sender's host frees it lazily) and the status done.
+//
+// Every message is buffered (packed into a bounce buffer at the sender's
+// stream position), so a blocking send never waits for its receiver: rings of
+// blocking sends are safe at every size (the reference guarantees it up to
+// its eager limit).  A nonblocking receive is posted at its stream position
+// and moves data at its wait, so nothing ever blocks a stream between the two.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace mpx {
+
+constexpr int kDmSlots = 2048;        // per receiving rank: unexpected messages + posted receives, each
+constexpr int kDmResults = 1 << 14;   // per receiving rank: receives in flight (posted, not yet copied)
+
+struct DmMsg {            // an unexpected message
+    int32_t state;        // 0 free, 1 queued
+    int32_t src, tag, ctx;
+    int64_t seq;
+    const uint8_t* data;  // bounce buffer (sender's device)
+    int64_t bytes;
+    uint32_t* consumed;   // pinned host word: set to cgen once the bytes are copied out
+    uint32_t cgen, pad;
+};
+
+struct DmRecv {           // a posted receive
+    int32_t state;
+    int32_t src, tag, ctx;    // patterns
+    int64_t seq;
+    int32_t result, pad;
+};
+
+struct DmResult {         // a receive's match, written by whichever side matched
+    int32_t ready;        // 1 once the fields below are valid
+    int32_t src, tag;
+    uint32_t ndone;       // k_dm_copy CTAs finished
+    int64_t bytes;
+    const uint8_t* data;
+    uint32_t* consumed;
+    uint32_t cgen, pad;
+};
+
+struct DmStatus {         // pinned host memory, one per result slot
+    int32_t done;         // 1: matched and copied
+    int32_t src, tag, err;
+    int64_t bytes;        // message bytes
+    int64_t pad;
+};
+
+struct DmBox {
+    int32_t lock;
+    int32_t hw_msg, hw_recv;  // entries at or above the high-water marks are free
+    int32_t err;              // sticky: an unexpected-queue overflow
+    int64_t next_seq;
+    DmMsg msg[kDmSlots];
+    DmRecv recv[kDmSlots];
+    DmResult result[kDmResults];
+};
+
+// launchers (dmatch.cu); `box` is the receiving rank's box
+cudaError_t dm_send(DmBox* box, int src, int tag, int ctx, const uint8_t* data, int64_t bytes, uint32_t* consumed,
+                    uint32_t cgen, cudaStream_t stream);
+cudaError_t dm_post(DmBox* box, int src, int tag, int ctx, int result, cudaStream_t stream);
+cudaError_t dm_wait(DmBox* box, int result, DmStatus* status, int64_t cap, cudaStream_t stream);
+cudaError_t dm_copy(DmBox* box, int result, uint8_t* dst, int64_t cap, DmStatus* status, int device,
+                    cudaStream_t stream);
+cudaError_t preload_dm_kernels();
+
+}  // namespace mpx

@@ -53,6 +53,7 @@
 
 #include "capi_common.hpp"
 #include "coll.hpp"
+#include "dmatch.hpp"
 #include "ipc.hpp"
 #include "kernels.hpp"
 #include "mpx.h"
@@ -466,6 +467,10 @@ struct ReqState {
     std::function<int(cudaStream_t)> at_wait;
     bool needs_wait = false;
     bool waited = false;
+    // device-matched receive (dmatch.hpp): the status lives in pinned host
+    // memory, written by the GPU when the match and the copy happen
+    DmStatus* dm = nullptr;
+    int64_t dm_cap = 0, dm_size = 0;
     std::mutex mu;
 };
 
@@ -510,6 +515,13 @@ struct World {
     std::string group;
     IpcWorld* ipc = nullptr;   // multi-process job (ipc.hpp); null: ranks are threads of this process
     int size = 0;
+    // matching mode (mpx_world_set_matching): -1 unset (host), 0 host, 1 device
+    int dm_mode = -1;
+    std::mutex dm_mu;
+    std::vector<DmBox*> dm_box;               // per rank, in that rank's device memory
+    std::vector<DmStatus*> dm_status;         // per rank, kDmResults, pinned host memory
+    std::vector<uint32_t> dm_next;            // per rank: next result slot
+    std::vector<std::vector<std::weak_ptr<Comm>>> dm_owner;   // blocking receive of a slot, to check for truncation
     int64_t eager_limit = 65536;
     std::vector<int> devices;
     std::vector<bool> joined;
@@ -686,6 +698,16 @@ struct Comm {
     std::atomic<int64_t> outstanding{0};
     int64_t coll_seq = 0;
     int ring = -1;                  // index into every device's ring area
+    // device matching: this communicator's bounce buffers not yet known to be
+    // consumed, and its blocking receives not yet checked for truncation
+    struct Bounce {
+        void* p;
+        uint32_t* flag;
+        uint32_t gen;
+    };
+    std::mutex dm_mu;
+    std::deque<Bounce> dm_bounce;
+    std::vector<int> dm_blocking;
 };
 
 Comm::~Comm() {
@@ -915,6 +937,11 @@ int ipc_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t count, Dat
 int ipc_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t count, Datatype* dt, int source, int tag,
              bool blocking, std::shared_ptr<ReqState>* out_req);
 
+int dm_send_op(const std::shared_ptr<Comm>& c, const void* buf, int64_t count, Datatype* dt, int dest, int tag,
+               bool blocking, std::shared_ptr<ReqState>* out_req);
+int dm_recv_op(const std::shared_ptr<Comm>& c, void* buf, int64_t count, Datatype* dt, int source, int tag,
+               bool blocking, std::shared_ptr<ReqState>* out_req);
+
 int do_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t buf_bytes, int64_t count, Datatype* dt, int dest, int tag,
             bool blocking, std::shared_ptr<ReqState>* out_req) {
     World* w = c->w;
@@ -927,6 +954,7 @@ int do_send(const std::shared_ptr<Comm>& c, const void* buf, int64_t buf_bytes, 
     if (dest < 0 || dest >= w->size) return fail(MPX_ERR_ARG, "dest %d out of range for size-%d communicator", dest, w->size);
     if (tag < 0) return fail(MPX_ERR_ARG, "tag %d out of range [0, 2147483647]", tag);
     MPX_RC(check_layout_region(dt, count, buf_bytes));
+    if (w->dm_mode == 1) return dm_send_op(c, buf, count, dt, dest, tag, blocking, out_req);
     Side s;
     s.rank = c->rank;
     s.device = c->device;
@@ -1106,6 +1134,7 @@ int do_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t buf_bytes, int64_
     if (tag < 0 && tag != MPX_ANY_TAG) return fail(MPX_ERR_ARG, "tag %d out of range [0, 2147483647]", tag);
     MPX_RC(check_layout_region(dt, count, buf_bytes));  // DtypeSink check at post time (p2p.py:63-64)
     if (w->ipc) return ipc_recv(c, buf, count, dt, source, tag, blocking, out_req);
+    if (w->dm_mode == 1) return dm_recv_op(c, buf, count, dt, source, tag, blocking, out_req);
     Side r;
     r.rank = c->rank;
     r.device = c->device;
@@ -1242,6 +1271,222 @@ int do_recv(const std::shared_ptr<Comm>& c, void* buf, int64_t buf_bytes, int64_
     if (!mpx_tracing()) release_event(ps.ev);
     if (out_req) *out_req = req;
     MPX_TRACE("recv r%d issued", c->rank);
+    return MPX_SUCCESS;
+}
+
+
+// ------------------------------------------------ device matching (dmatch.hpp)
+// The receiving rank's box (allocated on first use, on that rank's device;
+// a rank that has not joined yet is waited for) and its status array.
+int dm_box_of(World* w, int rank, DmBox** out) {
+    for (long t = 0;; ++t) {
+        {
+            std::lock_guard<std::mutex> g(w->dm_mu);
+            if (w->dm_box[(size_t)rank]) {
+                *out = w->dm_box[(size_t)rank];
+                return MPX_SUCCESS;
+            }
+            const int dev = w->devices[(size_t)rank];
+            if (dev >= 0) {
+                int cur = 0;
+                cudaGetDevice(&cur);
+                MPX_RC(set_device(dev));
+                DmBox* b = nullptr;
+                MPX_CU(cudaMalloc(reinterpret_cast<void**>(&b), sizeof(DmBox)));
+                cudaStream_t svc = w->service(dev);
+                MPX_CU(cudaMemsetAsync(b, 0, sizeof(DmBox), svc));
+                MPX_CU(cudaStreamSynchronize(svc));   // only the private service stream
+                DmStatus* st = nullptr;
+                MPX_CU(cudaHostAlloc(reinterpret_cast<void**>(&st), sizeof(DmStatus) * kDmResults,
+                                     cudaHostAllocMapped | cudaHostAllocPortable));
+                std::memset(static_cast<void*>(st), 0, sizeof(DmStatus) * kDmResults);
+                for (int i = 0; i < kDmResults; ++i) st[i].done = 1;   // every slot free
+                w->dm_status[(size_t)rank] = st;
+                w->dm_box[(size_t)rank] = b;
+                *out = b;
+                return set_device(cur);
+            }
+        }
+        if (t > 120000) return fail(MPX_ERR_STATE, "rank %d never joined world %s", rank, w->group.c_str());
+        struct timespec ts{0, 1000000L};
+        nanosleep(&ts, nullptr);
+    }
+}
+
+// Check a blocking receive's status for truncation (deferred error of its
+// communicator, raised at synchronize like the host path's).  w->dm_mu held.
+void dm_settle_locked(World* w, int rank, int slot) {
+    auto& own = w->dm_owner[(size_t)rank][(size_t)slot];
+    auto c = own.lock();
+    own.reset();
+    if (!c) return;
+    const volatile DmStatus* st = &w->dm_status[(size_t)rank][slot];
+    if (st->done && st->err == MPX_ERR_TRUNCATE)
+        defer_error(c, MPX_ERR_TRUNCATE, "message truncated: incoming data larger than the posted receive");
+    else if (st->done && st->err)
+        defer_error(c, st->err, "device matching: the unexpected-message queue overflowed");
+}
+
+// A result slot for a new receive of `rank`: the next one round-robin, which
+// must have completed its previous use.
+int dm_take_slot(World* w, int rank, int* slot) {
+    std::lock_guard<std::mutex> g(w->dm_mu);
+    const int s = (int)(w->dm_next[(size_t)rank]++ % (uint32_t)kDmResults);
+    volatile DmStatus* st = &w->dm_status[(size_t)rank][s];
+    if (!st->done)
+        return fail(MPX_ERR_EXHAUSTED, "device matching: more than %d receives of rank %d in flight", kDmResults, rank);
+    dm_settle_locked(w, rank, s);
+    st->done = 0;
+    st->err = 0;
+    st->src = -1;
+    st->tag = -1;
+    st->bytes = 0;
+    *slot = s;
+    return MPX_SUCCESS;
+}
+
+// Free this communicator's bounce buffers whose receivers have copied them
+// out (stream-ordered on its own stream: after the pack that wrote them).
+int dm_reclaim(const std::shared_ptr<Comm>& c) {
+    std::lock_guard<std::mutex> g(c->dm_mu);
+    for (auto it = c->dm_bounce.begin(); it != c->dm_bounce.end();) {
+        if (*reinterpret_cast<volatile uint32_t*>(it->flag) >= it->gen) {
+            ProfScope pf(P_FREE);
+            MPX_CU(cudaFreeAsync(it->p, c->stream));
+            it = c->dm_bounce.erase(it);
+        } else {
+            ++it;
+        }
+    }
+    return MPX_SUCCESS;
+}
+
+// Every message is packed into a bounce buffer at the sender's stream
+// position, then announced to the receiver's box (k_dm_send): the send is
+// complete at that point, blocking or not.
+int dm_send_op(const std::shared_ptr<Comm>& c, const void* buf, int64_t count, Datatype* dt, int dest, int tag,
+               bool blocking, std::shared_ptr<ReqState>* out_req) {
+    World* w = c->w;
+    DmBox* box = nullptr;
+    MPX_RC(dm_box_of(w, dest, &box));
+    MPX_RC(set_device(c->device));
+    MPX_RC(dm_reclaim(c));
+    const int64_t bytes = dt->size * count;
+    void* bounce = nullptr;
+    MPX_RC(staging_alloc(c->device, (size_t)bytes, c->stream, &bounce));
+    if (bytes > 0) {
+        ProfScope pl(P_LAUNCH);
+        MPX_RC(launch_move(c->device, dt, count, true, buf, bounce, bytes, c->stream));
+        MPX_RC(set_device(c->device));
+    }
+    uint32_t* flag = nullptr;
+    uint32_t gen = 0;
+    w->flags.take(&flag, &gen);
+    {
+        ProfScope pl(P_LAUNCH);
+        MPX_CU(dm_send(box, c->rank, tag, c->ctx, static_cast<const uint8_t*>(bounce), bytes, flag, gen, c->stream));
+    }
+    {
+        std::lock_guard<std::mutex> g(c->dm_mu);
+        c->dm_bounce.push_back({bounce, flag, gen});
+    }
+    MPX_TRACE("dm send r%d -> %d tag %d %lld B", c->rank, dest, tag, (long long)bytes);
+    if (!blocking) {
+        auto req = std::make_shared<ReqState>();
+        req->comm = c;
+        req->is_send = true;
+        req->matched = true;   // buffered: complete at its stream position
+        c->outstanding++;
+        if (out_req) *out_req = req;
+    }
+    return MPX_SUCCESS;
+}
+
+// The receive is posted at its stream position (k_dm_post); its data moves
+// at the wait (blocking: right away): k_dm_wait, then the copy -- straight
+// into the buffer for a contiguous layout; for a typed one into a landing
+// buffer pre-filled with the layout's current bytes (so a short message
+// leaves the rest of the layout as it was), unpacked afterwards.
+int dm_recv_op(const std::shared_ptr<Comm>& c, void* buf, int64_t count, Datatype* dt, int source, int tag,
+               bool blocking, std::shared_ptr<ReqState>* out_req) {
+    World* w = c->w;
+    const int64_t cap = dt->size * count;
+    int64_t off = 0;
+    const bool contig = contiguous_run(dt, count, &off);
+    if (!contig && cap > 0) {
+        int64_t q[8];
+        MPX_RC(mpx_layout_query(reinterpret_cast<mpx_datatype>(dt), count, q));
+        if (q[6]) return fail(MPX_ERR_UNSUPPORTED, "device matching: receive layouts with overlapping bytes are not supported");
+    }
+    DmBox* box = nullptr;
+    MPX_RC(dm_box_of(w, c->rank, &box));
+    int slot = 0;
+    MPX_RC(dm_take_slot(w, c->rank, &slot));
+    DmStatus* st = &w->dm_status[(size_t)c->rank][slot];
+    MPX_RC(set_device(c->device));
+    {
+        ProfScope pl(P_LAUNCH);
+        MPX_CU(dm_post(box, source, tag, c->ctx, slot, c->stream));
+    }
+    const int dev = c->device;
+    auto deliver = [dev, box, slot, st, cap, contig, off, dt, count, buf](cudaStream_t ws) -> int {
+        MPX_RC(set_device(dev));
+        ProfScope pl(P_LAUNCH);
+        MPX_CU(dm_wait(box, slot, st, cap, ws));
+        if (contig) {
+            MPX_CU(dm_copy(box, slot, static_cast<uint8_t*>(buf) + off, cap, st, dev, ws));
+            return MPX_SUCCESS;
+        }
+        void* landing = nullptr;
+        MPX_RC(staging_alloc(dev, (size_t)cap, ws, &landing));
+        if (cap > 0) MPX_RC(launch_move(dev, dt, count, true, buf, landing, cap, ws));
+        MPX_RC(set_device(dev));
+        MPX_CU(dm_copy(box, slot, static_cast<uint8_t*>(landing), cap, st, dev, ws));
+        if (cap > 0) MPX_RC(launch_move(dev, dt, count, false, landing, buf, cap, ws));
+        MPX_RC(set_device(dev));
+        MPX_CU(cudaFreeAsync(landing, ws));
+        return MPX_SUCCESS;
+    };
+    MPX_TRACE("dm recv r%d <- %d tag %d posted (slot %d)", c->rank, source, tag, slot);
+    if (blocking) {
+        {
+            std::lock_guard<std::mutex> g(w->dm_mu);
+            w->dm_owner[(size_t)c->rank][(size_t)slot] = c;
+        }
+        {
+            std::lock_guard<std::mutex> g(c->dm_mu);
+            c->dm_blocking.push_back(slot);
+        }
+        return deliver(c->stream);
+    }
+    auto req = std::make_shared<ReqState>();
+    req->comm = c;
+    req->dm = st;
+    req->dm_cap = cap;
+    req->dm_size = dt->size;
+    req->at_wait = deliver;
+    req->needs_wait = true;
+    c->outstanding++;
+    if (out_req) *out_req = req;
+    return MPX_SUCCESS;
+}
+
+// after the communicator's stream is drained: free consumed bounce buffers,
+// report truncated blocking receives
+int dm_after_sync(const std::shared_ptr<Comm>& c) {
+    World* w = c->w;
+    if (w->dm_mode != 1) return MPX_SUCCESS;
+    MPX_RC(dm_reclaim(c));
+    std::vector<int> slots;
+    {
+        std::lock_guard<std::mutex> g(c->dm_mu);
+        slots.swap(c->dm_blocking);
+    }
+    std::lock_guard<std::mutex> g(w->dm_mu);
+    for (int s : slots) {
+        auto o = w->dm_owner[(size_t)c->rank][(size_t)s].lock();
+        if (o.get() == c.get()) dm_settle_locked(w, c->rank, s);
+    }
     return MPX_SUCCESS;
 }
 
@@ -1784,6 +2029,28 @@ int mpx_world_barrier(mpx_world h) {
     return w->ipc->barrier();
 }
 
+int mpx_world_set_matching(mpx_world h, int device_side) {
+    auto* w = reinterpret_cast<World*>(h);
+    if (!w) return fail(MPX_ERR_STATE, "not a live world");
+    if (device_side != 0 && device_side != 1) return fail(MPX_ERR_ARG, "matching mode must be 0 (host) or 1 (device)");
+    if (w->ipc && device_side) return fail(MPX_ERR_UNSUPPORTED, "device matching is built for in-process worlds");
+    std::lock_guard<std::mutex> g(w->dm_mu);
+    if (w->dm_mode < 0) {
+        if (device_side) {
+            MPX_CU(preload_dm_kernels());
+            w->dm_box.assign((size_t)w->size, nullptr);
+            w->dm_status.assign((size_t)w->size, nullptr);
+            w->dm_next.assign((size_t)w->size, 0);
+            w->dm_owner.assign((size_t)w->size, std::vector<std::weak_ptr<Comm>>((size_t)kDmResults));
+        }
+        w->dm_mode = device_side;
+    } else if (w->dm_mode != device_side) {
+        return fail(MPX_ERR_ARG, "ranks of world %s disagree on the matching mode (%s here)", w->group.c_str(),
+                    device_side ? "device" : "host");
+    }
+    return MPX_SUCCESS;
+}
+
 int mpx_world_leave(mpx_world h, int rank) {
     auto* w = reinterpret_cast<World*>(h);
     if (w && w->ipc) {
@@ -1808,6 +2075,13 @@ int mpx_world_leave(mpx_world h, int rank) {
     w->joined[rank] = false;
     if (--w->live == 0) {
         w->stop_deferred();
+        for (size_t r = 0; r < w->dm_box.size(); ++r) {
+            if (w->dm_box[r]) {
+                set_device(w->devices[r]);
+                cudaFree(w->dm_box[r]);
+            }
+            if (w->dm_status[r]) cudaFreeHost(w->dm_status[r]);
+        }
         for (auto& kv : w->area) {
             set_device(kv.first);
             cudaFree(kv.second);
@@ -1932,6 +2206,18 @@ int mpx_request_status(mpx_request h, int64_t out[5]) {
     auto q = req_of(h);
     if (!q) return fail(MPX_ERR_ARG, "unknown request");
     std::lock_guard<std::mutex> g(q->mu);
+    if (q->dm) {   // device-matched receive: known once the GPU has matched and copied it
+        const volatile DmStatus* st = q->dm;
+        const bool done = st->done != 0;
+        const int64_t nb = st->bytes;
+        const int64_t moved = done ? std::min<int64_t>(nb, q->dm_cap) : 0;
+        out[0] = done;
+        out[1] = done ? st->src : -1;
+        out[2] = done ? st->tag : -1;
+        out[3] = done && q->dm_size ? moved / q->dm_size : 0;
+        out[4] = done ? st->err : MPX_SUCCESS;
+        return MPX_SUCCESS;
+    }
     out[0] = q->matched;
     out[1] = q->source;
     out[2] = q->tag;
@@ -1951,6 +2237,7 @@ int mpx_comm_synchronize(mpx_comm h) {
     if (!c) return fail(MPX_ERR_STATE, "device queue already destroyed");
     MPX_RC(set_device(c->device));
     MPX_RC(mpx_stream_wait(c->stream));
+    MPX_RC(dm_after_sync(c));
     std::lock_guard<std::mutex> g(c->err_mu);
     if (!c->deferred.empty()) {
         auto e = c->deferred.front();

@@ -27,6 +27,8 @@ from .errors import ArgError, ExhaustedError, PendingError, StateError, Unsuppor
 TRANSPORT_INPROC = "inproc"
 TRANSPORT_IPC = "ipc"          # one process per rank on one node
 DEFAULT_IPC_ARENA = 256 << 20  # per-rank staging arena of a multi-process world
+MATCH_HOST = "host"            # matching at enqueue time (default)
+MATCH_DEVICE = "device"        # matching on the GPU at stream time (csrc/dmatch.hpp)
 SERIAL_CONTEXT = "serial_context"
 DEVICE_QUEUE = "device_queue"
 CUDA_STREAM = "cuda_stream"
@@ -237,8 +239,9 @@ class Instance:
     """One rank of a running job (runtime.py:56-214)."""
 
     def __init__(self, rank, size, group, device, eager_limit, vci_pool, transport=TRANSPORT_INPROC,
-                 arena=DEFAULT_IPC_ARENA):
+                 arena=DEFAULT_IPC_ARENA, matching=MATCH_HOST):
         self.transport = transport
+        self.matching = matching
         self.rank = rank
         self.size = size
         self.group = group
@@ -264,6 +267,12 @@ class Instance:
         check(lib.mpx_world_join(group.encode(), size, rank, device, eager_limit,
                                  ctypes.byref(h)))
         self._world = h.value
+        try:
+            check(lib.mpx_world_set_matching(self._world, 1 if matching == MATCH_DEVICE else 0))
+        except BaseException:
+            lib.mpx_world_leave(self._world, rank)
+            self._group.leave()
+            raise
         from .comms import Communicator
         self.world = Communicator(self, 0, rank, size)
         self._comms = [self.world]
@@ -335,13 +344,20 @@ class Instance:
 
 
 def init(transport=None, rank=None, ranks=None, group=None, device=None,
-         eager_limit=None, vci_pool=None, **_ignored):
+         eager_limit=None, vci_pool=None, matching=None, **_ignored):
     """Bring up this rank (runtime.py:217-257).  transport must be "inproc"
     (the only in-scope transport: socket / multi-host bootstrap is out of
     scope)."""
     transport = _cfg(transport, "MINIMPI_TRANSPORT", TRANSPORT_INPROC, str).replace("-", "")
     if transport not in (TRANSPORT_INPROC, TRANSPORT_IPC):
         raise UnsupportedError("transport %r is out of scope for the B200 build" % transport)
+    # where point-to-point messages are matched (csrc/dmatch.hpp): "host" at
+    # enqueue time, or "device" when each rank's stream reaches the operation
+    matching = _cfg(matching, "MINIMPI_MATCHING", MATCH_HOST, str)
+    if matching not in (MATCH_HOST, MATCH_DEVICE):
+        raise ArgError("matching must be %r or %r, got %r" % (MATCH_HOST, MATCH_DEVICE, matching))
+    if matching == MATCH_DEVICE and transport == TRANSPORT_IPC:
+        raise UnsupportedError("device matching is built for in-process worlds (transport 'inproc')")
     if transport == TRANSPORT_IPC:
         # one process per rank: torchrun's RANK / WORLD_SIZE / LOCAL_RANK unless given
         rank = _cfg(rank, "MINIMPI_RANK", int(os.environ.get("RANK", "0")), int)
@@ -369,4 +385,4 @@ def init(transport=None, rank=None, ranks=None, group=None, device=None,
     if isinstance(device, torch.device):
         device = device.index or 0
     arena = int(os.environ.get("MPX_IPC_ARENA", DEFAULT_IPC_ARENA))
-    return Instance(rank, size, group, int(device), eager_limit, vci_pool, transport, arena)
+    return Instance(rank, size, group, int(device), eager_limit, vci_pool, transport, arena, matching)

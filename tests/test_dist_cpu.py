@@ -94,7 +94,7 @@ def test_ipc_init_takes_rank_and_size_from_torchrun(monkeypatch):
     seen = {}
 
     class FakeInstance:
-        def __init__(self, rank, size, group, device, eager, pool, transport, arena):
+        def __init__(self, rank, size, group, device, eager, pool, transport, arena, matching="host"):
             seen.update(rank=rank, size=size, group=group, device=device, transport=transport)
 
     for k in ("MINIMPI_RANK", "MINIMPI_SIZE", "MINIMPI_GROUP", "MINIMPI_TRANSPORT"):
@@ -108,3 +108,31 @@ def test_ipc_init_takes_rank_and_size_from_torchrun(monkeypatch):
     monkeypatch.setattr(runtime.torch.cuda, "device_count", lambda: 8)
     mp.init(transport="ipc")
     assert seen == {"rank": 1, "size": 2, "group": "job29533none", "device": 1, "transport": "ipc"}
+
+
+def test_matching_mode_checked_before_any_device_work(monkeypatch):
+    """init(matching=...): "host" (default) or "device" (csrc/dmatch.hpp),
+    kwarg > MINIMPI_MATCHING > default; device matching is for in-process
+    worlds only.  Checked before CUDA is touched."""
+    import paper_2402_12274_b200 as mp
+    from paper_2402_12274_b200 import runtime
+    seen = {}
+
+    class FakeInstance:
+        def __init__(self, rank, size, group, device, eager, pool, transport, arena, matching="host"):
+            seen["matching"] = matching
+
+    monkeypatch.setattr(runtime, "Instance", FakeInstance)
+    monkeypatch.setattr(runtime.torch.cuda, "device_count", lambda: 1)
+    monkeypatch.delenv("MINIMPI_MATCHING", raising=False)
+    with pytest.raises(mp.ArgError):
+        mp.init(matching="gpu")
+    with pytest.raises(mp.UnsupportedError):
+        mp.init(transport="ipc", matching="device")
+    mp.init()
+    assert seen["matching"] == "host"
+    monkeypatch.setenv("MINIMPI_MATCHING", "device")
+    mp.init()
+    assert seen["matching"] == "device"
+    mp.init(matching="host")
+    assert seen["matching"] == "host"

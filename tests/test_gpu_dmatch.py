@@ -1,0 +1,182 @@
+"""Device-resident matching (csrc/dmatch.hpp): the enqueue
+path's matching and point-to-point tests re-run with every world joined
+with matching="device" (MINIMPI_MATCHING=device), plus the cases that only
+device matching has: blocking rings beyond the eager limit (every message is
+buffered), ANY_SOURCE races between senders resolved on the GPU, short
+messages into typed receives, truncation reported from the device status.
+
+Mirrors /root/reference/pkg/tests/test_offload.py:41-210 and test_p2p.py
+(matching rules: transport.py:191-201,399-428)."""
+
+import pytest
+import torch
+
+import paper_2402_12274_b200 as mp
+from twin import host, pair
+
+# the host-matching suites, collected again here under device matching
+from test_gpu_enqueue import (  # noqa: F401
+    inst, queue, device_comm, u8, _ring,
+    test_deferred_error_surfaces_at_synchronize, test_awaited_request_error_lands_on_its_status,
+    test_cross_rank_device_pipeline, test_criterion_09a_saxpy_pipeline_without_host_sync,
+    test_criterion_09b_compute_overlaps_pending_receive, test_ring_nonblocking,
+    test_ring_blocking_within_eager_limit, test_ring_blocking_large_with_raised_eager_limit,
+    test_any_source_any_tag_and_fifo_order, test_typed_transfer_vector_to_contiguous,
+    test_receives_complete_out_of_posting_order, test_ring_baseline_sizes)
+from test_gpu_enqueue_stress import test_random_nonblocking_schedules  # noqa: F401
+
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(300)]
+
+
+@pytest.fixture(autouse=True)
+def device_matching(monkeypatch):
+    monkeypatch.setenv("MINIMPI_MATCHING", "device")
+
+
+def test_mode_is_device(inst):
+    assert inst.matching == "device"
+
+
+@pytest.mark.parametrize("n", [2, 4])
+@pytest.mark.parametrize("nbytes", [1 << 20, 16 << 20])
+def test_blocking_ring_beyond_eager_limit(n, nbytes):
+    """send-then-recv rings of blocking calls far above the eager limit: with
+    every message buffered at the sender no rank ever waits for its receiver
+    (the reference guarantees this only up to its eager limit)."""
+    _ring(n, nbytes, "u8", blocking=True)
+    _ring(n, nbytes, "vector", blocking=True)
+
+
+@pytest.mark.parametrize("n", [3, 5])
+def test_any_source_race_takes_every_sender_once(n):
+    """n-1 ranks send to rank 0 with one tag; rank 0 posts n-1 ANY_SOURCE
+    receives before any send can have arrived: the GPU assigns each message
+    to exactly one receive, in posting order of the receives."""
+    got = {}
+
+    def body(inst):
+        r = inst.rank
+        q = mp.queue_create(inst)
+        c, s = device_comm(inst, q)
+        if r == 0:
+            bufs = [torch.zeros(64, dtype=torch.uint8, device=inst.device) for _ in range(n - 1)]
+            with torch.cuda.stream(q.torch_stream):
+                torch.cuda._sleep(20000)   # the posts run after the senders have started
+            reqs = [mp.irecv_enqueue(c, b, 64, mp.BYTE, mp.ANY_SOURCE, 7) for b in bufs]
+            mp.waitall_enqueue(reqs)
+            mp.queue_synchronize(q)
+            got["src"] = [rq.status.source for rq in reqs]
+            got["data"] = [int(b[0].item()) for b in bufs]
+            got["same"] = all(bool((b == b[0]).all()) for b in bufs)
+        else:
+            mp.send(c, torch.full((64,), r, dtype=torch.uint8, device=inst.device), 64, mp.BYTE, 0, 7)
+            mp.queue_synchronize(q)
+        mp.comm_free(c)
+        mp.free_stream(s)
+        mp.queue_destroy(q)
+
+    host([body] * n)
+    assert sorted(got["src"]) == list(range(1, n))
+    assert got["data"] == got["src"] and got["same"]
+
+
+def test_short_message_into_typed_receive_keeps_the_rest():
+    """a message shorter than a typed receive fills a prefix of the layout;
+    the layout's other bytes and the gaps keep their values (datatype.py:705-728
+    prefix semantics)."""
+    got = {}
+
+    def rank0(inst):
+        q = mp.queue_create(inst)
+        c, s = device_comm(inst, q)
+        mp.send(c, torch.arange(1, 7, dtype=torch.int32, device=inst.device), 6, mp.INT32, 1, 3)
+        mp.queue_synchronize(q)
+        mp.comm_free(c)
+        mp.free_stream(s)
+        mp.queue_destroy(q)
+
+    def rank1(inst):
+        q = mp.queue_create(inst)
+        c, s = device_comm(inst, q)
+        vt = mp.type_vector(5, 2, 3, mp.INT32).commit()          # 10 ints over 15
+        dst = torch.full((15,), -1, dtype=torch.int32, device=inst.device)
+        rq = mp.irecv_enqueue(c, dst, 1, vt, 0, 3)
+        mp.wait_enqueue(rq)
+        mp.queue_synchronize(q)
+        got["dst"] = dst.cpu().tolist()
+        got["count"] = rq.status.count
+        got["err"] = rq.status.error
+        mp.type_free(vt)
+        mp.comm_free(c)
+        mp.free_stream(s)
+        mp.queue_destroy(q)
+
+    pair(rank0, rank1)
+    assert got["dst"] == [1, 2, -1, 3, 4, -1, 5, 6, -1, -1, -1, -1, -1, -1, -1]
+    assert got["err"] is None
+    assert got["count"] == 0      # 24 of 40 bytes: not a whole element of the vector type
+
+
+def test_zero_byte_messages_match_in_order():
+    got = {}
+
+    def rank0(inst):
+        q = mp.queue_create(inst)
+        c, s = device_comm(inst, q)
+        z = torch.zeros(1, dtype=torch.uint8, device=inst.device)
+        for t in (4, 5):
+            mp.send(c, z, 0, mp.BYTE, 1, t)
+        mp.queue_synchronize(q)
+        mp.comm_free(c)
+        mp.free_stream(s)
+        mp.queue_destroy(q)
+
+    def rank1(inst):
+        q = mp.queue_create(inst)
+        c, s = device_comm(inst, q)
+        z = torch.zeros(1, dtype=torch.uint8, device=inst.device)
+        a = mp.irecv_enqueue(c, z, 0, mp.BYTE, 0, mp.ANY_TAG)
+        b = mp.irecv_enqueue(c, z, 0, mp.BYTE, 0, mp.ANY_TAG)
+        mp.waitall_enqueue([a, b])
+        mp.queue_synchronize(q)
+        got["tags"] = [a.status.tag, b.status.tag]
+        got["counts"] = [a.status.count, b.status.count]
+        mp.comm_free(c)
+        mp.free_stream(s)
+        mp.queue_destroy(q)
+
+    pair(rank0, rank1)
+    assert got["tags"] == [4, 5] and got["counts"] == [0, 0]
+
+
+def test_ranks_must_agree_on_the_matching_mode():
+    """a rank joining with the other mode is refused (and leaves the world
+    cleanly: it can join again with the world's mode)"""
+    import threading
+    from twin import unique_group
+    group = unique_group("mode")
+    out = {}
+    joined = threading.Event()
+
+    def rank0():
+        i = mp.init(rank=0, ranks=2, group=group, device=0, matching="device")
+        joined.set()
+        out[0] = i.matching
+        i.finalize()
+
+    def rank1():
+        assert joined.wait(60)
+        try:
+            mp.init(rank=1, ranks=2, group=group, device=0, matching="host")
+        except mp.ArgError as e:
+            out["err"] = str(e)
+        i = mp.init(rank=1, ranks=2, group=group, device=0, matching="device")
+        out[1] = i.matching
+        i.finalize()
+
+    ts = [threading.Thread(target=f) for f in (rank0, rank1)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(120)
+    assert "disagree" in out.get("err", "") and out.get(0) == out.get(1) == "device"

@@ -1,5 +1,6 @@
 """Summarise an ncu report (development tool): key throughput / stall metrics
-per kernel launch.   python tools/ncu_summary.py report.ncu-rep [regex]"""
+per kernel launch, each value with its ncu unit (ncu scales byte counts to
+byte / Kbyte / Mbyte per metric).   python tools/ncu_summary.py report.ncu-rep [regex]"""
 import csv
 import io
 import re
@@ -21,7 +22,7 @@ def main():
     pat = sys.argv[2] if len(sys.argv) > 2 else "."
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    h = rows[0]
+    h, units = rows[0], rows[1]
     ki = h.index("Kernel Name")
     idx = [i for i, k in enumerate(h) if re.search(KEYS, k)]
     for r in rows[2:]:
@@ -29,7 +30,7 @@ def main():
             continue
         print(r[ki][:70])
         for i in idx:
-            print("    %-62s %s" % (h[i], r[i]))
+            print("    %-62s %s %s" % (h[i], r[i], units[i]))
 
 
 if __name__ == "__main__":
