@@ -757,14 +757,19 @@ k_iov_chain(const Chain c, int64_t k0, int64_t n, int64_t* __restrict__ out) {
 __global__ void __launch_bounds__(256)
 k_iov_span(const SpanPlan sp, int64_t k0, int64_t n, int64_t* __restrict__ out) {
     const int lane = threadIdx.x & 31;
-    const int64_t nw = (int64_t)gridDim.x * 8;
     longlong2* o2 = reinterpret_cast<longlong2*>(out);
-    for (int64_t ub = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * 32; ub < sp.nunits; ub += nw * 32) {
+    // an even split of the units over the warps (a grid-stride over 32-unit
+    // batches left a third of the launch in a tail of a few warps: ~2.1
+    // batches per warp on cfg3)
+    const int64_t nw = (int64_t)gridDim.x * 8, gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int64_t ua = sp.nunits / nw * gw + min(gw, sp.nunits % nw);
+    const int64_t uz = ua + sp.nunits / nw + (gw < sp.nunits % nw ? 1 : 0);
+    for (int64_t ub = ua; ub < uz; ub += 32) {
         // lane l: metadata of unit ub + l
         int64_t seg0 = 0, lay0 = 0, rlen = 0;
         int32_t segs = 0, body = -1, stride = 0;
         const int64_t u = ub + lane;
-        if (u < sp.nunits) {
+        if (u < uz) {
             const uint64_t o = fdiv((uint64_t)u, sp.m_nchunks, sp.s_nchunks);
             const int64_t c = u - (int64_t)o * sp.nchunks;
             const longlong2 ic = __ldg(sp.iovc + c);
@@ -786,7 +791,63 @@ k_iov_span(const SpanPlan sp, int64_t k0, int64_t n, int64_t* __restrict__ out) 
             rlen = ic.y;
             if (seg0 + segs <= k0 || seg0 >= k0 + n) segs = 0;
         }
-        const int cnt = (int)min((int64_t)32, sp.nunits - ub);
+        const int cnt = (int)min((int64_t)32, uz - ub);
+        // Flat batch: when every unit of the batch repeats ONE body of <= 4
+        // runs (cfg3: 2-run struct elements, ~26 per unit), the warp walks the
+        // batch's elements as one sequence -- lane per element, its unit found
+        // by a 5-step search over the units' element prefix held in the
+        // lanes -- instead of unit by unit (per-unit set-up dominated: ~52
+        // segments per unit).  Consecutive elements are consecutive in the
+        // output, so a warp store covers 32 whole elements.
+        {
+            const int bd0 = __shfl_sync(0xffffffffu, body, 0);
+            int nr0 = 0;
+            if (bd0 >= 0) nr0 = __ldg(&sp.bodies[bd0].nruns);
+            const int ne = nr0 == 2 ? segs >> 1 : nr0 > 0 ? segs / nr0 : 0;
+            const bool ok = segs == 0 || (body == bd0 && nr0 > 0 && nr0 <= 4 && ne * nr0 == segs);
+            if (__all_sync(0xffffffffu, ok) && bd0 >= 0 && nr0 <= 4) {
+                const SpanBody* B = sp.bodies + bd0;
+                int64_t ro[4];
+                int64_t rl[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    ro[r] = r < nr0 ? (int64_t)__ldg(&B->roff[r]) : 0;
+                    rl[r] = r < nr0 ? (int64_t)__ldg(&B->rlen[r]) : 0;
+                }
+                int incl = ne;   // inclusive prefix of elements over the units (lanes)
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= d) incl += v;
+                }
+                const int excl = incl - ne;
+                const int total = __shfl_sync(0xffffffffu, incl, 31);
+                longlong2* const ob = o2 - k0;
+                for (int t0 = 0; t0 < total; t0 += 32) {   // warp-uniform trips: the shuffles need every lane
+                    const int t = t0 + lane;
+                    int uu = 0;   // last unit whose first element is <= t (it holds element t)
+#pragma unroll
+                    for (int step = 16; step; step >>= 1)
+                        if (__shfl_sync(0xffffffffu, excl, uu + step) <= t) uu += step;
+                    const int e = t - __shfl_sync(0xffffffffu, excl, uu);
+                    const int64_t g = __shfl_sync(0xffffffffu, seg0, uu) + (int64_t)e * nr0;
+                    const int64_t b = __shfl_sync(0xffffffffu, lay0, uu) +
+                                      (int64_t)e * __shfl_sync(0xffffffffu, stride, uu);
+                    longlong2* const p = ob + g;
+                    if (t >= total) continue;
+                    if (nr0 == 2 && g >= k0 && g + 2 <= k0 + n && !(reinterpret_cast<uintptr_t>(p) & 31)) {
+                        asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(b + ro[0]), "l"(rl[0]),
+                                     "l"(b + ro[1]), "l"(rl[1])
+                                     : "memory");
+                    } else {
+#pragma unroll
+                        for (int r = 0; r < 4; ++r)
+                            if (r < nr0 && g + r >= k0 && g + r < k0 + n) p[r] = make_longlong2(b + ro[r], rl[r]);
+                    }
+                }
+                continue;
+            }
+        }
         for (int j = 0; j < cnt; ++j) {
             const int32_t sg = __shfl_sync(0xffffffffu, segs, j);
             if (sg == 0) continue;
@@ -1095,7 +1156,17 @@ cudaError_t launch_iov(const Plan& p, int64_t k0, int64_t n, int64_t* out, cudaS
     } else if (p.kind == PLAN_RUNS && !p.rt.split) {
         k_iov_runs<<<(unsigned)grid, 256, 0, stream>>>(p.rt, k0, n, out);
     } else if (p.kind == PLAN_SPAN && p.span.iovc) {
-        const int64_t g = std::max<int64_t>(1, std::min<int64_t>((p.span.nunits + 255) / 256, (int64_t)sm_count(p.device) * 8));
+        // one wave of resident CTAs: every warp takes an equal share of the units
+        static int resident = 0;
+        if (!resident) {
+            int b = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_iov_span, 256, 0) != cudaSuccess || b < 1) {
+                cudaGetLastError();
+                b = 4;
+            }
+            resident = b;
+        }
+        const int64_t g = std::max<int64_t>(1, std::min<int64_t>((p.span.nunits + 255) / 256, (int64_t)sm_count(p.device) * resident));
         k_iov_span<<<(unsigned)g, 256, 0, stream>>>(p.span, k0, n, out);
     } else {
         k_iov<<<(unsigned)grid, 256, 0, stream>>>(p.desc, k0, n, out);

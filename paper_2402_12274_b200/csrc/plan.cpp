@@ -496,7 +496,9 @@ bool build_perm(int64_t Eo, int64_t Ei, const std::vector<int64_t>& map, PermSpe
         std::vector<PermEntry> t;
         if (!perm_tables(Eo, Ei, E, 1, map, &probe, &t, false)) bytes = true;
     }
+    static const int64_t force_m = getenv("MPX_PERM_M") ? atoll(getenv("MPX_PERM_M")) : 0;   // A/B experiments
     for (int64_t m = 1; m * P <= wmax; ++m) {
+        if (force_m > 0 && m != force_m && force_m * P <= wmax) continue;
         PermSpec sp{};
         std::vector<PermEntry> t;
         if (!perm_tables(Eo, Ei, E, m, map, &sp, &t, bytes)) return false;
