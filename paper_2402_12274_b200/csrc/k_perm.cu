@@ -451,6 +451,118 @@ __device__ __forceinline__ void permute(const PermSpec& S, const Unit& U, uint32
     for (; kw < words; kw += W, kd += Dw4) edge(kw, kd);
 }
 
+#ifndef MPX_PACK_CARRY
+#define MPX_PACK_CARRY 1
+#endif
+constexpr bool kPackCarry = MPX_PACK_CARRY != 0;   // A/B switch (-DMPX_PACK_CARRY=0: per-unit edges)
+
+// Pack of one unit with a carried partial word.  A warp's units are
+// consecutive chunks whose packed outputs abut, so the last, partial output
+// word of unit u and the first, partial word of unit u + 1 are the same
+// word: its bytes from unit u ride in `carry` (every lane) to unit u + 1,
+// which merges them (one prmt) and stores the word whole.  The steps of a
+// unit are then interior steps, the last ones with clamped windows -- no
+// per-unit edge steps with byte masks.  Units whose head has no carry (the
+// warp's first unit) or whose tail cannot be handed over (the warp's last
+// unit, a unit cut by the limit) take the generic path, after storing any
+// carried bytes.
+//   head_ok:   `carry` holds bytes [0, po) of this unit's first output word
+//   tail_keep: the next unit abuts this one in the packed output
+// Returns whether the tail word was handed over in `carry`.
+template <int NS, bool MIXED>
+__device__ __forceinline__ bool permute_pack(const PermSpec& S, const Unit& U, uint32_t sbuf, int lane,
+                                             uint32_t& carry, bool head_ok, bool tail_keep) {
+    const int po = (int)(reinterpret_cast<uintptr_t>(U.out) & 3);
+    const int tb = (po + U.out_len) & 3;                  // bytes of the tail word (0: none)
+    const int w_hi = (U.out_len + po) >> 2;
+    head_ok = head_ok && po != 0;
+    tail_keep = tail_keep && tb != 0 && (w_hi > 0 || head_ok);
+    const bool bytes = MIXED && S.pad != 0;
+    if (bytes || (po && !head_ok) || (tb && !tail_keep) || !(U.flags & 2)) {
+        // carried bytes [0, po) of the first word are stored here; the rest
+        // of the unit by the generic path
+        if (head_ok && lane == 0) store_bytes(U.out - po, carry, (1u << po) - 1);
+        permute<true, NS, MIXED>(S, U, sbuf, lane);
+        return false;
+    }
+    const int a = (int)(reinterpret_cast<uintptr_t>(U.in) & 15);
+    const int ap = a & 3;
+    const int W = S.W;
+    const int wc = S.wc[po * 4 + ap];
+    const uint32_t Dw4 = 4u * (uint32_t)S.Dw;
+    const uint4* tab = reinterpret_cast<const uint4*>(S.tab) + (po * 4 + ap) * W;
+    const uint32_t A = sbuf + (uint32_t)(a & ~3);
+    uint32_t* ow = reinterpret_cast<uint32_t*>(U.out - po);
+    Slot e[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        const int j = lane + 32 * s;
+        uint4 t = make_uint4(0, 0, 0, 0);
+        if (j < wc) t = __ldg(tab + j);
+        e[s].w = A + t.x;
+        e[s].lo = t.y;
+        e[s].hi = t.z;
+        e[s].mix = t.w;
+    }
+    const int words = (po + U.out_len + 3) >> 2;
+    const uint32_t wmax = sbuf + (uint32_t)(kBuf - 16);
+    const uint32_t hsel = po == 1 ? 0x7650u : po == 2 ? 0x7610u : 0x7210u;   // bytes [0, po) from the carry
+    uint32_t tail = 0;
+    int kw = 0;
+    uint32_t kd = 0;
+    // the step holding word 0 merges the carry into it (po > 0); windows of
+    // steps that reach past the last whole word are clamped into the buffer
+    auto last_steps = [&](int kw, uint32_t kd) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            if (32 * s >= wc) break;
+            uint32_t r = gather_word(min(e[s].w + kd, wmax), e[s]);
+            const int gw = kw + (int)(e[s].lo >> 24);
+            uint32_t cov = (e[s].lo >> 16) & 0xF;   // 0: an unused slot (lanes past wc alias word kw)
+            if (gw == 0 && po && cov) {
+                r = prmt(carry, r, hsel);
+                cov = 0xF;
+            }
+            if (gw < w_hi) {
+                if (cov == 0xF) ow[gw] = r;
+            } else if (gw == w_hi && cov) {
+                tail = r;
+            }
+        }
+    };
+    if (po) {
+        if (W <= w_hi) {
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+                if (32 * s >= wc) break;
+                uint32_t r = gather_word(e[s].w, e[s]);
+                const int gw = (int)(e[s].lo >> 24);
+                uint32_t cov = (e[s].lo >> 16) & 0xF;
+                if (gw == 0 && cov) {
+                    r = prmt(carry, r, hsel);
+                    cov = 0xF;
+                }
+                if (cov == 0xF) ow[gw] = r;
+            }
+        } else {
+            last_steps(0, 0);
+        }
+        kw = W;
+        kd = Dw4;
+    }
+    for (; kw + W <= w_hi; kw += W, kd += Dw4) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            if (32 * s >= wc) break;
+            const uint32_t r = gather_word(e[s].w + kd, e[s]);
+            if (((e[s].lo >> 16) & 0xF) == 0xF) ow[kw + (int)(e[s].lo >> 24)] = r;
+        }
+    }
+    for (; kw < words; kw += W, kd += Dw4) last_steps(kw, kd);
+    carry = __reduce_or_sync(0xffffffffu, tail_keep ? tail : 0u);
+    return tail_keep;
+}
+
 template <bool PACK, int NS, bool TMA, bool MIXED>
 __global__ void __launch_bounds__(kWarps * 32, blocks_per_sm<NS>())
 k_perm(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t limit) {
@@ -469,6 +581,8 @@ k_perm(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__
     Pipe<TMA> pipe;
     pipe.init((uint32_t)__cvta_generic_to_shared(&bars[warp][0]), lane);
     uint32_t pb = 0;
+    uint32_t carry = 0;    // pack: the previous unit's tail word (permute_pack)
+    bool have = false;
     if (PACK && NS == 1) {
         // unit metadata 32 units per batch, distributed over the lanes (one
         // round of dependent loads per 32 units instead of per unit; measured
@@ -489,7 +603,14 @@ k_perm(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__
             }
             pipe.commit();
             pipe.wait(pb ? 1 : 0, cur.flags & 1);
-            if (cur.flags & 1) permute<PACK, NS, MIXED>(specs[cur.flags >> 8], cur, sbase + pb, lane);
+            if (cur.flags & 1) {
+                if (PACK && kPackCarry) {
+                    const bool abut = (nxt.flags & 1) && nxt.out == cur.out + cur.out_len;
+                    have = permute_pack<NS, MIXED>(specs[cur.flags >> 8], cur, sbase + pb, lane, carry, have, abut);
+                } else {
+                    permute<PACK, NS, MIXED>(specs[cur.flags >> 8], cur, sbase + pb, lane);
+                }
+            }
             __syncwarp();
             if (!more) break;
             cur = nxt;
@@ -514,7 +635,14 @@ k_perm(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__
             }
             pipe.commit();
             pipe.wait(pb ? 1 : 0, cur.flags & 1);
-            if (cur.flags & 1) permute<PACK, NS, MIXED>(specs[cur.flags >> 8], cur, sbase + pb, lane);
+            if (cur.flags & 1) {
+                if (PACK && kPackCarry) {
+                    const bool abut = (nxt.flags & 1) && nxt.out == cur.out + cur.out_len;
+                    have = permute_pack<NS, MIXED>(specs[cur.flags >> 8], cur, sbase + pb, lane, carry, have, abut);
+                } else {
+                    permute<PACK, NS, MIXED>(specs[cur.flags >> 8], cur, sbase + pb, lane);
+                }
+            }
             __syncwarp();
             if (!more) break;
             cur = nxt;
