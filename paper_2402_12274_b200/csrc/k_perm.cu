@@ -550,12 +550,32 @@ __device__ __forceinline__ bool permute_pack(const PermSpec& S, const Unit& U, u
         kw = W;
         kd = Dw4;
     }
-    for (; kw + W <= w_hi; kw += W, kd += Dw4) {
+    if (NS == 1) {
+        // one slot per lane: window address and store pointer advance by a
+        // constant per step (no per-step index math)
+        if (kw + W <= w_hi) {
+            const bool act = ((e[0].lo >> 16) & 0xF) == 0xF;
+            uint32_t wa = e[0].w + kd;
+            uint32_t* p = ow + kw + (int)(e[0].lo >> 24);
+            int left = w_hi - kw;
+            do {
+                const uint32_t r = gather_word(wa, e[0]);
+                if (act) *p = r;
+                wa += Dw4;
+                p += W;
+                left -= W;
+            } while (left >= W);
+            kw = w_hi - left;
+            kd = wa - e[0].w;
+        }
+    } else {
+        for (; kw + W <= w_hi; kw += W, kd += Dw4) {
 #pragma unroll
-        for (int s = 0; s < NS; ++s) {
-            if (32 * s >= wc) break;
-            const uint32_t r = gather_word(e[s].w + kd, e[s]);
-            if (((e[s].lo >> 16) & 0xF) == 0xF) ow[kw + (int)(e[s].lo >> 24)] = r;
+            for (int s = 0; s < NS; ++s) {
+                if (32 * s >= wc) break;
+                const uint32_t r = gather_word(e[s].w + kd, e[s]);
+                if (((e[s].lo >> 16) & 0xF) == 0xF) ow[kw + (int)(e[s].lo >> 24)] = r;
+            }
         }
     }
     for (; kw < words; kw += W, kd += Dw4) last_steps(kw, kd);
