@@ -436,16 +436,37 @@ __device__ __forceinline__ void permute(const PermSpec& S, const Unit& U, uint32
         kw = W;
         kd = Dw4;
     }
-    for (; kw + W <= w_hi; kw += W, kd += Dw4) {
+    if (NS == 1 && !bytes) {
+        // one slot per lane: window address and store pointer advance by a
+        // constant per step
+        if (kw + W <= w_hi) {
+            const uint32_t cov = (e[0].lo >> 16) & 0xF;
+            uint32_t wa = e[0].w + kd;
+            uint32_t* p = ow + kw + (int)(e[0].lo >> 24);
+            int left = w_hi - kw;
+            do {
+                const uint32_t r = gather_word(wa, e[0]);
+                if (cov == 0xF) *p = r;
+                else if (!PACK && cov) store_bytes(reinterpret_cast<uint8_t*>(p), r, cov);   // layout gap
+                wa += Dw4;
+                p += W;
+                left -= W;
+            } while (left >= W);
+            kw = w_hi - left;
+            kd = wa - e[0].w;
+        }
+    } else {
+        for (; kw + W <= w_hi; kw += W, kd += Dw4) {
 #pragma unroll
-        for (int s = 0; s < NS; ++s) {
-            if (32 * s >= wc) break;
-            const uint32_t r = bytes ? gather_bytes(e[s].w + kd, e[s], 0u, 0xFFFFFFFFu)
-                                     : gather_word(e[s].w + kd, e[s]);
-            const uint32_t cov = (e[s].lo >> 16) & 0xF;
-            uint32_t* p = ow + kw + (int)(e[s].lo >> 24);
-            if (cov == 0xF) *p = r;
-            else if (!PACK && cov) store_bytes(reinterpret_cast<uint8_t*>(p), r, cov);   // layout gap
+            for (int s = 0; s < NS; ++s) {
+                if (32 * s >= wc) break;
+                const uint32_t r = bytes ? gather_bytes(e[s].w + kd, e[s], 0u, 0xFFFFFFFFu)
+                                         : gather_word(e[s].w + kd, e[s]);
+                const uint32_t cov = (e[s].lo >> 16) & 0xF;
+                uint32_t* p = ow + kw + (int)(e[s].lo >> 24);
+                if (cov == 0xF) *p = r;
+                else if (!PACK && cov) store_bytes(reinterpret_cast<uint8_t*>(p), r, cov);   // layout gap
+            }
         }
     }
     for (; kw < words; kw += W, kd += Dw4) edge(kw, kd);
