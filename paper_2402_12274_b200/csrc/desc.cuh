@@ -49,7 +49,8 @@ struct Chain {
 constexpr int kSpanMaxBody = 256;
 constexpr int kSpanMaxRuns = 32;
 constexpr int kSpanMaxBodies = 8;
-constexpr int kSpanStage = 2048;     // bytes staged per warp per buffer (plus 32 B slack)
+constexpr int kSpanStage = 3072;     // bytes staged per warp per buffer (plus 32 B slack): one
+                                      // chunk per cfg3 block (<= 64 x 40 B) -- fewer, larger units
 constexpr int kSpanMaxOuter = 2;
 
 // one element of a span chunk: its runs relative to the element's span start

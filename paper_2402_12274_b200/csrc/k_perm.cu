@@ -704,6 +704,11 @@ bool local_device_memory(const void* ptr, int device) {
     return at.type == cudaMemoryTypeDevice && at.device == device;
 }
 
+template <typename F>
+cudaError_t set_smem(F f) {
+    return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+}
+
 bool disable_tma() {
     static const bool off = getenv("MPX_NO_TMA") != nullptr;   // A/B switch
     return off;
@@ -746,6 +751,27 @@ cudaError_t launch_dir(const Plan& p, const uint8_t* src, uint8_t* dst, int64_t 
     // leaner one (no byte path compiled in)
     bool mixed = false;
     for (const int32_t u : p.perm_use[PACK ? 1 : 0]) mixed = mixed || p.perm_specs[(size_t)(u >> 6)].pad != 0;
+    // > 48 KiB of dynamic shared memory needs the opt-in, per device and kernel
+    static bool smem_set[64][4][4] = {};
+    const int dslot = p.device >= 0 && p.device < 64 ? p.device : 0;
+    const int nsi = std::min(std::max(ns, 1), 4) - 1, vi = (tma ? 1 : 0) | (mixed ? 2 : 0);
+    if (!smem_set[dslot][nsi][vi]) {
+        cudaError_t e = cudaSuccess;
+#define MPX_PERM_ATTR(N)                                                                             \
+        do {                                                                                         \
+            if (mixed) e = tma ? set_smem(k_perm<PACK, N, true, true>) : set_smem(k_perm<PACK, N, false, true>); \
+            else e = tma ? set_smem(k_perm<PACK, N, true, false>) : set_smem(k_perm<PACK, N, false, false>); \
+        } while (0)
+        switch (nsi) {
+        case 0: MPX_PERM_ATTR(1); break;
+        case 1: MPX_PERM_ATTR(2); break;
+        case 2: MPX_PERM_ATTR(3); break;
+        default: MPX_PERM_ATTR(4); break;
+        }
+#undef MPX_PERM_ATTR
+        if (e != cudaSuccess) return e;
+        smem_set[dslot][nsi][vi] = true;
+    }
 #define MPX_PERM(N)                                                                              \
     do {                                                                                         \
         if (mixed) {                                                                             \

@@ -14,6 +14,7 @@ import ctypes
 import numpy as np
 
 K_FRONT = 16
+K_STAGE = 3072                             # desc.cuh kSpanStage: bytes staged per chunk
 
 
 def dump(mp, dt, count=1):
@@ -85,7 +86,7 @@ def _chunk(spec, tab, src, in_off, in_len, in_addr, dst, out_off, out_len, out_a
     a = in_addr & 15
     ap, po = a & 3, out_addr & 3
     # staged buffer: front slack, then the 16-byte blocks holding the input
-    buf = np.full(K_FRONT + 2080 + 64, 0xEE, np.uint8)
+    buf = np.full(K_FRONT + K_STAGE + 32 + 64, 0xEE, np.uint8)
     lo = in_off - a
     nv = (a + in_len + 15) >> 4
     for k in range(16 * nv):
