@@ -80,7 +80,8 @@ __device__ __forceinline__ int first_free(int hw, F is_free, int* sh) {
 }
 
 __device__ __forceinline__ void publish(DmResult* res, int src, int tag, int64_t bytes, const uint8_t* data,
-                                        uint32_t* consumed, uint32_t cgen) {
+                                        uint32_t* consumed, uint32_t cgen, int rdv, uint8_t* dst, int64_t cap,
+                                        int copier) {
     volatile DmResult* r = res;
     r->src = src;
     r->tag = tag;
@@ -88,8 +89,43 @@ __device__ __forceinline__ void publish(DmResult* res, int src, int tag, int64_t
     r->data = data;
     r->consumed = consumed;
     r->cgen = cgen;
+    r->rdv = rdv;
+    r->dst = dst;
+    r->n = bytes < cap ? bytes : cap;
+    r->copier = copier;
+    r->copied = 0;
+    r->xdone = 0;
     __threadfence_system();
     r->ready = 1;
+}
+
+// grid-stride byte copy, 16 / 4-byte words when both sides allow
+__device__ __forceinline__ void copy_bytes(const uint8_t* src, uint8_t* dst, int64_t n, int64_t tid, int64_t nth) {
+    if (n <= 0) return;
+    const uintptr_t mis = (reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst));
+    int64_t head = 0;
+    if ((mis & 15) == 0) {
+        const int64_t nv = n >> 4;
+        const uint4* s4 = reinterpret_cast<const uint4*>(src);
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+        for (int64_t i = tid; i < nv; i += nth) d4[i] = s4[i];
+        head = nv << 4;
+    } else if ((mis & 3) == 0) {
+        const int64_t nv = n >> 2;
+        const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
+        uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
+        for (int64_t i = tid; i < nv; i += nth) d4[i] = s4[i];
+        head = nv << 2;
+    }
+    for (int64_t i = head + tid; i < n; i += nth) dst[i] = src[i];
+}
+
+// the rendezvous copy is complete: release the sender, then the receiver
+__device__ __forceinline__ void rdv_complete(volatile DmResult* r) {
+    __threadfence_system();
+    *reinterpret_cast<volatile uint32_t*>(r->consumed) = r->cgen;
+    __threadfence_system();
+    r->copied = 1;
 }
 
 struct SendArgs {
@@ -99,6 +135,8 @@ struct SendArgs {
     const uint8_t* data;
     int64_t bytes;
     uint32_t* consumed;
+    int32_t* record;      // rendezvous: the matched result slot, or -1 (sender's own box)
+    int32_t rdv, pad;
 };
 
 // a message arrives at the receiving rank's box
@@ -121,7 +159,10 @@ __global__ void __launch_bounds__(kThreads) k_dm_send(const SendArgs a) {
         if (k != kNone) {   // the earliest posted receive takes it
             if (threadIdx.x == 0) {
                 const int i = (int)(k & 0xFFF);
-                publish(&b->result[vb->recv[i].result], a.src, a.tag, a.bytes, a.data, a.consumed, a.cgen);
+                volatile DmRecv& rv = vb->recv[i];
+                publish(&b->result[rv.result], a.src, a.tag, a.bytes, a.data, a.consumed, a.cgen, a.rdv,
+                        rv.dst, rv.cap, 0);
+                if (a.record) *reinterpret_cast<volatile int32_t*>(a.record) = rv.result;
                 vb->recv[i].state = 0;
                 int h = hw;
                 while (h > 0 && vb->recv[h - 1].state == 0) --h;
@@ -142,6 +183,8 @@ __global__ void __launch_bounds__(kThreads) k_dm_send(const SendArgs a) {
                     m.bytes = a.bytes;
                     m.consumed = a.consumed;
                     m.cgen = a.cgen;
+                    m.rdv = a.rdv;
+                    if (a.record) *reinterpret_cast<volatile int32_t*>(a.record) = -1;
                     __threadfence_system();
                     m.state = 1;
                     if (f + 1 > hm) vb->hw_msg = f + 1;
@@ -166,21 +209,27 @@ struct PostArgs {
     DmBox* box;
     int32_t src, tag, ctx;   // patterns
     int32_t result;
+    uint8_t* dst;            // where a rendezvous message lands
+    int64_t cap;
+    int32_t big, pad;        // big: a k_dm_xfer follows this post
 };
 
 // a receive is posted at its stream position
 __global__ void __launch_bounds__(kThreads) k_dm_post(const PostArgs a) {
     __shared__ unsigned long long best;
-    __shared__ int slot;
+    __shared__ int slot, small_copy;
     DmBox* b = a.box;
     volatile DmBox* vb = b;
     const uint64_t t0 = now_ns();
+    if (threadIdx.x == 0) small_copy = 0;
     for (;;) {
         if (threadIdx.x == 0) {
             lock(b);
             volatile DmResult* r = &b->result[a.result];
             r->ready = 0;
             r->ndone = 0;
+            r->copied = 0;
+            r->xdone = 0;
         }
         __syncthreads();
         const int hm = vb->hw_msg;
@@ -194,7 +243,9 @@ __global__ void __launch_bounds__(kThreads) k_dm_post(const PostArgs a) {
             if (threadIdx.x == 0) {
                 const int i = (int)(k & 0xFFF);
                 volatile DmMsg& m = vb->msg[i];
-                publish(&b->result[a.result], m.src, m.tag, m.bytes, m.data, m.consumed, m.cgen);
+                publish(&b->result[a.result], m.src, m.tag, m.bytes, m.data, m.consumed, m.cgen, m.rdv, a.dst,
+                        a.cap, 1);
+                small_copy = m.rdv && !a.big;   // a receive within the eager limit copies here
                 m.state = 0;
                 int h = hm;
                 while (h > 0 && vb->msg[h - 1].state == 0) --h;
@@ -210,6 +261,8 @@ __global__ void __launch_bounds__(kThreads) k_dm_post(const PostArgs a) {
                     r.tag = a.tag;
                     r.ctx = a.ctx;
                     r.result = a.result;
+                    r.dst = a.dst;
+                    r.cap = a.cap;
                     r.seq = vb->next_seq;
                     vb->next_seq = vb->next_seq + 1;
                     __threadfence_system();
@@ -227,8 +280,34 @@ __global__ void __launch_bounds__(kThreads) k_dm_post(const PostArgs a) {
             slot = done ? 1 : 0;
         }
         __syncthreads();
-        if (slot) return;
+        if (slot) break;
         __nanosleep(1000);
+    }
+    if (small_copy) {   // rendezvous message into a receive of <= eager-limit bytes
+        volatile DmResult* r = &b->result[a.result];
+        copy_bytes((const uint8_t*)r->data, (uint8_t*)r->dst, r->n, threadIdx.x, blockDim.x);
+        __syncthreads();
+        if (threadIdx.x == 0) rdv_complete(r);
+    }
+}
+
+// the rendezvous copy of the side that matched second: after k_dm_send on
+// the sender's stream (record: the slot the send matched, or -1) or after a
+// big receive's k_dm_post on the receiver's stream (record == nullptr: the
+// post's own slot `res`)
+__global__ void __launch_bounds__(kThreads) k_dm_xfer(DmBox* b, int res, const int32_t* record) {
+    const int side = record ? 0 : 1;
+    if (record) res = *reinterpret_cast<const volatile int32_t*>(record);
+    if (res < 0) return;
+    volatile DmResult* r = &b->result[res];
+    if (!r->ready || !r->rdv || r->copier != side) return;
+    __threadfence_system();
+    copy_bytes((const uint8_t*)r->data, (uint8_t*)r->dst, r->n, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+               (int64_t)gridDim.x * blockDim.x);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        if (atomicAdd((unsigned*)&b->result[res].xdone, 1u) == gridDim.x - 1) rdv_complete(r);
     }
 }
 
@@ -251,6 +330,11 @@ __global__ void __launch_bounds__(32) k_dm_wait(DmBox* b, int res, DmStatus* st,
         __nanosleep(ns);
         ns = ns < 1024 ? 2 * ns : ns;
     }
+    if (r->rdv)   // rendezvous: the side that matched second is copying
+        while (r->copied == 0) {
+            __nanosleep(ns);
+            ns = ns < 1024 ? 2 * ns : ns;
+        }
     __threadfence_system();
     volatile DmStatus* s = st;
     s->src = r->src;
@@ -265,33 +349,15 @@ __global__ void __launch_bounds__(kThreads) k_dm_copy(DmBox* b, int res, uint8_t
                                                       DmStatus* st) {
     volatile DmResult* r = &b->result[res];
     const bool ok = r->ready != 0;
+    const bool rdv = ok && r->rdv;   // already copied at match time (k_dm_wait saw it complete)
     const uint8_t* src = ok ? (const uint8_t*)r->data : nullptr;
-    const int64_t n = ok ? (r->bytes < cap ? r->bytes : cap) : 0;
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    if (n > 0) {
-        const uintptr_t mis = (reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst));
-        int64_t head = 0;
-        if ((mis & 15) == 0) {
-            const int64_t nv = n >> 4;
-            const uint4* s4 = reinterpret_cast<const uint4*>(src);
-            uint4* d4 = reinterpret_cast<uint4*>(dst);
-            for (int64_t i = tid; i < nv; i += nth) d4[i] = s4[i];
-            head = nv << 4;
-        } else if ((mis & 3) == 0) {
-            const int64_t nv = n >> 2;
-            const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
-            uint32_t* d4 = reinterpret_cast<uint32_t*>(dst);
-            for (int64_t i = tid; i < nv; i += nth) d4[i] = s4[i];
-            head = nv << 2;
-        }
-        for (int64_t i = head + tid; i < n; i += nth) dst[i] = src[i];
-    }
+    const int64_t n = ok && !rdv ? (r->bytes < cap ? r->bytes : cap) : 0;
+    copy_bytes(src, dst, n, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence_system();
         if (atomicAdd((unsigned*)&b->result[res].ndone, 1u) == gridDim.x - 1) {
-            if (ok) {
+            if (ok && !rdv) {
                 uint32_t* c = r->consumed;
                 *reinterpret_cast<volatile uint32_t*>(c) = r->cgen;
             }
@@ -303,16 +369,34 @@ __global__ void __launch_bounds__(kThreads) k_dm_copy(DmBox* b, int res, uint8_t
 
 }  // namespace
 
+namespace {
+unsigned xfer_grid(int64_t bytes, int device) {
+    const int64_t want = (bytes + (int64_t)kThreads * 64 - 1) / ((int64_t)kThreads * 64);
+    const int64_t cap = (int64_t)sm_count(device) * 4;
+    return (unsigned)(want < 1 ? 1 : want > cap ? cap : want);
+}
+}  // namespace
+
 cudaError_t dm_send(DmBox* box, int src, int tag, int ctx, const uint8_t* data, int64_t bytes, uint32_t* consumed,
                     uint32_t cgen, cudaStream_t stream) {
-    SendArgs a{box, src, tag, ctx, cgen, data, bytes, consumed};
+    SendArgs a{box, src, tag, ctx, cgen, data, bytes, consumed, nullptr, 0, 0};
     k_dm_send<<<1, kThreads, 0, stream>>>(a);
     return cudaGetLastError();
 }
 
-cudaError_t dm_post(DmBox* box, int src, int tag, int ctx, int result, cudaStream_t stream) {
-    PostArgs a{box, src, tag, ctx, result};
+cudaError_t dm_send_rdv(DmBox* box, int src, int tag, int ctx, const uint8_t* data, int64_t bytes,
+                        uint32_t* consumed, uint32_t cgen, int32_t* record, int device, cudaStream_t stream) {
+    SendArgs a{box, src, tag, ctx, cgen, data, bytes, consumed, record, 1, 0};
+    k_dm_send<<<1, kThreads, 0, stream>>>(a);
+    k_dm_xfer<<<xfer_grid(bytes, device), kThreads, 0, stream>>>(box, -1, record);
+    return cudaGetLastError();
+}
+
+cudaError_t dm_post(DmBox* box, int src, int tag, int ctx, int result, uint8_t* dst, int64_t cap, bool big,
+                    int device, cudaStream_t stream) {
+    PostArgs a{box, src, tag, ctx, result, dst, cap, big ? 1 : 0, 0};
     k_dm_post<<<1, kThreads, 0, stream>>>(a);
+    if (big) k_dm_xfer<<<xfer_grid(cap, device), kThreads, 0, stream>>>(box, result, nullptr);
     return cudaGetLastError();
 }
 
@@ -336,6 +420,7 @@ cudaError_t preload_dm_kernels() {
     if ((r = cudaFuncGetAttributes(&a, k_dm_post)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_dm_wait)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_dm_copy)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_dm_xfer)) != cudaSuccess) e = r;
     return e;
 }
 

@@ -31,11 +31,30 @@
 //              bounce buffer; its last CTA marks the bounce buffer consumed
 //              (the sender's host frees it lazily) and the status done.
 //
-// Every message is buffered (packed into a bounce buffer at the sender's
-// stream position), so a blocking send never waits for its receiver: rings of
-// blocking sends are safe at every size (the reference guarantees it up to
-// its eager limit).  A nonblocking receive is posted at its stream position
-// and moves data at its wait, so nothing ever blocks a stream between the two.
+// Eager messages (<= the eager limit, every blocking send, typed send
+// layouts) are buffered: packed into a bounce buffer at the sender's stream
+// position, so a blocking send never waits for its receiver (rings of
+// blocking sends are safe at every size; the reference guarantees it up to
+// its eager limit), and copied out at the receiver's wait.
+//
+// Rendezvous (a nonblocking send of a contiguous layout above the eager
+// limit): no bounce buffer -- the message announces the sender's own buffer,
+// and the data moves ONCE, at match time, on the stream of whichever side
+// matched second (transport.py's RTS/CTS pull, :355-375 / :548-602):
+//
+//   k_dm_xfer  after k_dm_send (sender's stream): copies into the posted
+//              receive's destination if the send matched one;
+//              after k_dm_post of a receive larger than the eager limit
+//              (receiver's stream): copies if the post matched a waiting
+//              rendezvous message (a smaller receive's k_dm_post copies the
+//              <= eager-limit prefix itself);
+//
+// then marks the result copied and writes the send's completion flag, which
+// the send's wait_enqueue waits for (cuStreamWaitValue32).  Copies never wait
+// for a wait_enqueue, so `irecv; isend; wait(send); wait(recv)` on every
+// rank cannot deadlock.  A typed receive's destination is a landing buffer
+// allocated and pre-filled with the layout's bytes at post time, unpacked
+// at the wait.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -51,10 +70,11 @@ struct DmMsg {            // an unexpected message
     int32_t state;        // 0 free, 1 queued
     int32_t src, tag, ctx;
     int64_t seq;
-    const uint8_t* data;  // bounce buffer (sender's device)
+    const uint8_t* data;  // bounce buffer, or the sender's buffer (rendezvous)
     int64_t bytes;
     uint32_t* consumed;   // pinned host word: set to cgen once the bytes are copied out
-    uint32_t cgen, pad;
+    uint32_t cgen;
+    int32_t rdv;          // 1: rendezvous (copied at match time)
 };
 
 struct DmRecv {           // a posted receive
@@ -62,6 +82,8 @@ struct DmRecv {           // a posted receive
     int32_t src, tag, ctx;    // patterns
     int64_t seq;
     int32_t result, pad;
+    uint8_t* dst;             // where a rendezvous message lands (buffer or landing)
+    int64_t cap;
 };
 
 struct DmResult {         // a receive's match, written by whichever side matched
@@ -71,7 +93,14 @@ struct DmResult {         // a receive's match, written by whichever side matche
     int64_t bytes;
     const uint8_t* data;
     uint32_t* consumed;
-    uint32_t cgen, pad;
+    uint32_t cgen;
+    int32_t rdv;          // rendezvous: the copy happens at match time ...
+    uint8_t* dst;         // ... into dst (n = min(bytes, cap) bytes)
+    int64_t n;
+    int32_t copier;       // 0: the sender's k_dm_xfer, 1: the receiver's (k_dm_xfer or k_dm_post)
+    int32_t copied;       // 1 once the rendezvous copy is complete
+    uint32_t xdone;       // k_dm_xfer CTAs finished
+    uint32_t pad2;
 };
 
 struct DmStatus {         // pinned host memory, one per result slot
@@ -81,6 +110,8 @@ struct DmStatus {         // pinned host memory, one per result slot
     int64_t pad;
 };
 
+constexpr int kDmRecords = 1 << 14;   // per sending rank: match records of rendezvous sends (ring)
+
 struct DmBox {
     int32_t lock;
     int32_t hw_msg, hw_recv;  // entries at or above the high-water marks are free
@@ -89,12 +120,20 @@ struct DmBox {
     DmMsg msg[kDmSlots];
     DmRecv recv[kDmSlots];
     DmResult result[kDmResults];
+    int32_t srec[kDmRecords];   // sends FROM this box's rank: the result slot a rendezvous send matched (-1: none)
 };
 
 // launchers (dmatch.cu); `box` is the receiving rank's box
 cudaError_t dm_send(DmBox* box, int src, int tag, int ctx, const uint8_t* data, int64_t bytes, uint32_t* consumed,
                     uint32_t cgen, cudaStream_t stream);
-cudaError_t dm_post(DmBox* box, int src, int tag, int ctx, int result, cudaStream_t stream);
+// rendezvous send: `data` is the sender's buffer; the match is recorded in
+// *record (in the sender's own box) and k_dm_xfer copies right behind it
+cudaError_t dm_send_rdv(DmBox* box, int src, int tag, int ctx, const uint8_t* data, int64_t bytes,
+                        uint32_t* consumed, uint32_t cgen, int32_t* record, int device, cudaStream_t stream);
+// `dst` / `cap`: where a rendezvous message lands; big: a k_dm_xfer follows
+// the post (cap above the eager limit), else k_dm_post copies itself
+cudaError_t dm_post(DmBox* box, int src, int tag, int ctx, int result, uint8_t* dst, int64_t cap, bool big,
+                    int device, cudaStream_t stream);
 cudaError_t dm_wait(DmBox* box, int result, DmStatus* status, int64_t cap, cudaStream_t stream);
 cudaError_t dm_copy(DmBox* box, int result, uint8_t* dst, int64_t cap, DmStatus* status, int device,
                     cudaStream_t stream);

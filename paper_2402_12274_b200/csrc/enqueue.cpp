@@ -521,6 +521,7 @@ struct World {
     std::vector<DmBox*> dm_box;               // per rank, in that rank's device memory
     std::vector<DmStatus*> dm_status;         // per rank, kDmResults, pinned host memory
     std::vector<uint32_t> dm_next;            // per rank: next result slot
+    std::vector<uint32_t> dm_rec_next;        // per rank: next rendezvous match record (DmBox::srec)
     std::vector<std::vector<std::weak_ptr<Comm>>> dm_owner;   // blocking receive of a slot, to check for truncation
     int64_t eager_limit = 65536;
     std::vector<int> devices;
@@ -1361,9 +1362,12 @@ int dm_reclaim(const std::shared_ptr<Comm>& c) {
     return MPX_SUCCESS;
 }
 
-// Every message is packed into a bounce buffer at the sender's stream
+// Eager: the message is packed into a bounce buffer at the sender's stream
 // position, then announced to the receiver's box (k_dm_send): the send is
-// complete at that point, blocking or not.
+// complete at that point, blocking or not.  Rendezvous (nonblocking,
+// contiguous, above the eager limit): the sender's own buffer is announced
+// and copied once by the side that matches second (k_dm_xfer); the send's
+// wait_enqueue waits for the copy's completion flag.
 int dm_send_op(const std::shared_ptr<Comm>& c, const void* buf, int64_t count, Datatype* dt, int dest, int tag,
                bool blocking, std::shared_ptr<ReqState>* out_req) {
     World* w = c->w;
@@ -1372,6 +1376,36 @@ int dm_send_op(const std::shared_ptr<Comm>& c, const void* buf, int64_t count, D
     MPX_RC(set_device(c->device));
     MPX_RC(dm_reclaim(c));
     const int64_t bytes = dt->size * count;
+    int64_t off = 0;
+    if (!blocking && bytes > w->eager_limit && dest != c->rank && contiguous_run(dt, count, &off)) {
+        DmBox* own = nullptr;
+        MPX_RC(dm_box_of(w, c->rank, &own));
+        uint32_t idx = 0;
+        {
+            std::lock_guard<std::mutex> g(w->dm_mu);
+            idx = w->dm_rec_next[(size_t)c->rank]++ % (uint32_t)kDmRecords;
+        }
+        uint32_t* flag = nullptr;
+        uint32_t gen = 0;
+        w->flags.take(&flag, &gen);
+        MPX_RC(set_device(c->device));
+        {
+            ProfScope pl(P_LAUNCH);
+            MPX_CU(dm_send_rdv(box, c->rank, tag, c->ctx, static_cast<const uint8_t*>(buf) + off, bytes, flag, gen,
+                               &own->srec[idx], c->device, c->stream));
+        }
+        MPX_TRACE("dm send r%d -> %d tag %d %lld B (rendezvous)", c->rank, dest, tag, (long long)bytes);
+        auto req = std::make_shared<ReqState>();
+        req->comm = c;
+        req->is_send = true;
+        req->matched = true;
+        req->flag = flag;      // wait_enqueue: the stream waits for the copy
+        req->gen = gen;
+        req->needs_wait = true;
+        c->outstanding++;
+        if (out_req) *out_req = req;
+        return MPX_SUCCESS;
+    }
     void* bounce = nullptr;
     MPX_RC(staging_alloc(c->device, (size_t)bytes, c->stream, &bounce));
     if (bytes > 0) {
@@ -1424,24 +1458,30 @@ int dm_recv_op(const std::shared_ptr<Comm>& c, void* buf, int64_t count, Datatyp
     MPX_RC(dm_take_slot(w, c->rank, &slot));
     DmStatus* st = &w->dm_status[(size_t)c->rank][slot];
     MPX_RC(set_device(c->device));
+    const int dev = c->device;
+    // a typed receive lands in a buffer holding the layout's current bytes
+    // (a short message leaves the rest of the layout as it was), prepared at
+    // the post: a rendezvous message may be copied in at match time
+    void* landing = nullptr;
+    if (!contig) {
+        MPX_RC(staging_alloc(dev, (size_t)cap, c->stream, &landing));
+        if (cap > 0) MPX_RC(launch_move(dev, dt, count, true, buf, landing, cap, c->stream));
+        MPX_RC(set_device(dev));
+    }
+    uint8_t* land = contig ? static_cast<uint8_t*>(buf) + off : static_cast<uint8_t*>(landing);
     {
         ProfScope pl(P_LAUNCH);
-        MPX_CU(dm_post(box, source, tag, c->ctx, slot, c->stream));
+        MPX_CU(dm_post(box, source, tag, c->ctx, slot, land, cap, cap > w->eager_limit, dev, c->stream));
     }
-    const int dev = c->device;
-    auto deliver = [dev, box, slot, st, cap, contig, off, dt, count, buf](cudaStream_t ws) -> int {
+    auto deliver = [dev, box, slot, st, cap, contig, dt, count, buf, land, landing](cudaStream_t ws) -> int {
         MPX_RC(set_device(dev));
         ProfScope pl(P_LAUNCH);
         MPX_CU(dm_wait(box, slot, st, cap, ws));
         if (contig) {
-            MPX_CU(dm_copy(box, slot, static_cast<uint8_t*>(buf) + off, cap, st, dev, ws));
+            MPX_CU(dm_copy(box, slot, land, cap, st, dev, ws));
             return MPX_SUCCESS;
         }
-        void* landing = nullptr;
-        MPX_RC(staging_alloc(dev, (size_t)cap, ws, &landing));
-        if (cap > 0) MPX_RC(launch_move(dev, dt, count, true, buf, landing, cap, ws));
-        MPX_RC(set_device(dev));
-        MPX_CU(dm_copy(box, slot, static_cast<uint8_t*>(landing), cap, st, dev, ws));
+        MPX_CU(dm_copy(box, slot, land, cap, st, dev, ws));
         if (cap > 0) MPX_RC(launch_move(dev, dt, count, false, landing, buf, cap, ws));
         MPX_RC(set_device(dev));
         MPX_CU(cudaFreeAsync(landing, ws));
@@ -2041,6 +2081,7 @@ int mpx_world_set_matching(mpx_world h, int device_side) {
             w->dm_box.assign((size_t)w->size, nullptr);
             w->dm_status.assign((size_t)w->size, nullptr);
             w->dm_next.assign((size_t)w->size, 0);
+            w->dm_rec_next.assign((size_t)w->size, 0);
             w->dm_owner.assign((size_t)w->size, std::vector<std::weak_ptr<Comm>>((size_t)kDmResults));
         }
         w->dm_mode = device_side;

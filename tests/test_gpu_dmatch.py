@@ -180,3 +180,156 @@ def test_ranks_must_agree_on_the_matching_mode():
     for t in ts:
         t.join(120)
     assert "disagree" in out.get("err", "") and out.get(0) == out.get(1) == "device"
+
+
+# ---- rendezvous (nonblocking contiguous sends above the eager limit) --------
+
+def _comm(inst):
+    q = mp.queue_create(inst)
+    c, s = device_comm(inst, q)
+    return q, c, s
+
+
+def _close(q, c, s):
+    mp.comm_free(c)
+    mp.free_stream(s)
+    mp.queue_destroy(q)
+
+
+@pytest.mark.parametrize("n", [2, 4])
+@pytest.mark.parametrize("nbytes", [(1 << 16) + 4, 4 << 20])
+@pytest.mark.parametrize("order", ["recv_first", "send_first"])
+def test_rendezvous_wait_send_before_recv(n, nbytes, order):
+    """every rank: irecv, isend, wait(send), wait(recv) (or isend first) with
+    distinct payloads per rank and iteration.  The data moves at match time
+    on the stream of the side that matched second, so a send's completion
+    never depends on the receiver's wait: no cycle, whatever the order."""
+    got = {}
+
+    def body(inst):
+        r = inst.rank
+        q, c, s = _comm(inst)
+        ok = True
+        for it in range(3):
+            src = torch.full((nbytes,), (r * 7 + it) % 251, dtype=torch.uint8, device=inst.device)
+            dst = torch.zeros(nbytes, dtype=torch.uint8, device=inst.device)
+            if order == "recv_first":
+                rr = mp.irecv_enqueue(c, dst, nbytes, mp.BYTE, (r - 1) % n, it)
+                sr = mp.isend_enqueue(c, src, nbytes, mp.BYTE, (r + 1) % n, it)
+            else:
+                sr = mp.isend_enqueue(c, src, nbytes, mp.BYTE, (r + 1) % n, it)
+                rr = mp.irecv_enqueue(c, dst, nbytes, mp.BYTE, (r - 1) % n, it)
+            mp.wait_enqueue(sr)
+            mp.wait_enqueue(rr)
+            mp.queue_synchronize(q)
+            want = ((r - 1) % n * 7 + it) % 251
+            ok = ok and bool((dst == want).all()) and rr.status.count == nbytes and rr.status.source == (r - 1) % n
+        got[r] = ok
+        _close(q, c, s)
+
+    host([body] * n)
+    assert all(got[r] for r in range(n)), got
+
+
+@pytest.mark.parametrize("cap", [1 << 12, 1 << 20])
+def test_rendezvous_truncation_both_copy_sides(cap):
+    """a 2 MiB rendezvous message into a smaller receive: the prefix lands
+    (copied by k_dm_post itself for a receive within the eager limit, by the
+    receiver's k_dm_xfer above it, or by the sender's k_dm_xfer when the
+    receive was posted first), the status reports ERR_TRUNCATE, the sender
+    completes."""
+    nbytes = 2 << 20
+    for first in ("recv", "send"):
+        got = {}
+
+        def rank0(inst):
+            q, c, s = _comm(inst)
+            src = torch.arange(nbytes, dtype=torch.int64, device=inst.device).to(torch.uint8)
+            if first == "recv":
+                with torch.cuda.stream(q.torch_stream):
+                    torch.cuda._sleep(2000000)   # the receive is posted first
+            sr = mp.isend_enqueue(c, src, nbytes, mp.BYTE, 1, 9)
+            mp.wait_enqueue(sr)
+            mp.queue_synchronize(q)
+            got["sent"] = True
+            _close(q, c, s)
+
+        def rank1(inst):
+            q, c, s = _comm(inst)
+            if first == "send":
+                with torch.cuda.stream(q.torch_stream):
+                    torch.cuda._sleep(2000000)   # the message arrives first
+            dst = torch.full((cap + 64,), 0xAB, dtype=torch.uint8, device=inst.device)
+            rr = mp.irecv_enqueue(c, dst, cap, mp.BYTE, 0, 9)
+            mp.wait_enqueue(rr)
+            mp.queue_synchronize(q)
+            h = dst.cpu()
+            got["prefix"] = bool((h[:cap] == torch.arange(cap, dtype=torch.int64).to(torch.uint8)).all())
+            got["rest"] = bool((h[cap:] == 0xAB).all())
+            got["err"] = rr.status.error
+            _close(q, c, s)
+
+        pair(rank0, rank1)
+        assert got["sent"] and got["prefix"] and got["rest"], (first, got)
+        assert got["err"] == "ERR_TRUNCATE", (first, got)
+
+
+def test_rendezvous_into_typed_receive():
+    """a contiguous rendezvous message into a vector receive lands in the
+    landing buffer prepared at the post and is unpacked at the wait."""
+    n_el = 1 << 16                                    # 64 Ki doubles = 512 KiB payload
+    got = {}
+
+    def rank0(inst):
+        q, c, s = _comm(inst)
+        src = torch.arange(n_el, dtype=torch.float64, device=inst.device)
+        sr = mp.isend_enqueue(c, src, n_el, mp.FLOAT64, 1, 2)
+        mp.wait_enqueue(sr)
+        mp.queue_synchronize(q)
+        _close(q, c, s)
+
+    def rank1(inst):
+        q, c, s = _comm(inst)
+        vt = mp.type_vector(n_el // 4, 4, 8, mp.FLOAT64).commit()
+        dst = torch.full((2 * n_el,), -1.0, dtype=torch.float64, device=inst.device)
+        rr = mp.irecv_enqueue(c, dst, 1, vt, 0, 2)
+        mp.wait_enqueue(rr)
+        mp.queue_synchronize(q)
+        exp = torch.full((2 * n_el,), -1.0, dtype=torch.float64)
+        exp.view(-1, 8)[:, :4] = torch.arange(n_el, dtype=torch.float64).view(-1, 4)
+        got["ok"] = bool(torch.equal(dst.cpu(), exp))
+        got["count"] = rr.status.count
+        mp.type_free(vt)
+        _close(q, c, s)
+
+    pair(rank0, rank1)
+    assert got["ok"] and got["count"] == 1
+
+
+@pytest.mark.parametrize("n", [3, 5])
+def test_rendezvous_any_source_takes_every_sender_once(n):
+    """large isends from n-1 ranks into ANY_SOURCE receives of rank 0."""
+    nbytes = 1 << 20
+    got = {}
+
+    def body(inst):
+        r = inst.rank
+        q, c, s = _comm(inst)
+        if r == 0:
+            bufs = [torch.zeros(nbytes, dtype=torch.uint8, device=inst.device) for _ in range(n - 1)]
+            reqs = [mp.irecv_enqueue(c, b, nbytes, mp.BYTE, mp.ANY_SOURCE, 7) for b in bufs]
+            mp.waitall_enqueue(reqs)
+            mp.queue_synchronize(q)
+            got["src"] = [rq.status.source for rq in reqs]
+            got["data"] = [int(b[0].item()) for b in bufs]
+            got["same"] = all(bool((b == b[0]).all()) for b in bufs)
+        else:
+            sr = mp.isend_enqueue(c, torch.full((nbytes,), r, dtype=torch.uint8, device=inst.device), nbytes,
+                                  mp.BYTE, 0, 7)
+            mp.wait_enqueue(sr)
+            mp.queue_synchronize(q)
+        _close(q, c, s)
+
+    host([body] * n)
+    assert sorted(got["src"]) == list(range(1, n))
+    assert got["data"] == got["src"] and got["same"]
