@@ -49,7 +49,10 @@ struct Chain {
 constexpr int kSpanMaxBody = 256;
 constexpr int kSpanMaxRuns = 32;
 constexpr int kSpanMaxBodies = 8;
-constexpr int kSpanStage = 3072;     // bytes staged per warp per buffer (plus 32 B slack): one
+#ifndef MPX_SPAN_STAGE
+#define MPX_SPAN_STAGE 3072
+#endif
+constexpr int kSpanStage = MPX_SPAN_STAGE;     // bytes staged per warp per buffer (plus 32 B slack): one
                                       // chunk per cfg3 block (<= 64 x 40 B) -- fewer, larger units
 constexpr int kSpanMaxOuter = 2;
 
