@@ -746,7 +746,8 @@ cudaError_t launch_dir(const Plan& p, const uint8_t* src, uint8_t* dst, int64_t 
     // (peer and pinned-host buffers keep cp.async).  Measured (ncu, cfg3):
     // pack 290 us with TMA vs 299 us with cp.async; unpack -- small packed
     // chunks -- 433 vs 402-415 us, so unpack stays on cp.async.
-    const bool tma = PACK && local_device_memory(src, p.device) && !disable_tma();
+    static const bool unpack_tma = getenv("MPX_UNPACK_TMA") != nullptr;   // A/B switch
+    const bool tma = (PACK || unpack_tma) && local_device_memory(src, p.device) && !disable_tma();
     // byte-form specs need the mixed kernel; word-window-only plans get the
     // leaner one (no byte path compiled in)
     bool mixed = false;
