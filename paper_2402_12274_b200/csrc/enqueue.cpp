@@ -2449,7 +2449,7 @@ int mpx_allreduce_enqueue(mpx_comm h, const void* sendbuf, void* recvbuf, int64_
     if (algo == 2) {
         if (!distinct) return fail(MPX_ERR_UNSUPPORTED, "NCCL allreduce needs one device per rank");
         if (!nccl_available()) return fail(MPX_ERR_UNSUPPORTED, "libnccl.so.2 not available");
-        ncclComm_t nc;
+        ncclComm_t nc = nullptr;
         MPX_RC(w->ipc ? nccl_comm_ipc(c, &nc) : nccl_comm_for(c, &nc));
         MPX_RC(set_device(c->device));
         ncclResult_t r = g_nccl.allReduce(sendbuf, recvbuf, (size_t)count, nccl_type(dtype_code), ncclSum, nc,
