@@ -624,7 +624,10 @@ k_perm(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__
     uint32_t pb = 0;
     uint32_t carry = 0;    // pack: the previous unit's tail word (permute_pack)
     bool have = false;
-    if (PACK && NS == 1) {
+#ifndef MPX_UNPACK_BATCH
+#define MPX_UNPACK_BATCH 0
+#endif
+    if (NS == 1 && (PACK || MPX_UNPACK_BATCH)) {
         // unit metadata 32 units per batch, distributed over the lanes (one
         // round of dependent loads per 32 units instead of per unit; measured
         // faster for pack, slower for unpack)
@@ -641,6 +644,7 @@ k_perm(const SpanPlan sp, const uint8_t* __restrict__ src, uint8_t* __restrict__
                 if (i == 0) batch = load_batch<PACK>(sp, u + 1, u1, src, dst, limit, lane);
                 nxt = bcast(batch, i);
                 if (nxt.flags & 1) pipe.issue(sbase + (pb ^ kSlot), pb ? 0 : 1, nxt, lane);
+                if (!PACK && (nxt.flags & 1)) prefetch_out(nxt, lane);
             }
             pipe.commit();
             pipe.wait(pb ? 1 : 0, cur.flags & 1);
