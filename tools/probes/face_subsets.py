@@ -32,7 +32,8 @@ for name, sub in subsets.items():
     outs = [torch.empty(mp.packed_size(d), dtype=torch.uint8, device=dev) for d in ds]
     tp, tu = [], []
     for it in range(12):
-        flush.zero_()
+        flush.zero_()                 # evict, then read so no dirty flush line is written back in the timing
+        flush.sum(dtype=torch.int64)
         torch.cuda._sleep(200000)
         a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         a.record()
