@@ -27,6 +27,27 @@ __global__ void gather(const float* __restrict__ a, float* __restrict__ out, int
     }
 }
 
+// row order experiments: ORD 0 = consecutive threads on consecutive y rows
+// (2056 B apart); 1 = consecutive threads on consecutive z planes (1 MiB
+// apart); 2 = a warp covers 8 y rows x 4 z planes (packed side still whole
+// 32-byte sectors)
+template <int ORD>
+__global__ void gather_ord(const float* __restrict__ a, float* __restrict__ out, int rows) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x, n = gridDim.x * blockDim.x;
+    for (int r = t; r < rows; r += n) {
+        int z, y;
+        if (ORD == 0) { z = r / 512; y = r % 512; }
+        else if (ORD == 1) { z = r % 512; y = r / 512; }
+        else {   // r = ((zb * 64 + yb) * 4 + zi) * 8 + yi
+            const int yi = r & 7, zi = (r >> 3) & 3, yb = (r >> 5) & 63, zb = r >> 11;
+            z = zb * 4 + zi;
+            y = yb * 8 + yi;
+        }
+        const long long i = (long long)z * (514 * 514) + (long long)y * 514;
+        out[z * 512 + y] = __ldcg(a + i + 514 * 514 + 514 + 1);
+    }
+}
+
 __global__ void scatter(float* __restrict__ a, const float* __restrict__ in, int rows, int step) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x, n = gridDim.x * blockDim.x;
     for (int r = t; r < rows; r += n) {
@@ -74,6 +95,15 @@ int main() {
         gather<4><<<1024, 256>>>(a, out + rows, rows, 511);
     });
     time("scatter grid=1024", [&] { scatter<<<1024, 256>>>(a, out, rows, 0); });
+    for (int blocks : {1024, 4096}) {
+        char nm[64];
+        snprintf(nm, 64, "order 0 (y-consecutive) grid=%d", blocks);
+        time(nm, [&] { gather_ord<0><<<blocks, 256>>>(a, out, rows); });
+        snprintf(nm, 64, "order 1 (z-consecutive) grid=%d", blocks);
+        time(nm, [&] { gather_ord<1><<<blocks, 256>>>(a, out, rows); });
+        snprintf(nm, 64, "order 2 (8y x 4z tiles) grid=%d", blocks);
+        time(nm, [&] { gather_ord<2><<<blocks, 256>>>(a, out, rows); });
+    }
     time("empty launch after flush", [&] { gather<1><<<1, 32>>>(a, out, 0, 0); });
     {
         float best = 1e9;
