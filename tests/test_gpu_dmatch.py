@@ -1,8 +1,8 @@
 """Device-resident matching (csrc/dmatch.hpp): the enqueue
 path's matching and point-to-point tests re-run with every world joined
 with matching="device" (MINIMPI_MATCHING=device), plus the cases that only
-device matching has: blocking rings beyond the eager limit (every message is
-buffered), ANY_SOURCE races between senders resolved on the GPU, short
+device matching has: blocking rings beyond the eager limit (every blocking
+send is buffered), rendezvous copies at match time, ANY_SOURCE races between senders resolved on the GPU, short
 messages into typed receives, truncation reported from the device status.
 
 Mirrors /root/reference/pkg/tests/test_offload.py:41-210 and test_p2p.py
@@ -41,7 +41,7 @@ def test_mode_is_device(inst):
 @pytest.mark.parametrize("nbytes", [1 << 20, 16 << 20])
 def test_blocking_ring_beyond_eager_limit(n, nbytes):
     """send-then-recv rings of blocking calls far above the eager limit: with
-    every message buffered at the sender no rank ever waits for its receiver
+    every blocking send buffered at the sender no rank ever waits for its receiver
     (the reference guarantees this only up to its eager limit)."""
     _ring(n, nbytes, "u8", blocking=True)
     _ring(n, nbytes, "vector", blocking=True)
