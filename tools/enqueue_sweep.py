@@ -3,7 +3,7 @@
 vector(N/32,4,8) f64 datatype with the dependent scale kernels) and
 allreduce_enqueue (f32, i64) over in-process ranks, sizes 8 B .. 256 MiB.
 With one GPU every rank shares it: the "link" is HBM, not NVLink.
-Writes one JSON object (gpurun_out/enqueue_sweep_r01.json)."""
+Writes one JSON object (gpurun_out/enqueue_sweep_<tag>.json, tag = argv[1], default r02)."""
 import json
 import os
 import sys
@@ -35,7 +35,8 @@ def main():
             r = eb.allreduce(n, nb // 4, iters=it, warmup=2, algo="native", group="sa-%d-%d" % (n, lg))
             out["allreduce"].append({k: r[k] for k in ("ranks", "bytes", "algo", "ms_per_iter", "busbw_GBps", "correct")})
             print(json.dumps(out["allreduce"][-1]), flush=True)
-    path = os.path.join(ROOT, "gpurun_out", "enqueue_sweep_r01.json")
+    tag = sys.argv[1] if len(sys.argv) > 1 else "r02"
+    path = os.path.join(ROOT, "gpurun_out", "enqueue_sweep_%s.json" % tag)
     os.makedirs(os.path.dirname(path), exist_ok=True)
     with open(path, "w") as f:
         json.dump(out, f, indent=1)
