@@ -11,6 +11,7 @@
 
 #include <climits>
 #include <cstdint>
+#include <cstring>
 
 #include "dmatch.hpp"
 #include "kernels.hpp"
@@ -21,6 +22,13 @@ namespace mpx {
 namespace {
 
 constexpr int kThreads = 256;
+
+template <int W> struct DVec;
+template <> struct DVec<16> { using T = uint4; };
+template <> struct DVec<8> { using T = uint2; };
+template <> struct DVec<4> { using T = uint32_t; };
+template <> struct DVec<2> { using T = uint16_t; };
+template <> struct DVec<1> { using T = uint8_t; };
 constexpr unsigned long long kNone = ~0ull;
 constexpr uint64_t kGiveUpNs = 20ull * 1000000000ull;   // a full queue for 20 s: report and drop
 
@@ -79,29 +87,56 @@ __device__ __forceinline__ int first_free(int hw, F is_free, int* sh) {
     return r == INT_MAX ? -1 : r;
 }
 
-__device__ __forceinline__ void publish(DmResult* res, int src, int tag, int64_t bytes, const uint8_t* data,
-                                        uint32_t* consumed, uint32_t cgen, int rdv, uint8_t* dst, int64_t cap,
-                                        int copier) {
-    volatile DmResult* r = res;
-    r->src = src;
-    r->tag = tag;
-    r->bytes = bytes;
-    r->data = data;
-    r->consumed = consumed;
-    r->cgen = cgen;
-    r->rdv = rdv;
-    r->dst = dst;
-    r->n = bytes < cap ? bytes : cap;
-    r->copier = copier;
-    r->copied = 0;
-    r->xdone = 0;
-    __threadfence_system();
-    r->ready = 1;
+// 8-byte word copies of the plain-old-data box records (volatile: another
+// rank's kernel may read them over NVLink)
+template <typename T>
+__device__ __forceinline__ void vput(volatile T* dst, const T& src) {
+    static_assert(sizeof(T) % 8 == 0, "8-byte words");
+    const uint64_t* s = reinterpret_cast<const uint64_t*>(&src);
+    volatile uint64_t* d = reinterpret_cast<volatile uint64_t*>(dst);
+#pragma unroll 4
+    for (int i = 0; i < (int)(sizeof(T) / 8); ++i) d[i] = s[i];
+}
+template <typename T>
+__device__ __forceinline__ void vget(T* dst, const volatile T* src) {
+    const volatile uint64_t* s = reinterpret_cast<const volatile uint64_t*>(src);
+    uint64_t* d = reinterpret_cast<uint64_t*>(dst);
+#pragma unroll 4
+    for (int i = 0; i < (int)(sizeof(T) / 8); ++i) d[i] = s[i];
+}
+
+// block-cooperative copy of a layout record: one 8-byte word per thread, so
+// the volatile loads (L2 / NVLink round trips) overlap instead of queueing
+constexpr int kLayWords = (int)(sizeof(DmLay) / 8);
+static_assert(kLayWords <= kThreads, "one word per thread");
+__device__ __forceinline__ void coop_lay(volatile DmLay* dst, const volatile DmLay* src) {
+    if (threadIdx.x < kLayWords)
+        reinterpret_cast<volatile uint64_t*>(dst)[threadIdx.x] =
+            reinterpret_cast<const volatile uint64_t*>(src)[threadIdx.x];
+}
+
+__device__ __forceinline__ int64_t gcd64(int64_t a, int64_t b) {
+    while (b) {
+        const int64_t t = a % b;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
+template <int W>
+__device__ __forceinline__ void chain_pieces(const Chain& sc, const uint8_t* sb, const Chain& dc, uint8_t* db,
+                                             int64_t np, int64_t g, int64_t tid, int64_t nth) {
+    using T = typename DVec<W>::T;
+    for (int64_t p = tid; p < np; p += nth) {
+        const int64_t so = chain_off(sc, p * g), dof = chain_off(dc, p * g);
+        for (int64_t w = 0; w < g; w += W)
+            *reinterpret_cast<T*>(db + dof + w) = *reinterpret_cast<const T*>(sb + so + w);
+    }
 }
 
 // grid-stride byte copy, 16 / 4-byte words when both sides allow
 __device__ __forceinline__ void copy_bytes(const uint8_t* src, uint8_t* dst, int64_t n, int64_t tid, int64_t nth) {
-    if (n <= 0) return;
     const uintptr_t mis = (reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst));
     int64_t head = 0;
     if ((mis & 15) == 0) {
@@ -118,6 +153,53 @@ __device__ __forceinline__ void copy_bytes(const uint8_t* src, uint8_t* dst, int
         head = nv << 2;
     }
     for (int64_t i = head + tid; i < n; i += nth) dst[i] = src[i];
+}
+
+// packed bytes [0, n) from layout s of buffer sb to layout d of buffer db
+// (copy_between semantics, datatype.py:760-797): the packed stream cut into
+// pieces of g = gcd(run lengths, 64) bytes, contiguous on both sides, moved
+// with the widest word both sides allow; the < g tail byte by byte
+__device__ __forceinline__ void chain_copy(const DmLay& s, const uint8_t* sb, const DmLay& d, uint8_t* db, int64_t n,
+                                           int64_t tid, int64_t nth) {
+    if (n <= 0) return;
+    if (s.c.depth == 0 && d.c.depth == 0) {   // contiguous on both sides: a plain copy
+        copy_bytes(sb + s.c.base, db + d.c.base, n, tid, nth);
+        return;
+    }
+    const int64_t g = gcd64(gcd64(s.c.L, d.c.L), 64);
+    int w = s.align < d.align ? s.align : d.align;
+    w = w > 16 ? 16 : w;
+    const uintptr_t m = reinterpret_cast<uintptr_t>(sb) | reinterpret_cast<uintptr_t>(db) | (uintptr_t)g;
+    while (w > 1 && (m & (uintptr_t)(w - 1))) w >>= 1;
+    const int64_t np = n / g;
+    switch (w) {
+    case 16: chain_pieces<16>(s.c, sb, d.c, db, np, g, tid, nth); break;
+    case 8: chain_pieces<8>(s.c, sb, d.c, db, np, g, tid, nth); break;
+    case 4: chain_pieces<4>(s.c, sb, d.c, db, np, g, tid, nth); break;
+    case 2: chain_pieces<2>(s.c, sb, d.c, db, np, g, tid, nth); break;
+    default: chain_pieces<1>(s.c, sb, d.c, db, np, g, tid, nth); break;
+    }
+    for (int64_t P = np * g + tid; P < n; P += nth) db[chain_off(d.c, P)] = sb[chain_off(s.c, P)];
+}
+
+__device__ __forceinline__ void publish(DmResult* res, int src, int tag, int64_t bytes, const uint8_t* data,
+                                        uint32_t* consumed, uint32_t cgen, int rdv, uint8_t* dst, int64_t cap,
+                                        int copier) {
+    volatile DmResult* r = res;   // slay / dlay: copied by the block before (coop_lay)
+    r->src = src;
+    r->tag = tag;
+    r->bytes = bytes;
+    r->data = data;
+    r->consumed = consumed;
+    r->cgen = cgen;
+    r->rdv = rdv;
+    r->dst = dst;
+    r->n = bytes < cap ? bytes : cap;
+    r->copier = copier;
+    r->copied = 0;
+    r->xdone = 0;
+    __threadfence_system();
+    r->ready = 1;
 }
 
 // the rendezvous copy is complete: release the sender, then the receiver
@@ -137,6 +219,7 @@ struct SendArgs {
     uint32_t* consumed;
     int32_t* record;      // rendezvous: the matched result slot, or -1 (sender's own box)
     int32_t rdv, pad;
+    DmLay lay;            // relative to data
 };
 
 // a message arrives at the receiving rank's box
@@ -157,6 +240,13 @@ __global__ void __launch_bounds__(kThreads) k_dm_send(const SendArgs a) {
         }, &best);
         bool done = true;
         if (k != kNone) {   // the earliest posted receive takes it
+            {
+                const int i = (int)(k & 0xFFF);
+                volatile DmResult* rr = &b->result[vb->recv[i].result];
+                coop_lay(&rr->slay, &a.lay);
+                coop_lay(&rr->dlay, &vb->recv[i].lay);
+                __syncthreads();
+            }
             if (threadIdx.x == 0) {
                 const int i = (int)(k & 0xFFF);
                 volatile DmRecv& rv = vb->recv[i];
@@ -184,6 +274,7 @@ __global__ void __launch_bounds__(kThreads) k_dm_send(const SendArgs a) {
                     m.consumed = a.consumed;
                     m.cgen = a.cgen;
                     m.rdv = a.rdv;
+                    vput(&m.lay, a.lay);
                     if (a.record) *reinterpret_cast<volatile int32_t*>(a.record) = -1;
                     __threadfence_system();
                     m.state = 1;
@@ -209,9 +300,10 @@ struct PostArgs {
     DmBox* box;
     int32_t src, tag, ctx;   // patterns
     int32_t result;
-    uint8_t* dst;            // where a rendezvous message lands
+    uint8_t* dst;            // where the message lands
     int64_t cap;
     int32_t big, pad;        // big: a k_dm_xfer follows this post
+    DmLay lay;               // relative to dst
 };
 
 // a receive is posted at its stream position
@@ -240,6 +332,9 @@ __global__ void __launch_bounds__(kThreads) k_dm_post(const PostArgs a) {
         }, &best);
         bool done = true;
         if (k != kNone) {   // the earliest unexpected message
+            coop_lay(&b->result[a.result].slay, &vb->msg[(int)(k & 0xFFF)].lay);
+            coop_lay(&b->result[a.result].dlay, &a.lay);
+            __syncthreads();
             if (threadIdx.x == 0) {
                 const int i = (int)(k & 0xFFF);
                 volatile DmMsg& m = vb->msg[i];
@@ -263,6 +358,7 @@ __global__ void __launch_bounds__(kThreads) k_dm_post(const PostArgs a) {
                     r.result = a.result;
                     r.dst = a.dst;
                     r.cap = a.cap;
+                    vput(&r.lay, a.lay);
                     r.seq = vb->next_seq;
                     vb->next_seq = vb->next_seq + 1;
                     __threadfence_system();
@@ -284,8 +380,11 @@ __global__ void __launch_bounds__(kThreads) k_dm_post(const PostArgs a) {
         __nanosleep(1000);
     }
     if (small_copy) {   // rendezvous message into a receive of <= eager-limit bytes
+        __shared__ DmLay sl;
         volatile DmResult* r = &b->result[a.result];
-        copy_bytes((const uint8_t*)r->data, (uint8_t*)r->dst, r->n, threadIdx.x, blockDim.x);
+        coop_lay(&sl, &r->slay);
+        __syncthreads();
+        chain_copy(sl, (const uint8_t*)r->data, a.lay, a.dst, r->n, threadIdx.x, blockDim.x);
         __syncthreads();
         if (threadIdx.x == 0) rdv_complete(r);
     }
@@ -296,13 +395,30 @@ __global__ void __launch_bounds__(kThreads) k_dm_post(const PostArgs a) {
 // big receive's k_dm_post on the receiver's stream (record == nullptr: the
 // post's own slot `res`)
 __global__ void __launch_bounds__(kThreads) k_dm_xfer(DmBox* b, int res, const int32_t* record) {
-    const int side = record ? 0 : 1;
-    if (record) res = *reinterpret_cast<const volatile int32_t*>(record);
-    if (res < 0) return;
+    // one thread decides for the block: a sender may publish into this slot
+    // while the block starts (the decision must be uniform for the barriers)
+    __shared__ int go, slot_sh;
+    if (threadIdx.x == 0) {
+        const int side = record ? 0 : 1;
+        const int rs = record ? *reinterpret_cast<const volatile int32_t*>(record) : res;
+        int ok = 0;
+        if (rs >= 0) {
+            volatile DmResult* q = &b->result[rs];
+            ok = q->ready && q->rdv && q->copier == side;
+        }
+        go = ok;
+        slot_sh = rs;
+    }
+    __syncthreads();
+    if (!go) return;
+    res = slot_sh;
     volatile DmResult* r = &b->result[res];
-    if (!r->ready || !r->rdv || r->copier != side) return;
     __threadfence_system();
-    copy_bytes((const uint8_t*)r->data, (uint8_t*)r->dst, r->n, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+    __shared__ DmLay sl, dl;
+    coop_lay(&sl, &r->slay);
+    coop_lay(&dl, &r->dlay);
+    __syncthreads();
+    chain_copy(sl, (const uint8_t*)r->data, dl, (uint8_t*)r->dst, r->n, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
                (int64_t)gridDim.x * blockDim.x);
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -345,14 +461,19 @@ __global__ void __launch_bounds__(32) k_dm_wait(DmBox* b, int res, DmStatus* st,
 
 // copy the part of the message that fits; the last CTA releases the bounce
 // buffer and completes the status
-__global__ void __launch_bounds__(kThreads) k_dm_copy(DmBox* b, int res, uint8_t* __restrict__ dst, int64_t cap,
-                                                      DmStatus* st) {
+__global__ void __launch_bounds__(kThreads) k_dm_copy(DmBox* b, int res, int64_t cap, DmStatus* st) {
     volatile DmResult* r = &b->result[res];
     const bool ok = r->ready != 0;
     const bool rdv = ok && r->rdv;   // already copied at match time (k_dm_wait saw it complete)
-    const uint8_t* src = ok ? (const uint8_t*)r->data : nullptr;
     const int64_t n = ok && !rdv ? (r->bytes < cap ? r->bytes : cap) : 0;
-    copy_bytes(src, dst, n, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+    if (n > 0) {   // the bounce buffer (contiguous) into the receive's layout
+        __shared__ DmLay sl, dl;
+        coop_lay(&sl, &r->slay);
+        coop_lay(&dl, &r->dlay);
+        __syncthreads();
+        chain_copy(sl, (const uint8_t*)r->data, dl, (uint8_t*)r->dst, n, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                   (int64_t)gridDim.x * blockDim.x);
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence_system();
@@ -379,22 +500,22 @@ unsigned xfer_grid(int64_t bytes, int device) {
 
 cudaError_t dm_send(DmBox* box, int src, int tag, int ctx, const uint8_t* data, int64_t bytes, uint32_t* consumed,
                     uint32_t cgen, cudaStream_t stream) {
-    SendArgs a{box, src, tag, ctx, cgen, data, bytes, consumed, nullptr, 0, 0};
+    SendArgs a{box, src, tag, ctx, cgen, data, bytes, consumed, nullptr, 0, 0, dm_contig_lay(0, bytes)};
     k_dm_send<<<1, kThreads, 0, stream>>>(a);
     return cudaGetLastError();
 }
 
-cudaError_t dm_send_rdv(DmBox* box, int src, int tag, int ctx, const uint8_t* data, int64_t bytes,
+cudaError_t dm_send_rdv(DmBox* box, int src, int tag, int ctx, const uint8_t* data, const DmLay& lay, int64_t bytes,
                         uint32_t* consumed, uint32_t cgen, int32_t* record, int device, cudaStream_t stream) {
-    SendArgs a{box, src, tag, ctx, cgen, data, bytes, consumed, record, 1, 0};
+    SendArgs a{box, src, tag, ctx, cgen, data, bytes, consumed, record, 1, 0, lay};
     k_dm_send<<<1, kThreads, 0, stream>>>(a);
     k_dm_xfer<<<xfer_grid(bytes, device), kThreads, 0, stream>>>(box, -1, record);
     return cudaGetLastError();
 }
 
-cudaError_t dm_post(DmBox* box, int src, int tag, int ctx, int result, uint8_t* dst, int64_t cap, bool big,
-                    int device, cudaStream_t stream) {
-    PostArgs a{box, src, tag, ctx, result, dst, cap, big ? 1 : 0, 0};
+cudaError_t dm_post(DmBox* box, int src, int tag, int ctx, int result, uint8_t* dst, const DmLay& lay, int64_t cap,
+                    bool big, int device, cudaStream_t stream) {
+    PostArgs a{box, src, tag, ctx, result, dst, cap, big ? 1 : 0, 0, lay};
     k_dm_post<<<1, kThreads, 0, stream>>>(a);
     if (big) k_dm_xfer<<<xfer_grid(cap, device), kThreads, 0, stream>>>(box, result, nullptr);
     return cudaGetLastError();
@@ -405,12 +526,24 @@ cudaError_t dm_wait(DmBox* box, int result, DmStatus* status, int64_t cap, cudaS
     return cudaGetLastError();
 }
 
-cudaError_t dm_copy(DmBox* box, int result, uint8_t* dst, int64_t cap, DmStatus* status, int device,
-                    cudaStream_t stream) {
+cudaError_t dm_copy(DmBox* box, int result, int64_t cap, DmStatus* status, int device, cudaStream_t stream) {
     const int64_t want = (cap + (int64_t)kThreads * 64 - 1) / ((int64_t)kThreads * 64);
     const int64_t grid = want < 1 ? 1 : (want > (int64_t)sm_count(device) * 4 ? (int64_t)sm_count(device) * 4 : want);
-    k_dm_copy<<<(unsigned)grid, kThreads, 0, stream>>>(box, result, dst, cap, status);
+    k_dm_copy<<<(unsigned)grid, kThreads, 0, stream>>>(box, result, cap, status);
     return cudaGetLastError();
+}
+
+DmLay dm_contig_lay(int64_t off, int64_t bytes) {
+    DmLay l;
+    memset(&l, 0, sizeof l);
+    l.c.base = off;
+    l.c.L = bytes > 0 ? bytes : 1;
+    l.c.depth = 0;
+    host_magic((uint64_t)l.c.L, &l.c.m_L, &l.c.s_L);
+    int64_t a = 16;
+    while (a > 1 && ((off | l.c.L) & (a - 1))) a >>= 1;
+    l.align = (int32_t)a;
+    return l;
 }
 
 cudaError_t preload_dm_kernels() {

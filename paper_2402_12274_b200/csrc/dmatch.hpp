@@ -31,16 +31,23 @@
 //              bounce buffer; its last CTA marks the bounce buffer consumed
 //              (the sender's host frees it lazily) and the status done.
 //
-// Eager messages (<= the eager limit, every blocking send, typed send
-// layouts) are buffered: packed into a bounce buffer at the sender's stream
-// position, so a blocking send never waits for its receiver (rings of
+// Every message and every posted receive carries its layout as a chain
+// (DmLay: contiguous or Rep^k(Run) -- vector, hvector, subarray faces), and
+// every copy is a chain-to-chain zipper (`chain_copy`: the packed stream cut
+// into pieces contiguous on both sides), so a strided message lands in a
+// strided receive in one pass.  Receives of other layouts (struct / indexed)
+// land in a contiguous buffer unpacked at the wait.
+//
+// Eager messages (<= the eager limit, every blocking send, send layouts that
+// are not chains) are buffered: packed into a bounce buffer at the sender's
+// stream position, so a blocking send never waits for its receiver (rings of
 // blocking sends are safe at every size; the reference guarantees it up to
 // its eager limit), and copied out at the receiver's wait.
 //
-// Rendezvous (a nonblocking send of a contiguous layout above the eager
-// limit): no bounce buffer -- the message announces the sender's own buffer,
-// and the data moves ONCE, at match time, on the stream of whichever side
-// matched second (transport.py's RTS/CTS pull, :355-375 / :548-602):
+// Rendezvous (a nonblocking send of a chain layout above the eager limit):
+// no bounce buffer -- the message announces the sender's own buffer and
+// layout, and the data moves ONCE, at match time, on the stream of whichever
+// side matched second (transport.py's RTS/CTS pull, :355-375 / :548-602):
 //
 //   k_dm_xfer  after k_dm_send (sender's stream): copies into the posted
 //              receive's destination if the send matched one;
@@ -61,7 +68,17 @@
 
 #include <cstdint>
 
+#include "desc.cuh"
+
 namespace mpx {
+
+// a side's layout relative to its buffer pointer: a chain (desc.cuh; a
+// contiguous run is a chain of depth 0) and the widest word every run start
+// and length allow
+struct DmLay {
+    Chain c;
+    int32_t align, pad;
+};
 
 constexpr int kDmSlots = 2048;        // per receiving rank: unexpected messages + posted receives, each
 constexpr int kDmResults = 1 << 14;   // per receiving rank: receives in flight (posted, not yet copied)
@@ -75,6 +92,7 @@ struct DmMsg {            // an unexpected message
     uint32_t* consumed;   // pinned host word: set to cgen once the bytes are copied out
     uint32_t cgen;
     int32_t rdv;          // 1: rendezvous (copied at match time)
+    DmLay lay;            // the message's layout relative to data (bounce: contiguous)
 };
 
 struct DmRecv {           // a posted receive
@@ -82,8 +100,9 @@ struct DmRecv {           // a posted receive
     int32_t src, tag, ctx;    // patterns
     int64_t seq;
     int32_t result, pad;
-    uint8_t* dst;             // where a rendezvous message lands (buffer or landing)
+    uint8_t* dst;             // where a message lands (buffer or landing)
     int64_t cap;
+    DmLay lay;                // relative to dst
 };
 
 struct DmResult {         // a receive's match, written by whichever side matched
@@ -101,6 +120,7 @@ struct DmResult {         // a receive's match, written by whichever side matche
     int32_t copied;       // 1 once the rendezvous copy is complete
     uint32_t xdone;       // k_dm_xfer CTAs finished
     uint32_t pad2;
+    DmLay slay, dlay;     // the message's layout (relative to data), the receive's (relative to dst)
 };
 
 struct DmStatus {         // pinned host memory, one per result slot
@@ -124,18 +144,24 @@ struct DmBox {
 };
 
 // launchers (dmatch.cu); `box` is the receiving rank's box
+// eager send: `data` = the bounce buffer (packed, contiguous)
 cudaError_t dm_send(DmBox* box, int src, int tag, int ctx, const uint8_t* data, int64_t bytes, uint32_t* consumed,
                     uint32_t cgen, cudaStream_t stream);
-// rendezvous send: `data` is the sender's buffer; the match is recorded in
-// *record (in the sender's own box) and k_dm_xfer copies right behind it
-cudaError_t dm_send_rdv(DmBox* box, int src, int tag, int ctx, const uint8_t* data, int64_t bytes,
+// rendezvous send: `data` is the sender's buffer, `lay` its layout; the
+// match is recorded in *record (in the sender's own box) and k_dm_xfer
+// copies right behind it
+cudaError_t dm_send_rdv(DmBox* box, int src, int tag, int ctx, const uint8_t* data, const DmLay& lay, int64_t bytes,
                         uint32_t* consumed, uint32_t cgen, int32_t* record, int device, cudaStream_t stream);
-// `dst` / `cap`: where a rendezvous message lands; big: a k_dm_xfer follows
+// `dst` / `lay` / `cap`: where the message lands; big: a k_dm_xfer follows
 // the post (cap above the eager limit), else k_dm_post copies itself
-cudaError_t dm_post(DmBox* box, int src, int tag, int ctx, int result, uint8_t* dst, int64_t cap, bool big,
-                    int device, cudaStream_t stream);
+cudaError_t dm_post(DmBox* box, int src, int tag, int ctx, int result, uint8_t* dst, const DmLay& lay, int64_t cap,
+                    bool big, int device, cudaStream_t stream);
+// a layout that is one contiguous run of `bytes` at offset `off`
+DmLay dm_contig_lay(int64_t off, int64_t bytes);
 cudaError_t dm_wait(DmBox* box, int result, DmStatus* status, int64_t cap, cudaStream_t stream);
-cudaError_t dm_copy(DmBox* box, int result, uint8_t* dst, int64_t cap, DmStatus* status, int device,
+// eager messages: copy into the receive's destination (its layout, recorded
+// at the post); rendezvous: already there
+cudaError_t dm_copy(DmBox* box, int result, int64_t cap, DmStatus* status, int device,
                     cudaStream_t stream);
 cudaError_t preload_dm_kernels();
 

@@ -1362,6 +1362,18 @@ int dm_reclaim(const std::shared_ptr<Comm>& c) {
     return MPX_SUCCESS;
 }
 
+// The layout of (dt, count) as a chain for the device copies (dmatch.hpp):
+// contiguous or Rep^k(Run), non-overlapping; false for other layouts.
+bool dm_chain_lay(int dev, Datatype* dt, int64_t count, cudaStream_t st, DmLay* out) {
+    std::string err;
+    auto p = get_plan(dt, count, dev, st, &err);
+    if (!p || p->kind != PLAN_CHAIN || p->overlap) return false;
+    std::memset(out, 0, sizeof *out);
+    out->c = p->chain;
+    out->align = p->chain_align;
+    return true;
+}
+
 // Eager: the message is packed into a bounce buffer at the sender's stream
 // position, then announced to the receiver's box (k_dm_send): the send is
 // complete at that point, blocking or not.  Rendezvous (nonblocking,
@@ -1376,8 +1388,8 @@ int dm_send_op(const std::shared_ptr<Comm>& c, const void* buf, int64_t count, D
     MPX_RC(set_device(c->device));
     MPX_RC(dm_reclaim(c));
     const int64_t bytes = dt->size * count;
-    int64_t off = 0;
-    if (!blocking && bytes > w->eager_limit && dest != c->rank && contiguous_run(dt, count, &off)) {
+    DmLay lay;
+    if (!blocking && bytes > w->eager_limit && dest != c->rank && dm_chain_lay(c->device, dt, count, c->stream, &lay)) {
         DmBox* own = nullptr;
         MPX_RC(dm_box_of(w, c->rank, &own));
         uint32_t idx = 0;
@@ -1391,7 +1403,7 @@ int dm_send_op(const std::shared_ptr<Comm>& c, const void* buf, int64_t count, D
         MPX_RC(set_device(c->device));
         {
             ProfScope pl(P_LAUNCH);
-            MPX_CU(dm_send_rdv(box, c->rank, tag, c->ctx, static_cast<const uint8_t*>(buf) + off, bytes, flag, gen,
+            MPX_CU(dm_send_rdv(box, c->rank, tag, c->ctx, static_cast<const uint8_t*>(buf), lay, bytes, flag, gen,
                                &own->srec[idx], c->device, c->stream));
         }
         MPX_TRACE("dm send r%d -> %d tag %d %lld B (rendezvous)", c->rank, dest, tag, (long long)bytes);
@@ -1445,9 +1457,10 @@ int dm_recv_op(const std::shared_ptr<Comm>& c, void* buf, int64_t count, Datatyp
                bool blocking, std::shared_ptr<ReqState>* out_req) {
     World* w = c->w;
     const int64_t cap = dt->size * count;
-    int64_t off = 0;
-    const bool contig = contiguous_run(dt, count, &off);
-    if (!contig && cap > 0) {
+    DmLay lay;
+    // chain layouts (contiguous, vector, subarray faces ...) receive in place
+    const bool direct = dm_chain_lay(c->device, dt, count, c->stream, &lay);
+    if (!direct && cap > 0) {
         int64_t q[8];
         MPX_RC(mpx_layout_query(reinterpret_cast<mpx_datatype>(dt), count, q));
         if (q[6]) return fail(MPX_ERR_UNSUPPORTED, "device matching: receive layouts with overlapping bytes are not supported");
@@ -1459,29 +1472,28 @@ int dm_recv_op(const std::shared_ptr<Comm>& c, void* buf, int64_t count, Datatyp
     DmStatus* st = &w->dm_status[(size_t)c->rank][slot];
     MPX_RC(set_device(c->device));
     const int dev = c->device;
-    // a typed receive lands in a buffer holding the layout's current bytes
-    // (a short message leaves the rest of the layout as it was), prepared at
-    // the post: a rendezvous message may be copied in at match time
+    // other typed receives land in a buffer holding the layout's current
+    // bytes (a short message leaves the rest of the layout as it was),
+    // prepared at the post (a rendezvous message may be copied in at match
+    // time) and unpacked at the wait
     void* landing = nullptr;
-    if (!contig) {
+    if (!direct) {
         MPX_RC(staging_alloc(dev, (size_t)cap, c->stream, &landing));
         if (cap > 0) MPX_RC(launch_move(dev, dt, count, true, buf, landing, cap, c->stream));
         MPX_RC(set_device(dev));
+        lay = dm_contig_lay(0, cap);
     }
-    uint8_t* land = contig ? static_cast<uint8_t*>(buf) + off : static_cast<uint8_t*>(landing);
+    uint8_t* land = direct ? static_cast<uint8_t*>(buf) : static_cast<uint8_t*>(landing);
     {
         ProfScope pl(P_LAUNCH);
-        MPX_CU(dm_post(box, source, tag, c->ctx, slot, land, cap, cap > w->eager_limit, dev, c->stream));
+        MPX_CU(dm_post(box, source, tag, c->ctx, slot, land, lay, cap, cap > w->eager_limit, dev, c->stream));
     }
-    auto deliver = [dev, box, slot, st, cap, contig, dt, count, buf, land, landing](cudaStream_t ws) -> int {
+    auto deliver = [dev, box, slot, st, cap, direct, dt, count, buf, landing](cudaStream_t ws) -> int {
         MPX_RC(set_device(dev));
         ProfScope pl(P_LAUNCH);
         MPX_CU(dm_wait(box, slot, st, cap, ws));
-        if (contig) {
-            MPX_CU(dm_copy(box, slot, land, cap, st, dev, ws));
-            return MPX_SUCCESS;
-        }
-        MPX_CU(dm_copy(box, slot, land, cap, st, dev, ws));
+        MPX_CU(dm_copy(box, slot, cap, st, dev, ws));
+        if (direct) return MPX_SUCCESS;
         if (cap > 0) MPX_RC(launch_move(dev, dt, count, false, landing, buf, cap, ws));
         MPX_RC(set_device(dev));
         MPX_CU(cudaFreeAsync(landing, ws));
