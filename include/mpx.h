@@ -237,7 +237,8 @@ int mpx_world_barrier(mpx_world w);
  * 0 = on the host when an operation is enqueued (default), 1 = on the GPU
  * when each rank's stream reaches the operation (posted / unexpected queues
  * in the receiver's device memory; eager messages buffered, nonblocking
- * contiguous sends above the eager limit copied once at match time).  The ranks must
+ * sends of chain layouts above the eager limit copied once at match time,
+ * layout to layout).  The ranks must
  * agree (MPX_ERR_ARG otherwise); multi-process worlds: host only
  * (MPX_ERR_UNSUPPORTED).  Replaces the matching of transport.py:191-201,
  * 399-428 (executor-thread order, offload.py:87-102). */
