@@ -333,3 +333,44 @@ def test_rendezvous_any_source_takes_every_sender_once(n):
     host([body] * n)
     assert sorted(got["src"]) == list(range(1, n))
     assert got["data"] == got["src"] and got["same"]
+
+
+@pytest.mark.parametrize("nx", [16, 256])      # 16: eager (4 KiB), 256: rendezvous (1 MiB)
+def test_chain_to_chain_face_into_vector(nx):
+    """an x-face of a 3-D float32 array (one element per row: a chain of
+    depth 2) into a vector(n/2, 2, 4) receive: one chain-to-chain copy, eager
+    at the wait or rendezvous at match time (copy_between semantics,
+    datatype.py:760-797); bytes outside the receive layout untouched."""
+    n3 = nx + 2
+    got = {}
+
+    def rank0(inst):
+        q, c, s = _comm(inst)
+        # int32 payload (exact at every index) moved as 4-byte FLOAT32 elements
+        a = torch.arange(n3 ** 3, dtype=torch.int32, device=inst.device)
+        face = mp.type_create_subarray([n3, n3, n3], [nx, nx, 1], [1, 1, 1], mp.FLOAT32).commit()
+        sr = mp.isend_enqueue(c, a, 1, face, 1, 5)
+        mp.wait_enqueue(sr)
+        mp.queue_synchronize(q)
+        mp.type_free(face)
+        _close(q, c, s)
+
+    def rank1(inst):
+        q, c, s = _comm(inst)
+        n = nx * nx
+        vt = mp.type_vector(n // 2, 2, 4, mp.FLOAT32).commit()
+        dst = torch.full((2 * n,), -1, dtype=torch.int32, device=inst.device)
+        rr = mp.irecv_enqueue(c, dst, 1, vt, 0, 5)
+        mp.wait_enqueue(rr)
+        mp.queue_synchronize(q)
+        a = torch.arange(n3 ** 3, dtype=torch.int32).view(n3, n3, n3)
+        face = a[1:nx + 1, 1:nx + 1, 1].reshape(-1)
+        exp = torch.full((2 * n,), -1, dtype=torch.int32)
+        exp.view(-1, 4)[:, :2] = face.view(-1, 2)
+        got["ok"] = bool(torch.equal(dst.cpu(), exp))
+        got["count"] = rr.status.count
+        mp.type_free(vt)
+        _close(q, c, s)
+
+    pair(rank0, rank1)
+    assert got["ok"] and got["count"] == 1
