@@ -115,6 +115,21 @@ __device__ __forceinline__ void coop_lay(volatile DmLay* dst, const volatile DmL
             reinterpret_cast<const volatile uint64_t*>(src)[threadIdx.x];
 }
 
+// a contiguous run of `bytes` at offset 0 (device side; lay_off never
+// divides on a depth-0 chain, so no magic numbers)
+__device__ __forceinline__ DmLay dm_contig_lay_dev(int64_t bytes) {
+    DmLay l;
+    memset(&l, 0, sizeof l);
+    l.c.L = bytes > 0 ? bytes : 1;
+    l.align = 16;
+    return l;
+}
+
+// layout offset of packed byte P (a depth-0 chain is one run covering every P)
+__device__ __forceinline__ int64_t lay_off(const Chain& c, int64_t P) {
+    return c.depth == 0 ? c.base + P : chain_off(c, P);
+}
+
 __device__ __forceinline__ int64_t gcd64(int64_t a, int64_t b) {
     while (b) {
         const int64_t t = a % b;
@@ -129,7 +144,7 @@ __device__ __forceinline__ void chain_pieces(const Chain& sc, const uint8_t* sb,
                                              int64_t np, int64_t g, int64_t tid, int64_t nth) {
     using T = typename DVec<W>::T;
     for (int64_t p = tid; p < np; p += nth) {
-        const int64_t so = chain_off(sc, p * g), dof = chain_off(dc, p * g);
+        const int64_t so = lay_off(sc, p * g), dof = lay_off(dc, p * g);
         for (int64_t w = 0; w < g; w += W)
             *reinterpret_cast<T*>(db + dof + w) = *reinterpret_cast<const T*>(sb + so + w);
     }
@@ -179,7 +194,7 @@ __device__ __forceinline__ void chain_copy(const DmLay& s, const uint8_t* sb, co
     case 2: chain_pieces<2>(s.c, sb, d.c, db, np, g, tid, nth); break;
     default: chain_pieces<1>(s.c, sb, d.c, db, np, g, tid, nth); break;
     }
-    for (int64_t P = np * g + tid; P < n; P += nth) db[chain_off(d.c, P)] = sb[chain_off(s.c, P)];
+    for (int64_t P = np * g + tid; P < n; P += nth) db[lay_off(d.c, P)] = sb[lay_off(s.c, P)];
 }
 
 __device__ __forceinline__ void publish(DmResult* res, int src, int tag, int64_t bytes, const uint8_t* data,
@@ -220,14 +235,22 @@ struct SendArgs {
     int32_t* record;      // rendezvous: the matched result slot, or -1 (sender's own box)
     int32_t rdv, pad;
     DmLay lay;            // relative to data
+    uint8_t* bounce;      // eager, chain layout: the block packs data (lay) into bounce first
 };
 
 // a message arrives at the receiving rank's box
-__global__ void __launch_bounds__(kThreads) k_dm_send(const SendArgs a) {
+__global__ void __launch_bounds__(kThreads) k_dm_send(SendArgs a) {
     __shared__ unsigned long long best;
     __shared__ int slot;
     DmBox* b = a.box;
     volatile DmBox* vb = b;
+    if (a.bounce) {   // eager message of a chain layout: pack it here (no separate pack launch)
+        chain_copy(a.lay, a.data, dm_contig_lay_dev(a.bytes), a.bounce, a.bytes, threadIdx.x, blockDim.x);
+        __threadfence();
+        __syncthreads();
+        a.data = a.bounce;
+        a.lay = dm_contig_lay_dev(a.bytes);
+    }
     const uint64_t t0 = now_ns();
     for (;;) {
         if (threadIdx.x == 0) lock(b);
@@ -459,6 +482,66 @@ __global__ void __launch_bounds__(32) k_dm_wait(DmBox* b, int res, DmStatus* st,
     s->err = r->bytes > cap ? MPX_ERR_TRUNCATE : MPX_SUCCESS;
 }
 
+// a receive within the eager limit: wait and copy in ONE single-CTA kernel
+// (one launch per receive instead of two)
+__global__ void __launch_bounds__(kThreads) k_dm_wait_copy(DmBox* b, int res, DmStatus* st, int64_t cap) {
+    __shared__ int state;   // 0: failed (box error), 1: copy, 2: rendezvous (already copied)
+    __shared__ DmLay sl, dl;
+    volatile DmResult* r = &b->result[res];
+    volatile DmBox* vb = b;
+    if (threadIdx.x == 0) {
+        unsigned ns = 32;
+        state = 1;
+        while (r->ready == 0) {
+            if (vb->err) {
+                state = 0;
+                break;
+            }
+            __nanosleep(ns);
+            ns = ns < 1024 ? 2 * ns : ns;
+        }
+        if (state && r->rdv) {
+            state = 2;
+            while (r->copied == 0) {
+                __nanosleep(ns);
+                ns = ns < 1024 ? 2 * ns : ns;
+            }
+        }
+        __threadfence_system();
+    }
+    __syncthreads();
+    const int stt = state;
+    int64_t n = 0;
+    if (stt == 1) {
+        n = r->bytes < cap ? r->bytes : cap;
+        coop_lay(&sl, &r->slay);
+        coop_lay(&dl, &r->dlay);
+        __syncthreads();
+        chain_copy(sl, (const uint8_t*)r->data, dl, (uint8_t*)r->dst, n, threadIdx.x, blockDim.x);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile DmStatus* s = st;
+        if (stt == 0) {
+            s->err = vb->err;
+            s->src = -1;
+            s->tag = -1;
+            s->bytes = 0;
+        } else {
+            s->src = r->src;
+            s->tag = r->tag;
+            s->bytes = r->bytes;
+            s->err = r->bytes > cap ? MPX_ERR_TRUNCATE : MPX_SUCCESS;
+            if (stt == 1) {
+                __threadfence_system();
+                *reinterpret_cast<volatile uint32_t*>(r->consumed) = r->cgen;
+            }
+        }
+        __threadfence_system();
+        s->done = 1;
+    }
+}
+
 // copy the part of the message that fits; the last CTA releases the bounce
 // buffer and completes the status
 __global__ void __launch_bounds__(kThreads) k_dm_copy(DmBox* b, int res, int64_t cap, DmStatus* st) {
@@ -500,14 +583,26 @@ unsigned xfer_grid(int64_t bytes, int device) {
 
 cudaError_t dm_send(DmBox* box, int src, int tag, int ctx, const uint8_t* data, int64_t bytes, uint32_t* consumed,
                     uint32_t cgen, cudaStream_t stream) {
-    SendArgs a{box, src, tag, ctx, cgen, data, bytes, consumed, nullptr, 0, 0, dm_contig_lay(0, bytes)};
+    SendArgs a{box, src, tag, ctx, cgen, data, bytes, consumed, nullptr, 0, 0, dm_contig_lay(0, bytes), nullptr};
     k_dm_send<<<1, kThreads, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t dm_send_packed(DmBox* box, int src, int tag, int ctx, const uint8_t* data, const DmLay& lay,
+                           uint8_t* bounce, int64_t bytes, uint32_t* consumed, uint32_t cgen, cudaStream_t stream) {
+    SendArgs a{box, src, tag, ctx, cgen, data, bytes, consumed, nullptr, 0, 0, lay, bounce};
+    k_dm_send<<<1, kThreads, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t dm_wait_copy(DmBox* box, int result, DmStatus* status, int64_t cap, cudaStream_t stream) {
+    k_dm_wait_copy<<<1, kThreads, 0, stream>>>(box, result, status, cap);
     return cudaGetLastError();
 }
 
 cudaError_t dm_send_rdv(DmBox* box, int src, int tag, int ctx, const uint8_t* data, const DmLay& lay, int64_t bytes,
                         uint32_t* consumed, uint32_t cgen, int32_t* record, int device, cudaStream_t stream) {
-    SendArgs a{box, src, tag, ctx, cgen, data, bytes, consumed, record, 1, 0, lay};
+    SendArgs a{box, src, tag, ctx, cgen, data, bytes, consumed, record, 1, 0, lay, nullptr};
     k_dm_send<<<1, kThreads, 0, stream>>>(a);
     k_dm_xfer<<<xfer_grid(bytes, device), kThreads, 0, stream>>>(box, -1, record);
     return cudaGetLastError();
@@ -554,6 +649,7 @@ cudaError_t preload_dm_kernels() {
     if ((r = cudaFuncGetAttributes(&a, k_dm_wait)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_dm_copy)) != cudaSuccess) e = r;
     if ((r = cudaFuncGetAttributes(&a, k_dm_xfer)) != cudaSuccess) e = r;
+    if ((r = cudaFuncGetAttributes(&a, k_dm_wait_copy)) != cudaSuccess) e = r;
     return e;
 }
 

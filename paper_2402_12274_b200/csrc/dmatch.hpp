@@ -156,6 +156,15 @@ cudaError_t dm_send_rdv(DmBox* box, int src, int tag, int ctx, const uint8_t* da
 // the post (cap above the eager limit), else k_dm_post copies itself
 cudaError_t dm_post(DmBox* box, int src, int tag, int ctx, int result, uint8_t* dst, const DmLay& lay, int64_t cap,
                     bool big, int device, cudaStream_t stream);
+// messages and receives up to this size take the fused single-CTA kernels:
+// pack inside k_dm_send, wait + copy in one k_dm_wait_copy
+constexpr int64_t kDmFusedBytes = 64 << 10;
+// eager send of a chain layout <= kDmFusedBytes: k_dm_send packs `data`
+// (layout `lay`) into `bounce` itself
+cudaError_t dm_send_packed(DmBox* box, int src, int tag, int ctx, const uint8_t* data, const DmLay& lay,
+                           uint8_t* bounce, int64_t bytes, uint32_t* consumed, uint32_t cgen, cudaStream_t stream);
+// a receive of <= kDmFusedBytes: k_dm_wait + k_dm_copy in one kernel
+cudaError_t dm_wait_copy(DmBox* box, int result, DmStatus* status, int64_t cap, cudaStream_t stream);
 // a layout that is one contiguous run of `bytes` at offset `off`
 DmLay dm_contig_lay(int64_t off, int64_t bytes);
 cudaError_t dm_wait(DmBox* box, int result, DmStatus* status, int64_t cap, cudaStream_t stream);

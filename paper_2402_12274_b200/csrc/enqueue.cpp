@@ -1420,7 +1420,9 @@ int dm_send_op(const std::shared_ptr<Comm>& c, const void* buf, int64_t count, D
     }
     void* bounce = nullptr;
     MPX_RC(staging_alloc(c->device, (size_t)bytes, c->stream, &bounce));
-    if (bytes > 0) {
+    // a small message of a chain layout is packed by k_dm_send itself
+    const bool fused = bytes > 0 && bytes <= kDmFusedBytes && dm_chain_lay(c->device, dt, count, c->stream, &lay);
+    if (bytes > 0 && !fused) {
         ProfScope pl(P_LAUNCH);
         MPX_RC(launch_move(c->device, dt, count, true, buf, bounce, bytes, c->stream));
         MPX_RC(set_device(c->device));
@@ -1430,7 +1432,12 @@ int dm_send_op(const std::shared_ptr<Comm>& c, const void* buf, int64_t count, D
     w->flags.take(&flag, &gen);
     {
         ProfScope pl(P_LAUNCH);
-        MPX_CU(dm_send(box, c->rank, tag, c->ctx, static_cast<const uint8_t*>(bounce), bytes, flag, gen, c->stream));
+        MPX_RC(set_device(c->device));
+        if (fused)
+            MPX_CU(dm_send_packed(box, c->rank, tag, c->ctx, static_cast<const uint8_t*>(buf), lay,
+                                  static_cast<uint8_t*>(bounce), bytes, flag, gen, c->stream));
+        else
+            MPX_CU(dm_send(box, c->rank, tag, c->ctx, static_cast<const uint8_t*>(bounce), bytes, flag, gen, c->stream));
     }
     {
         std::lock_guard<std::mutex> g(c->dm_mu);
@@ -1491,8 +1498,12 @@ int dm_recv_op(const std::shared_ptr<Comm>& c, void* buf, int64_t count, Datatyp
     auto deliver = [dev, box, slot, st, cap, direct, dt, count, buf, landing](cudaStream_t ws) -> int {
         MPX_RC(set_device(dev));
         ProfScope pl(P_LAUNCH);
-        MPX_CU(dm_wait(box, slot, st, cap, ws));
-        MPX_CU(dm_copy(box, slot, cap, st, dev, ws));
+        if (cap <= kDmFusedBytes) {   // wait and copy in one single-CTA kernel
+            MPX_CU(dm_wait_copy(box, slot, st, cap, ws));
+        } else {
+            MPX_CU(dm_wait(box, slot, st, cap, ws));
+            MPX_CU(dm_copy(box, slot, cap, st, dev, ws));
+        }
         if (direct) return MPX_SUCCESS;
         if (cap > 0) MPX_RC(launch_move(dev, dt, count, false, landing, buf, cap, ws));
         MPX_RC(set_device(dev));
