@@ -353,17 +353,26 @@ bool ev_done(cudaEvent_t e) {
 // streams kept distinct per owner, _lib.own_stream.)
 class StreamPool {
   public:
+    // The free stream made earliest: the first batch sits on distinct
+    // hardware queues, so while at most that many streams are live (<= 10
+    // in-process ranks per device) no two live streams share a queue, however
+    // many streams leaked owners have made the pool grow.
     cudaError_t acquire(int dev, cudaStream_t* out) {
         {
             std::lock_guard<std::mutex> g(mu_);
             auto& f = free_[dev];
             if (!f.empty()) {
-                *out = f.back();
-                f.pop_back();
+                size_t best = 0;
+                for (size_t i = 1; i < f.size(); ++i)
+                    if (ordinal_[f[i]] < ordinal_[f[best]]) best = i;
+                *out = f[best];
+                f.erase(f.begin() + (long)best);
                 return cudaSuccess;
             }
         }
         MPX_TRACE("stream pool of device %d empty: creating a stream on the data path", dev);
+        static const bool dbg = std::getenv("MPX_POOL_DEBUG") != nullptr;
+        if (dbg) fprintf(stderr, "[mpx pool] device %d: stream created on the data path\n", dev);
         int cur = -1;
         cudaGetDevice(&cur);
         if (cur != dev) cudaSetDevice(dev);
@@ -372,6 +381,7 @@ class StreamPool {
         if (e == cudaSuccess) {
             std::lock_guard<std::mutex> g(mu_);
             made_.insert(*out);
+            ordinal_[*out] = made_.size();
         }
         return e;
     }
@@ -411,6 +421,9 @@ class StreamPool {
             std::lock_guard<std::mutex> g(mu_);
             free_[dev].push_back(s);
             made_.insert(s);
+            ordinal_[s] = made_.size();
+            static const bool dbg = std::getenv("MPX_POOL_DEBUG") != nullptr;
+            if (dbg) fprintf(stderr, "[mpx pool] device %d: stream #%zu created (reserve %zu)\n", dev, made_.size(), n);
         }
     }
     // queued work on a released stream simply runs ahead of its next owner's
@@ -434,6 +447,7 @@ class StreamPool {
     std::mutex mu_;
     std::map<int, std::vector<cudaStream_t>> free_;
     std::set<cudaStream_t> made_;
+    std::map<cudaStream_t, size_t> ordinal_;   // creation order (queue placement)
     std::set<int> batched_;
 };
 
@@ -2042,10 +2056,16 @@ int mpx_world_join(const char* group, int size, int rank, int device, int64_t ea
     }
     if (w->size != size) return fail(MPX_ERR_ARG, "world %s has %d ranks, not %d", group, w->size, size);
     if (w->joined[rank]) return fail(MPX_ERR_STATE, "rank %d already joined world %s", rank, group);
-    // streams for this rank's queue, world communicator and side stream (+ the
-    // device's late and service streams), made now (see StreamPool::reserve)
-    // -- and no more: every extra stream shares a hardware queue sooner
-    MPX_CU(stream_pool().reserve(device, (size_t)std::min(64, 3 * size + 2)));
+    // streams for the queue, world communicator and side stream of this rank
+    // and of the ranks still to join (+ the device's late and service
+    // streams), made now (see StreamPool::reserve) -- and no more: every
+    // extra stream shares a hardware queue sooner.  (Topping the free list up
+    // to 3 x size at every join made the pool grow by ~3 streams per joined
+    // rank: 120 streams over the test suite, where two ranks' streams on one
+    // hardware queue can park each other in a memop handshake.)
+    int still = 0;
+    for (int r = 0; r < size; ++r) still += w->joined[r] ? 0 : 1;
+    MPX_CU(stream_pool().reserve(device, (size_t)std::min(64, 3 * still + 2)));
     MPX_RC(setup_device(w, device, ndev));
     w->joined[rank] = true;
     w->devices[rank] = device;

@@ -57,3 +57,24 @@ def to_tuple_spec(spec):
         return tuple([kind] + [to_tuple_spec(x) if isinstance(x, list) and x and
                                isinstance(x[0], str) else x for x in spec[1:]])
     return spec
+
+
+@pytest.fixture(autouse=True)
+def _release_leftover_queues():
+    """Test hygiene: device queues a test did not destroy go back to libmpx's
+    stream pool when the test ends.  A queue's stream is never reclaimed by
+    the garbage collector (work may still be ordered on it), so leaked queues
+    used to grow the pool past the device's hardware queues over a long
+    suite; two ranks' streams sharing a hardware queue can then park each
+    other in a stream-memop handshake."""
+    yield
+    qmod = sys.modules.get("paper_2402_12274_b200.queues")
+    if qmod is None:
+        return
+    with qmod._lock:
+        left = [q for q in qmod._QUEUES.values() if not q.destroyed]
+    for q in left:
+        try:
+            q.destroy()
+        except Exception:
+            pass
