@@ -97,13 +97,6 @@ __device__ __forceinline__ void vput(volatile T* dst, const T& src) {
 #pragma unroll 4
     for (int i = 0; i < (int)(sizeof(T) / 8); ++i) d[i] = s[i];
 }
-template <typename T>
-__device__ __forceinline__ void vget(T* dst, const volatile T* src) {
-    const volatile uint64_t* s = reinterpret_cast<const volatile uint64_t*>(src);
-    uint64_t* d = reinterpret_cast<uint64_t*>(dst);
-#pragma unroll 4
-    for (int i = 0; i < (int)(sizeof(T) / 8); ++i) d[i] = s[i];
-}
 
 // block-cooperative copy of a layout record: one 8-byte word per thread, so
 // the volatile loads (L2 / NVLink round trips) overlap instead of queueing

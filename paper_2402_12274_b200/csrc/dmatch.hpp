@@ -31,6 +31,11 @@
 //              bounce buffer; its last CTA marks the bounce buffer consumed
 //              (the sender's host frees it lazily) and the status done.
 //
+// Messages and receives of <= 64 KiB take fused single-CTA forms: k_dm_send
+// packs a chain-layout message into its bounce buffer itself (no pack
+// launch), and k_dm_wait_copy waits and copies in one kernel -- the same
+// launch count per message as host matching.
+//
 // Every message and every posted receive carries its layout as a chain
 // (DmLay: contiguous or Rep^k(Run) -- vector, hvector, subarray faces), and
 // every copy is a chain-to-chain zipper (`chain_copy`: the packed stream cut
