@@ -39,7 +39,21 @@ template <> struct Vec<4> { using T = uint32_t; };
 template <> struct Vec<2> { using T = uint16_t; };
 template <> struct Vec<1> { using T = uint8_t; };
 
-constexpr int kChainThreads = 256;
+// Chain kernels run 64-thread CTAs (A/B on one box, round 2, bench step =
+// fused pack + unpack of the 12 halo faces): 256 threads 0.0767-0.0776 ms,
+// 128 threads 0.0745-0.0751, 64 threads 0.0717-0.0718 with the caps below.
+// Smaller CTAs retire and refill SMs at a finer grain, so the tail of the
+// latency-bound x-face rows overlaps the y/z rows better; the vector(N/64,
+// 32, 64) pack / unpack also gain (107.5 -> 87.6 / 98.4 -> 83.5 us) and the
+// contiguous 256 MiB copy is unchanged (90.6 -> 89.2 us).  The
+// MPX_* overrides exist for such A/B builds only (build.py MPX_NVCC_FLAGS).
+#ifndef MPX_CHAIN_THREADS
+#define MPX_CHAIN_THREADS 64
+#endif
+#ifndef MPX_PACK_MINB
+#define MPX_PACK_MINB 24
+#endif
+constexpr int kChainThreads = MPX_CHAIN_THREADS;
 
 // Scattered layout-side loads of short rows.  Measured on the fused halo
 // pack (ncu, profiles/): L1-allocating loads 31.6 us, L2-only (.cg) 36.0 us,
@@ -373,17 +387,18 @@ __device__ __forceinline__ void chain_job_body(const ChainJob& j, int64_t blk) {
 }
 
 // Separate entry points so each direction gets its own register budget
-// (A/B on the bench step, round 2): pack at 6 CTAs/SM (40 registers) 33.8 ->
-// 32.0 us; unpack (with the destination prefetches) at 4 CTAs/SM (64
-// registers) 52.1 -> 48.5 us -- 5 CTAs 48.2 (spills), 6 CTAs 49.4.
-__global__ void __launch_bounds__(kChainThreads, 6) k_chain_pack(const ChainBatch b) { chain_body<true>(b); }
+// (A/B on the bench step, round 2, then at 256 threads): pack at 1536
+// threads/SM (40 registers) 33.8 -> 32.0 us; unpack (with the destination
+// prefetches) at 1024 threads/SM (64 registers) 52.1 -> 48.5 us -- 1280
+// threads 48.2 (spills), 1536 threads 49.4.  Same budgets at 64 threads.
+__global__ void __launch_bounds__(kChainThreads, MPX_PACK_MINB) k_chain_pack(const ChainBatch b) { chain_body<true>(b); }
 // one layout: the job by value (~250 B of parameters instead of the batch's
 // ~4 KB: MPX_PROF measured 4.3-4.9 us of host time per single-layout launch)
-__global__ void __launch_bounds__(kChainThreads, 6) k_chain1_pack(const ChainJob j) {
+__global__ void __launch_bounds__(kChainThreads, MPX_PACK_MINB) k_chain1_pack(const ChainJob j) {
     chain_job_body<true>(j, blockIdx.x);
 }
 #ifndef MPX_UNPACK_MINB
-#define MPX_UNPACK_MINB 4
+#define MPX_UNPACK_MINB 16
 #endif
 #if MPX_UNPACK_MINB
 __global__ void __launch_bounds__(kChainThreads, MPX_UNPACK_MINB) k_chain_unpack(const ChainBatch b) { chain_body<false>(b); }
@@ -933,11 +948,24 @@ void chain_setup(const Plan& p, bool pack, ChainJob* j) {
 
 cudaError_t launch_chain_batch(ChainBatch& b, bool pack, int device, cudaStream_t stream) {
     if (b.njobs == 0) return cudaSuccess;
-    (void)pack;
     // Enough CTAs that every row gets its own warp (row mode, <= 2 KiB per
-    // warp pass) or its own thread (element mode) up to 8 CTAs per SM per
-    // job; bigger jobs loop (grid-stride) with 4 rows / 4 chunks in flight.
-    const int64_t cap = (int64_t)sm_count(device) * 8;
+    // warp pass) or its own thread (element mode) up to a cap of CTAs per SM
+    // per job; bigger jobs loop (grid-stride) with 4 rows / 4 chunks in
+    // flight.  Caps (64-thread CTAs): unpack 8, element / wide-mode pack 16,
+    // row mode 8 (A/B: pack caps 8 / 12 / 16 / 24 -> bench-step pack 31.7 /
+    // 31.6 / 30.3 / 31.7 us; a row-mode pack cap of 16 slows the contiguous
+    // 256 MiB pack 89.2 -> 92.7 us; an unpack cap of 6 gains nothing).
+#ifndef MPX_CHAIN_CAP
+#define MPX_CHAIN_CAP 8
+#endif
+#ifndef MPX_CHAIN_PACK_CAP
+#define MPX_CHAIN_PACK_CAP 16
+#endif
+#ifndef MPX_CHAIN_ROW_CAP
+#define MPX_CHAIN_ROW_CAP 8
+#endif
+    const int64_t cap = (int64_t)sm_count(device) * (pack ? MPX_CHAIN_PACK_CAP : MPX_CHAIN_CAP);
+    const int64_t row_cap = (int64_t)sm_count(device) * MPX_CHAIN_ROW_CAP;
     int64_t total = 0;
     for (int i = 0; i < b.njobs; ++i) {
         ChainJob& j = b.job[i];
@@ -957,7 +985,7 @@ cudaError_t launch_chain_batch(ChainBatch& b, bool pack, int device, cudaStream_
             const int64_t per = (!pack && big) ? (j.mode == CHAIN_ELEM ? MPX_ELEM_RPT : MPX_WIDE_RPT) : 1;
             want = (j.rows + per * kChainThreads - 1) / (per * kChainThreads);
         }
-        j.nblk = (int32_t)std::max<int64_t>(1, std::min<int64_t>(want, cap));
+        j.nblk = (int32_t)std::max<int64_t>(1, std::min<int64_t>(want, j.mode == CHAIN_ROW ? row_cap : cap));
         j.gsize = 1;
         j.gpos = 0;
         j.blk0 = -1;
