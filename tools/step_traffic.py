@@ -1,6 +1,6 @@
 """DRAM traffic of the bench step as a STEP (roofline.traffic evidence).
 
-    ncu --replay-mode range --profile-from-start off --cache-control all \
+    ncu --replay-mode range --cache-control all \
         --clock-control none --metrics dram__bytes_read.sum,dram__bytes_write.sum \
         --csv --log-file gpurun_out/step_range.csv python tools/step_traffic.py
 
