@@ -1160,15 +1160,26 @@ cudaError_t launch_zip(const Plan& ps, const Plan& pd, const uint8_t* src, uint8
     const uintptr_t m = reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | (uintptr_t)g;
     while (w > 1 && (m & (uintptr_t)(w - 1))) w >>= 1;
     if (npieces > 0) {
-        const int64_t want = (npieces + 511) / 512;
-        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count(ps.device) * 8));
+        // 128-thread CTAs, <= 8 per SM (A/B on the 2-rank vector(N/32,4,8)
+        // ring, `profiles/r02l_ab_zip.txt`: 256 threads 0.147-0.154 / 1.66-1.68
+        // ms at 64 MiB / 1 GiB, 128 threads 0.138-0.141 / 1.61-1.62, 64
+        // threads x 16 the same, 64 x 32 or 128 x 16 no gain)
+#ifndef MPX_ZIP_THREADS
+#define MPX_ZIP_THREADS 128
+#endif
+#ifndef MPX_ZIP_CAP
+#define MPX_ZIP_CAP 8
+#endif
+        constexpr int kZipThreads = MPX_ZIP_THREADS;
+        const int64_t want = (npieces + 2 * kZipThreads - 1) / (2 * kZipThreads);
+        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count(ps.device) * MPX_ZIP_CAP));
         const int gi = (int)g;
         switch (w) {
-        case 16: k_zip<16><<<(unsigned)grid, 256, 0, stream>>>(ps.chain, pd.chain, src, dst, npieces, gi); break;
-        case 8: k_zip<8><<<(unsigned)grid, 256, 0, stream>>>(ps.chain, pd.chain, src, dst, npieces, gi); break;
-        case 4: k_zip<4><<<(unsigned)grid, 256, 0, stream>>>(ps.chain, pd.chain, src, dst, npieces, gi); break;
-        case 2: k_zip<2><<<(unsigned)grid, 256, 0, stream>>>(ps.chain, pd.chain, src, dst, npieces, gi); break;
-        default: k_zip<1><<<(unsigned)grid, 256, 0, stream>>>(ps.chain, pd.chain, src, dst, npieces, gi); break;
+        case 16: k_zip<16><<<(unsigned)grid, kZipThreads, 0, stream>>>(ps.chain, pd.chain, src, dst, npieces, gi); break;
+        case 8: k_zip<8><<<(unsigned)grid, kZipThreads, 0, stream>>>(ps.chain, pd.chain, src, dst, npieces, gi); break;
+        case 4: k_zip<4><<<(unsigned)grid, kZipThreads, 0, stream>>>(ps.chain, pd.chain, src, dst, npieces, gi); break;
+        case 2: k_zip<2><<<(unsigned)grid, kZipThreads, 0, stream>>>(ps.chain, pd.chain, src, dst, npieces, gi); break;
+        default: k_zip<1><<<(unsigned)grid, kZipThreads, 0, stream>>>(ps.chain, pd.chain, src, dst, npieces, gi); break;
         }
     }
     if (npieces * g < bytes) k_zip_tail<<<1, 32, 0, stream>>>(ps.chain, pd.chain, src, dst, npieces * g, bytes);
